@@ -1,0 +1,166 @@
+/*
+ * hs_cuda.h -- thin C-ABI over the B200 (sm_100a) conjugation engine.
+ *
+ * This is the drop-in boundary of the hot path named in BASELINE.json north_star: the
+ * single-pass k-local conjugation rho -> U rho U^dagger and the Kraus sum
+ * sum_a K_a rho K_a^dagger on a hermitian operator stored in the reference's tiled
+ * lower-triangle layout.  Plain pointers and sizes only; every entry point returns an int
+ * status (HS_OK == 0) and never throws; hs_last_error() gives the message of the calling
+ * thread's last failure.  The C++ host API (include/hermsim_b200/hermsim.hpp), which keeps
+ * the reference's C++ surface, is layered on top of these calls.
+ *
+ * Reference interfaces replaced (arXiv 2604.15765, /root/reference/proj):
+ *   hs_state_*            TiledHermitian(n, m) ctor/dtor, data(), element_count()
+ *                         (include/hermsim/storage.hpp:60-96, src/storage.cpp:77-84)
+ *   hs_apply_transfer     apply_tiled_intra / apply_tiled_cross / apply_tiled_twoqubit
+ *                         (include/hermsim/kernels.hpp:73-83, src/kernels.cpp:176-188,430-444)
+ *   hs_apply_unitary      rank-1 channels through the direct block update of SPEC.md
+ *                         conjugation_kernels ("Unitary rank-1 channels may use the direct block
+ *                         update Eq. (2)"); also replaces the k = 3 dense round trip
+ *                         (src/kernels.cpp:498-505)
+ *   hs_apply_kraus        apply_generic for any k <= 3 (src/kernels.cpp:457-506)
+ *   hs_apply_hadamard     apply_hadamard (include/hermsim/native.hpp:43-44, src/native.cpp:343-361)
+ *   hs_apply_diagonal_phase  apply_diagonal_phase (native.hpp:39-41, native.cpp:238-324)
+ *   hs_apply_pauli        apply_pauli_x / apply_pauli_y (native.hpp:29-34, native.cpp:99-230)
+ *   hs_apply_permutation  apply_permutation (native.hpp:46-47, native.cpp:511-549)
+ *   hs_expectation        tr(rho O) of PAPER.md:412-417 / SPEC.md observables (absent from the
+ *                         reference code; strict ti > tj bound per SPEC.md)
+ *
+ * Conventions
+ *   - Payload layout is byte-identical to TiledHermitian: tile (ti >= tj) at element offset
+ *     (ti(ti+1)/2 + tj) * M^2, tiles and elements row-major, diagonal tiles hold all M^2
+ *     elements, complex128 interleaved (re, im).  `count` arguments are complex elements.
+ *   - "Bound" entry points take targets ASCENDING; local basis bit l <-> targets[l] (the result
+ *     of bind_channel, src/channel.cpp:196-268).  Matrices are row-major complex128.
+ *   - All device work is ordered on the state's CUDA stream and asynchronous, except the
+ *     calls documented as synchronising (download, expectation, trace, frobenius).
+ *   - One state may be used by one host thread at a time (the reference's exclusive-access
+ *     rule).
+ */
+#ifndef HS_CUDA_H
+#define HS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum hs_status {
+    HS_OK = 0,
+    HS_ERR_INVALID = -1,     /* std::invalid_argument in the reference */
+    HS_ERR_RANGE = -2,       /* std::out_of_range in the reference */
+    HS_ERR_CUDA = -3,        /* CUDA runtime failure (incl. missing device) */
+    HS_ERR_NOMEM = -4,       /* device allocation failed */
+    HS_ERR_UNSUPPORTED = -5  /* valid request this build does not implement */
+};
+
+/* KernelPath (include/hermsim/kernels.hpp:12-24); same numbering. */
+enum hs_kernel_path {
+    HS_PATH_DENSE_GENERIC = 0,
+    HS_PATH_PACKED_GENERIC = 1,
+    HS_PATH_TILED_INTRA = 2,
+    HS_PATH_TILED_CROSS = 3,
+    HS_PATH_TILED_MIXED = 4,
+    HS_PATH_DENSE_FALLBACK = 5,
+    HS_PATH_NATIVE_PAULI_X = 6,
+    HS_PATH_NATIVE_PAULI_Y = 7,
+    HS_PATH_NATIVE_PHASE = 8,
+    HS_PATH_NATIVE_HADAMARD = 9,
+    HS_PATH_NATIVE_PERMUTATION = 10
+};
+
+/* ApplyPlan (kernels.hpp:48-52) plus GPU launch facts. */
+typedef struct hs_plan {
+    int32_t path;           /* hs_kernel_path */
+    int32_t k;              /* number of targets */
+    uint32_t targets[3];    /* ascending */
+    uint64_t subcases[3];   /* cross_tile (A), cross_tile_adj (B), cross_tile_diag (C) */
+    int32_t grid_bits;      /* g: targets >= m */
+    int32_t launches;       /* kernels launched by this call */
+    uint64_t touched_bytes; /* bytes read + written by the launch (algorithmic) */
+} hs_plan;
+
+typedef struct hs_state hs_state;
+
+const char* hs_last_error(void);
+const char* hs_version(void);
+int hs_device_count(int* out);
+
+/* ---- state (TiledHermitian) ------------------------------------------------------------ */
+/* Allocates the tiled payload in HBM (zero-filled, like AlignedArray, types.hpp:37-42).
+ * Limits as the reference: 1 <= n <= 30, 0 <= m <= n + 2 (storage.cpp:12-20); this build
+ * additionally requires m <= 5 (tiles of at most 32 x 32). */
+int hs_state_create(int n, int m, int device, hs_state** out);
+int hs_state_free(hs_state* h);
+int hs_state_info(const hs_state* h, int* n, int* m, uint64_t* count, uint64_t* grid);
+/* Host payload <-> HBM.  `host` may be pageable or pinned; the copy is synchronous. */
+int hs_state_upload(hs_state* h, const double* host, uint64_t count);
+int hs_state_download(const hs_state* h, double* host, uint64_t count);
+/* Stream-ordered variants: `host` must be pinned (cudaHostAlloc / hs_host_alloc). */
+int hs_state_upload_async(hs_state* h, const double* host, uint64_t count);
+int hs_state_download_async(const hs_state* h, double* host, uint64_t count);
+/* Partial copies of `count` complex elements starting at element `offset`. */
+int hs_state_upload_range(hs_state* h, const double* host, uint64_t offset, uint64_t count);
+int hs_state_download_range(const hs_state* h, double* host, uint64_t offset, uint64_t count);
+int hs_state_copy(hs_state* dst, const hs_state* src);
+int hs_state_zero(hs_state* h);
+int hs_state_synchronize(const hs_state* h);
+/* Replaces the state's stream (cudaStream_t, NULL = a fresh non-blocking stream). */
+int hs_state_set_stream(hs_state* h, void* stream);
+void* hs_state_stream(const hs_state* h);
+void* hs_state_device_ptr(hs_state* h);
+
+int hs_host_alloc(uint64_t bytes, void** out);   /* pinned host memory */
+int hs_host_free(void* p);
+
+/* ---- bound engine entry points ------------------------------------------------------- */
+/* Kraus channel through its row-stacked transfer matrix (kernels.cpp:27-37): `s` is
+ * 4^k x 4^k complex, k in {1, 2}.  plan may be NULL. */
+int hs_apply_transfer(hs_state* h, int k, const double* s_rowstacked, const uint32_t* targets, hs_plan* plan);
+/* Unitary conjugation B -> U B U^dagger per coupled block, direct form; k in {1, 2, 3}. */
+int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* targets, hs_plan* plan);
+/* Generic Kraus set {L_a} (nops matrices 2^k x 2^k), k in {1, 2, 3}. */
+int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32_t* targets, hs_plan* plan);
+int hs_apply_hadamard(hs_state* h, uint32_t target, hs_plan* plan);
+/* Diagonal phase diag(p0, p1) (Z, S, T, Rz): phases = 2 complex of unit modulus. */
+int hs_apply_diagonal_phase(hs_state* h, uint32_t target, const double* phases, hs_plan* plan);
+/* Pauli X (y == 0) or Y (y != 0). */
+int hs_apply_pauli(hs_state* h, uint32_t target, int y, hs_plan* plan);
+/* Basis permutation (CX, SWAP, Toffoli, ...): table[x] = image of local basis x (bound). */
+int hs_apply_permutation(hs_state* h, int k, const uint32_t* table, const uint32_t* targets, hs_plan* plan);
+/* Generalised monomial U = P D: out(r, c) = d_r conj(d_c) B(pinv(r), pinv(c)); `perm` is the
+ * bound table (NULL = identity), `diag` 2^k complex (NULL = all ones). */
+int hs_apply_monomial(hs_state* h, int k, const uint32_t* perm, const double* diag, const uint32_t* targets,
+                      hs_plan* plan);
+
+/* ---- observables ---------------------------------------------------------------------- */
+/* tr(rho O) = sum_diag Re<O_t, rho_t>_F + 2 sum_{ti > tj} Re<O_t, rho_t>_F; deterministic
+ * fixed-order reduction; synchronising. */
+int hs_expectation(const hs_state* rho, const hs_state* obs, double* out);
+int hs_trace(const hs_state* h, double* out);
+int hs_frobenius(const hs_state* h, double* out);
+
+/* ---- seeded synthetic inputs (bench / test harness, computed on the device) ------------ */
+/* rho = (1/rank) sum_i |psi_i><psi_i|; psi = rank x 2^n complex (host, normalised).  Every
+ * stored element is formed with explicitly rounded products and sums in a fixed order, so
+ * the payload is bit-identical to the host construction hsg_rho_payload (harness.c). */
+int hs_state_fill_mixture(hs_state* h, int rank, const double* psi);
+/* O = sum_s coef_s P_s for Pauli strings with X-mask x[s], Z-mask z[s] (Y sets both) and
+ * ny[s] = #Y; bit-identical to hsg_pauli_payload (harness.c). */
+int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uint64_t* z, const int32_t* ny,
+                            const double* coef);
+
+/* ---- device timing helpers (CUDA events on the state's stream) ------------------------ */
+int hs_event_create(void** ev);
+int hs_event_destroy(void* ev);
+int hs_event_record(void* ev, const hs_state* h);
+int hs_event_elapsed_ms(void* start, void* stop, float* ms);  /* synchronises on stop */
+/* Number of kernel launches issued by this process so far (for gpu_launches accounting). */
+uint64_t hs_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HS_CUDA_H */

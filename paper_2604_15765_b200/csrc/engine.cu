@@ -1,0 +1,1596 @@
+// engine.cu -- B200 (sm_100a) conjugation engine behind the C-ABI of include/hs_cuda.h.
+//
+// Hot path (BASELINE.json north_star): rho -> sum_a L_a B L_a^dagger on every coupled
+// 2^k x 2^k block B of a hermitian operator held in the reference's tiled lower-triangle
+// layout (include/hermsim/storage.hpp:60-96).  The reference walks the blocks with CPU loops
+// (quad_kernels.hpp:85-217, kernels.cpp:198-444, native.cpp); here one pass over HBM:
+//
+//   * A "unit" is the set of logical tiles one grid base pair couples: 2^g x 2^g tiles for the
+//     g targets that are tile-grid bits (g = 0: one stored tile).  Logical tile (R, C) is the
+//     stored tile (tr[R], tc[C]) when tr[R] >= tc[C] and otherwise the conjugate transpose of
+//     the stored tile (tc[C], tr[R]) -- Algorithm 3's subcases A/B generalised to k <= 3
+//     (SURVEY 8a').
+//   * Path U: off-diagonal units (tbi > tbj), and every tile when g == 0.  A CTA stages a slab of
+//     a unit (all its logical tiles, a set of in-tile rows closed under the in-tile target bits)
+//     into shared memory in LOGICAL layout -- direct tiles row-wise, adjoint tiles read along
+//     stored rows (sector-aligned column chunks) and transposed + conjugated on the way in --
+//     applies the block transform in shared memory, and writes everything back.  Every stored
+//     element belongs to exactly one slab, so slabs are independent CTAs.
+//   * Path D: diagonal units (tbi == tbj, g >= 1), where logical (R, C) and (C, R) alias one
+//     stored tile.  Blocks are visited on the lower wedge of in-tile base pairs and hermitian
+//     mirrors are written explicitly (cross_tile_diag, quad_kernels.hpp:158-176, and the
+//     diagonal branch of tiled_two_cross, kernels.cpp:281-297, generalised; this also carries
+//     the corrected tiled_two_mixed mirror indices).
+//   * Block transforms: transfer matrix S (k = 1, 2; kernels.cpp:27-77), real Hadamard quad
+//     (native.cpp:332-339), direct two-stage U B U^dagger (k = 2, 3), monomial U = P D covering
+//     Pauli X/Y, diagonal phases and permutations (native.cpp:99-549) with untouched logical
+//     tiles skipped entirely, and a Kraus sum for k = 3.
+//
+// All data is complex128 (double2).  No tensor cores: the path is HBM-bound.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hs_cuda.h"
+
+namespace {
+
+constexpr int NTHR = 256;          // threads per CTA
+constexpr uint32_t CAP = 2048;     // target complex elements staged per CTA item (32 KiB)
+constexpr uint32_t CAPD = 2048;    // same for diagonal-unit items
+constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in smem)
+constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_MASK = (1ull << 56) - 1;
+
+enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5 };
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            return set_err(HS_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+    } while (0)
+
+// ----------------------------------------------------------------------------- geometry
+struct Geo {
+    // storage
+    uint32_t m, M, Mp, logM;
+    uint64_t G;
+    // operation
+    uint32_t k, kin, g, D;
+    uint32_t gr_pos[3];   // grid target bits (a - m), ascending
+    uint32_t in_mask;     // in-tile target bits
+    uint64_t nb;          // grid bases G >> g
+    // path U
+    uint64_t nU_units, nU_items;
+    uint32_t offdiag;     // 1: units are grid base pairs tbi > tbj; 0: units are stored tiles
+    uint32_t U, logU, SR, logSR, slabs, logSlabs, logNT, logNG, E;
+    uint32_t nxb, logNxb, nyb, logNyb;
+    uint32_t Epad;        // shared elements of a U item
+    uint8_t xdep[32];     // xs -> in-tile row offset
+    uint8_t sdep[32];     // slab -> in-tile row base
+    uint8_t xb_tab[32];   // row-base index -> xs base
+    uint8_t yb_tab[32];   // column-base index -> y base
+    uint8_t xs_in[8], y_in[8];
+    uint8_t xs_rin[32], xs_base[32], y_cin[32], y_base[32];
+    uint16_t comp_off[64];
+    uint64_t active;      // logical tiles (R * NG + C) that must be staged (monomial skip)
+    // path D
+    uint64_t nD_units, nD_items;
+    uint32_t nbase, BPI, itemsD;
+    uint64_t nblkD;
+};
+
+template <int NS>
+struct Coef {
+    double2 s[NS];
+    uint8_t pinv[8];
+    uint64_t fone;   // monomial: bit (rho*D+gamma) set when the factor is exactly 1
+};
+
+uint32_t pdep(uint32_t v, uint32_t mask) {
+    uint32_t r = 0;
+    for (uint32_t b = 0, i = 0; b < 32; ++b)
+        if (mask >> b & 1u) {
+            if (v >> i & 1u)
+                r |= 1u << b;
+            ++i;
+        }
+    return r;
+}
+uint32_t pext(uint32_t v, uint32_t mask) {
+    uint32_t r = 0;
+    for (uint32_t b = 0, i = 0; b < 32; ++b)
+        if (mask >> b & 1u) {
+            if (v >> b & 1u)
+                r |= 1u << i;
+            ++i;
+        }
+    return r;
+}
+uint32_t ilog2(uint64_t v) {
+    uint32_t r = 0;
+    while ((1ull << r) < v)
+        ++r;
+    return r;
+}
+
+// ------------------------------------------------------------------------ device helpers
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // c + a*b
+    c.x = fma(a.x, b.x, c.x);
+    c.x = fma(-a.y, b.y, c.x);
+    c.y = fma(a.x, b.y, c.y);
+    c.y = fma(a.y, b.x, c.y);
+    return c;
+}
+__device__ __forceinline__ double2 cfmaconj(double2 a, double2 b, double2 c) {  // c + a*conj(b)
+    c.x = fma(a.x, b.x, c.x);
+    c.x = fma(a.y, b.y, c.x);
+    c.y = fma(a.y, b.x, c.y);
+    c.y = fma(-a.x, b.y, c.y);
+    return c;
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 ldg2(const double2* p) { return *p; }
+
+__device__ __forceinline__ uint64_t tri(uint64_t t) { return t * (t + 1) / 2; }
+
+// insert_bits (bit_index.hpp:40-51) on grid indices
+__device__ __forceinline__ uint64_t ins_bits(uint64_t s, uint32_t a, const uint32_t* pos, uint32_t k) {
+    for (uint32_t l = 0; l < k; ++l) {
+        const uint32_t p = pos[l];
+        const uint64_t right = s & ((1ull << p) - 1);
+        s = ((((s >> p) << 1) | ((a >> l) & 1u)) << p) | right;
+    }
+    return s;
+}
+
+// u -> (i > j) with u = i(i-1)/2 + j
+__device__ __forceinline__ void tri_strict(uint64_t u, uint64_t& i, uint64_t& j) {
+    uint64_t r = (uint64_t)((1.0 + sqrt(1.0 + 8.0 * (double)u)) * 0.5);
+    while (r * (r - 1) / 2 > u)
+        --r;
+    while ((r + 1) * r / 2 <= u)
+        ++r;
+    i = r;
+    j = u - r * (r - 1) / 2;
+}
+// u -> (i >= j) with u = i(i+1)/2 + j
+__device__ __forceinline__ void tri_loose(uint64_t u, uint64_t& i, uint64_t& j) {
+    uint64_t r = (uint64_t)((sqrt(1.0 + 8.0 * (double)u) - 1.0) * 0.5);
+    while (r * (r + 1) / 2 > u)
+        --r;
+    while ((r + 1) * (r + 2) / 2 <= u)
+        ++r;
+    i = r;
+    j = u - r * (r + 1) / 2;
+}
+
+// ------------------------------------------------------------------- block transforms
+// The transforms see a block through (base, off[]) : element (rho, gamma) lives at
+// sm[base + off[rho * D + gamma]].  They are shared by paths U and D.
+
+// S-form, k = 1 (TransferQuad, kernels.cpp:66-77): v row-stacked (h00, h01, h10, h11)
+template <int MODE>
+__device__ __forceinline__ void xf_quad(double2* sm, uint32_t base, const uint16_t* off, const Coef<16>& cf) {
+    double2 v0 = sm[base + off[0]], v1 = sm[base + off[1]], v2 = sm[base + off[2]], v3 = sm[base + off[3]];
+    double2 w0, w1, w2, w3;
+    if (MODE == M_HAD) {  // HadamardQuad (native.cpp:332-339)
+        const double2 a = make_double2(v0.x + v1.x, v0.y + v1.y), b = make_double2(v0.x - v1.x, v0.y - v1.y);
+        const double2 c = make_double2(v2.x + v3.x, v2.y + v3.y), d = make_double2(v2.x - v3.x, v2.y - v3.y);
+        w0 = make_double2(0.5 * (a.x + c.x), 0.5 * (a.y + c.y));
+        w1 = make_double2(0.5 * (b.x + d.x), 0.5 * (b.y + d.y));
+        w2 = make_double2(0.5 * (a.x - c.x), 0.5 * (a.y - c.y));
+        w3 = make_double2(0.5 * (b.x - d.x), 0.5 * (b.y - d.y));
+    } else {
+        const double2* s = cf.s;
+        w0 = cmul(s[0], v0); w0 = cfma(s[1], v1, w0); w0 = cfma(s[2], v2, w0); w0 = cfma(s[3], v3, w0);
+        w1 = cmul(s[4], v0); w1 = cfma(s[5], v1, w1); w1 = cfma(s[6], v2, w1); w1 = cfma(s[7], v3, w1);
+        w2 = cmul(s[8], v0); w2 = cfma(s[9], v1, w2); w2 = cfma(s[10], v2, w2); w2 = cfma(s[11], v3, w2);
+        w3 = cmul(s[12], v0); w3 = cfma(s[13], v1, w3); w3 = cfma(s[14], v2, w3); w3 = cfma(s[15], v3, w3);
+    }
+    sm[base + off[0]] = w0;
+    sm[base + off[1]] = w1;
+    sm[base + off[2]] = w2;
+    sm[base + off[3]] = w3;
+}
+
+// S-form, k = 2 (matvec<16>, kernels.cpp:39-48)
+__device__ __forceinline__ void xf_s16(double2* sm, uint32_t base, const uint16_t* off, const Coef<256>& cf) {
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        v[i] = sm[base + off[i]];
+#pragma unroll 4
+    for (int r = 0; r < 16; ++r) {
+        double2 acc = cmul(cf.s[r * 16], v[0]);
+#pragma unroll
+        for (int c = 1; c < 16; ++c)
+            acc = cfma(cf.s[r * 16 + c], v[c], acc);
+        sm[base + off[r]] = acc;
+    }
+}
+
+// Direct form, stage 1: row rho of B <- B[rho, :] L^dagger  (Y = B L^dagger)
+template <int K, int NS>
+__device__ __forceinline__ void xf_row(double2* sm, uint32_t base, const uint16_t* off, uint32_t rho,
+                                       const double2* L) {
+    constexpr int D = 1 << K;
+    double2 v[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c)
+        v[c] = sm[base + off[rho * D + c]];
+#pragma unroll
+    for (int c = 0; c < D; ++c) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < D; ++t)
+            acc = cfmaconj(v[t], L[c * D + t], acc);  // sum_t B[rho][t] conj(L[c][t])
+        sm[base + off[rho * D + c]] = acc;
+    }
+}
+// Direct form, stage 2: column gamma <- L Y[:, gamma]
+template <int K>
+__device__ __forceinline__ void xf_col(double2* sm, uint32_t base, const uint16_t* off, uint32_t gamma,
+                                       const double2* L) {
+    constexpr int D = 1 << K;
+    double2 v[D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+        v[r] = sm[base + off[r * D + gamma]];
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < D; ++t)
+            acc = cfma(L[r * D + t], v[t], acc);
+        sm[base + off[r * D + gamma]] = acc;
+    }
+}
+
+// Kraus sum (k = 3 generic, r > 1): out = sum_a L_a B L_a^dagger, per block, with the block
+// held in shared memory: X (input) -> T (= X L_a^dagger) -> O (+= L_a T).  Runs the row/column
+// stages over three buffers.
+// (handled inline in the kernels; see run_compute)
+
+// --------------------------------------------------------------------------- kernel body
+struct KrausArgs {
+    const double2* ops;  // nops x D x D (device)
+    int nops;
+};
+
+// Block base for path U: ((uu << logNT) * SR + xb_tab[xbi]) * Mp + yb_tab[ybi]
+struct UAddr {
+    const Geo* G;
+    const uint8_t* xb;
+    const uint8_t* yb;
+    __device__ __forceinline__ uint32_t base(uint32_t b) const {
+        const uint32_t ybi = b & (G->nyb - 1);
+        const uint32_t xbi = (b >> G->logNyb) & (G->nxb - 1);
+        const uint32_t uu = b >> (G->logNyb + G->logNxb);
+        return (((uu << G->logNT) * G->SR) + xb[xbi]) * G->Mp + yb[ybi];
+    }
+    __device__ __forceinline__ uint32_t unit(uint32_t b) const { return b >> (G->logNyb + G->logNxb); }
+};
+struct DAddr {
+    uint32_t shift;  // 2K
+    __device__ __forceinline__ uint32_t base(uint32_t b) const { return b << shift; }
+};
+
+// Runs the compute stage(s) of MODE over `nblk` blocks addressed by A; valid(b) filters.
+template <int K, int MODE, int NS, class A, class V>
+__device__ __forceinline__ void compute_blocks(double2* sm, double2* sm2, double2* sm3, const uint16_t* off,
+                                               uint32_t nblk, const A& addr, const V& valid, const Coef<NS>& cf,
+                                               const KrausArgs& ka, uint32_t stage_order_nyb_log, double2* lsm) {
+    constexpr int D = 1 << K;
+    const int tid = threadIdx.x;
+    if constexpr (MODE == M_S1 || MODE == M_HAD) {
+        for (uint32_t b = tid; b < nblk; b += NTHR)
+            if (valid(b))
+                xf_quad<MODE>(sm, addr.base(b), off, *reinterpret_cast<const Coef<16>*>(&cf));
+    } else if constexpr (MODE == M_S2) {
+        for (uint32_t b = tid; b < nblk; b += NTHR)
+            if (valid(b))
+                xf_s16(sm, addr.base(b), off, *reinterpret_cast<const Coef<256>*>(&cf));
+    } else if constexpr (MODE == M_DIRECT) {
+        // items (b, rho): keep the fastest-varying block index innermost so lanes hit
+        // consecutive columns; stage_order_nyb_log = log2 of that fastest extent.
+        const uint32_t lo = stage_order_nyb_log, lomask = (1u << lo) - 1;
+        const uint32_t items = nblk * D;
+        for (uint32_t w = tid; w < items; w += NTHR) {
+            const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo);
+            const uint32_t rho = (w >> lo) % D;
+            if (valid(b))
+                xf_row<K, NS>(sm, addr.base(b), off, rho, cf.s);
+        }
+        __syncthreads();
+        for (uint32_t w = tid; w < items; w += NTHR) {
+            const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo);
+            const uint32_t gamma = (w >> lo) % D;
+            if (valid(b))
+                xf_col<K>(sm, addr.base(b), off, gamma, cf.s);
+        }
+    } else if constexpr (MODE == M_KRAUS) {
+        // sm = X (input), sm2 = T, sm3 = O; all share the same addressing.
+        const uint32_t lo = stage_order_nyb_log, lomask = (1u << lo) - 1;
+        const uint32_t items = nblk * D;
+        for (uint32_t w = tid; w < items; w += NTHR) {
+            const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo);
+            const uint32_t r = (w >> lo) % D;
+            if (valid(b)) {
+                const uint32_t base = addr.base(b);
+#pragma unroll
+                for (int c = 0; c < D; ++c)
+                    sm3[base + off[r * D + c]] = make_double2(0.0, 0.0);
+            }
+        }
+        double2* Lr = lsm;  // L_a staged in shared memory (after the three block buffers)
+        for (int a = 0; a < ka.nops; ++a) {
+            __syncthreads();
+            for (int i = tid; i < D * D; i += NTHR)
+                Lr[i] = ka.ops[(size_t)a * D * D + i];
+            __syncthreads();
+            for (uint32_t w = tid; w < items; w += NTHR) {  // T = X L^dagger (rows)
+                const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo);
+                const uint32_t rho = (w >> lo) % D;
+                if (!valid(b))
+                    continue;
+                const uint32_t base = addr.base(b);
+                double2 v[D];
+#pragma unroll
+                for (int c = 0; c < D; ++c)
+                    v[c] = sm[base + off[rho * D + c]];
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int t = 0; t < D; ++t)
+                        acc = cfmaconj(v[t], Lr[c * D + t], acc);
+                    sm2[base + off[rho * D + c]] = acc;
+                }
+            }
+            __syncthreads();
+            for (uint32_t w = tid; w < items; w += NTHR) {  // O += L T (columns)
+                const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo);
+                const uint32_t gamma = (w >> lo) % D;
+                if (!valid(b))
+                    continue;
+                const uint32_t base = addr.base(b);
+                double2 v[D];
+#pragma unroll
+                for (int r = 0; r < D; ++r)
+                    v[r] = sm2[base + off[r * D + gamma]];
+#pragma unroll
+                for (int r = 0; r < D; ++r) {
+                    double2 acc = sm3[base + off[r * D + gamma]];
+#pragma unroll
+                    for (int t = 0; t < D; ++t)
+                        acc = cfma(Lr[r * D + t], v[t], acc);
+                    sm3[base + off[r * D + gamma]] = acc;
+                }
+            }
+        }
+        __syncthreads();
+        for (uint32_t w = tid; w < items; w += NTHR) {  // copy O back into X
+            const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo);
+            const uint32_t r = (w >> lo) % D;
+            if (valid(b)) {
+                const uint32_t base = addr.base(b);
+#pragma unroll
+                for (int c = 0; c < D; ++c)
+                    sm[base + off[r * D + c]] = sm3[base + off[r * D + c]];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- path U
+template <int K, int MODE, int NS>
+__device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, double2* __restrict__ st,
+                       uint64_t item, double2* sm, uint64_t* ttab, uint16_t* off) {
+    const int tid = threadIdx.x;
+    constexpr int D = 1 << K;
+    const uint64_t ug = item >> G.logSlabs;
+    const uint32_t slab = (uint32_t)(item & (G.slabs - 1));
+    const uint32_t x0 = G.sdep[slab];
+    const uint64_t u0 = ug << G.logU;
+    const uint32_t ntt = G.U << G.logNT;
+    const uint32_t NGm = (1u << G.logNG) - 1;
+
+    for (uint32_t i = tid; i < ntt; i += NTHR) {
+        const uint32_t uu = i >> G.logNT, T = i & ((1u << G.logNT) - 1);
+        const uint64_t u = u0 + uu;
+        uint64_t ent;
+        if (u >= G.nU_units) {
+            ent = F_BAD;
+        } else if (!G.offdiag) {
+            ent = u;
+        } else {
+            uint64_t tbi, tbj;
+            tri_strict(u, tbi, tbj);
+            const uint32_t R = T >> G.logNG, C = T & NGm;
+            const uint64_t tr = ins_bits(tbi, R, G.gr_pos, G.g), tc = ins_bits(tbj, C, G.gr_pos, G.g);
+            ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
+        }
+        if (MODE == M_MONO && !((G.active >> T) & 1ull))
+            ent |= F_SKIP;
+        ttab[i] = ent;
+    }
+    for (uint32_t i = tid; i < (uint32_t)(D * D); i += NTHR)
+        off[i] = G.comp_off[i];
+    __syncthreads();
+
+    const uint32_t logTE = G.logSR + G.logM, TEm = (1u << logTE) - 1;
+    const uint32_t Mm = G.M - 1, SRm = G.SR - 1;
+    const uint32_t Mp = G.Mp;
+
+    // ---- load: HBM -> shared (logical layout, adjoint tiles transposed + conjugated)
+    for (uint32_t e0 = 0; e0 < G.E; e0 += NTHR * 8) {
+        double2 v[8];
+        uint32_t dst[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t e = e0 + j * NTHR + tid;
+            dst[j] = 0xffffffffu;
+            if (e < G.E) {
+                const uint32_t tt = e >> logTE, l = e & TEm;
+                const uint64_t ent = ttab[tt];
+                if (!(ent & (F_BAD | F_SKIP))) {
+                    const uint64_t tb = (ent & F_MASK) << (2 * G.logM);
+                    uint32_t xs, y;
+                    uint64_t src;
+                    if (!(ent & F_ADJ)) {
+                        xs = l >> G.logM;
+                        y = l & Mm;
+                        src = tb + ((uint64_t)(x0 | G.xdep[xs]) << G.logM) + y;
+                    } else {
+                        y = l >> G.logSR;
+                        xs = l & SRm;
+                        src = tb + ((uint64_t)y << G.logM) + (x0 | G.xdep[xs]);
+                    }
+                    v[j] = ldg2(st + src);
+                    if (ent & F_ADJ)
+                        v[j].y = -v[j].y;
+                    dst[j] = (tt * G.SR + xs) * Mp + y;
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (dst[j] != 0xffffffffu)
+                sm[dst[j]] = v[j];
+    }
+    __syncthreads();
+
+    // ---- transform
+    if constexpr (MODE != M_MONO) {
+        UAddr A{&G, G.xb_tab, G.yb_tab};
+        const uint32_t nblk = G.U << (G.logNxb + G.logNyb);
+        const uint64_t nU = G.nU_units;
+        auto valid = [&](uint32_t b) { return u0 + A.unit(b) < nU; };
+        double2* sm2 = sm + G.Epad;
+        double2* sm3 = sm + 2 * G.Epad;
+        compute_blocks<K, MODE, NS>(sm, sm2, sm3, off, nblk, A, valid, cf, ka, G.logNyb, sm + 3 * G.Epad);
+        __syncthreads();
+    }
+
+    // ---- store: shared -> HBM
+    for (uint32_t e0 = 0; e0 < G.E; e0 += NTHR * 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t e = e0 + j * NTHR + tid;
+            if (e >= G.E)
+                continue;
+            const uint32_t tt = e >> logTE, l = e & TEm;
+            const uint64_t ent = ttab[tt];
+            if (ent & (F_BAD | F_SKIP))
+                continue;
+            const uint64_t tb = (ent & F_MASK) << (2 * G.logM);
+            const bool adj = (ent & F_ADJ) != 0;
+            uint32_t xs, y;
+            uint64_t dstg;
+            if (!adj) {
+                xs = l >> G.logM;
+                y = l & Mm;
+                dstg = tb + ((uint64_t)(x0 | G.xdep[xs]) << G.logM) + y;
+            } else {
+                y = l >> G.logSR;
+                xs = l & SRm;
+                dstg = tb + ((uint64_t)y << G.logM) + (x0 | G.xdep[xs]);
+            }
+            double2 w;
+            if constexpr (MODE == M_MONO) {
+                const uint32_t uu = tt >> G.logNT, T = tt & ((1u << G.logNT) - 1);
+                const uint32_t R = T >> G.logNG, C = T & NGm;
+                const uint32_t rho = (R << G.kin) | G.xs_rin[xs], gam = (C << G.kin) | G.y_cin[y];
+                const uint32_t rs = cf.pinv[rho], gs = cf.pinv[gam];
+                const uint32_t kinm = (1u << G.kin) - 1;
+                const uint32_t src = (((uu << G.logNT) + ((rs >> G.kin) << G.logNG) + (gs >> G.kin)) * G.SR +
+                                      (G.xs_base[xs] | G.xs_in[rs & kinm])) * Mp +
+                                     (G.y_base[y] | G.y_in[gs & kinm]);
+                w = sm[src];
+                const uint32_t fi = rho * D + gam;
+                if (!((cf.fone >> fi) & 1ull))
+                    w = cmul(cf.s[fi], w);
+            } else {
+                w = sm[(tt * G.SR + xs) * Mp + y];
+            }
+            if (adj)
+                w.y = -w.y;
+            st[dstg] = w;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------- path D
+template <int K, int MODE, int NS>
+__device__ void path_d(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, double2* __restrict__ st,
+                       uint64_t item, double2* sm, uint64_t* tabs, uint32_t* bpos, uint16_t* off) {
+    constexpr int D = 1 << K, DD = D * D;
+    const int tid = threadIdx.x;
+    const uint64_t tb = item / G.itemsD;
+    const uint64_t b0 = (item % G.itemsD) * G.BPI;
+    uint64_t* trow = tabs;  // NG entries: tr[R]
+    const uint32_t NG = 1u << G.logNG;
+    for (uint32_t i = tid; i < NG; i += NTHR)
+        trow[i] = ins_bits(tb, i, G.gr_pos, G.g);
+    for (uint32_t i = tid; i < G.BPI; i += NTHR) {
+        const uint64_t b = b0 + i;
+        uint32_t v = 0xffffffffu;
+        if (b < G.nblkD) {
+            uint64_t xi, yi;
+            tri_loose(b, xi, yi);
+            v = ((uint32_t)xi << 16) | (uint32_t)yi;
+        }
+        bpos[i] = v;
+    }
+    for (uint32_t i = tid; i < (uint32_t)DD; i += NTHR)
+        off[i] = (uint16_t)i;
+    __syncthreads();
+    const uint32_t kinm = (1u << G.kin) - 1;
+    const uint32_t E = G.BPI * DD;
+    const uint32_t logM = G.logM;
+
+    // ---- gather (monomial permutation applied here)
+    for (uint32_t e = tid; e < E; e += NTHR) {
+        const uint32_t lb = e / DD, comp = e % DD;
+        const uint32_t bp = bpos[lb];
+        if (bp == 0xffffffffu)
+            continue;
+        uint32_t rho = comp / D, gam = comp % D;
+        double2 f = make_double2(1.0, 0.0);
+        bool one = true;
+        if constexpr (MODE == M_MONO) {
+            one = (cf.fone >> comp) & 1ull;
+            f = cf.s[comp];
+            rho = cf.pinv[rho];
+            gam = cf.pinv[gam];
+        }
+        const uint32_t xb = G.yb_tab[bp >> 16], yb = G.yb_tab[bp & 0xffffu];
+        const uint32_t R = rho >> G.kin, C = gam >> G.kin;
+        const uint32_t x = xb | G.y_in[rho & kinm], y = yb | G.y_in[gam & kinm];
+        double2 v;
+        if (R >= C) {
+            v = st[((tri(trow[R]) + trow[C]) << (2 * logM)) + ((uint64_t)x << logM) + y];
+        } else {
+            v = st[((tri(trow[C]) + trow[R]) << (2 * logM)) + ((uint64_t)y << logM) + x];
+            v.y = -v.y;
+        }
+        if (!one)
+            v = cmul(f, v);
+        sm[e] = v;
+    }
+    __syncthreads();
+    if constexpr (MODE != M_MONO) {
+        DAddr A{2u * K};
+        auto valid = [&](uint32_t b) { return bpos[b] != 0xffffffffu; };
+        compute_blocks<K, MODE, NS>(sm, sm + E, sm + 2 * E, off, G.BPI, A, valid, cf, ka, 0, sm + 3 * E);
+        __syncthreads();
+    }
+    // ---- scatter with the wedge rules (see file header)
+    for (uint32_t e = tid; e < E; e += NTHR) {
+        const uint32_t lb = e / DD, comp = e % DD;
+        const uint32_t bp = bpos[lb];
+        if (bp == 0xffffffffu)
+            continue;
+        const uint32_t xbi = bp >> 16, ybi = bp & 0xffffu;
+        const uint32_t rho = comp / D, gam = comp % D;
+        if (xbi == ybi && rho < gam)
+            continue;
+        const uint32_t xb = G.yb_tab[xbi], yb = G.yb_tab[ybi];
+        const uint32_t R = rho >> G.kin, C = gam >> G.kin;
+        const uint32_t x = xb | G.y_in[rho & kinm], y = yb | G.y_in[gam & kinm];
+        const double2 w = sm[e];
+        if (R > C) {
+            st[((tri(trow[R]) + trow[C]) << (2 * logM)) + ((uint64_t)x << logM) + y] = w;
+        } else if (R < C) {
+            st[((tri(trow[C]) + trow[R]) << (2 * logM)) + ((uint64_t)y << logM) + x] = cconj(w);
+        } else {
+            const uint64_t t0 = (tri(trow[R]) + trow[R]) << (2 * logM);
+            st[t0 + ((uint64_t)x << logM) + y] = w;
+            if (x != y)
+                st[t0 + ((uint64_t)y << logM) + x] = cconj(w);
+        }
+    }
+}
+
+template <int K, int MODE, int NS>
+__global__ void __launch_bounds__(NTHR) conj_kernel(const Geo G, const Coef<NS> cf, const KrausArgs ka,
+                                                    double2* __restrict__ st) {
+    extern __shared__ __align__(16) double2 smem[];
+    __shared__ uint64_t tabs[MAX_TT];
+    __shared__ uint32_t bpos[CAPD / 4];
+    __shared__ uint16_t off[64];
+    const uint64_t item = blockIdx.x + (uint64_t)blockIdx.y * gridDim.x;
+    if (item < G.nD_items)
+        path_d<K, MODE, NS>(G, cf, ka, st, item, smem, tabs, bpos, off);
+    else if (item < G.nD_items + G.nU_items)
+        path_u<K, MODE, NS>(G, cf, ka, st, item - G.nD_items, smem, tabs, off);
+}
+
+// ------------------------------------------------------------------------- reductions
+// Per-CTA partial sums over a contiguous tile range, fixed order, then a single-CTA
+// ordered sum: deterministic for a given grid (SPEC.md observables: fixed-order reduction).
+constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs
+
+__device__ double block_sum(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = NTHR / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// kind 0: Re<a, b>_F (expectation); kind 1: |a|^2 (frobenius); kind 2: trace (diagonal elements)
+__global__ void __launch_bounds__(NTHR) reduce_kernel(const double2* __restrict__ a, const double2* __restrict__ b,
+                                                      uint64_t ntiles, uint32_t logM, int kind, double* partials) {
+    __shared__ double sh[NTHR];
+    const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+    const uint32_t MM = 1u << (2 * logM), M = 1u << logM;
+    double dsum = 0.0, osum = 0.0;
+    if (t0 < t1) {
+        uint64_t ti, tj;
+        tri_loose(t0, ti, tj);
+        for (uint64_t t = t0; t < t1; ++t) {
+            const double2* pa = a + (t << (2 * logM));
+            const double2* pb = b + (t << (2 * logM));
+            double acc = 0.0;
+            if (kind == 2) {
+                if (ti == tj)
+                    for (uint32_t p = threadIdx.x; p < M; p += NTHR)
+                        acc += pa[p * M + p].x;
+            } else {
+                for (uint32_t p = threadIdx.x; p < MM; p += NTHR) {
+                    const double2 x = pa[p], y = pb[p];
+                    acc = fma(x.x, y.x, acc);
+                    acc = fma(x.y, y.y, acc);
+                }
+            }
+            if (ti == tj)
+                dsum += acc;
+            else
+                osum += acc;
+            if (++tj > ti) {
+                ++ti;
+                tj = 0;
+            }
+        }
+    }
+    dsum = block_sum(dsum, sh);
+    osum = block_sum(osum, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = dsum;
+        partials[2 * blockIdx.x + 1] = osum;
+    }
+}
+
+__global__ void finish_kernel(const double* partials, int nparts, int kind, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double d = 0.0, o = 0.0;
+        for (int i = 0; i < nparts; ++i) {
+            d += partials[2 * i];
+            o += partials[2 * i + 1];
+        }
+        out[0] = kind == 2 ? d : d + 2.0 * o;
+    }
+}
+
+// ------------------------------------------------------------------------- generators
+// rho(i, j) = (1/rank) sum_a psi_a[i] conj(psi_a[j]) with explicit rounding (no contraction),
+// bit-identical to hsg_rho_payload (harness.c).
+__global__ void fill_mixture_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, const double2* psi,
+                                    int rank, double inv) {
+    const uint32_t M = 1u << logM;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        tri_loose(t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 acc = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            for (int a = 0; a < rank; ++a) {
+                const double2 p = psi[(uint64_t)a * N + i], q = psi[(uint64_t)a * N + j];
+                const double re = __dadd_rn(__dmul_rn(p.x, q.x), __dmul_rn(p.y, q.y));
+                const double im = __dsub_rn(__dmul_rn(p.y, q.x), __dmul_rn(p.x, q.y));
+                acc.x = __dadd_rn(acc.x, re);
+                acc.y = __dadd_rn(acc.y, im);
+            }
+            acc.x = __dmul_rn(acc.x, inv);
+            acc.y = __dmul_rn(acc.y, inv);
+        }
+        st[e] = acc;
+    }
+}
+
+struct PauliArgs {
+    const uint64_t* x;
+    const uint64_t* z;
+    const int32_t* ny;
+    const double* coef;
+    int count;
+};
+
+__global__ void fill_pauli_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, PauliArgs pa) {
+    const uint32_t M = 1u << logM;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        tri_loose(t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 acc = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            const uint64_t ij = i ^ j;
+            for (int s = 0; s < pa.count; ++s) {
+                if (pa.x[s] != ij)
+                    continue;
+                double v = pa.coef[s];
+                if (__popcll(j & pa.z[s]) & 1)
+                    v = -v;
+                const int ph = pa.ny[s] & 3;  // i^ny
+                if (ph == 0)
+                    acc.x = __dadd_rn(acc.x, v);
+                else if (ph == 1)
+                    acc.y = __dadd_rn(acc.y, v);
+                else if (ph == 2)
+                    acc.x = __dadd_rn(acc.x, -v);
+                else
+                    acc.y = __dadd_rn(acc.y, -v);
+            }
+        }
+        st[e] = acc;
+    }
+}
+
+}  // namespace
+
+// =============================================================================== host side
+struct hs_state {
+    int n, m, device;
+    uint64_t N, M, G, count;
+    double2* d = nullptr;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double* red = nullptr;  // reduction scratch: 2 * RED_BLOCKS partials + result
+    double2* kraus = nullptr;  // device buffer for k = 3 Kraus operators
+    size_t kraus_cap = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev)
+            cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev)
+            cudaSetDevice(prev);
+    }
+};
+
+int check_targets(const hs_state* h, int k, const uint32_t* t) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (k < 1 || k > 3 || !t)
+        return set_err(HS_ERR_INVALID, "locality must be 1..3");
+    for (int i = 0; i < k; ++i) {
+        if (t[i] >= (uint32_t)h->n)
+            return set_err(HS_ERR_RANGE, "target qubit out of range");
+        if (i > 0 && t[i - 1] >= t[i])
+            return set_err(HS_ERR_INVALID, "bound targets must be strictly ascending");
+    }
+    return HS_OK;
+}
+
+// Builds the launch geometry of one k-local operation on state h.
+void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extra_buffers) {
+    std::memset(&G, 0, sizeof(G));
+    G.m = h->m;
+    G.M = 1u << h->m;
+    G.logM = h->m;
+    G.Mp = G.M >= 8 ? G.M + 1 : G.M;
+    G.G = h->G;
+    G.k = k;
+    G.D = 1u << k;
+    uint32_t in_mask = 0;
+    uint32_t g = 0;
+    for (int l = 0; l < k; ++l) {
+        if (t[l] < (uint32_t)h->m)
+            in_mask |= 1u << t[l];
+        else
+            G.gr_pos[g++] = t[l] - h->m;
+    }
+    G.in_mask = in_mask;
+    G.g = g;
+    G.kin = k - g;
+    G.logNG = g;
+    G.logNT = 2 * g;
+    const uint32_t NT = 1u << (2 * g);
+    G.nb = G.G >> g;
+    if (g == 0) {
+        G.offdiag = 0;
+        G.nU_units = G.G * (G.G + 1) / 2;
+        G.nD_units = 0;
+    } else {
+        G.offdiag = 1;
+        G.nU_units = G.nb * (G.nb - 1) / 2;
+        G.nD_units = G.nb;
+    }
+    const uint32_t M = G.M;
+    const uint64_t unit_elems = (uint64_t)NT * M * M;
+    uint32_t cmask;
+    if (unit_elems <= CAP) {
+        G.SR = M;
+        G.slabs = 1;
+        uint32_t U = (uint32_t)(CAP / unit_elems);
+        if ((uint64_t)U * NT > MAX_TT)
+            U = std::max<uint32_t>(1, MAX_TT / NT);
+        G.U = U;
+        cmask = M - 1;
+    } else {
+        G.U = 1;
+        const uint32_t base = in_mask | (M >= 2 ? 1u : 0u);
+        uint32_t SR = (uint32_t)(CAP / ((uint64_t)NT * M));
+        SR = std::max<uint32_t>(SR, 1u << __builtin_popcount(base));
+        SR = std::min<uint32_t>(SR, M);
+        cmask = base;
+        for (uint32_t b = 0; b < h->m && (uint32_t)__builtin_popcount(cmask) < ilog2(SR); ++b)
+            cmask |= 1u << b;
+        G.SR = SR;
+        G.slabs = M / SR;
+    }
+    G.logU = ilog2(G.U);
+    G.logSR = ilog2(G.SR);
+    G.logSlabs = ilog2(G.slabs);
+    G.E = G.U * NT * G.SR * M;
+    G.Epad = G.U * NT * G.SR * G.Mp;
+    for (uint32_t xs = 0; xs < G.SR; ++xs)
+        G.xdep[xs] = (uint8_t)pdep(xs, cmask);
+    for (uint32_t s = 0; s < G.slabs; ++s)
+        G.sdep[s] = (uint8_t)pdep(s, (M - 1) & ~cmask);
+    G.nU_items = ((G.nU_units + G.U - 1) / G.U) * G.slabs;
+    // in-tile target bits as seen in slab-row (xs) coordinates
+    uint32_t xs_tmask = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        if (in_mask >> b & 1u)
+            xs_tmask |= 1u << __builtin_popcount(cmask & ((1u << b) - 1));
+    G.nxb = G.SR >> G.kin;
+    G.nyb = M >> G.kin;
+    G.logNxb = ilog2(G.nxb);
+    G.logNyb = ilog2(G.nyb);
+    for (uint32_t i = 0; i < G.nxb; ++i)
+        G.xb_tab[i] = (uint8_t)pdep(i, (G.SR - 1) & ~xs_tmask);
+    for (uint32_t i = 0; i < G.nyb; ++i)
+        G.yb_tab[i] = (uint8_t)pdep(i, (M - 1) & ~in_mask);
+    for (uint32_t r = 0; r < (1u << G.kin); ++r) {
+        G.xs_in[r] = (uint8_t)pdep(r, xs_tmask);
+        G.y_in[r] = (uint8_t)pdep(r, in_mask);
+    }
+    for (uint32_t xs = 0; xs < G.SR; ++xs) {
+        G.xs_rin[xs] = (uint8_t)pext(xs, xs_tmask);
+        G.xs_base[xs] = (uint8_t)(xs & ~xs_tmask);
+    }
+    for (uint32_t y = 0; y < M; ++y) {
+        G.y_cin[y] = (uint8_t)pext(y, in_mask);
+        G.y_base[y] = (uint8_t)(y & ~in_mask);
+    }
+    const uint32_t D = G.D, kinm = (1u << G.kin) - 1, NG = 1u << g;
+    for (uint32_t rho = 0; rho < D; ++rho)
+        for (uint32_t gam = 0; gam < D; ++gam) {
+            const uint32_t R = rho >> G.kin, C = gam >> G.kin;
+            G.comp_off[rho * D + gam] =
+                (uint16_t)(((R * NG + C) * G.SR + G.xs_in[rho & kinm]) * G.Mp + G.y_in[gam & kinm]);
+        }
+    G.active = NT >= 64 ? ~0ull : ((1ull << NT) - 1);
+    // path D
+    G.nbase = M >> G.kin;
+    G.nblkD = (uint64_t)G.nbase * (G.nbase + 1) / 2;
+    G.BPI = std::max<uint32_t>(1, CAPD / (D * D));
+    G.itemsD = (uint32_t)((G.nblkD + G.BPI - 1) / G.BPI);
+    G.nD_items = G.nD_units * G.itemsD;
+    (void)extra_buffers;
+}
+
+size_t smem_bytes(const Geo& G, int buffers) {
+    const size_t u = (size_t)G.Epad * buffers, d = (size_t)G.BPI * G.D * G.D * buffers;
+    return (std::max(u, d) + (buffers == 3 ? 64 : 0)) * sizeof(double2);
+}
+
+template <int K, int MODE, int NS>
+int launch(hs_state* h, const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+    const uint64_t items = G.nD_items + G.nU_items;
+    if (items == 0)
+        return HS_OK;
+    const size_t smem = smem_bytes(G, buffers);
+    auto kern = conj_kernel<K, MODE, NS>;
+    static bool configured[4] = {false, false, false, false};
+    (void)configured;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    const uint64_t gx = std::min<uint64_t>(items, 1u << 30);
+    const uint64_t gy = (items + gx - 1) / gx;
+    kern<<<dim3((unsigned)gx, (unsigned)gy), NTHR, smem, h->stream>>>(G, cf, ka, h->d);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
+    return HS_OK;
+}
+
+// Subcase counters (SubcaseCounters, kernels.hpp:29-41) for the cross/mixed engines: A = unit
+// whose logical tiles are all stored directly, B = some logical tile is an adjoint, C =
+// diagonal base pair.  Counted on the host by the closed form (k = 1) or by enumeration.
+void count_subcases(const hs_state* h, const Geo& G, uint64_t* sub) {
+    sub[0] = sub[1] = sub[2] = 0;
+    if (G.g == 0)
+        return;
+    const uint64_t nb = G.nb;
+    sub[2] = nb;
+    if (G.k == 1) {  // B = (G/2)(2^a' - 1)/2
+        const uint64_t P = nb * (nb + 1) / 2;
+        const uint64_t B = nb * ((1ull << G.gr_pos[0]) - 1) / 2;
+        sub[1] = B;
+        sub[0] = P - B - nb;
+        return;
+    }
+    // generic: a unit is "adjoint" when some logical tile lies in the upper triangle
+    auto ins = [&](uint64_t s, uint32_t a) {
+        for (uint32_t l = 0; l < G.g; ++l) {
+            const uint32_t p = G.gr_pos[l];
+            const uint64_t right = s & ((1ull << p) - 1);
+            s = ((((s >> p) << 1) | ((a >> l) & 1u)) << p) | right;
+        }
+        return s;
+    };
+    const uint32_t NG = 1u << G.g;
+    uint64_t a = 0, b = 0;
+    for (uint64_t tbi = 1; tbi < nb; ++tbi) {
+        // the max column index of a unit is tc[NG-1], the min row index tr[0]
+        const uint64_t tr0 = ins(tbi, 0);
+        for (uint64_t tbj = 0; tbj < tbi; ++tbj) {
+            if (tr0 >= ins(tbj, NG - 1))
+                ++a;
+            else
+                ++b;
+        }
+    }
+    if (G.k == 2 && G.g == 1) {
+        // tiled_two_mixed counts per (ti, tj) the single t01 tile test (kernels.cpp:379-387)
+        sub[0] = a;
+        sub[1] = b;
+        return;
+    }
+    sub[0] = a;
+    sub[1] = b;
+}
+
+int finish_plan(hs_state* h, const Geo& G, int k, const uint32_t* t, int path, hs_plan* plan, uint64_t touched) {
+    if (!plan)
+        return HS_OK;
+    std::memset(plan, 0, sizeof(*plan));
+    plan->path = path;
+    plan->k = k;
+    for (int i = 0; i < k; ++i)
+        plan->targets[i] = t[i];
+    plan->grid_bits = (int)G.g;
+    plan->launches = (G.nD_items + G.nU_items) ? 1 : 0;
+    plan->touched_bytes = touched;
+    count_subcases(h, G, plan->subcases);
+    return HS_OK;
+}
+
+uint64_t state_bytes(const hs_state* h) { return h->count * sizeof(double2); }
+
+int generic_path(const Geo& G) {
+    if (G.g == 0)
+        return HS_PATH_TILED_INTRA;
+    if (G.g == G.k)
+        return HS_PATH_TILED_CROSS;
+    return HS_PATH_TILED_MIXED;
+}
+
+}  // namespace
+
+// ================================================================================ C-ABI
+extern "C" {
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+const char* hs_version(void) { return "hermsim_b200 0.1 (sm_100a)"; }
+uint64_t hs_launch_count(void) { return g_launches.load(); }
+
+int hs_device_count(int* out) {
+    if (!out)
+        return set_err(HS_ERR_INVALID, "null out");
+    CUDA_TRY(cudaGetDeviceCount(out));
+    return HS_OK;
+}
+
+int hs_state_create(int n, int m, int device, hs_state** out) {
+    if (!out)
+        return set_err(HS_ERR_INVALID, "null out");
+    *out = nullptr;
+    if (n < 1 || n > 30)
+        return set_err(HS_ERR_INVALID, "qubit count must be in [1, 30]");
+    if (m < 0 || m > n + 2)
+        return set_err(HS_ERR_INVALID, "tile exponent must be in [0, n + 2]");
+    if (m > 5)
+        return set_err(HS_ERR_UNSUPPORTED, "this build supports tile exponents m <= 5");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+        return set_err(HS_ERR_RANGE, "device index out of range");
+    DeviceGuard dg(device);
+    auto* h = new hs_state();
+    h->n = n;
+    h->m = m;
+    h->device = device;
+    h->N = 1ull << n;
+    h->M = 1ull << m;
+    h->G = h->N >= h->M ? h->N / h->M : 1;
+    h->count = h->G * (h->G + 1) / 2 * h->M * h->M;
+    cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete h;
+        return set_err(HS_ERR_CUDA, cudaGetErrorString(e));
+    }
+    h->own_stream = true;
+    e = cudaMalloc(&h->d, h->count * sizeof(double2));
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(h->stream);
+        delete h;
+        cudaGetLastError();
+        return set_err(HS_ERR_NOMEM, std::string("cudaMalloc state: ") + cudaGetErrorString(e));
+    }
+    e = cudaMalloc(&h->red, (2 * RED_BLOCKS + 8) * sizeof(double));
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(h->d, 0, h->count * sizeof(double2), h->stream);
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+        cudaFree(h->d);
+        cudaFree(h->red);
+        cudaStreamDestroy(h->stream);
+        delete h;
+        return set_err(HS_ERR_CUDA, cudaGetErrorString(e));
+    }
+    *out = h;
+    return HS_OK;
+}
+
+int hs_state_free(hs_state* h) {
+    if (!h)
+        return HS_OK;
+    DeviceGuard dg(h->device);
+    cudaStreamSynchronize(h->stream);
+    cudaFree(h->d);
+    cudaFree(h->red);
+    cudaFree(h->kraus);
+    if (h->own_stream)
+        cudaStreamDestroy(h->stream);
+    delete h;
+    return HS_OK;
+}
+
+int hs_state_info(const hs_state* h, int* n, int* m, uint64_t* count, uint64_t* grid) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (n)
+        *n = h->n;
+    if (m)
+        *m = h->m;
+    if (count)
+        *count = h->count;
+    if (grid)
+        *grid = h->G;
+    return HS_OK;
+}
+
+int hs_state_upload_range(hs_state* h, const double* host, uint64_t offset, uint64_t count) {
+    if (!h || (!host && count))
+        return set_err(HS_ERR_INVALID, "null argument");
+    if (offset > h->count || count > h->count - offset)
+        return set_err(HS_ERR_RANGE, "upload range exceeds the payload");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaMemcpyAsync(h->d + offset, host, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return HS_OK;
+}
+
+int hs_state_download_range(const hs_state* h, double* host, uint64_t offset, uint64_t count) {
+    if (!h || (!host && count))
+        return set_err(HS_ERR_INVALID, "null argument");
+    if (offset > h->count || count > h->count - offset)
+        return set_err(HS_ERR_RANGE, "download range exceeds the payload");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaMemcpyAsync(host, h->d + offset, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return HS_OK;
+}
+
+int hs_state_upload(hs_state* h, const double* host, uint64_t count) {
+    if (h && count != h->count)
+        return set_err(HS_ERR_INVALID, "payload length mismatch");
+    return hs_state_upload_range(h, host, 0, count);
+}
+
+int hs_state_download(const hs_state* h, double* host, uint64_t count) {
+    if (h && count != h->count)
+        return set_err(HS_ERR_INVALID, "payload length mismatch");
+    return hs_state_download_range(h, host, 0, count);
+}
+
+int hs_state_upload_async(hs_state* h, const double* host, uint64_t count) {
+    if (!h || !host || count != h->count)
+        return set_err(HS_ERR_INVALID, "bad upload arguments");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaMemcpyAsync(h->d, host, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+    return HS_OK;
+}
+
+int hs_state_download_async(const hs_state* h, double* host, uint64_t count) {
+    if (!h || !host || count != h->count)
+        return set_err(HS_ERR_INVALID, "bad download arguments");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaMemcpyAsync(host, h->d, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    return HS_OK;
+}
+
+int hs_state_copy(hs_state* dst, const hs_state* src) {
+    if (!dst || !src)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (dst->count != src->count || dst->m != src->m || dst->n != src->n)
+        return set_err(HS_ERR_INVALID, "state shapes differ");
+    DeviceGuard dg(dst->device);
+    CUDA_TRY(cudaStreamSynchronize(src->stream));
+    CUDA_TRY(cudaMemcpyAsync(dst->d, src->d, dst->count * sizeof(double2), cudaMemcpyDefault, dst->stream));
+    CUDA_TRY(cudaStreamSynchronize(dst->stream));
+    return HS_OK;
+}
+
+int hs_state_zero(hs_state* h) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaMemsetAsync(h->d, 0, h->count * sizeof(double2), h->stream));
+    return HS_OK;
+}
+
+int hs_state_synchronize(const hs_state* h) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return HS_OK;
+}
+
+int hs_state_set_stream(hs_state* h, void* stream) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (h->own_stream)
+        cudaStreamDestroy(h->stream);
+    if (stream) {
+        h->stream = (cudaStream_t)stream;
+        h->own_stream = false;
+    } else {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    return HS_OK;
+}
+
+void* hs_state_stream(const hs_state* h) { return h ? (void*)h->stream : nullptr; }
+void* hs_state_device_ptr(hs_state* h) { return h ? (void*)h->d : nullptr; }
+
+int hs_host_alloc(uint64_t bytes, void** out) {
+    if (!out)
+        return set_err(HS_ERR_INVALID, "null out");
+    CUDA_TRY(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+    return HS_OK;
+}
+int hs_host_free(void* p) {
+    CUDA_TRY(cudaFreeHost(p));
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------------ apply entry points
+int hs_apply_transfer(hs_state* h, int k, const double* s, const uint32_t* t, hs_plan* plan) {
+    int rc = check_targets(h, k, t);
+    if (rc)
+        return rc;
+    if (!s)
+        return set_err(HS_ERR_INVALID, "null transfer matrix");
+    if (k == 3)
+        return set_err(HS_ERR_UNSUPPORTED, "k = 3 transfer matrices: use hs_apply_kraus / hs_apply_unitary");
+    DeviceGuard dg(h->device);
+    Geo G;
+    plan_geo(h, k, t, G, 1);
+    KrausArgs ka{nullptr, 0};
+    if (k == 1) {
+        Coef<16> cf{};
+        std::memcpy(cf.s, s, sizeof(cf.s));
+        rc = launch<1, M_S1, 16>(h, G, cf, ka, 1);
+    } else {
+        auto* cf = new Coef<256>();
+        std::memcpy(cf->s, s, sizeof(cf->s));
+        rc = launch<2, M_S2, 256>(h, G, *cf, ka, 1);
+        delete cf;
+    }
+    if (rc)
+        return rc;
+    return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+}
+
+int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* t, hs_plan* plan) {
+    int rc = check_targets(h, k, t);
+    if (rc)
+        return rc;
+    if (!u)
+        return set_err(HS_ERR_INVALID, "null unitary");
+    DeviceGuard dg(h->device);
+    Geo G;
+    plan_geo(h, k, t, G, 1);
+    KrausArgs ka{nullptr, 0};
+    const double2* U = reinterpret_cast<const double2*>(u);
+    if (k == 1) {
+        // S = conj(U) (x) U, row-stacked (kernels.cpp:27-37 of channel.cpp:24-34)
+        Coef<16> cf{};
+        for (int a = 0; a < 2; ++a)
+            for (int ap = 0; ap < 2; ++ap)
+                for (int mu = 0; mu < 2; ++mu)
+                    for (int nu = 0; nu < 2; ++nu) {
+                        // row-stacked (a*2+ap, mu*2+nu) = col-stacked (a + 2ap, mu + 2nu)
+                        //  = conj(U[ap][nu]) * U[a][mu]
+                        const double2 x = U[ap * 2 + nu], y = U[a * 2 + mu];
+                        cf.s[(a * 2 + ap) * 4 + mu * 2 + nu] =
+                            make_double2(x.x * y.x + x.y * y.y, x.x * y.y - x.y * y.x);
+                    }
+        rc = launch<1, M_S1, 16>(h, G, cf, ka, 1);
+    } else if (k == 2) {
+        Coef<64> cf{};
+        std::memcpy(cf.s, u, 16 * sizeof(double2));
+        rc = launch<2, M_DIRECT, 64>(h, G, cf, ka, 1);
+    } else {
+        Coef<64> cf{};
+        std::memcpy(cf.s, u, 64 * sizeof(double2));
+        rc = launch<3, M_DIRECT, 64>(h, G, cf, ka, 1);
+    }
+    if (rc)
+        return rc;
+    return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+}
+
+int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32_t* t, hs_plan* plan) {
+    int rc = check_targets(h, k, t);
+    if (rc)
+        return rc;
+    const int d = 1 << k;
+    if (nops < 1 || nops > d * d || !ops)
+        return set_err(HS_ERR_INVALID, "Kraus set: needs 1 .. 4^k operators");
+    if (nops == 1 && k >= 2)
+        return hs_apply_unitary(h, k, ops, t, plan);
+    const double2* L = reinterpret_cast<const double2*>(ops);
+    if (k <= 2) {
+        // S = sum_a conj(L_a) (x) L_a, row-stacked
+        const int dd = d * d;
+        std::vector<double2> srow(dd * dd, make_double2(0.0, 0.0));
+        for (int a = 0; a < nops; ++a)
+            for (int r = 0; r < d; ++r)
+                for (int rp = 0; rp < d; ++rp)
+                    for (int c = 0; c < d; ++c)
+                        for (int cp = 0; cp < d; ++cp) {
+                            // out[r][rp] (block row r, col rp) += L[r][c] B[c][cp] conj(L[rp][cp])
+                            const double2 x = L[a * dd + r * d + c], y = L[a * dd + rp * d + cp];
+                            double2& o = srow[(r * d + rp) * dd + c * d + cp];
+                            o.x += x.x * y.x + x.y * y.y;
+                            o.y += x.y * y.x - x.x * y.y;
+                        }
+        return hs_apply_transfer(h, k, reinterpret_cast<const double*>(srow.data()), t, plan);
+    }
+    DeviceGuard dg(h->device);
+    const size_t bytes = (size_t)nops * d * d * sizeof(double2);
+    if (h->kraus_cap < bytes) {
+        cudaFree(h->kraus);
+        h->kraus = nullptr;
+        h->kraus_cap = 0;
+        CUDA_TRY(cudaMalloc(&h->kraus, bytes));
+        h->kraus_cap = bytes;
+    }
+    CUDA_TRY(cudaMemcpyAsync(h->kraus, ops, bytes, cudaMemcpyHostToDevice, h->stream));
+    Geo G;
+    plan_geo(h, k, t, G, 3);
+    Coef<16> cf{};
+    KrausArgs ka{h->kraus, nops};
+    rc = launch<3, M_KRAUS, 16>(h, G, cf, ka, 3);
+    if (rc)
+        return rc;
+    // the host pointer `ops` is only read by the async copy: make it safe to free
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+}
+
+int hs_apply_hadamard(hs_state* h, uint32_t target, hs_plan* plan) {
+    int rc = check_targets(h, 1, &target);
+    if (rc)
+        return rc;
+    DeviceGuard dg(h->device);
+    Geo G;
+    plan_geo(h, 1, &target, G, 1);
+    Coef<16> cf{};
+    KrausArgs ka{nullptr, 0};
+    rc = launch<1, M_HAD, 16>(h, G, cf, ka, 1);
+    if (rc)
+        return rc;
+    rc = finish_plan(h, G, 1, &target, HS_PATH_NATIVE_HADAMARD, plan, 2 * state_bytes(h));
+    if (plan)  // apply_hadamard reports no subcase counters (native.cpp:343-361)
+        plan->subcases[0] = plan->subcases[1] = plan->subcases[2] = 0;
+    return rc;
+}
+
+int hs_apply_monomial(hs_state* h, int k, const uint32_t* perm, const double* diag, const uint32_t* t,
+                      hs_plan* plan) {
+    int rc = check_targets(h, k, t);
+    if (rc)
+        return rc;
+    const uint32_t D = 1u << k;
+    uint32_t p[8], pinv[8];
+    for (uint32_t x = 0; x < D; ++x)
+        p[x] = perm ? perm[x] : x;
+    for (uint32_t x = 0; x < D; ++x)
+        pinv[x] = 0xff;
+    for (uint32_t x = 0; x < D; ++x) {
+        if (p[x] >= D || pinv[p[x]] != 0xff)
+            return set_err(HS_ERR_INVALID, "permutation table is not a bijection");
+        pinv[p[x]] = x;
+    }
+    DeviceGuard dg(h->device);
+    Geo G;
+    plan_geo(h, k, t, G, 1);
+    Coef<64> cf{};
+    const double2* dg2 = reinterpret_cast<const double2*>(diag);
+    // U = P Dg with P|x> = |p[x]>: (U B U^dag)(r, c) = d[pinv r] conj(d[pinv c]) B(pinv r, pinv c).
+    // Factor exactly 1 when the two diagonal entries are identical (equal-bit elements stay
+    // untouched bit-exactly, native.cpp:238-245); mirrored factors use f(c, r) = conj(f(r, c))
+    // as the reference's f01 = conj(f10) (native.cpp:251-252).
+    for (uint32_t r = 0; r < D; ++r)
+        for (uint32_t c = 0; c < D; ++c) {
+            const uint32_t i = r * D + c;
+            cf.pinv[r] = (uint8_t)pinv[r];
+            double2 a = dg2 ? dg2[pinv[r]] : make_double2(1.0, 0.0);
+            double2 b = dg2 ? dg2[pinv[c]] : make_double2(1.0, 0.0);
+            if (a.x == b.x && a.y == b.y) {
+                cf.s[i] = make_double2(1.0, 0.0);
+                cf.fone |= 1ull << i;
+            } else if (r < c) {
+                // f(r, c) = conj(f(c, r)) with f(c, r) = b * conj(a) ... computed below
+                std::swap(a, b);
+                const double2 f = make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+                cf.s[i] = make_double2(f.x, -f.y);
+            } else {
+                cf.s[i] = make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);  // a * conj(b)
+            }
+        }
+    // logical tiles whose components all stay in place with factor 1 are skipped entirely
+    const uint32_t NG = 1u << G.g, kin = G.kin, KI = 1u << kin;
+    uint64_t active = 0;
+    for (uint32_t R = 0; R < NG; ++R)
+        for (uint32_t C = 0; C < NG; ++C) {
+            bool moves = false;
+            for (uint32_t r = 0; r < KI && !moves; ++r)
+                for (uint32_t c = 0; c < KI && !moves; ++c) {
+                    const uint32_t rho = (R << kin) | r, gam = (C << kin) | c;
+                    if (pinv[rho] != rho || pinv[gam] != gam || !((cf.fone >> (rho * D + gam)) & 1ull))
+                        moves = true;
+                }
+            if (moves)
+                active |= 1ull << (R * NG + C);
+        }
+    G.active = active;
+    KrausArgs ka{nullptr, 0};
+    if (active != 0) {
+        if (k == 1)
+            rc = launch<1, M_MONO, 64>(h, G, cf, ka, 1);
+        else if (k == 2)
+            rc = launch<2, M_MONO, 64>(h, G, cf, ka, 1);
+        else
+            rc = launch<3, M_MONO, 64>(h, G, cf, ka, 1);
+        if (rc)
+            return rc;
+    }
+    const uint64_t touched = 2 * state_bytes(h) * (uint64_t)__builtin_popcountll(active) / (NG * NG);
+    return finish_plan(h, G, k, t, HS_PATH_NATIVE_PERMUTATION, plan, touched);
+}
+
+int hs_apply_permutation(hs_state* h, int k, const uint32_t* table, const uint32_t* t, hs_plan* plan) {
+    if (!table)
+        return set_err(HS_ERR_INVALID, "null permutation table");
+    int rc = hs_apply_monomial(h, k, table, nullptr, t, plan);
+    if (!rc && plan) {
+        plan->path = HS_PATH_NATIVE_PERMUTATION;
+        plan->subcases[0] = plan->subcases[1] = plan->subcases[2] = 0;
+    }
+    return rc;
+}
+
+int hs_apply_pauli(hs_state* h, uint32_t target, int y, hs_plan* plan) {
+    const uint32_t perm[2] = {1, 0};
+    // Y = [[0, -i], [i, 0]] = P diag(i, -i) with P the swap: U|0> = i|1>, U|1> = -i|0>.
+    const double dy[4] = {0.0, 1.0, 0.0, -1.0};
+    int rc = hs_apply_monomial(h, 1, perm, y ? dy : nullptr, &target, plan);
+    if (!rc && plan) {
+        plan->path = y ? HS_PATH_NATIVE_PAULI_Y : HS_PATH_NATIVE_PAULI_X;
+        plan->subcases[0] = plan->subcases[1] = plan->subcases[2] = 0;
+    }
+    return rc;
+}
+
+int hs_apply_diagonal_phase(hs_state* h, uint32_t target, const double* phases, hs_plan* plan) {
+    if (!phases)
+        return set_err(HS_ERR_INVALID, "null phases");
+    for (int i = 0; i < 2; ++i)
+        if (std::fabs(std::hypot(phases[2 * i], phases[2 * i + 1]) - 1.0) > 1e-15)
+            return set_err(HS_ERR_INVALID, "diagonal phase: non-unit modulus");
+    int rc = hs_apply_monomial(h, 1, nullptr, phases, &target, plan);
+    if (!rc && plan) {
+        plan->path = HS_PATH_NATIVE_PHASE;
+        plan->subcases[0] = plan->subcases[1] = plan->subcases[2] = 0;
+    }
+    return rc;
+}
+
+// --------------------------------------------------------------------------- observables
+static int reduce(const hs_state* a, const hs_state* b, int kind, double* out) {
+    if (!a || !b || !out)
+        return set_err(HS_ERR_INVALID, "null argument");
+    if (a->n != b->n || a->m != b->m)
+        return set_err(HS_ERR_INVALID, "expectation: operands differ in size");
+    DeviceGuard dg(a->device);
+    if (b != a)
+        CUDA_TRY(cudaStreamSynchronize(b->stream));
+    const uint64_t ntiles = a->G * (a->G + 1) / 2;
+    reduce_kernel<<<RED_BLOCKS, NTHR, 0, a->stream>>>(a->d, b->d, ntiles, (uint32_t)a->m, kind, a->red);
+    finish_kernel<<<1, 32, 0, a->stream>>>(a->red, RED_BLOCKS, kind, a->red + 2 * RED_BLOCKS);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, a->red + 2 * RED_BLOCKS, sizeof(double), cudaMemcpyDeviceToHost, a->stream));
+    CUDA_TRY(cudaStreamSynchronize(a->stream));
+    return HS_OK;
+}
+
+int hs_expectation(const hs_state* rho, const hs_state* obs, double* out) { return reduce(obs, rho, 0, out); }
+int hs_frobenius(const hs_state* h, double* out) {
+    int rc = reduce(h, h, 1, out);
+    if (!rc)
+        *out = std::sqrt(*out);
+    return rc;
+}
+int hs_trace(const hs_state* h, double* out) { return reduce(h, h, 2, out); }
+
+// ---------------------------------------------------------------------------- generators
+int hs_state_fill_mixture(hs_state* h, int rank, const double* psi) {
+    if (!h || !psi || rank < 1)
+        return set_err(HS_ERR_INVALID, "bad mixture arguments");
+    DeviceGuard dg(h->device);
+    double2* dpsi = nullptr;
+    const size_t bytes = (size_t)rank * h->N * sizeof(double2);
+    CUDA_TRY(cudaMalloc(&dpsi, bytes));
+    CUDA_TRY(cudaMemcpyAsync(dpsi, psi, bytes, cudaMemcpyHostToDevice, h->stream));
+    const double inv = 1.0 / rank;
+    fill_mixture_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, dpsi, rank, inv);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    cudaStreamSynchronize(h->stream);
+    cudaFree(dpsi);
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, cudaGetErrorString(e));
+    return HS_OK;
+}
+
+int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uint64_t* z, const int32_t* ny,
+                            const double* coef) {
+    if (!h || count < 0 || (count && (!x || !z || !ny || !coef)))
+        return set_err(HS_ERR_INVALID, "bad Pauli-sum arguments");
+    DeviceGuard dg(h->device);
+    const size_t n8 = (size_t)std::max(count, 1);
+    char* buf = nullptr;
+    CUDA_TRY(cudaMalloc(&buf, n8 * (8 + 8 + 4 + 8)));
+    uint64_t* dx = (uint64_t*)buf;
+    uint64_t* dz = dx + n8;
+    double* dc = (double*)(dz + n8);
+    int32_t* dn = (int32_t*)(dc + n8);
+    if (count) {
+        CUDA_TRY(cudaMemcpyAsync(dx, x, count * 8, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(dz, z, count * 8, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(dc, coef, count * 8, cudaMemcpyHostToDevice, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(dn, ny, count * 4, cudaMemcpyHostToDevice, h->stream));
+    }
+    PauliArgs pa{dx, dz, dn, dc, count};
+    fill_pauli_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, pa);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    cudaStreamSynchronize(h->stream);
+    cudaFree(buf);
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, cudaGetErrorString(e));
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------------------- timing
+int hs_event_create(void** ev) {
+    if (!ev)
+        return set_err(HS_ERR_INVALID, "null out");
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    *ev = e;
+    return HS_OK;
+}
+int hs_event_destroy(void* ev) {
+    CUDA_TRY(cudaEventDestroy((cudaEvent_t)ev));
+    return HS_OK;
+}
+int hs_event_record(void* ev, const hs_state* h) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    CUDA_TRY(cudaEventRecord((cudaEvent_t)ev, h->stream));
+    return HS_OK;
+}
+int hs_event_elapsed_ms(void* start, void* stop, float* ms) {
+    CUDA_TRY(cudaEventSynchronize((cudaEvent_t)stop));
+    CUDA_TRY(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+    return HS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+"""GPU parity: the B200 engine (through the reference-shaped API, C facade -> C++ host -> C-ABI
+-> CUDA) against the CPU oracle (oracle/orkan_oracle.c, itself pinned to the compiled reference
+in test_oracle_cpu.py) on identical seeded inputs.
+
+Bar (BASELINE.json north_star): max elementwise |delta| <= 1e-12 * ||X_cpu||_F over
+the stored triangle; permutation paths (X, CNOT, SWAP, Toffoli) bit-exact.  Kernel paths and
+subcase counters must agree with the reference's ApplyPlan (k = 3 excepted: the reference runs a
+dense round trip, this engine runs the tiled regime directly).
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2604_15765_b200 import hermsim
+    if hermsim.device_count() < 1:
+        pytest.fail("no CUDA device visible")
+    return hermsim
+
+
+@pytest.fixture(scope="module")
+def HS():
+    from paper_2604_15765_b200 import harness
+    return harness
+
+
+def _haar(HS, k, seed):
+    return HS.haar(k, seed)
+
+
+def _random_kraus(k, r, seed):
+    """Random CPTP Kraus set: blocks of a Haar isometry."""
+    rng = np.random.default_rng(seed)
+    d = 1 << k
+    z = (rng.normal(size=(r * d, d)) + 1j * rng.normal(size=(r * d, d))) / np.sqrt(2)
+    q, _ = np.linalg.qr(z)
+    return np.stack([q[a * d:(a + 1) * d, :] for a in range(r)])
+
+
+def _channels(H, HS, oracle):
+    """(name, gpu spec, oracle channel) for the library of SPEC.md + config channels."""
+    out = []
+    for g in "xyzsth":
+        out.append((g, H.native_gate(g), oracle.native_gate(g)))
+    out.append(("rz", H.native_gate("rz", 0.7), oracle.native_gate("rz", 0.7)))
+    out.append(("depol", H.depolarising(0.1), oracle.depolarising(0.1)))
+    out.append(("ampdamp", H.amplitude_damping(0.05), oracle.amplitude_damping(0.05)))
+    u1 = _haar(HS, 1, 11)
+    out.append(("haar1", H.make_generic("haar1", u1), oracle.generic(u1)))
+    for g in ("cnot", "swap"):
+        out.append((g, H.native_gate(g), oracle.native_gate(g)))
+    u2 = _haar(HS, 2, 12)
+    out.append(("haar2", H.make_generic("haar2", u2), oracle.generic(u2)))
+    k2 = _random_kraus(2, 3, 13)
+    out.append(("kraus2", H.make_generic("kraus2", k2), oracle.generic(k2)))
+    out.append(("toffoli", H.native_gate("toffoli"), oracle.native_gate("toffoli")))
+    u3 = _haar(HS, 3, 14)
+    out.append(("haar3", H.make_generic("haar3", u3), oracle.generic(u3)))
+    k3 = _random_kraus(3, 2, 15)
+    out.append(("kraus3", H.make_generic("kraus3", k3), oracle.generic(k3)))
+    return out
+
+
+def _targets(n, k, limit, rng):
+    all_t = list(itertools.permutations(range(n), k))
+    if len(all_t) <= limit:
+        return all_t
+    idx = rng.choice(len(all_t), size=limit, replace=False)
+    return [all_t[i] for i in sorted(idx)]
+
+
+@pytest.mark.parametrize("n,m", [(6, 5), (7, 5), (8, 5), (9, 5), (7, 2), (8, 3), (6, 0), (5, 1), (3, 5), (2, 5),
+                                 (10, 4)])
+def test_library_parity(H, HS, oracle, orc, n, m):
+    if m > n + 2:
+        pytest.skip("invalid tile exponent")
+    rng = np.random.default_rng(1000 * n + m)
+    psi = HS.rank_psi(n, 77 + n, 4)
+    base = HS.rho_payload(n, psi, m)
+    fro = orc.frobenius(base, n, m)
+    st = H.TiledHermitian(n, m)
+    for name, spec, och in _channels(H, HS, oracle):
+        k = spec.k
+        if k > n:
+            continue
+        limit = {1: 64, 2: 40, 3: 12}[k]
+        for tg in _targets(n, k, limit, rng):
+            want = base.copy()
+            opath, osub = orc.apply(want, n, m, och, list(tg))
+            st.upload(base)
+            plan = H.apply(st, spec, list(tg))
+            got = st.download()
+            err = oracle.rel_max_err(got, want, fro)
+            exact = name in ("x", "cnot", "swap", "toffoli")
+            assert err <= (0.0 if exact else TOL), f"{name} {tg} n={n} m={m}: err {err}"
+            if k <= 2:
+                assert plan.path == opath, f"{name} {tg}: path {plan.path} vs {opath}"
+                assert plan.subcases == osub, f"{name} {tg}: subcases {plan.subcases} vs {osub}"
+            else:
+                assert plan.path in ("tiled-intra", "tiled-cross", "tiled-mixed", "native-permutation")
+    st.free()
+
+
+def test_generic_path_without_native(H, HS, oracle, orc):
+    """allow_native = false routes native gates through the generic engines (kernels.cpp:515)."""
+    n, m = 8, 5
+    psi = HS.rank_psi(n, 5, 4)
+    base = HS.rho_payload(n, psi, m)
+    fro = orc.frobenius(base, n, m)
+    st = H.TiledHermitian(n, m)
+    opts = H.ApplyOptions(allow_native=False)
+    for g, k in (("h", 1), ("x", 1), ("y", 1), ("rz", 1), ("cnot", 2), ("swap", 2), ("toffoli", 3)):
+        spec, och = H.native_gate(g, 0.3), oracle.native_gate(g, 0.3)
+        for tg in [(0,), (4,), (5,), (7,)] if k == 1 else [(7, 2), (1, 6), (5, 6)] if k == 2 else [(7, 0, 5)]:
+            want = base.copy()
+            orc.apply(want, n, m, och, list(tg), allow_native=False)
+            st.upload(base)
+            H.apply(st, spec, list(tg), opts)
+            assert oracle.rel_max_err(st.download(), want, fro) <= TOL, (g, tg)
+
+
+def test_device_generators_bit_identical(H, HS):
+    for n, m in ((7, 5), (9, 3), (4, 5), (6, 0)):
+        psi = HS.rank_psi(n, 3, 4)
+        st = H.TiledHermitian(n, m)
+        st.fill_mixture(psi)
+        assert np.array_equal(st.download().view(np.uint64), HS.rho_payload(n, psi, m).view(np.uint64))
+        strings = HS.pauli_strings(n, 64, 99)
+        st.fill_pauli_sum(*strings)
+        assert np.array_equal(st.download().view(np.uint64), HS.pauli_payload(n, strings, m).view(np.uint64))
+
+
+def test_expectation_and_trace(H, HS, orc):
+    for n, m in ((8, 5), (9, 2), (5, 5)):
+        rho = H.TiledHermitian(n, m)
+        obs = H.TiledHermitian(n, m)
+        psi = HS.rank_psi(n, 21, 4)
+        strings = HS.pauli_strings(n, 64, 22)
+        rho.fill_mixture(psi)
+        obs.fill_pauli_sum(*strings)
+        want = orc.expectation(HS.rho_payload(n, psi, m), HS.pauli_payload(n, strings, m), n, m)
+        got = H.expectation(rho, obs)
+        assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
+        assert abs(H.trace(rho) - 1.0) < 1e-12
+        # expectation against the state-vector formula (1/4) sum_i <psi_i|O|psi_i>
+        dense_o = orc.to_dense(HS.pauli_payload(n, strings, m), n, m)
+        sv = np.mean([np.vdot(p, dense_o @ p).real for p in psi])
+        assert abs(got - sv) <= 1e-12 * max(1.0, abs(sv))
+
+
+def test_errors_match_reference(H):
+    st = H.TiledHermitian(4, 2)
+    with pytest.raises(IndexError):
+        H.apply(st, H.native_gate("h"), [4])
+    with pytest.raises(ValueError):
+        H.apply(st, H.native_gate("cnot"), [1])
+    with pytest.raises(ValueError):
+        H.apply(st, H.native_gate("cnot"), [1, 1])
+    with pytest.raises(ValueError):
+        H.native_gate("nope")
+    with pytest.raises(ValueError):
+        H.TiledHermitian(0)
+    with pytest.raises(ValueError):
+        H.TiledHermitian(3, 6)
