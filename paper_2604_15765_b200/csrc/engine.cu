@@ -45,6 +45,7 @@ namespace {
 constexpr int NTHR = 256;          // threads per CTA
 constexpr uint32_t CAP = 2048;     // target complex elements staged per CTA item (32 KiB)
 constexpr uint32_t CAPD = 2048;    // same for diagonal-unit items
+constexpr uint32_t CAP_WHOLE = 4096;  // units up to 64 KiB are staged as whole stored tiles
 constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in smem)
 constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_MASK = (1ull << 56) - 1;
 
@@ -93,6 +94,21 @@ struct Geo {
     uint64_t nD_units, nD_items;
     uint32_t nbase, BPI, itemsD;
     uint64_t nblkD;
+    // pipelined path U (pipe_kernel)
+    uint32_t TS;          // shared elements reserved per logical tile slab (SR * M + max(SR, M))
+    uint32_t SRp;         // pitch of an adjoint tile kept in stored orientation (SR + 1)
+    uint32_t nruns;       // maximal runs of consecutive in-tile rows inside a slab
+    uint8_t run_xs[32], run_len[32];
+    uint32_t stages;      // shared-memory ring depth
+    uint32_t stage_elems; // elements per stage buffer
+    uint16_t cdir[64], cadj[64];  // component offsets from the unit base (direct / adjoint orientation)
+    uint8_t ttr[64];              // logical tile (R * NG + C) of each component
+    uint32_t diag_map;            // transform walks 8x8 position blocks diagonally
+};
+
+// Per-CTA copies of the small index tables of Geo (shared memory).
+struct Tabs {
+    uint8_t xdep[32], xb[32], yb[32], xs_rin[32], xs_base[32], y_cin[32], y_base[32], xs_in[8], y_in[8];
 };
 
 template <int NS>
@@ -100,6 +116,11 @@ struct Coef {
     double2 s[NS];
     uint8_t pinv[8];
     uint64_t fone;   // monomial: bit (rho*D+gamma) set when the factor is exactly 1
+    // monomial, in place: non-trivial cycles of the component map c -> src(c); out[cyc[j]] =
+    // f[cyc[j]] * in[cyc[j+1]] within each cycle [cyc_off[i], cyc_off[i+1])
+    uint8_t cyc[64];
+    uint8_t cyc_off[66];
+    uint32_t ncyc;
 };
 
 uint32_t pdep(uint32_t v, uint32_t mask) {
@@ -403,8 +424,8 @@ __device__ __forceinline__ void compute_blocks(double2* sm, double2* sm2, double
 
 // ---------------------------------------------------------------------------- path U
 template <int K, int MODE, int NS>
-__device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, double2* __restrict__ st,
-                       uint64_t item, double2* sm, uint64_t* ttab, uint16_t* off) {
+__device__ void path_u(const Geo& G, const Tabs& T, const Coef<NS>& cf, const KrausArgs& ka,
+                       double2* __restrict__ st, uint64_t item, double2* sm, uint64_t* ttab, uint16_t* off) {
     const int tid = threadIdx.x;
     constexpr int D = 1 << K;
     const uint64_t ug = item >> G.logSlabs;
@@ -415,7 +436,7 @@ __device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
     const uint32_t NGm = (1u << G.logNG) - 1;
 
     for (uint32_t i = tid; i < ntt; i += NTHR) {
-        const uint32_t uu = i >> G.logNT, T = i & ((1u << G.logNT) - 1);
+        const uint32_t uu = i >> G.logNT, lt = i & ((1u << G.logNT) - 1);
         const uint64_t u = u0 + uu;
         uint64_t ent;
         if (u >= G.nU_units) {
@@ -425,11 +446,11 @@ __device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
         } else {
             uint64_t tbi, tbj;
             tri_strict(u, tbi, tbj);
-            const uint32_t R = T >> G.logNG, C = T & NGm;
+            const uint32_t R = lt >> G.logNG, C = lt & NGm;
             const uint64_t tr = ins_bits(tbi, R, G.gr_pos, G.g), tc = ins_bits(tbj, C, G.gr_pos, G.g);
             ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
         }
-        if (MODE == M_MONO && !((G.active >> T) & 1ull))
+        if (MODE == M_MONO && !((G.active >> lt) & 1ull))
             ent |= F_SKIP;
         ttab[i] = ent;
     }
@@ -459,11 +480,11 @@ __device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
                     if (!(ent & F_ADJ)) {
                         xs = l >> G.logM;
                         y = l & Mm;
-                        src = tb + ((uint64_t)(x0 | G.xdep[xs]) << G.logM) + y;
+                        src = tb + ((uint64_t)(x0 | T.xdep[xs]) << G.logM) + y;
                     } else {
                         y = l >> G.logSR;
                         xs = l & SRm;
-                        src = tb + ((uint64_t)y << G.logM) + (x0 | G.xdep[xs]);
+                        src = tb + ((uint64_t)y << G.logM) + (x0 | T.xdep[xs]);
                     }
                     v[j] = ldg2(st + src);
                     if (ent & F_ADJ)
@@ -481,7 +502,7 @@ __device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
 
     // ---- transform
     if constexpr (MODE != M_MONO) {
-        UAddr A{&G, G.xb_tab, G.yb_tab};
+        UAddr A{&G, T.xb, T.yb};
         const uint32_t nblk = G.U << (G.logNxb + G.logNyb);
         const uint64_t nU = G.nU_units;
         auto valid = [&](uint32_t b) { return u0 + A.unit(b) < nU; };
@@ -509,22 +530,22 @@ __device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
             if (!adj) {
                 xs = l >> G.logM;
                 y = l & Mm;
-                dstg = tb + ((uint64_t)(x0 | G.xdep[xs]) << G.logM) + y;
+                dstg = tb + ((uint64_t)(x0 | T.xdep[xs]) << G.logM) + y;
             } else {
                 y = l >> G.logSR;
                 xs = l & SRm;
-                dstg = tb + ((uint64_t)y << G.logM) + (x0 | G.xdep[xs]);
+                dstg = tb + ((uint64_t)y << G.logM) + (x0 | T.xdep[xs]);
             }
             double2 w;
             if constexpr (MODE == M_MONO) {
-                const uint32_t uu = tt >> G.logNT, T = tt & ((1u << G.logNT) - 1);
-                const uint32_t R = T >> G.logNG, C = T & NGm;
-                const uint32_t rho = (R << G.kin) | G.xs_rin[xs], gam = (C << G.kin) | G.y_cin[y];
+                const uint32_t uu = tt >> G.logNT, lt = tt & ((1u << G.logNT) - 1);
+                const uint32_t R = lt >> G.logNG, C = lt & NGm;
+                const uint32_t rho = (R << G.kin) | T.xs_rin[xs], gam = (C << G.kin) | T.y_cin[y];
                 const uint32_t rs = cf.pinv[rho], gs = cf.pinv[gam];
                 const uint32_t kinm = (1u << G.kin) - 1;
                 const uint32_t src = (((uu << G.logNT) + ((rs >> G.kin) << G.logNG) + (gs >> G.kin)) * G.SR +
-                                      (G.xs_base[xs] | G.xs_in[rs & kinm])) * Mp +
-                                     (G.y_base[y] | G.y_in[gs & kinm]);
+                                      (T.xs_base[xs] | T.xs_in[rs & kinm])) * Mp +
+                                     (T.y_base[y] | T.y_in[gs & kinm]);
                 w = sm[src];
                 const uint32_t fi = rho * D + gam;
                 if (!((cf.fone >> fi) & 1ull))
@@ -541,8 +562,9 @@ __device__ void path_u(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
 
 // ---------------------------------------------------------------------------- path D
 template <int K, int MODE, int NS>
-__device__ void path_d(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, double2* __restrict__ st,
-                       uint64_t item, double2* sm, uint64_t* tabs, uint32_t* bpos, uint16_t* off) {
+__device__ void path_d(const Geo& G, const Tabs& T, const Coef<NS>& cf, const KrausArgs& ka,
+                       double2* __restrict__ st, uint64_t item, double2* sm, uint64_t* tabs, uint32_t* bpos,
+                       uint16_t* off) {
     constexpr int D = 1 << K, DD = D * D;
     const int tid = threadIdx.x;
     const uint64_t tb = item / G.itemsD;
@@ -583,9 +605,9 @@ __device__ void path_d(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
             rho = cf.pinv[rho];
             gam = cf.pinv[gam];
         }
-        const uint32_t xb = G.yb_tab[bp >> 16], yb = G.yb_tab[bp & 0xffffu];
+        const uint32_t xb = T.yb[bp >> 16], yb = T.yb[bp & 0xffffu];
         const uint32_t R = rho >> G.kin, C = gam >> G.kin;
-        const uint32_t x = xb | G.y_in[rho & kinm], y = yb | G.y_in[gam & kinm];
+        const uint32_t x = xb | T.y_in[rho & kinm], y = yb | T.y_in[gam & kinm];
         double2 v;
         if (R >= C) {
             v = st[((tri(trow[R]) + trow[C]) << (2 * logM)) + ((uint64_t)x << logM) + y];
@@ -614,9 +636,9 @@ __device__ void path_d(const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, do
         const uint32_t rho = comp / D, gam = comp % D;
         if (xbi == ybi && rho < gam)
             continue;
-        const uint32_t xb = G.yb_tab[xbi], yb = G.yb_tab[ybi];
+        const uint32_t xb = T.yb[xbi], yb = T.yb[ybi];
         const uint32_t R = rho >> G.kin, C = gam >> G.kin;
-        const uint32_t x = xb | G.y_in[rho & kinm], y = yb | G.y_in[gam & kinm];
+        const uint32_t x = xb | T.y_in[rho & kinm], y = yb | T.y_in[gam & kinm];
         const double2 w = sm[e];
         if (R > C) {
             st[((tri(trow[R]) + trow[C]) << (2 * logM)) + ((uint64_t)x << logM) + y] = w;
@@ -638,11 +660,447 @@ __global__ void __launch_bounds__(NTHR) conj_kernel(const Geo G, const Coef<NS> 
     __shared__ uint64_t tabs[MAX_TT];
     __shared__ uint32_t bpos[CAPD / 4];
     __shared__ uint16_t off[64];
+    __shared__ Tabs T;
+    // index tables are read with per-thread indices: stage them in shared memory (indexed
+    // kernel-parameter reads would serialise in the constant cache)
+    {
+        const int t = threadIdx.x;
+        if (t < 32) {
+            T.xdep[t] = G.xdep[t];
+            T.xb[t] = G.xb_tab[t];
+            T.yb[t] = G.yb_tab[t];
+            T.xs_rin[t] = G.xs_rin[t];
+            T.xs_base[t] = G.xs_base[t];
+            T.y_cin[t] = G.y_cin[t];
+            T.y_base[t] = G.y_base[t];
+            if (t < 8) {
+                T.xs_in[t] = G.xs_in[t];
+                T.y_in[t] = G.y_in[t];
+            }
+        }
+    }
     const uint64_t item = blockIdx.x + (uint64_t)blockIdx.y * gridDim.x;
     if (item < G.nD_items)
-        path_d<K, MODE, NS>(G, cf, ka, st, item, smem, tabs, bpos, off);
+        path_d<K, MODE, NS>(G, T, cf, ka, st, item, smem, tabs, bpos, off);
     else if (item < G.nD_items + G.nU_items)
-        path_u<K, MODE, NS>(G, cf, ka, st, item - G.nD_items, smem, tabs, off);
+        path_u<K, MODE, NS>(G, T, cf, ka, st, item - G.nD_items, smem, tabs, off);
+}
+
+// ------------------------------------------------------------- pipelined path U (TMA bulk copies)
+// Persistent CTAs (one per SM) stream U-path items through a ring of `stages` shared-memory
+// buffers: warp 0 issues cp.async.bulk loads (global -> shared, completion on an mbarrier with
+// expect_tx) for items i+1 .. i+stages-1 while all warps transform item i in place; warp 0 then
+// issues cp.async.bulk stores (shared -> global, bulk groups) and refills the buffer freed by
+// item i-1 once its store has finished reading shared memory.  Direct logical tiles keep their
+// stored row-major layout (pitch M); adjoint tiles keep their STORED orientation with pitch
+// SR + 1, so the transposed reads of the transform are bank-conflict free; conjugation is
+// applied on read and write.  No per-element index arithmetic is spent on the HBM side.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+constexpr int MAX_STAGES = 4;
+
+// Fills the item's logical-tile table: stored tile index | F_ADJ / F_SKIP / F_BAD.
+template <int MODE>
+__device__ __forceinline__ void item_tiles(const Geo& G, uint64_t item, uint64_t* gt, uint32_t lane) {
+    const uint64_t u0 = (item >> G.logSlabs) << G.logU;
+    const uint32_t ntt = G.U << G.logNT, NGm = (1u << G.logNG) - 1;
+    for (uint32_t i = lane; i < ntt; i += 32) {
+        const uint32_t uu = i >> G.logNT, lt = i & ((1u << G.logNT) - 1);
+        const uint64_t u = u0 + uu;
+        uint64_t ent;
+        if (u >= G.nU_units) {
+            ent = F_BAD;
+        } else if (!G.offdiag) {
+            ent = u;
+        } else {
+            uint64_t tbi, tbj;
+            tri_strict(u, tbi, tbj);
+            const uint64_t tr = ins_bits(tbi, lt >> G.logNG, G.gr_pos, G.g);
+            const uint64_t tc = ins_bits(tbj, lt & NGm, G.gr_pos, G.g);
+            ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
+        }
+        if (MODE == M_MONO && !((G.active >> lt) & 1ull))
+            ent |= F_SKIP;
+        gt[i] = ent;
+    }
+}
+
+// Issues (STORE = false) the bulk loads of an item into stage buffer `sb` or (STORE = true) the
+// bulk stores back; executed by the 32 lanes of warp 0.
+template <bool STORE>
+__device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_t item, const uint64_t* gt,
+                                            double2* sb, double2* __restrict__ st, uint64_t* bar, uint32_t lane) {
+    const uint32_t x0 = G.sdep[item & (G.slabs - 1)];
+    const uint32_t ntt = G.U << G.logNT;
+    const uint32_t sbase = smem_u32(sb);
+    for (uint32_t tt = 0; tt < ntt; ++tt) {
+        const uint64_t ent = gt[tt];
+        if (ent & (F_BAD | F_SKIP))
+            continue;
+        const uint64_t gbase = (ent & F_MASK) << (2 * G.logM);
+        const uint32_t tsm = sbase + tt * G.TS * 16u;
+        if (G.SR == G.M) {  // whole stored tile, either orientation: one bulk copy
+            if (lane == 0) {
+                const uint32_t bytes = (1u << (2 * G.logM)) << 4;
+                if (STORE)
+                    bulk_s2g(st + gbase, tsm, bytes);
+                else
+                    bulk_g2s(tsm, st + gbase, bytes, bar);
+            }
+        } else if (!(ent & F_ADJ)) {
+            for (uint32_t r = lane; r < G.nruns; r += 32) {
+                const uint32_t xs0 = G.run_xs[r], len = G.run_len[r];
+                const uint64_t g = gbase + ((uint64_t)(x0 | T.xdep[xs0]) << G.logM);
+                const uint32_t s = tsm + ((xs0 << G.logM) << 4);
+                const uint32_t bytes = (len << G.logM) << 4;
+                if (STORE)
+                    bulk_s2g(st + g, s, bytes);
+                else
+                    bulk_g2s(s, st + g, bytes, bar);
+            }
+        } else {
+            const uint32_t nch = G.nruns << G.logM;
+            for (uint32_t c = lane; c < nch; c += 32) {
+                const uint32_t y = c / G.nruns, r = c - y * G.nruns;
+                const uint32_t xs0 = G.run_xs[r], len = G.run_len[r];
+                const uint64_t g = gbase + ((uint64_t)y << G.logM) + (x0 | T.xdep[xs0]);
+                const uint32_t s = tsm + ((y * G.SRp + xs0) << 4);
+                if (STORE)
+                    bulk_s2g(st + g, s, len << 4);
+                else
+                    bulk_g2s(s, st + g, len << 4, bar);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t item_bytes(const Geo& G, const uint64_t* gt) {
+    const uint32_t ntt = G.U << G.logNT;
+    uint32_t n = 0;
+    for (uint32_t tt = 0; tt < ntt; ++tt)
+        n += !(gt[tt] & (F_BAD | F_SKIP));
+    return n * ((G.SR << G.logM) << 4);
+}
+
+// Consumer-side addressing.  Component i = rho * D + gamma of a block lives in logical tile
+// ttr[i] of its unit; its shared-memory offset is unit_base + (adjoint ? a0 + cadj[i] : d0 +
+// cdir[i]) with d0 / a0 the block's base offset in direct (pitch M) / adjoint (pitch SR + 1)
+// orientation.  cdir / cadj / ttr are per-operation constants (kernel parameters, uniform
+// indices); the adjoint pattern of a unit is one 64-bit mask.
+constexpr int NCONS = 512;                  // consumer threads (16 warps)
+constexpr int NTHR_PIPE = NCONS + 32;       // + 1 producer warp
+constexpr int MAX_UA = 64;                  // units per item with adjoint masks (g >= 1)
+
+struct CBlk {
+    uint32_t ub, d0, a0;
+    uint64_t am;
+};
+__device__ __forceinline__ CBlk cblk(const Geo& G, const Tabs& T, const uint64_t* am_tab, uint32_t b, uint32_t& uu) {
+    uint32_t xbi, ybi;
+    if (G.diag_map) {
+        // 8 consecutive blocks take 8 distinct rows AND 8 distinct columns (mod 8): lanes of a
+        // quarter-warp then hit 8 different 16-byte bank groups in row-major (direct) and in
+        // transposed (adjoint) orientation alike
+        const uint32_t i = b & 7, d = (b >> 3) & 7;
+        uint32_t r = b >> 6;
+        const uint32_t ybh = r & ((G.nyb >> 3) - 1);
+        r >>= G.logNyb - 3;
+        const uint32_t xbh = r & ((G.nxb >> 3) - 1);
+        uu = r >> (G.logNxb - 3);
+        xbi = (xbh << 3) | i;
+        ybi = (ybh << 3) | ((i + d) & 7);
+    } else {
+        ybi = b & (G.nyb - 1);
+        xbi = (b >> G.logNyb) & (G.nxb - 1);
+        uu = b >> (G.logNyb + G.logNxb);
+    }
+    const uint32_t xs = T.xb[xbi], y = T.yb[ybi];
+    CBlk c;
+    c.ub = (uu << G.logNT) * G.TS;
+    c.d0 = (xs << G.logM) + y;
+    c.a0 = y * G.SRp + xs;
+    c.am = G.g ? am_tab[uu] : 0ull;
+    return c;
+}
+__device__ __forceinline__ uint32_t caddr(const Geo& G, const CBlk& c, uint32_t i, bool& cj) {
+    cj = (c.am >> G.ttr[i]) & 1ull;
+    return c.ub + (cj ? c.a0 + G.cadj[i] : c.d0 + G.cdir[i]);
+}
+__device__ __forceinline__ double2 ldc(const double2* sb, uint32_t a, bool cj) {
+    double2 v = sb[a];
+    if (cj)
+        v.y = -v.y;
+    return v;
+}
+__device__ __forceinline__ void stc(double2* sb, uint32_t a, bool cj, double2 v) {
+    if (cj)
+        v.y = -v.y;
+    sb[a] = v;
+}
+
+template <int K, int MODE, int NS>
+__device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const Coef<NS>& cf, const uint64_t* am,
+                                             uint32_t nvalid_units, double2* sb) {
+    constexpr int D = 1 << K;
+    const int tid = threadIdx.x;
+    const uint32_t nblk = G.U << (G.logNxb + G.logNyb);
+    const uint32_t lo = G.diag_map ? 3u : G.logNyb, lomask = (1u << lo) - 1;
+    if constexpr (MODE == M_S1 || MODE == M_HAD) {
+        const Coef<16>& c16 = *reinterpret_cast<const Coef<16>*>(&cf);
+        for (uint32_t b = tid; b < nblk; b += NCONS) {
+            uint32_t uu;
+            const CBlk c = cblk(G, T, am, b, uu);
+            if (uu >= nvalid_units)
+                continue;
+            bool c0, c1, c2, c3;
+            const uint32_t a0 = caddr(G, c, 0, c0), a1 = caddr(G, c, 1, c1);
+            const uint32_t a2 = caddr(G, c, 2, c2), a3 = caddr(G, c, 3, c3);
+            const double2 v0 = ldc(sb, a0, c0), v1 = ldc(sb, a1, c1), v2 = ldc(sb, a2, c2), v3 = ldc(sb, a3, c3);
+            double2 w0, w1, w2, w3;
+            if (MODE == M_HAD) {  // HadamardQuad (native.cpp:332-339)
+                const double2 a = make_double2(v0.x + v1.x, v0.y + v1.y), bb = make_double2(v0.x - v1.x, v0.y - v1.y);
+                const double2 cc = make_double2(v2.x + v3.x, v2.y + v3.y), d = make_double2(v2.x - v3.x, v2.y - v3.y);
+                w0 = make_double2(0.5 * (a.x + cc.x), 0.5 * (a.y + cc.y));
+                w1 = make_double2(0.5 * (bb.x + d.x), 0.5 * (bb.y + d.y));
+                w2 = make_double2(0.5 * (a.x - cc.x), 0.5 * (a.y - cc.y));
+                w3 = make_double2(0.5 * (bb.x - d.x), 0.5 * (bb.y - d.y));
+            } else {  // TransferQuad (kernels.cpp:66-77)
+                const double2* s = c16.s;
+                w0 = cmul(s[0], v0); w0 = cfma(s[1], v1, w0); w0 = cfma(s[2], v2, w0); w0 = cfma(s[3], v3, w0);
+                w1 = cmul(s[4], v0); w1 = cfma(s[5], v1, w1); w1 = cfma(s[6], v2, w1); w1 = cfma(s[7], v3, w1);
+                w2 = cmul(s[8], v0); w2 = cfma(s[9], v1, w2); w2 = cfma(s[10], v2, w2); w2 = cfma(s[11], v3, w2);
+                w3 = cmul(s[12], v0); w3 = cfma(s[13], v1, w3); w3 = cfma(s[14], v2, w3); w3 = cfma(s[15], v3, w3);
+            }
+            stc(sb, a0, c0, w0);
+            stc(sb, a1, c1, w1);
+            stc(sb, a2, c2, w2);
+            stc(sb, a3, c3, w3);
+        }
+    } else if constexpr (MODE == M_S2) {
+        const Coef<256>& c256 = *reinterpret_cast<const Coef<256>*>(&cf);
+        for (uint32_t b = tid; b < nblk; b += NCONS) {
+            uint32_t uu;
+            const CBlk c = cblk(G, T, am, b, uu);
+            if (uu >= nvalid_units)
+                continue;
+            double2 v[16];
+            uint32_t a[16];
+            uint32_t cjm = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                bool cj;
+                a[i] = caddr(G, c, i, cj);
+                cjm |= (uint32_t)cj << i;
+                v[i] = ldc(sb, a[i], cj);
+            }
+#pragma unroll 2
+            for (int r = 0; r < 16; ++r) {
+                double2 acc = cmul(c256.s[r * 16], v[0]);
+#pragma unroll
+                for (int q = 1; q < 16; ++q)
+                    acc = cfma(c256.s[r * 16 + q], v[q], acc);
+                stc(sb, a[r], (cjm >> r) & 1u, acc);
+            }
+        }
+    } else if constexpr (MODE == M_DIRECT) {
+        const uint32_t items = nblk * D;
+        for (uint32_t w = tid; w < items; w += NCONS) {  // Y = B L^dagger, row by row
+            const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo), rho = (w >> lo) % D;
+            uint32_t uu;
+            const CBlk c = cblk(G, T, am, b, uu);
+            if (uu >= nvalid_units)
+                continue;
+            double2 v[D];
+            uint32_t a[D];
+            uint32_t cjm = 0;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                bool cj;
+                a[q] = caddr(G, c, rho * D + q, cj);
+                cjm |= (uint32_t)cj << q;
+                v[q] = ldc(sb, a[q], cj);
+            }
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int t = 0; t < D; ++t)
+                    acc = cfmaconj(v[t], cf.s[q * D + t], acc);
+                stc(sb, a[q], (cjm >> q) & 1u, acc);
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NCONS) : "memory");  // consumer warps only
+        for (uint32_t w = tid; w < items; w += NCONS) {  // out = L Y, column by column
+            const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo), gam = (w >> lo) % D;
+            uint32_t uu;
+            const CBlk c = cblk(G, T, am, b, uu);
+            if (uu >= nvalid_units)
+                continue;
+            double2 v[D];
+            uint32_t a[D];
+            uint32_t cjm = 0;
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                bool cj;
+                a[r] = caddr(G, c, r * D + gam, cj);
+                cjm |= (uint32_t)cj << r;
+                v[r] = ldc(sb, a[r], cj);
+            }
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int t = 0; t < D; ++t)
+                    acc = cfma(cf.s[r * D + t], v[t], acc);
+                stc(sb, a[r], (cjm >> r) & 1u, acc);
+            }
+        }
+    } else if constexpr (MODE == M_MONO) {
+        // in-place cycles of the component map; untouched components cost nothing
+        const uint32_t nc = cf.ncyc;
+        const uint32_t items = nblk * nc;
+        for (uint32_t w = tid; w < items; w += NCONS) {
+            const uint32_t b = (w & lomask) | (((w >> lo) / nc) << lo), ci = (w >> lo) % nc;
+            uint32_t uu;
+            const CBlk c = cblk(G, T, am, b, uu);
+            if (uu >= nvalid_units)
+                continue;
+            const uint32_t c0 = cf.cyc_off[ci], len = cf.cyc_off[ci + 1] - c0;
+            double2 v[16];
+            uint32_t a[16];
+            uint32_t cjm = 0;
+            for (uint32_t j = 0; j < len; ++j) {
+                bool cj;
+                a[j] = caddr(G, c, cf.cyc[c0 + j], cj);
+                cjm |= (uint32_t)cj << j;
+                v[j] = ldc(sb, a[j], cj);
+            }
+            for (uint32_t j = 0; j < len; ++j) {
+                const uint32_t comp = cf.cyc[c0 + j];
+                double2 x = v[j + 1 == len ? 0 : j + 1];
+                if (!((cf.fone >> comp) & 1ull))
+                    x = cmul(cf.s[comp], x);
+                stc(sb, a[j], (cjm >> j) & 1u, x);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+template <int K, int MODE, int NS>
+__global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
+    extern __shared__ __align__(128) double2 ring[];
+    __shared__ __align__(8) uint64_t full[MAX_STAGES];
+    __shared__ __align__(8) uint64_t done[MAX_STAGES];
+    __shared__ uint64_t gt[MAX_STAGES][MAX_TT];
+    __shared__ uint64_t am[MAX_STAGES][MAX_UA];
+    __shared__ Tabs T;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid < 32) {
+        T.xdep[tid] = G.xdep[tid];
+        T.xb[tid] = G.xb_tab[tid];
+        T.yb[tid] = G.yb_tab[tid];
+        T.xs_rin[tid] = G.xs_rin[tid];
+        T.xs_base[tid] = G.xs_base[tid];
+        T.y_cin[tid] = G.y_cin[tid];
+        T.y_base[tid] = G.y_base[tid];
+        if (tid < 8) {
+            T.xs_in[tid] = G.xs_in[tid];
+            T.y_in[tid] = G.y_in[tid];
+        }
+    }
+    if (tid == 0) {
+        for (uint32_t s = 0; s < G.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], NCONS / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t nItems = G.nU_items;
+    const uint32_t S = G.stages;
+    const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    if (warp == NCONS / 32) {
+        // ---- producer warp: bulk loads into the ring, bulk stores out of it
+        for (uint64_t j = 0; j < nlocal + S; ++j) {
+            const uint32_t s = (uint32_t)(j % S);
+            double2* sb = ring + (size_t)s * G.stage_elems;
+            if (j >= S) {
+                const uint64_t jj = j - S;
+                mbar_wait(&done[s], (uint32_t)((jj / S) & 1));
+                item_copies<true>(G, T, blockIdx.x + jj * gridDim.x, gt[s], sb, st, nullptr, lane);
+                bulk_commit();
+            }
+            if (j < nlocal) {
+                if (j >= S)
+                    bulk_wait_read0();  // the store of item j - S has left stage s
+                const uint64_t item = blockIdx.x + j * gridDim.x;
+                item_tiles<MODE>(G, item, gt[s], lane);
+                __syncwarp();
+                if (G.g)
+                    for (uint32_t uu = lane; uu < G.U && uu < MAX_UA; uu += 32) {
+                        uint64_t mask = 0;
+                        for (uint32_t t = 0; t < (1u << G.logNT); ++t)
+                            mask |= (uint64_t)((gt[s][(uu << G.logNT) + t] & F_ADJ) != 0) << t;
+                        am[s][uu] = mask;
+                    }
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive_expect(&full[s], item_bytes(G, gt[s]));
+                __syncwarp();
+                item_copies<false>(G, T, item, gt[s], sb, st, &full[s], lane);
+            }
+        }
+        bulk_wait_all();
+        return;
+    }
+    // ---- consumer warps: transform each staged item in place
+    for (uint64_t i = 0; i < nlocal; ++i) {
+        const uint32_t s = (uint32_t)(i % S);
+        double2* sb = ring + (size_t)s * G.stage_elems;
+        const uint64_t item = blockIdx.x + i * gridDim.x;
+        const uint64_t u0 = (item >> G.logSlabs) << G.logU;
+        const uint32_t nvalid = G.nU_units - u0 < G.U ? (uint32_t)(G.nU_units - u0) : G.U;
+        mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+        pipe_compute<K, MODE, NS>(G, T, cf, am[s], nvalid, sb);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0)
+            mbar_arrive(&done[s]);
+    }
 }
 
 // ------------------------------------------------------------------------- reductions
@@ -870,10 +1328,10 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
     const uint32_t M = G.M;
     const uint64_t unit_elems = (uint64_t)NT * M * M;
     uint32_t cmask;
-    if (unit_elems <= CAP) {
+    if (unit_elems <= CAP_WHOLE) {  // whole stored tiles per item (one 16 KiB bulk copy each)
         G.SR = M;
         G.slabs = 1;
-        uint32_t U = (uint32_t)(CAP / unit_elems);
+        uint32_t U = (uint32_t)(CAP_WHOLE / unit_elems);
         if ((uint64_t)U * NT > MAX_TT)
             U = std::max<uint32_t>(1, MAX_TT / NT);
         G.U = U;
@@ -939,6 +1397,32 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
     G.BPI = std::max<uint32_t>(1, CAPD / (D * D));
     G.itemsD = (uint32_t)((G.nblkD + G.BPI - 1) / G.BPI);
     G.nD_items = G.nD_units * G.itemsD;
+    // pipelined path U
+    // whole tiles keep their stored orientation unpadded (the diagonal lane mapping of the
+    // transform keeps both orientations bank-conflict free); slabs pad adjoint rows by one
+    G.SRp = G.SR == M ? M : G.SR + 1;
+    G.TS = G.SR * M + (G.SRp == G.SR ? 0 : M);
+    G.diag_map = (G.nxb >= 8 && G.nyb >= 8) ? 1 : 0;
+    G.nruns = 0;
+    for (uint32_t xs = 0; xs < G.SR; ++xs) {
+        if (xs == 0 || G.xdep[xs] != G.xdep[xs - 1] + 1) {
+            G.run_xs[G.nruns] = (uint8_t)xs;
+            G.run_len[G.nruns] = 0;
+            ++G.nruns;
+        }
+        ++G.run_len[G.nruns - 1];
+    }
+    for (uint32_t rho = 0; rho < D; ++rho)
+        for (uint32_t gam = 0; gam < D; ++gam) {
+            const uint32_t R = rho >> G.kin, C = gam >> G.kin, i = rho * D + gam;
+            const uint32_t xs = G.xs_in[rho & kinm], y = G.y_in[gam & kinm];
+            G.ttr[i] = (uint8_t)(R * NG + C);
+            G.cdir[i] = (uint16_t)((R * NG + C) * G.TS + xs * M + y);
+            G.cadj[i] = (uint16_t)((R * NG + C) * G.TS + y * G.SRp + xs);
+        }
+    G.stage_elems = ((G.U << G.logNT) * G.TS + 7) & ~7u;
+    const uint32_t budget = 200u * 1024u / 16u;  // elements of shared memory for the ring
+    G.stages = std::min<uint32_t>(MAX_STAGES, budget / G.stage_elems);
     (void)extra_buffers;
 }
 
@@ -947,25 +1431,58 @@ size_t smem_bytes(const Geo& G, int buffers) {
     return (std::max(u, d) + (buffers == 3 ? 64 : 0)) * sizeof(double2);
 }
 
+int sm_count(int device) {
+    static int cache[64] = {0};
+    if (device < 0 || device >= 64)
+        return 148;
+    if (!cache[device]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0)
+            v = 148;
+        cache[device] = v;
+    }
+    return cache[device];
+}
+
 template <int K, int MODE, int NS>
-int launch(hs_state* h, const Geo& G, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
-    const uint64_t items = G.nD_items + G.nU_items;
-    if (items == 0)
-        return HS_OK;
-    const size_t smem = smem_bytes(G, buffers);
-    auto kern = conj_kernel<K, MODE, NS>;
-    static bool configured[4] = {false, false, false, false};
-    (void)configured;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess)
-        return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    const uint64_t gx = std::min<uint64_t>(items, 1u << 30);
-    const uint64_t gy = (items + gx - 1) / gx;
-    kern<<<dim3((unsigned)gx, (unsigned)gy), NTHR, smem, h->stream>>>(G, cf, ka, h->d);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaGetLastError();
-    if (e != cudaSuccess)
-        return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
+int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+    Geo G = G0;
+    const bool pipe = MODE != M_KRAUS && G.stages >= 3 && G.nU_items > 0;
+    cudaError_t e;
+    // slab kernel: diagonal units (path D) and, when the pipeline does not apply, path U too
+    const uint64_t nU_slab = pipe ? 0 : G.nU_items;
+    const uint64_t items = G.nD_items + nU_slab;
+    if (items) {
+        Geo Gs = G;
+        Gs.nU_items = nU_slab;
+        if (!nU_slab)
+            Gs.Epad = 0;  // diagonal units only: size shared memory for path D alone
+        const size_t smem = smem_bytes(Gs, buffers);
+        auto kern = conj_kernel<K, MODE, NS>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+        const uint64_t gx = std::min<uint64_t>(items, 1u << 30);
+        const uint64_t gy = (items + gx - 1) / gx;
+        kern<<<dim3((unsigned)gx, (unsigned)gy), NTHR, smem, h->stream>>>(Gs, cf, ka, h->d);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
+    }
+    if (pipe) {
+        const size_t smem = (size_t)G.stages * G.stage_elems * sizeof(double2);
+        auto kern = pipe_kernel<K, MODE, NS>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(pipe): ") + cudaGetErrorString(e));
+        const uint64_t grid = std::min<uint64_t>(G.nU_items, (uint64_t)sm_count(h->device));
+        kern<<<(unsigned)grid, NTHR_PIPE, smem, h->stream>>>(G, cf, h->d);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return set_err(HS_ERR_CUDA, std::string("pipe_kernel launch: ") + cudaGetErrorString(e));
+    }
     return HS_OK;
 }
 
@@ -1423,6 +1940,28 @@ int hs_apply_monomial(hs_state* h, int k, const uint32_t* perm, const double* di
                 cf.s[i] = make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);  // a * conj(b)
             }
         }
+    // cycles of the component map c = (r, c') -> src(c) = (pinv r, pinv c') for the in-place
+    // transform; fixed components with factor exactly 1 are left out (never touched)
+    {
+        bool seen[64] = {false};
+        uint32_t pos = 0;
+        cf.ncyc = 0;
+        cf.cyc_off[0] = 0;
+        for (uint32_t c0 = 0; c0 < D * D; ++c0) {
+            if (seen[c0])
+                continue;
+            uint32_t len = 0, c = c0;
+            do {
+                seen[c] = true;
+                cf.cyc[pos + len++] = (uint8_t)c;
+                c = pinv[c / D] * D + pinv[c % D];
+            } while (c != c0);
+            if (len == 1 && ((cf.fone >> c0) & 1ull))
+                continue;  // untouched element
+            pos += len;
+            cf.cyc_off[++cf.ncyc] = (uint8_t)pos;
+        }
+    }
     // logical tiles whose components all stay in place with factor 1 are skipped entirely
     const uint32_t NG = 1u << G.g, kin = G.kin, KI = 1u << kin;
     uint64_t active = 0;
