@@ -47,7 +47,8 @@ constexpr uint32_t CAP = 2048;     // target complex elements staged per CTA ite
 constexpr uint32_t CAPD = 2048;    // same for diagonal-unit items
 constexpr uint32_t CAP_WHOLE = 4096;  // units up to 64 KiB are staged as whole stored tiles
 constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in smem)
-constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_MASK = (1ull << 56) - 1;
+constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_NOSTORE = 1ull << 60,
+                   F_MASK = (1ull << 56) - 1;
 
 enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5 };
 
@@ -104,6 +105,7 @@ struct Geo {
     uint16_t cdir[64], cadj[64];  // component offsets from the unit base (direct / adjoint orientation)
     uint8_t ttr[64];              // logical tile (R * NG + C) of each component
     uint32_t diag_map;            // transform walks 8x8 position blocks diagonally
+    uint32_t pipe_diag;           // pipeline also owns the diagonal units (whole-tile items)
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
@@ -742,10 +744,17 @@ __device__ __forceinline__ void item_tiles(const Geo& G, uint64_t item, uint64_t
             ent = u;
         } else {
             uint64_t tbi, tbj;
-            tri_strict(u, tbi, tbj);
+            if (G.pipe_diag)
+                tri_loose(u, tbi, tbj);  // diagonal units too (tbi == tbj)
+            else
+                tri_strict(u, tbi, tbj);
             const uint64_t tr = ins_bits(tbi, lt >> G.logNG, G.gr_pos, G.g);
             const uint64_t tc = ins_bits(tbj, lt & NGm, G.gr_pos, G.g);
             ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
+            // on a diagonal unit logical (R, C), R < C, aliases stored (C, R): it is staged as a
+            // separate read-only copy (input of the transform) and never written back
+            if (tbi == tbj && (lt >> G.logNG) < (lt & NGm))
+                ent |= F_NOSTORE;
         }
         if (MODE == M_MONO && !((G.active >> lt) & 1ull))
             ent |= F_SKIP;
@@ -761,21 +770,28 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
     const uint32_t x0 = G.sdep[item & (G.slabs - 1)];
     const uint32_t ntt = G.U << G.logNT;
     const uint32_t sbase = smem_u32(sb);
+    if (G.SR == G.M) {  // whole stored tiles, either orientation: one bulk copy each, lane-parallel
+        const uint32_t bytes = (1u << (2 * G.logM)) << 4;
+        for (uint32_t tt = lane; tt < ntt; tt += 32) {
+            const uint64_t ent = gt[tt];
+            if ((ent & (F_BAD | F_SKIP)) || (STORE && (ent & F_NOSTORE)))
+                continue;
+            const uint64_t gbase = (ent & F_MASK) << (2 * G.logM);
+            const uint32_t tsm = sbase + tt * G.TS * 16u;
+            if (STORE)
+                bulk_s2g(st + gbase, tsm, bytes);
+            else
+                bulk_g2s(tsm, st + gbase, bytes, bar);
+        }
+        return;
+    }
     for (uint32_t tt = 0; tt < ntt; ++tt) {
         const uint64_t ent = gt[tt];
-        if (ent & (F_BAD | F_SKIP))
+        if ((ent & (F_BAD | F_SKIP)) || (STORE && (ent & F_NOSTORE)))
             continue;
         const uint64_t gbase = (ent & F_MASK) << (2 * G.logM);
         const uint32_t tsm = sbase + tt * G.TS * 16u;
-        if (G.SR == G.M) {  // whole stored tile, either orientation: one bulk copy
-            if (lane == 0) {
-                const uint32_t bytes = (1u << (2 * G.logM)) << 4;
-                if (STORE)
-                    bulk_s2g(st + gbase, tsm, bytes);
-                else
-                    bulk_g2s(tsm, st + gbase, bytes, bar);
-            }
-        } else if (!(ent & F_ADJ)) {
+        if (!(ent & F_ADJ)) {
             for (uint32_t r = lane; r < G.nruns; r += 32) {
                 const uint32_t xs0 = G.run_xs[r], len = G.run_len[r];
                 const uint64_t g = gbase + ((uint64_t)(x0 | T.xdep[xs0]) << G.logM);
@@ -816,7 +832,7 @@ __device__ __forceinline__ uint32_t item_bytes(const Geo& G, const uint64_t* gt)
 // orientation.  cdir / cadj / ttr are per-operation constants (kernel parameters, uniform
 // indices); the adjoint pattern of a unit is one 64-bit mask.
 constexpr int NCONS = 512;                  // consumer threads (16 warps)
-constexpr int NTHR_PIPE = NCONS + 32;       // + 1 producer warp
+constexpr int NTHR_PIPE = NCONS + 32 * 4;   // + one producer warp per ring stage (<= MAX_STAGES)
 constexpr int MAX_UA = 64;                  // units per item with adjoint masks (g >= 1)
 
 struct CBlk {
@@ -1026,6 +1042,7 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
     __shared__ __align__(8) uint64_t done[MAX_STAGES];
     __shared__ uint64_t gt[MAX_STAGES][MAX_TT];
     __shared__ uint64_t am[MAX_STAGES][MAX_UA];
+    __shared__ uint64_t gnext[MAX_STAGES][MAX_TT];
     __shared__ Tabs T;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid < 32) {
@@ -1053,35 +1070,52 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
     const uint32_t S = G.stages;
     const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
-    if (warp == NCONS / 32) {
-        // ---- producer warp: bulk loads into the ring, bulk stores out of it
-        for (uint64_t j = 0; j < nlocal + S; ++j) {
-            const uint32_t s = (uint32_t)(j % S);
-            double2* sb = ring + (size_t)s * G.stage_elems;
+    if (warp >= NCONS / 32) {
+        // ---- producer warps: warp p owns ring stage p (items j = p, p + S, ...).  A bulk
+        // store can only be awaited by the thread that issued it, so giving every stage its own
+        // producer lets the stages' store-drain / metadata / load-issue latencies overlap.
+        const uint32_t p = warp - NCONS / 32;
+        if (p >= S)
+            return;
+        const uint32_t ntt = G.U << G.logNT;
+        uint64_t* gn = gnext[p];
+        double2* sb = ring + (size_t)p * G.stage_elems;
+        for (uint64_t j = p; j < nlocal + S; j += S) {
+            uint32_t bytes = 0;
+            if (j < nlocal) {  // metadata of item j, prepared before the stage is free
+                item_tiles<MODE>(G, blockIdx.x + j * gridDim.x, gn, lane);
+                __syncwarp();
+                uint32_t cnt = 0;
+                for (uint32_t t = lane; t < ntt; t += 32)
+                    cnt += !(gn[t] & (F_BAD | F_SKIP));
+                for (int o = 16; o; o >>= 1)
+                    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                bytes = cnt * ((G.SR << G.logM) << 4);
+            }
             if (j >= S) {
                 const uint64_t jj = j - S;
-                mbar_wait(&done[s], (uint32_t)((jj / S) & 1));
-                item_copies<true>(G, T, blockIdx.x + jj * gridDim.x, gt[s], sb, st, nullptr, lane);
+                mbar_wait(&done[p], (uint32_t)((jj / S) & 1));
+                item_copies<true>(G, T, blockIdx.x + jj * gridDim.x, gt[p], sb, st, nullptr, lane);
                 bulk_commit();
             }
             if (j < nlocal) {
-                if (j >= S)
-                    bulk_wait_read0();  // the store of item j - S has left stage s
-                const uint64_t item = blockIdx.x + j * gridDim.x;
-                item_tiles<MODE>(G, item, gt[s], lane);
+                for (uint32_t t = lane; t < ntt; t += 32)
+                    gt[p][t] = gn[t];
                 __syncwarp();
                 if (G.g)
                     for (uint32_t uu = lane; uu < G.U && uu < MAX_UA; uu += 32) {
                         uint64_t mask = 0;
                         for (uint32_t t = 0; t < (1u << G.logNT); ++t)
-                            mask |= (uint64_t)((gt[s][(uu << G.logNT) + t] & F_ADJ) != 0) << t;
-                        am[s][uu] = mask;
+                            mask |= (uint64_t)((gn[(uu << G.logNT) + t] & F_ADJ) != 0) << t;
+                        am[p][uu] = mask;
                     }
+                if (j >= S)
+                    bulk_wait_read0();  // the store of item j - S has left the stage
                 __syncwarp();
                 if (lane == 0)
-                    mbar_arrive_expect(&full[s], item_bytes(G, gt[s]));
+                    mbar_arrive_expect(&full[p], bytes);
                 __syncwarp();
-                item_copies<false>(G, T, item, gt[s], sb, st, &full[s], lane);
+                item_copies<false>(G, T, blockIdx.x + j * gridDim.x, gt[p], sb, st, &full[p], lane);
             }
         }
         bulk_wait_all();
@@ -1447,7 +1481,14 @@ int sm_count(int device) {
 template <int K, int MODE, int NS>
 int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
     Geo G = G0;
-    const bool pipe = MODE != M_KRAUS && G.stages >= 3 && G.nU_items > 0;
+    const bool pipe = MODE != M_KRAUS && G.stages >= 3 && (G.nU_items > 0 || G.nD_items > 0);
+    if (pipe && G.g >= 1 && G.slabs == 1) {
+        // whole-unit items: the pipeline handles the diagonal base pairs as well
+        G.pipe_diag = 1;
+        G.nU_units = G.nb * (G.nb + 1) / 2;
+        G.nU_items = (G.nU_units + G.U - 1) / G.U;
+        G.nD_items = 0;
+    }
     cudaError_t e;
     // slab kernel: diagonal units (path D) and, when the pipeline does not apply, path U too
     const uint64_t nU_slab = pipe ? 0 : G.nU_items;
@@ -1470,7 +1511,7 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         if (e != cudaSuccess)
             return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
     }
-    if (pipe) {
+    if (pipe && G.nU_items > 0) {
         const size_t smem = (size_t)G.stages * G.stage_elems * sizeof(double2);
         auto kern = pipe_kernel<K, MODE, NS>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

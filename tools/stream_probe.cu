@@ -106,6 +106,70 @@ __global__ void __launch_bounds__(NCONS + 32, 1) v2(double2* __restrict__ a, uin
     }
 }
 
+// v3: 64 KiB items = 4 x 16 KiB chunks taken from `streams` separate address regions
+template <int NCONS>
+__global__ void __launch_bounds__(NCONS + 32, 1) v3(double2* __restrict__ a, uint64_t n, uint32_t S, uint32_t streams) {
+    extern __shared__ __align__(128) double2 ring[];
+    __shared__ __align__(8) uint64_t full[8], done[8];
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t chunk = 1024, per = 4 * chunk;  // elements
+    if (tid == 0) {
+        for (uint32_t s = 0; s < S; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[s])), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&done[s])), "r"(NCONS / 32));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t nItems = n / per;
+    const uint64_t region = n / streams;            // elements per region
+    const uint32_t cps = 4 / streams;               // chunks per stream per item
+    auto addr = [&](uint64_t item, uint32_t c) -> double2* {
+        const uint32_t r = c / cps, k = c % cps;
+        return a + r * region + item * (uint64_t)cps * chunk + (uint64_t)k * chunk;
+    };
+    const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    if (warp == NCONS / 32) {
+        for (uint64_t j = 0; j < nlocal + S; ++j) {
+            const uint32_t s = j % S;
+            double2* sb = ring + (size_t)s * per;
+            if (j >= S) {
+                const uint64_t jj = j - S;
+                mwait(&done[s], (jj / S) & 1);
+                if (lane < 4)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(addr(blockIdx.x + jj * gridDim.x, lane)),
+                                 "r"(su32(sb) + lane * chunk * 16), "r"(chunk * 16) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            if (j < nlocal) {
+                if (j >= S)
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(per * 16) : "memory");
+                __syncwarp();
+                if (lane < 4)
+                    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(sb) + lane * chunk * 16),
+                                 "l"(addr(blockIdx.x + j * gridDim.x, lane)), "r"(chunk * 16), "r"(su32(&full[s])) : "memory");
+            }
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        return;
+    }
+    for (uint64_t i = 0; i < nlocal; ++i) {
+        const uint32_t s = i % S;
+        double2* sb = ring + (size_t)s * per;
+        mwait(&full[s], (i / S) & 1);
+        for (uint32_t e = tid; e < per; e += NCONS) {
+            double2 v = sb[e];
+            sb[e] = make_double2(0.5 * v.x, 0.5 * v.y);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&done[s])) : "memory");
+    }
+}
+
 int main(int argc, char** argv) {
     const uint64_t bytes = (argc > 1 ? atoll(argv[1]) : 34376515584ull);
     const uint64_t n = bytes / 16;
@@ -154,6 +218,13 @@ int main(int argc, char** argv) {
         snprintf(nm, 80, "v2 TMA ring chunk=%uKB S=%u pieces=%u", c.chunk_kb, c.S, c.pieces);
         CK(cudaFuncSetAttribute(v2<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         report(nm, [&] { v2<256><<<sms, 288, smem>>>(a, n, chunk, c.S, c.pieces); });
+    }
+    for (uint32_t streams : {1u, 2u, 4u}) {
+        const size_t smem = 3 * 4096 * 16;
+        char nm[80];
+        snprintf(nm, 80, "v3 64KB items of 4x16KB from %u stream(s), S=3", streams);
+        CK(cudaFuncSetAttribute(v3<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        report(nm, [&] { v3<512><<<sms, 544, smem>>>(a, n, 3, streams); });
     }
     // two CTAs per SM
     for (auto c : {Cfg{16, 4, 1}, Cfg{32, 3, 1}, Cfg{24, 4, 1}}) {
