@@ -106,11 +106,18 @@ struct Geo {
     uint8_t ttr[64];              // logical tile (R * NG + C) of each component
     uint32_t diag_map;            // transform walks 8x8 position blocks diagonally
     uint32_t pipe_diag;           // pipeline also owns the diagonal units (whole-tile items)
+    uint32_t PD;                  // row pitch of a direct logical tile in shared memory
+    uint32_t logical;             // adjoint tiles staged transposed (logical layout, gather kernel)
+    // gather kernel (square sub-blocks of S0 x S0 positions, g >= 2)
+    uint32_t S0, logS0, nsb_side, log_nsb_side;
+    uint64_t nG_items;
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
 struct Tabs {
     uint8_t xdep[32], xb[32], yb[32], xs_rin[32], xs_base[32], y_cin[32], y_base[32], xs_in[8], y_in[8];
+    uint16_t cdir[64], cadj[64];  // component offsets (copied from Geo: indexed per thread)
+    uint8_t ttr[64];
 };
 
 template <int NS>
@@ -861,14 +868,14 @@ __device__ __forceinline__ CBlk cblk(const Geo& G, const Tabs& T, const uint64_t
     const uint32_t xs = T.xb[xbi], y = T.yb[ybi];
     CBlk c;
     c.ub = (uu << G.logNT) * G.TS;
-    c.d0 = (xs << G.logM) + y;
-    c.a0 = y * G.SRp + xs;
+    c.d0 = xs * G.PD + y;
+    c.a0 = G.logical ? c.d0 : y * G.SRp + xs;
     c.am = G.g ? am_tab[uu] : 0ull;
     return c;
 }
-__device__ __forceinline__ uint32_t caddr(const Geo& G, const CBlk& c, uint32_t i, bool& cj) {
-    cj = (c.am >> G.ttr[i]) & 1ull;
-    return c.ub + (cj ? c.a0 + G.cadj[i] : c.d0 + G.cdir[i]);
+__device__ __forceinline__ uint32_t caddr(const Tabs& T, const CBlk& c, uint32_t i, bool& cj) {
+    cj = (c.am >> T.ttr[i]) & 1ull;
+    return c.ub + (cj ? c.a0 + T.cadj[i] : c.d0 + T.cdir[i]);
 }
 __device__ __forceinline__ double2 ldc(const double2* sb, uint32_t a, bool cj) {
     double2 v = sb[a];
@@ -882,7 +889,7 @@ __device__ __forceinline__ void stc(double2* sb, uint32_t a, bool cj, double2 v)
     sb[a] = v;
 }
 
-template <int K, int MODE, int NS>
+template <int K, int MODE, int NS, int NC = NCONS>
 __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const Coef<NS>& cf, const uint64_t* am,
                                              uint32_t nvalid_units, double2* sb) {
     constexpr int D = 1 << K;
@@ -891,14 +898,14 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
     const uint32_t lo = G.diag_map ? 3u : G.logNyb, lomask = (1u << lo) - 1;
     if constexpr (MODE == M_S1 || MODE == M_HAD) {
         const Coef<16>& c16 = *reinterpret_cast<const Coef<16>*>(&cf);
-        for (uint32_t b = tid; b < nblk; b += NCONS) {
+        for (uint32_t b = tid; b < nblk; b += NC) {
             uint32_t uu;
             const CBlk c = cblk(G, T, am, b, uu);
             if (uu >= nvalid_units)
                 continue;
             bool c0, c1, c2, c3;
-            const uint32_t a0 = caddr(G, c, 0, c0), a1 = caddr(G, c, 1, c1);
-            const uint32_t a2 = caddr(G, c, 2, c2), a3 = caddr(G, c, 3, c3);
+            const uint32_t a0 = caddr(T, c, 0, c0), a1 = caddr(T, c, 1, c1);
+            const uint32_t a2 = caddr(T, c, 2, c2), a3 = caddr(T, c, 3, c3);
             const double2 v0 = ldc(sb, a0, c0), v1 = ldc(sb, a1, c1), v2 = ldc(sb, a2, c2), v3 = ldc(sb, a3, c3);
             double2 w0, w1, w2, w3;
             if (MODE == M_HAD) {  // HadamardQuad (native.cpp:332-339)
@@ -922,7 +929,7 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
         }
     } else if constexpr (MODE == M_S2) {
         const Coef<256>& c256 = *reinterpret_cast<const Coef<256>*>(&cf);
-        for (uint32_t b = tid; b < nblk; b += NCONS) {
+        for (uint32_t b = tid; b < nblk; b += NC) {
             uint32_t uu;
             const CBlk c = cblk(G, T, am, b, uu);
             if (uu >= nvalid_units)
@@ -933,7 +940,7 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 bool cj;
-                a[i] = caddr(G, c, i, cj);
+                a[i] = caddr(T, c, i, cj);
                 cjm |= (uint32_t)cj << i;
                 v[i] = ldc(sb, a[i], cj);
             }
@@ -948,7 +955,7 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
         }
     } else if constexpr (MODE == M_DIRECT) {
         const uint32_t items = nblk * D;
-        for (uint32_t w = tid; w < items; w += NCONS) {  // Y = B L^dagger, row by row
+        for (uint32_t w = tid; w < items; w += NC) {  // Y = B L^dagger, row by row
             const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo), rho = (w >> lo) % D;
             uint32_t uu;
             const CBlk c = cblk(G, T, am, b, uu);
@@ -960,7 +967,7 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
 #pragma unroll
             for (int q = 0; q < D; ++q) {
                 bool cj;
-                a[q] = caddr(G, c, rho * D + q, cj);
+                a[q] = caddr(T, c, rho * D + q, cj);
                 cjm |= (uint32_t)cj << q;
                 v[q] = ldc(sb, a[q], cj);
             }
@@ -973,8 +980,8 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                 stc(sb, a[q], (cjm >> q) & 1u, acc);
             }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(NCONS) : "memory");  // consumer warps only
-        for (uint32_t w = tid; w < items; w += NCONS) {  // out = L Y, column by column
+        asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");  // consumer warps only
+        for (uint32_t w = tid; w < items; w += NC) {  // out = L Y, column by column
             const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo), gam = (w >> lo) % D;
             uint32_t uu;
             const CBlk c = cblk(G, T, am, b, uu);
@@ -986,7 +993,7 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
 #pragma unroll
             for (int r = 0; r < D; ++r) {
                 bool cj;
-                a[r] = caddr(G, c, r * D + gam, cj);
+                a[r] = caddr(T, c, r * D + gam, cj);
                 cjm |= (uint32_t)cj << r;
                 v[r] = ldc(sb, a[r], cj);
             }
@@ -1003,19 +1010,35 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
         // in-place cycles of the component map; untouched components cost nothing
         const uint32_t nc = cf.ncyc;
         const uint32_t items = nblk * nc;
-        for (uint32_t w = tid; w < items; w += NCONS) {
+        for (uint32_t w = tid; w < items; w += NC) {
             const uint32_t b = (w & lomask) | (((w >> lo) / nc) << lo), ci = (w >> lo) % nc;
             uint32_t uu;
             const CBlk c = cblk(G, T, am, b, uu);
             if (uu >= nvalid_units)
                 continue;
             const uint32_t c0 = cf.cyc_off[ci], len = cf.cyc_off[ci + 1] - c0;
+            if (len <= 2) {  // fixed points with a factor, and transpositions (all library gates)
+                const uint32_t p0 = cf.cyc[c0], p1 = cf.cyc[c0 + len - 1];
+                bool j0, j1;
+                const uint32_t a0 = caddr(T, c, p0, j0), a1 = caddr(T, c, p1, j1);
+                const double2 v0 = ldc(sb, a0, j0), v1 = ldc(sb, a1, j1);
+                double2 x0 = v1, x1 = v0;  // out[p0] = f in[p1], out[p1] = f in[p0]
+                if (!((cf.fone >> p0) & 1ull))
+                    x0 = cmul(cf.s[p0], x0);
+                stc(sb, a0, j0, x0);
+                if (len == 2) {
+                    if (!((cf.fone >> p1) & 1ull))
+                        x1 = cmul(cf.s[p1], x1);
+                    stc(sb, a1, j1, x1);
+                }
+                continue;
+            }
             double2 v[16];
             uint32_t a[16];
             uint32_t cjm = 0;
             for (uint32_t j = 0; j < len; ++j) {
                 bool cj;
-                a[j] = caddr(G, c, cf.cyc[c0 + j], cj);
+                a[j] = caddr(T, c, cf.cyc[c0 + j], cj);
                 cjm |= (uint32_t)cj << j;
                 v[j] = ldc(sb, a[j], cj);
             }
@@ -1057,6 +1080,11 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
             T.xs_in[tid] = G.xs_in[tid];
             T.y_in[tid] = G.y_in[tid];
         }
+    }
+    if (tid < 64) {
+        T.cdir[tid] = G.cdir[tid];
+        T.cadj[tid] = G.cadj[tid];
+        T.ttr[tid] = G.ttr[tid];
     }
     if (tid == 0) {
         for (uint32_t s = 0; s < G.stages; ++s) {
@@ -1135,6 +1163,143 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
         if (lane == 0)
             mbar_arrive(&done[s]);
     }
+}
+
+
+// ------------------------------------------------------------- gather kernel (g >= 2: sub-blocks)
+// Units with >= 2 grid bits couple 16 or 64 stored tiles, too many for whole-tile staging.  An item
+// is then one S0 x S0 sub-block of positions (closed under the in-tile target bits) of every
+// logical tile of a unit (4096 elements, 64 KiB); rows of S0 elements are whole cache lines in
+// both orientations.  All 512 threads gather with cp.async (16 B each, adjoint tiles transposed on
+// the way in, padded pitch S0 + 1), 3-stage software pipeline (commit/wait groups), transform in
+// shared memory, and write back with coalesced st.global along stored rows.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int K, int MODE, int NS, int NC>
+__global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
+    extern __shared__ __align__(128) double2 ring[];
+    __shared__ uint64_t gt[MAX_STAGES][64];
+    __shared__ uint64_t am[MAX_STAGES][1];
+    __shared__ Tabs T;
+    const uint32_t tid = threadIdx.x;
+    if (tid < 32) {
+        T.xdep[tid] = G.xdep[tid];
+        T.xb[tid] = G.xb_tab[tid];
+        T.yb[tid] = G.yb_tab[tid];
+        if (tid < 8) {
+            T.xs_in[tid] = G.xs_in[tid];
+            T.y_in[tid] = G.y_in[tid];
+        }
+    }
+    if (tid < 64) {
+        T.cdir[tid] = G.cdir[tid];
+        T.cadj[tid] = G.cadj[tid];
+        T.ttr[tid] = G.ttr[tid];
+    }
+    const uint64_t nItems = G.nG_items;
+    const uint32_t S = G.stages;
+    const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint32_t NT = 1u << G.logNT, NGm = (1u << G.logNG) - 1;
+    const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
+    // NC is a multiple of S0^2: every element this thread moves sits at the same sub-block
+    // position (i, jj) in stored order, in tiles tt = tid / S0^2 + k * NC / S0^2
+    const uint32_t r = tid & ((1u << logT) - 1), i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
+    const uint32_t tt0 = tid >> logT, ttstep = NC >> logT;
+    const uint32_t sm_d = i0 * P + j0, sm_a = j0 * P + i0;  // logical slot, direct / adjoint
+    const uint32_t nsbm = (1u << (2 * G.log_nsb_side)) - 1;
+
+    auto item_of = [&](uint64_t j) { return blockIdx.x + j * gridDim.x; };
+    auto prep = [&](uint64_t j, uint32_t s) {
+        const uint64_t u = item_of(j) >> (2 * G.log_nsb_side);
+        if (tid < NT) {
+            uint64_t tbi, tbj;
+            tri_strict(u, tbi, tbj);
+            const uint64_t tr = ins_bits(tbi, tid >> G.logNG, G.gr_pos, G.g);
+            const uint64_t tc = ins_bits(tbj, tid & NGm, G.gr_pos, G.g);
+            uint64_t ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
+            if (MODE == M_MONO && !((G.active >> tid) & 1ull))
+                ent |= F_SKIP;
+            gt[s][tid] = ent;
+        }
+    };
+    auto mask_of = [&](uint32_t s) {
+        if (tid < 32) {
+            unsigned long long m = 0;
+            for (uint32_t t = tid; t < NT; t += 32)
+                m |= (unsigned long long)((gt[s][t] & F_ADJ) != 0) << t;
+            for (int o = 16; o; o >>= 1)
+                m |= __shfl_xor_sync(0xffffffffu, m, o);
+            if (tid == 0)
+                am[s][0] = m;
+        }
+    };
+    // global offsets (within a tile) of this thread's sub-block position, direct / adjoint
+    auto offsets = [&](uint64_t item, uint32_t& od, uint32_t& oa) {
+        const uint32_t sb = (uint32_t)(item & nsbm);
+        const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
+        od = ((x0 | T.xdep[i0]) << G.logM) + (y0 | T.xdep[j0]);
+        oa = ((y0 | T.xdep[i0]) << G.logM) + (x0 | T.xdep[j0]);
+    };
+    auto issue = [&](uint64_t j) {
+        const uint32_t s = (uint32_t)(j % S);
+        uint32_t od, oa;
+        offsets(item_of(j), od, oa);
+        const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
+        for (uint32_t tt = tt0; tt < NT; tt += ttstep) {
+            const uint64_t ent = gt[s][tt];
+            if (ent & F_SKIP)
+                continue;
+            const bool adj = (ent & F_ADJ) != 0;
+            const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
+            cp_async16(base + (tt * G.TS + (adj ? sm_a : sm_d)) * 16u, st + g);
+        }
+    };
+    __syncthreads();
+    for (uint32_t j = 0; j + 1 < S; ++j) {
+        if (j < nlocal)
+            prep(j, j % S);
+        __syncthreads();
+        if (j < nlocal) {
+            mask_of(j % S);
+            issue(j);
+        }
+        cp_async_commit();
+    }
+    for (uint64_t i = 0; i < nlocal; ++i) {
+        const uint32_t s = (uint32_t)(i % S);
+        cp_async_wait<1>();  // S = 3: all but the most recent group (item i + 1) have landed
+        __syncthreads();
+        double2* sb = ring + (size_t)s * G.stage_elems;
+        pipe_compute<K, MODE, NS, NC>(G, T, cf, am[s], 1, sb);
+        __syncthreads();
+        // write back along stored rows (adjoint components are already in stored, conjugated form)
+        {
+            uint32_t od, oa;
+            offsets(item_of(i), od, oa);
+            for (uint32_t tt = tt0; tt < NT; tt += ttstep) {
+                const uint64_t ent = gt[s][tt];
+                if (ent & F_SKIP)
+                    continue;
+                const bool adj = (ent & F_ADJ) != 0;
+                st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + (adj ? sm_a : sm_d)];
+            }
+        }
+        const uint64_t j = i + S - 1;
+        if (j < nlocal)
+            prep(j, (uint32_t)(j % S));
+        __syncthreads();
+        if (j < nlocal) {
+            mask_of((uint32_t)(j % S));
+            issue(j);
+        }
+        cp_async_commit();
+    }
+    cp_async_wait<0>();
 }
 
 // ------------------------------------------------------------------------- reductions
@@ -1437,6 +1602,8 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
     G.SRp = G.SR == M ? M : G.SR + 1;
     G.TS = G.SR * M + (G.SRp == G.SR ? 0 : M);
     G.diag_map = (G.nxb >= 8 && G.nyb >= 8) ? 1 : 0;
+    G.PD = M;
+    G.logical = 0;
     G.nruns = 0;
     for (uint32_t xs = 0; xs < G.SR; ++xs) {
         if (xs == 0 || G.xdep[xs] != G.xdep[xs - 1] + 1) {
@@ -1465,6 +1632,58 @@ size_t smem_bytes(const Geo& G, int buffers) {
     return (std::max(u, d) + (buffers == 3 ? 64 : 0)) * sizeof(double2);
 }
 
+
+// Geometry of the gather kernel for an operation whose units do not fit whole (g >= 2).
+void plan_gather(Geo& G) {
+    const uint32_t M = G.M, g = G.g, NT = 1u << (2 * g), NG = 1u << g, kin = G.kin;
+    const uint32_t in_mask = G.in_mask;
+    uint32_t S0 = 1;
+    while (NT * (2 * S0) * (2 * S0) <= 4096 && 2 * S0 <= M)
+        S0 *= 2;
+    S0 = std::max<uint32_t>(S0, 1u << __builtin_popcount(in_mask));
+    S0 = std::min<uint32_t>(S0, M);
+    uint32_t cmask = in_mask;
+    for (uint32_t b = 0; b < G.m && (uint32_t)__builtin_popcount(cmask) < ilog2(S0); ++b)
+        cmask |= 1u << b;
+    G.S0 = S0;
+    G.logS0 = ilog2(S0);
+    G.nsb_side = M / S0;
+    G.log_nsb_side = ilog2(G.nsb_side);
+    for (uint32_t i = 0; i < 32; ++i)
+        G.xdep[i] = i < S0 ? (uint8_t)pdep(i, cmask) : 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        G.sdep[b] = b < G.nsb_side ? (uint8_t)pdep(b, (M - 1) & ~cmask) : 0;
+    uint32_t xs_tmask = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        if (in_mask >> b & 1u)
+            xs_tmask |= 1u << __builtin_popcount(cmask & ((1u << b) - 1));
+    G.SR = S0;
+    G.logSR = G.logS0;
+    G.nxb = G.nyb = S0 >> kin;
+    G.logNxb = G.logNyb = ilog2(G.nxb);
+    for (uint32_t i = 0; i < 32; ++i)
+        G.xb_tab[i] = G.yb_tab[i] = i < G.nxb ? (uint8_t)pdep(i, (S0 - 1) & ~xs_tmask) : 0;
+    for (uint32_t r = 0; r < 8; ++r)
+        G.xs_in[r] = G.y_in[r] = r < (1u << kin) ? (uint8_t)pdep(r, xs_tmask) : 0;
+    G.PD = S0 + 1;
+    G.SRp = S0 + 1;
+    G.logical = 1;
+    G.TS = S0 * (S0 + 1);
+    const uint32_t D = G.D, kinm = (1u << kin) - 1;
+    for (uint32_t rho = 0; rho < D; ++rho)
+        for (uint32_t gam = 0; gam < D; ++gam) {
+            const uint32_t R = rho >> kin, C = gam >> kin, i = rho * D + gam;
+            G.ttr[i] = (uint8_t)(R * NG + C);
+            G.cdir[i] = G.cadj[i] = (uint16_t)((R * NG + C) * G.TS + G.xs_in[rho & kinm] * G.PD + G.y_in[gam & kinm]);
+        }
+    G.diag_map = (G.nxb >= 8 && G.nyb >= 8) ? 1 : 0;
+    G.U = 1;
+    G.logU = 0;
+    G.stage_elems = (NT * G.TS + 7) & ~7u;
+    G.stages = 3;
+    G.nG_items = (G.nb * (G.nb - 1) / 2) << (2 * G.log_nsb_side);
+}
+
 int sm_count(int device) {
     static int cache[64] = {0};
     if (device < 0 || device >= 64)
@@ -1481,6 +1700,43 @@ int sm_count(int device) {
 template <int K, int MODE, int NS>
 int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
     Geo G = G0;
+    if (MODE != M_KRAUS && G.g >= 2 && G.slabs > 1) {
+        // units of 16 / 64 stored tiles: sub-block gather kernel for the off-diagonal units,
+        // the slab kernel's wedge path for the diagonal ones
+        cudaError_t e;
+        if (G.nD_items) {
+            Geo Gs = G;
+            Gs.nU_items = 0;
+            Gs.Epad = 0;
+            const size_t smem = smem_bytes(Gs, buffers);
+            auto kern = conj_kernel<K, MODE, NS>;
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+            kern<<<(unsigned)G.nD_items, NTHR, smem, h->stream>>>(Gs, cf, ka, h->d);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            e = cudaGetLastError();
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
+        }
+        Geo Gg = G;
+        plan_gather(Gg);
+        if (Gg.nG_items) {
+            const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
+            constexpr int NC = K == 3 ? 256 : NCONS;  // k = 3 blocks need the registers
+            auto kern = gather_kernel<K, MODE, NS, NC>;
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather): ") + cudaGetErrorString(e));
+            const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
+            kern<<<(unsigned)grid, NC, smem, h->stream>>>(Gg, cf, h->d);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            e = cudaGetLastError();
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("gather_kernel launch: ") + cudaGetErrorString(e));
+        }
+        return HS_OK;
+    }
     const bool pipe = MODE != M_KRAUS && G.stages >= 3 && (G.nU_items > 0 || G.nD_items > 0);
     if (pipe && G.g >= 1 && G.slabs == 1) {
         // whole-unit items: the pipeline handles the diagonal base pairs as well
