@@ -152,6 +152,11 @@ int hs_state_fill_mixture(hs_state* h, int rank, const double* psi);
 int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uint64_t* z, const int32_t* ny,
                             const double* coef);
 
+/* max over stored elements of |h - (1/rank) sum |psi_i><psi_i|| (componentwise), computed on
+ * the device with the same rounding as hs_state_fill_mixture: full-size verification of a
+ * state against evolved pure states without a second copy in HBM.  Synchronising. */
+int hs_state_distance_mixture(const hs_state* h, int rank, const double* psi, double* max_abs);
+
 /* ---- device timing helpers (CUDA events on the state's stream) ------------------------ */
 int hs_event_create(void** ev);
 int hs_event_destroy(void* ev);

@@ -96,6 +96,7 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_frobenius", i, [vp, c_double_p])
     _sig(L, "hs_state_fill_mixture", i, [vp, i, c_double_p])
     _sig(L, "hs_state_fill_pauli_sum", i, [vp, i, c_u64_p, c_u64_p, c_i32_p, c_double_p])
+    _sig(L, "hs_state_distance_mixture", i, [vp, i, c_double_p, c_double_p])
     _sig(L, "hs_event_create", i, [pp])
     _sig(L, "hs_event_destroy", i, [vp])
     _sig(L, "hs_event_record", i, [vp, vp])

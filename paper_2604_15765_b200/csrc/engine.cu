@@ -1404,6 +1404,45 @@ __global__ void fill_mixture_kernel(double2* st, uint64_t count, uint32_t logM, 
     }
 }
 
+
+// max_e |st[e] - rho_psi(e)| over the stored payload, rho_psi = (1/rank) sum |psi_i><psi_i| built
+// exactly as fill_mixture_kernel (verification of full-size states without a second copy)
+__global__ void dist_mixture_kernel(const double2* st, uint64_t count, uint32_t logM, uint64_t N, const double2* psi,
+                                    int rank, double inv, double* out) {
+    __shared__ double sh[NTHR];
+    const uint32_t M = 1u << logM;
+    double mx = 0.0;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        tri_loose(t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 acc = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            for (int a = 0; a < rank; ++a) {
+                const double2 p = psi[(uint64_t)a * N + i], q = psi[(uint64_t)a * N + j];
+                acc.x = __dadd_rn(acc.x, __dadd_rn(__dmul_rn(p.x, q.x), __dmul_rn(p.y, q.y)));
+                acc.y = __dadd_rn(acc.y, __dsub_rn(__dmul_rn(p.y, q.x), __dmul_rn(p.x, q.y)));
+            }
+            acc.x = __dmul_rn(acc.x, inv);
+            acc.y = __dmul_rn(acc.y, inv);
+        }
+        const double2 v = st[e];
+        mx = fmax(mx, fmax(fabs(v.x - acc.x), fabs(v.y - acc.y)));
+    }
+    sh[threadIdx.x] = mx;
+    __syncthreads();
+    for (int s = NTHR / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        out[blockIdx.x] = sh[0];
+}
+
 struct PauliArgs {
     const uint64_t* x;
     const uint64_t* z;
@@ -2401,6 +2440,34 @@ int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uin
     cudaFree(buf);
     if (e != cudaSuccess)
         return set_err(HS_ERR_CUDA, cudaGetErrorString(e));
+    return HS_OK;
+}
+
+
+int hs_state_distance_mixture(const hs_state* h, int rank, const double* psi, double* max_abs) {
+    if (!h || !psi || rank < 1 || !max_abs)
+        return set_err(HS_ERR_INVALID, "bad distance arguments");
+    DeviceGuard dg(h->device);
+    double2* dpsi = nullptr;
+    const size_t bytes = (size_t)rank * h->N * sizeof(double2);
+    CUDA_TRY(cudaMalloc(&dpsi, bytes));
+    CUDA_TRY(cudaMemcpyAsync(dpsi, psi, bytes, cudaMemcpyHostToDevice, h->stream));
+    dist_mixture_kernel<<<RED_BLOCKS, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, dpsi, rank,
+                                                             1.0 / rank, h->red);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    std::vector<double> part(RED_BLOCKS);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(part.data(), h->red, RED_BLOCKS * sizeof(double), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(h->stream);
+    cudaFree(dpsi);
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, cudaGetErrorString(e));
+    double mx = 0.0;
+    for (double v : part)
+        mx = std::max(mx, v);
+    *max_abs = mx;
     return HS_OK;
 }
 

@@ -61,6 +61,35 @@ def rho_payload_range(n: int, psi: np.ndarray, t0: int, t1: int, m: int = 5) -> 
     return out
 
 
+def rho_payload_threaded(n: int, psi: np.ndarray, m: int = 5, out: np.ndarray | None = None,
+                         threads: int | None = None) -> np.ndarray:
+    """rho_payload over disjoint tile ranges on all host cores (ctypes releases the GIL)."""
+    import os
+    import threading
+    psi = np.ascontiguousarray(psi, np.complex128)
+    cnt = payload_count(n, m)
+    if out is None:
+        out = np.empty(cnt, np.complex128)
+    G = (1 << n) >> m if n >= m else 1
+    T = G * (G + 1) // 2
+    threads = threads or os.cpu_count() or 1
+    bounds = [T * i // threads for i in range(threads + 1)]
+    L = nat.harness()
+
+    def work(i):
+        t0, t1 = bounds[i], bounds[i + 1]
+        if t1 > t0:
+            view = out[t0 << (2 * m): t1 << (2 * m)]
+            L.hsg_rho_payload_range(n, m, psi.shape[0], _dp(psi), _dp(view), t0, t1)
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return out
+
+
 def haar(k: int, seed: int) -> np.ndarray:
     """Haar 2^k x 2^k unitary: QR (Gram-Schmidt) of a complex Gaussian, phase-fixed."""
     d = 1 << k

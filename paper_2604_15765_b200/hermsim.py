@@ -145,6 +145,14 @@ class TiledHermitian:
             self.handle, len(x), x.ctypes.data_as(nat.c_u64_p), z.ctypes.data_as(nat.c_u64_p),
             ny.ctypes.data_as(nat.c_i32_p), _dp(coef)), "fill_pauli_sum")
 
+    def distance_to_mixture(self, psi: np.ndarray) -> float:
+        """max |stored element - (1/rank) sum |psi_i><psi_i|| over the payload (device-side)."""
+        psi = np.ascontiguousarray(psi, np.complex128)
+        out = ctypes.c_double()
+        nat.check(nat.engine().hs_state_distance_mixture(self.handle, psi.shape[0], _dp(psi), ctypes.byref(out)),
+                  "distance_to_mixture")
+        return out.value
+
     def free(self) -> None:
         if getattr(self, "_h", None) is not None:
             nat.engine().hs_state_free(self._h)

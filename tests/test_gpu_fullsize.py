@@ -1,0 +1,232 @@
+"""Parity at BASELINE.json's full sizes (GPU box: 1 x B200, 196 GB host RAM, 16 cores).
+
+* C0 (n = 12): the whole 12-op sequence, elementwise against the compiled reference on identical
+  inputs.
+* C1 (n = 14) / C2 (n = 16): op subsets that cover every tiled regime, elementwise against the
+  compiled reference (hermsim::apply, threads = nproc) on the identical full-size payload.
+* C3 (n = 16): the full 100-op Heisenberg circuit, tr(rho O) against an independent state-vector
+  computation (1/4) sum_i <W psi_i| O |W psi_i>, |delta| <= 1e-12 ||rho||_F ||O||_F.
+* C4 (n = 17, 137 GB state): one full layer without the depolarising channels, elementwise against
+  the mixture of the state vectors evolved by that layer (computed on the device, no second copy),
+  plus trace preservation through a full layer with the channels.
+Tolerance: max |delta| <= 1e-12 * ||X||_F, ||X||_F the logical Frobenius norm.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def H():
+    from paper_2604_15765_b200 import hermsim
+    if hermsim.device_count() < 1:
+        pytest.fail("no CUDA device visible")
+    return hermsim
+
+
+@pytest.fixture(scope="module")
+def HS():
+    from paper_2604_15765_b200 import harness
+    return harness
+
+
+def _spec(H, op):
+    if op.kind == "h":
+        return H.native_gate("h")
+    if op.kind == "cnot":
+        return H.native_gate("cnot")
+    if op.kind == "rz":
+        return H.native_gate("rz", op.param)
+    if op.kind == "depol":
+        return H.depolarising(op.param)
+    if op.kind == "ampdamp":
+        return H.amplitude_damping(op.param)
+    if op.kind == "unitary":
+        return H.make_generic("u", op.matrix)
+    return H.dual_channel(H.make_generic("u", op.matrix))
+
+
+def _ref_channel(O, op):
+    if op.kind in ("h", "cnot"):
+        return O.native_gate(op.kind)
+    if op.kind == "rz":
+        return O.native_gate("rz", op.param)
+    if op.kind == "depol":
+        return O.depolarising(op.param)
+    if op.kind == "ampdamp":
+        return O.amplitude_damping(op.param)
+    if op.kind == "unitary":
+        return O.generic(op.matrix)
+    return O.dual(O.generic(op.matrix))
+
+
+def _compare_with_ref(st, refview, n, m, chunk=1 << 26):
+    """max |gpu - ref| / ||ref||_F, streaming the device payload in chunks."""
+    cnt = st.element_count()
+    G = (1 << n) >> m
+    tile = 1 << (2 * m)
+    # logical Frobenius norm: diagonal tiles once, the rest twice
+    dsum = osum = 0.0
+    maxd = 0.0
+    t = 0
+    for off in range(0, cnt, chunk):
+        c = min(chunk, cnt - off)
+        got = st.download_range(off, c)
+        want = refview[off:off + c]
+        maxd = max(maxd, float(np.max(np.abs(got - want))))
+        sq = (np.abs(want) ** 2).reshape(-1, tile).sum(axis=1)
+        ntile = c // tile
+        idx = np.arange(t, t + ntile)
+        ti = ((np.sqrt(8.0 * idx + 1) - 1) // 2).astype(np.int64)
+        ti -= (ti * (ti + 1) // 2 > idx)
+        ti += ((ti + 1) * (ti + 2) // 2 <= idx)
+        tj = idx - ti * (ti + 1) // 2
+        dsum += float(sq[ti == tj].sum())
+        osum += float(sq[ti != tj].sum())
+        t += ntile
+    assert t == G * (G + 1) // 2
+    return maxd / np.sqrt(dsum + 2 * osum)
+
+
+def _run_pair(H, HS, oracle, cfg, n, ops, seed):
+    """Same ops on the GPU and on the compiled reference, identical full-size input."""
+    ref = oracle.Reference()
+    m = 5
+    psi = HS.rank_psi(n, seed, 4)
+    st = H.TiledHermitian(n, m)
+    st.fill_mixture(psi)
+    h = ref.create(n, m)
+    view = ref.view(h)
+    HS.rho_payload_threaded(n, psi, m, out=view)
+    threads = os.cpu_count() or 1
+    for op in ops:
+        H.apply(st, _spec(H, op), list(op.targets))
+        ref.apply(h, _ref_channel(oracle, op), list(op.targets), threads=threads)
+    err = _compare_with_ref(st, view, n, m)
+    ref.free(h)
+    st.free()
+    return err
+
+
+def test_c0_full_sequence_vs_reference(H, HS, oracle):
+    err = _run_pair(H, HS, oracle, "c0", 12, HS.config_ops("c0"), HS.SEEDS["c0"])
+    assert err <= TOL, err
+
+
+def test_c1_regimes_vs_reference_n14(H, HS, oracle):
+    ops = HS.config_ops("c1")
+    pairs = [(0, 1), (1, 0), (2, 9), (9, 2), (4, 13), (13, 7), (7, 13), (12, 11), (6, 5), (3, 4)]
+    pick = []
+    for i in range(0, len(ops), 2):
+        if tuple(ops[i].targets) in pairs:
+            pick += [ops[i], ops[i + 1]]
+    assert len(pick) == 2 * len(pairs)
+    err = _run_pair(H, HS, oracle, "c1", 14, pick, HS.SEEDS["c1"])
+    assert err <= TOL, err
+
+
+def test_c2_regimes_vs_reference_n16(H, HS, oracle):
+    ops = HS.config_ops("c2")
+    pick = [op for op in ops if op.targets[0] in (0, 4, 5, 15)]
+    err = _run_pair(H, HS, oracle, "c2", 16, pick, HS.SEEDS["c2"])
+    assert err <= TOL, err
+
+
+# ------------------------------------------------------------------------ state vectors
+def _apply_sv(psi, n, u, targets):
+    """psi (2^n,) <- U on `targets` (constructor order: first listed = most significant local bit)."""
+    k = len(targets)
+    t = psi.reshape([2] * n)
+    axes = [n - 1 - q for q in targets]
+    t = np.moveaxis(t, axes, list(range(k)))
+    sh = t.shape
+    t = (u @ t.reshape(1 << k, -1)).reshape(sh)
+    return np.moveaxis(t, list(range(k)), axes).reshape(-1)
+
+
+def _pauli_expect(phi, strings):
+    x, z, ny, coef = strings
+    idx = np.arange(phi.size, dtype=np.uint64)
+    total = 0.0
+    for s in range(len(x)):
+        sign = 1.0 - 2.0 * (np.bitwise_count(idx & z[s]) & 1)
+        pphi = np.empty_like(phi)
+        pphi[idx ^ x[s]] = (1j ** int(ny[s])) * sign * phi
+        total += coef[s] * np.vdot(phi, pphi).real
+    return total
+
+
+def test_c3_expectation_vs_statevector(H, HS):
+    n, m = 16, 5
+    seed = HS.SEEDS["c3"]
+    strings = HS.pauli_strings(n, 64, seed)
+    psi = HS.rank_psi(n, seed + 1, 4)
+    obs = H.TiledHermitian(n, m)
+    obs.fill_pauli_sum(*strings)
+    ops = HS.config_ops("c3")
+    for op in ops:
+        H.apply(obs, _spec(H, op), list(op.targets))
+    rho = H.TiledHermitian(n, m)
+    rho.fill_mixture(psi)
+    got = H.expectation(rho, obs)
+    fro_o = H.frobenius(obs)
+    fro_r = H.frobenius(rho)
+    rho.free()
+    obs.free()
+    # O_final = W^dag O W, W = U_1 U_2 ... U_100  =>  tr(rho O_final) = 1/4 sum <W psi|O|W psi>
+    want = 0.0
+    for p in psi:
+        phi = p.copy()
+        for op in reversed(ops):
+            phi = _apply_sv(phi, n, op.matrix, op.targets)
+        want += _pauli_expect(phi, strings) / 4
+    assert abs(got - want) <= TOL * fro_r * fro_o, (got, want)
+
+
+def _layer_unitaries(HS, n, layer_ops):
+    r = 1 / np.sqrt(2)
+    mats = []
+    for op in layer_ops:
+        if op.kind == "rz":
+            th = op.param
+            mats.append((np.diag([np.exp(-0.5j * th), np.exp(0.5j * th)]), op.targets))
+        elif op.kind == "h":
+            mats.append((np.array([[r, r], [r, -r]]), op.targets))
+        elif op.kind == "cnot":
+            mats.append((np.array([[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]]), op.targets))
+    return mats
+
+
+@pytest.mark.parametrize("n", [13, 17])
+def test_c4_layer_vs_statevector(H, HS, n):
+    m = 5
+    ops = HS.config_ops("c4", n)
+    per_layer = 2 * n + n // 2 + n
+    layer = ops[:per_layer]
+    unitary_ops = [op for op in layer if op.kind != "depol"]
+    psi = HS.rank_psi(n, HS.SEEDS["c4"], 4)
+    st = H.TiledHermitian(n, m)
+    st.fill_mixture(psi)
+    for op in unitary_ops:
+        H.apply(st, _spec(H, op), list(op.targets))
+    evolved = []
+    for p in psi:
+        phi = p.copy()
+        for u, tg in _layer_unitaries(HS, n, unitary_ops):
+            phi = _apply_sv(phi, n, u, tg)
+        evolved.append(phi)
+    dist = st.distance_to_mixture(np.stack(evolved))
+    fro = H.frobenius(st)
+    assert dist <= TOL * fro, (dist, fro)
+    # the depolarising channels of the layer preserve the trace
+    for op in layer:
+        if op.kind == "depol":
+            H.apply(st, _spec(H, op), list(op.targets))
+    assert abs(H.trace(st) - 1.0) < 1e-12
+    st.free()
