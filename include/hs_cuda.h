@@ -157,6 +157,26 @@ int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uin
  * state against evolved pure states without a second copy in HBM.  Synchronising. */
 int hs_state_distance_mixture(const hs_state* h, int rank, const double* psi, double* max_abs);
 
+/* ---- sharding across GPUs (XOR blocks over the top log2(P) tile-row bits) -----
+ * Shard s of P holds the stored tiles (ti >= tj) with (ti >> logB) ^ (tj >> logB) == s, B = G / P:
+ * shard 0 the P diagonal blocks (triangular), shard s != 0 the P/2 rectangular blocks (a, a ^ s),
+ * a > a ^ s.  P = 1 is exactly the reference layout.  Operations whose targets avoid the top
+ * log2(P) qubits are shard-local; an operation with one top target pairs shard s with
+ * s ^ 2^c: each side needs the partner's payload in its exchange buffer (hs_state_exchange over
+ * NCCL, or hs_state_exchange_from for shards in one process), computes every shared unit and
+ * stores only its own tiles.  More than one top target: HS_ERR_UNSUPPORTED. */
+int hs_state_create_sharded(int n, int m, int device, int nshards, int shard, hs_state** out);
+int hs_state_shard_info(const hs_state* h, int* nshards, int* shard, uint64_t* block_rows);
+/* partner shard of an operation on `targets` (any order), -1 when shard-local */
+int hs_op_partner(const hs_state* h, int k, const uint32_t* targets, int* partner);
+int hs_state_recv_alloc(hs_state* h);
+int hs_state_exchange_from(hs_state* h, const hs_state* peer);  /* recv <- peer payload (device/peer copy) */
+int hs_nccl_unique_id(void* id128);                               /* ncclUniqueId (128 bytes) */
+int hs_state_comm_init(hs_state* h, const void* id128, int nranks, int rank);  /* rank == shard */
+int hs_state_exchange(hs_state* h, int partner);                  /* NCCL send/recv, stream-ordered */
+/* linear partial sums of one shard: kind 0 tr(rho O), 1 squared Frobenius, 2 trace (sum over shards) */
+int hs_reduce_partial(const hs_state* a, const hs_state* b, int kind, double* out);
+
 /* ---- device timing helpers (CUDA events on the state's stream) ------------------------ */
 int hs_event_create(void** ev);
 int hs_event_destroy(void* ev);

@@ -97,6 +97,15 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_state_fill_mixture", i, [vp, i, c_double_p])
     _sig(L, "hs_state_fill_pauli_sum", i, [vp, i, c_u64_p, c_u64_p, c_i32_p, c_double_p])
     _sig(L, "hs_state_distance_mixture", i, [vp, i, c_double_p, c_double_p])
+    _sig(L, "hs_state_create_sharded", i, [i, i, i, i, i, pp])
+    _sig(L, "hs_state_shard_info", i, [vp, c_int_p, c_int_p, c_u64_p])
+    _sig(L, "hs_op_partner", i, [vp, i, c_u32_p, c_int_p])
+    _sig(L, "hs_state_recv_alloc", i, [vp])
+    _sig(L, "hs_state_exchange_from", i, [vp, vp])
+    _sig(L, "hs_nccl_unique_id", i, [vp])
+    _sig(L, "hs_state_comm_init", i, [vp, vp, i, i])
+    _sig(L, "hs_state_exchange", i, [vp, i])
+    _sig(L, "hs_reduce_partial", i, [vp, vp, i, c_double_p])
     _sig(L, "hs_event_create", i, [pp])
     _sig(L, "hs_event_destroy", i, [vp])
     _sig(L, "hs_event_record", i, [vp, vp])

@@ -28,6 +28,8 @@
 //
 // All data is complex128 (double2).  No tensor cores: the path is HBM-bound.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -48,7 +50,7 @@ constexpr uint32_t CAPD = 2048;    // same for diagonal-unit items
 constexpr uint32_t CAP_WHOLE = 4096;  // units up to 64 KiB are staged as whole stored tiles
 constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in smem)
 constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_NOSTORE = 1ull << 60,
-                   F_MASK = (1ull << 56) - 1;
+                   F_REMOTE = 1ull << 59, F_MASK = (1ull << 56) - 1;
 
 enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5 };
 
@@ -111,6 +113,12 @@ struct Geo {
     // gather kernel (square sub-blocks of S0 x S0 positions, g >= 2)
     uint32_t S0, logS0, nsb_side, log_nsb_side;
     uint64_t nG_items;
+    // sharding (XOR blocks over the top Plog tile-index bits; Plog == 0: the reference layout)
+    uint32_t Plog, shard, logB;   // 2^Plog shards, this shard, 2^logB tile rows per block
+    uint32_t cross, cbit;         // the op has a target on top bit cbit: shard <-> shard ^ 2^cbit
+    uint32_t q, Pulog, logBu;     // local units: group q over 2^Pulog blocks of 2^logBu grid bases
+    const double2* recv;          // partner shard payload (cross ops)
+    uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
@@ -211,6 +219,90 @@ __device__ __forceinline__ void tri_loose(uint64_t u, uint64_t& i, uint64_t& j) 
         ++r;
     i = r;
     j = u - r * (r + 1) / 2;
+}
+
+// ----------------------------------------------------------------------- shard addressing
+// XOR blocks: stored tile (ti >= tj) belongs to shard (ti >> logB) ^ (tj >> logB).  Shard 0
+// stores the 2^Plog diagonal blocks (triangular, B(B+1)/2 tiles each), shard s != 0 the 2^(Plog-1)
+// rectangular blocks (a, a ^ s) with a > a ^ s (B x B tiles, row-major), ordered by a with bit
+// msb(s) removed.  With Plog == 0 this is exactly the reference's triangle (storage.hpp:78-83).
+__device__ __forceinline__ uint32_t msb32(uint32_t v) { return 31u - __clz(v); }
+__device__ __forceinline__ uint32_t del_bit(uint32_t a, uint32_t h) {
+    return ((a >> (h + 1)) << h) | (a & ((1u << h) - 1));
+}
+__device__ __forceinline__ uint32_t ins_one(uint32_t v, uint32_t h) {
+    return ((v >> h) << (h + 1)) | (1u << h) | (v & ((1u << h) - 1));
+}
+__device__ __forceinline__ uint32_t shard_of(uint32_t Plog, uint32_t logB, uint64_t tr, uint64_t tc) {
+    return Plog ? (uint32_t)((tr >> logB) ^ (tc >> logB)) : 0u;
+}
+__device__ __forceinline__ uint64_t shard_index(uint32_t Plog, uint32_t logB, uint64_t tr, uint64_t tc, uint32_t s) {
+    if (!Plog)
+        return tri(tr) + tc;
+    const uint32_t a = (uint32_t)(tr >> logB);
+    const uint64_t Bm = (1ull << logB) - 1, r = tr & Bm, c = tc & Bm;
+    if (s == 0)
+        return (uint64_t)a * ((Bm + 1) * (Bm + 2) / 2) + tri(r) + c;
+    return ((uint64_t)del_bit(a, msb32(s)) << (2 * logB)) + (r << logB) + c;
+}
+// local tile index -> (ti, tj) in shard s
+__device__ __forceinline__ void shard_decode(uint32_t Plog, uint32_t logB, uint32_t s, uint64_t t, uint64_t& ti,
+                                             uint64_t& tj) {
+    if (!Plog) {
+        tri_loose(t, ti, tj);
+        return;
+    }
+    const uint64_t B = 1ull << logB;
+    if (s == 0) {
+        const uint64_t per = B * (B + 1) / 2, a = t / per;
+        uint64_t r, c;
+        tri_loose(t - a * per, r, c);
+        ti = a * B + r;
+        tj = a * B + c;
+    } else {
+        const uint32_t a = ins_one((uint32_t)(t >> (2 * logB)), msb32(s)), b = a ^ s;
+        const uint64_t v = t & (B * B - 1);
+        ti = (uint64_t)a * B + (v >> logB);
+        tj = (uint64_t)b * B + (v & (B - 1));
+    }
+}
+// (stored-tile index | F_ADJ | F_REMOTE) of logical tile (tr, tc) for this operation's shard
+__device__ __forceinline__ uint64_t tile_entry(const Geo& G, uint64_t tr, uint64_t tc) {
+    const bool adj = tr < tc;
+    const uint64_t hi = adj ? tc : tr, lo = adj ? tr : tc;
+    const uint32_t own = shard_of(G.Plog, G.logB, hi, lo);
+    uint64_t ent = shard_index(G.Plog, G.logB, hi, lo, own);
+    if (adj)
+        ent |= F_ADJ;
+    if (own != G.shard)
+        ent |= F_REMOTE | F_NOSTORE;
+    return ent;
+}
+// local unit u -> grid base pair (tbi, tbj); strict: off-diagonal units only
+__device__ __forceinline__ void unit_decode(const Geo& G, uint64_t u, bool strict, uint64_t& tbi, uint64_t& tbj) {
+    if (!G.Pulog) {
+        if (strict)
+            tri_strict(u, tbi, tbj);
+        else
+            tri_loose(u, tbi, tbj);
+        return;
+    }
+    const uint64_t Bu = 1ull << G.logBu;
+    if (G.q == 0) {
+        const uint64_t per = strict ? Bu * (Bu - 1) / 2 : Bu * (Bu + 1) / 2, a = u / per;
+        uint64_t r, c;
+        if (strict)
+            tri_strict(u - a * per, r, c);
+        else
+            tri_loose(u - a * per, r, c);
+        tbi = a * Bu + r;
+        tbj = a * Bu + c;
+    } else {
+        const uint32_t a = ins_one((uint32_t)(u >> (2 * G.logBu)), msb32(G.q)), b = a ^ G.q;
+        const uint64_t v = u & (Bu * Bu - 1);
+        tbi = (uint64_t)a * Bu + (v >> G.logBu);
+        tbj = (uint64_t)b * Bu + (v & (Bu - 1));
+    }
 }
 
 // ------------------------------------------------------------------- block transforms
@@ -454,10 +546,10 @@ __device__ void path_u(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
             ent = u;
         } else {
             uint64_t tbi, tbj;
-            tri_strict(u, tbi, tbj);
+            unit_decode(G, u, true, tbi, tbj);
             const uint32_t R = lt >> G.logNG, C = lt & NGm;
             const uint64_t tr = ins_bits(tbi, R, G.gr_pos, G.g), tc = ins_bits(tbj, C, G.gr_pos, G.g);
-            ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
+            ent = tile_entry(G, tr, tc);
         }
         if (MODE == M_MONO && !((G.active >> lt) & 1ull))
             ent |= F_SKIP;
@@ -495,7 +587,7 @@ __device__ void path_u(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
                         xs = l & SRm;
                         src = tb + ((uint64_t)y << G.logM) + (x0 | T.xdep[xs]);
                     }
-                    v[j] = ldg2(st + src);
+                    v[j] = ldg2(((ent & F_REMOTE) ? G.recv : st) + src);
                     if (ent & F_ADJ)
                         v[j].y = -v[j].y;
                     dst[j] = (tt * G.SR + xs) * Mp + y;
@@ -530,7 +622,7 @@ __device__ void path_u(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
                 continue;
             const uint32_t tt = e >> logTE, l = e & TEm;
             const uint64_t ent = ttab[tt];
-            if (ent & (F_BAD | F_SKIP))
+            if (ent & (F_BAD | F_SKIP | F_NOSTORE))
                 continue;
             const uint64_t tb = (ent & F_MASK) << (2 * G.logM);
             const bool adj = (ent & F_ADJ) != 0;
@@ -619,9 +711,11 @@ __device__ void path_d(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
         const uint32_t x = xb | T.y_in[rho & kinm], y = yb | T.y_in[gam & kinm];
         double2 v;
         if (R >= C) {
-            v = st[((tri(trow[R]) + trow[C]) << (2 * logM)) + ((uint64_t)x << logM) + y];
+            const uint64_t ent = tile_entry(G, trow[R], trow[C]);
+            v = ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)x << logM) + y];
         } else {
-            v = st[((tri(trow[C]) + trow[R]) << (2 * logM)) + ((uint64_t)y << logM) + x];
+            const uint64_t ent = tile_entry(G, trow[C], trow[R]);
+            v = ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)y << logM) + x];
             v.y = -v.y;
         }
         if (!one)
@@ -649,12 +743,15 @@ __device__ void path_d(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
         const uint32_t R = rho >> G.kin, C = gam >> G.kin;
         const uint32_t x = xb | T.y_in[rho & kinm], y = yb | T.y_in[gam & kinm];
         const double2 w = sm[e];
+        const uint64_t ent = R >= C ? tile_entry(G, trow[R], trow[C]) : tile_entry(G, trow[C], trow[R]);
+        if (ent & F_REMOTE)
+            continue;  // the partner shard stores this tile
+        const uint64_t t0 = (ent & F_MASK) << (2 * logM);
         if (R > C) {
-            st[((tri(trow[R]) + trow[C]) << (2 * logM)) + ((uint64_t)x << logM) + y] = w;
+            st[t0 + ((uint64_t)x << logM) + y] = w;
         } else if (R < C) {
-            st[((tri(trow[C]) + trow[R]) << (2 * logM)) + ((uint64_t)y << logM) + x] = cconj(w);
+            st[t0 + ((uint64_t)y << logM) + x] = cconj(w);
         } else {
-            const uint64_t t0 = (tri(trow[R]) + trow[R]) << (2 * logM);
             st[t0 + ((uint64_t)x << logM) + y] = w;
             if (x != y)
                 st[t0 + ((uint64_t)y << logM) + x] = cconj(w);
@@ -751,13 +848,10 @@ __device__ __forceinline__ void item_tiles(const Geo& G, uint64_t item, uint64_t
             ent = u;
         } else {
             uint64_t tbi, tbj;
-            if (G.pipe_diag)
-                tri_loose(u, tbi, tbj);  // diagonal units too (tbi == tbj)
-            else
-                tri_strict(u, tbi, tbj);
+            unit_decode(G, u, !G.pipe_diag, tbi, tbj);  // pipe_diag: diagonal units too
             const uint64_t tr = ins_bits(tbi, lt >> G.logNG, G.gr_pos, G.g);
             const uint64_t tc = ins_bits(tbj, lt & NGm, G.gr_pos, G.g);
-            ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
+            ent = tile_entry(G, tr, tc);
             // on a diagonal unit logical (R, C), R < C, aliases stored (C, R): it is staged as a
             // separate read-only copy (input of the transform) and never written back
             if (tbi == tbj && (lt >> G.logNG) < (lt & NGm))
@@ -788,7 +882,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
             if (STORE)
                 bulk_s2g(st + gbase, tsm, bytes);
             else
-                bulk_g2s(tsm, st + gbase, bytes, bar);
+                bulk_g2s(tsm, ((ent & F_REMOTE) ? G.recv : st) + gbase, bytes, bar);
         }
         return;
     }
@@ -798,6 +892,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
             continue;
         const uint64_t gbase = (ent & F_MASK) << (2 * G.logM);
         const uint32_t tsm = sbase + tt * G.TS * 16u;
+        const double2* src = (ent & F_REMOTE) ? G.recv : st;
         if (!(ent & F_ADJ)) {
             for (uint32_t r = lane; r < G.nruns; r += 32) {
                 const uint32_t xs0 = G.run_xs[r], len = G.run_len[r];
@@ -807,7 +902,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
                 if (STORE)
                     bulk_s2g(st + g, s, bytes);
                 else
-                    bulk_g2s(s, st + g, bytes, bar);
+                    bulk_g2s(s, src + g, bytes, bar);
             }
         } else {
             const uint32_t nch = G.nruns << G.logM;
@@ -819,7 +914,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
                 if (STORE)
                     bulk_s2g(st + g, s, len << 4);
                 else
-                    bulk_g2s(s, st + g, len << 4, bar);
+                    bulk_g2s(s, src + g, len << 4, bar);
             }
         }
     }
@@ -1218,10 +1313,10 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
         const uint64_t u = item_of(j) >> (2 * G.log_nsb_side);
         if (tid < NT) {
             uint64_t tbi, tbj;
-            tri_strict(u, tbi, tbj);
+            unit_decode(G, u, true, tbi, tbj);
             const uint64_t tr = ins_bits(tbi, tid >> G.logNG, G.gr_pos, G.g);
             const uint64_t tc = ins_bits(tbj, tid & NGm, G.gr_pos, G.g);
-            uint64_t ent = tr >= tc ? tri(tr) + tc : ((tri(tc) + tr) | F_ADJ);
+            uint64_t ent = tile_entry(G, tr, tc);
             if (MODE == M_MONO && !((G.active >> tid) & 1ull))
                 ent |= F_SKIP;
             gt[s][tid] = ent;
@@ -1256,7 +1351,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
                 continue;
             const bool adj = (ent & F_ADJ) != 0;
             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
-            cp_async16(base + (tt * G.TS + (adj ? sm_a : sm_d)) * 16u, st + g);
+            cp_async16(base + (tt * G.TS + (adj ? sm_a : sm_d)) * 16u, ((ent & F_REMOTE) ? G.recv : st) + g);
         }
     };
     __syncthreads();
@@ -1283,7 +1378,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
             offsets(item_of(i), od, oa);
             for (uint32_t tt = tt0; tt < NT; tt += ttstep) {
                 const uint64_t ent = gt[s][tt];
-                if (ent & F_SKIP)
+                if (ent & (F_SKIP | F_NOSTORE))
                     continue;
                 const bool adj = (ent & F_ADJ) != 0;
                 st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + (adj ? sm_a : sm_d)];
@@ -1307,6 +1402,10 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
 // ordered sum: deterministic for a given grid (SPEC.md observables: fixed-order reduction).
 constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs
 
+struct SD {  // shard descriptor of a state's local payload
+    uint32_t Plog, logB, shard;
+};
+
 __device__ double block_sum(double v, double* sh) {
     sh[threadIdx.x] = v;
     __syncthreads();
@@ -1322,16 +1421,16 @@ __device__ double block_sum(double v, double* sh) {
 
 // kind 0: Re<a, b>_F (expectation); kind 1: |a|^2 (frobenius); kind 2: trace (diagonal elements)
 __global__ void __launch_bounds__(NTHR) reduce_kernel(const double2* __restrict__ a, const double2* __restrict__ b,
-                                                      uint64_t ntiles, uint32_t logM, int kind, double* partials) {
+                                                      uint64_t ntiles, uint32_t logM, int kind, double* partials, SD sd) {
     __shared__ double sh[NTHR];
     const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
     const uint64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
     const uint32_t MM = 1u << (2 * logM), M = 1u << logM;
     double dsum = 0.0, osum = 0.0;
     if (t0 < t1) {
-        uint64_t ti, tj;
-        tri_loose(t0, ti, tj);
         for (uint64_t t = t0; t < t1; ++t) {
+            uint64_t ti, tj;
+            shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
             const double2* pa = a + (t << (2 * logM));
             const double2* pb = b + (t << (2 * logM));
             double acc = 0.0;
@@ -1350,10 +1449,6 @@ __global__ void __launch_bounds__(NTHR) reduce_kernel(const double2* __restrict_
                 dsum += acc;
             else
                 osum += acc;
-            if (++tj > ti) {
-                ++ti;
-                tj = 0;
-            }
         }
     }
     dsum = block_sum(dsum, sh);
@@ -1379,14 +1474,14 @@ __global__ void finish_kernel(const double* partials, int nparts, int kind, doub
 // rho(i, j) = (1/rank) sum_a psi_a[i] conj(psi_a[j]) with explicit rounding (no contraction),
 // bit-identical to hsg_rho_payload (harness.c).
 __global__ void fill_mixture_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, const double2* psi,
-                                    int rank, double inv) {
+                                    int rank, double inv, SD sd) {
     const uint32_t M = 1u << logM;
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
          e += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t t = e >> (2 * logM);
         const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
         uint64_t ti, tj;
-        tri_loose(t, ti, tj);
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
         const uint64_t i = ti * M + r, j = tj * M + c;
         double2 acc = make_double2(0.0, 0.0);
         if (i < N && j < N) {
@@ -1408,7 +1503,7 @@ __global__ void fill_mixture_kernel(double2* st, uint64_t count, uint32_t logM, 
 // max_e |st[e] - rho_psi(e)| over the stored payload, rho_psi = (1/rank) sum |psi_i><psi_i| built
 // exactly as fill_mixture_kernel (verification of full-size states without a second copy)
 __global__ void dist_mixture_kernel(const double2* st, uint64_t count, uint32_t logM, uint64_t N, const double2* psi,
-                                    int rank, double inv, double* out) {
+                                    int rank, double inv, double* out, SD sd) {
     __shared__ double sh[NTHR];
     const uint32_t M = 1u << logM;
     double mx = 0.0;
@@ -1417,7 +1512,7 @@ __global__ void dist_mixture_kernel(const double2* st, uint64_t count, uint32_t 
         const uint64_t t = e >> (2 * logM);
         const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
         uint64_t ti, tj;
-        tri_loose(t, ti, tj);
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
         const uint64_t i = ti * M + r, j = tj * M + c;
         double2 acc = make_double2(0.0, 0.0);
         if (i < N && j < N) {
@@ -1451,14 +1546,14 @@ struct PauliArgs {
     int count;
 };
 
-__global__ void fill_pauli_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, PauliArgs pa) {
+__global__ void fill_pauli_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, PauliArgs pa, SD sd) {
     const uint32_t M = 1u << logM;
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
          e += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t t = e >> (2 * logM);
         const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
         uint64_t ti, tj;
-        tri_loose(t, ti, tj);
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
         const uint64_t i = ti * M + r, j = tj * M + c;
         double2 acc = make_double2(0.0, 0.0);
         if (i < N && j < N) {
@@ -1496,9 +1591,52 @@ struct hs_state {
     double* red = nullptr;  // reduction scratch: 2 * RED_BLOCKS partials + result
     double2* kraus = nullptr;  // device buffer for k = 3 Kraus operators
     size_t kraus_cap = 0;
+    // sharding (XOR blocks): 2^Plog shards of 2^logB tile rows per block; this is shard `shard`
+    uint32_t Plog = 0, logB = 0, shard = 0;
+    double2* recv = nullptr;  // partner shard payload for cross-shard operations
+    uint64_t recv_count = 0;
+    void* comm = nullptr;     // ncclComm_t
 };
 
 namespace {
+
+// NCCL, loaded on first use (the engine itself does not depend on it): whichever libnccl.so.2 the
+// process already has (PyTorch's bundled one) or the system library.
+struct NcclApi {
+    bool tried = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    if (!api.tried) {
+        api.tried = true;
+        void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (lib) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(lib, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(lib, "ncclCommDestroy");
+            api.Send = (decltype(api.Send))dlsym(lib, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(lib, "ncclRecv");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(lib, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(lib, "ncclGroupEnd");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(lib, "ncclGetErrorString");
+        }
+    }
+    return api;
+}
+
+uint64_t shard_count_of(const hs_state* h, uint32_t shard) {
+    const uint64_t B = 1ull << h->logB, P = 1ull << h->Plog;
+    const uint64_t tiles = shard == 0 ? P * (B * (B + 1) / 2) : (P / 2) * B * B;
+    return tiles * h->M * h->M;
+}
 
 struct DeviceGuard {
     int prev = -1;
@@ -1554,14 +1692,48 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
     G.logNT = 2 * g;
     const uint32_t NT = 1u << (2 * g);
     G.nb = G.G >> g;
+    // sharding: which units this shard works on (local unit enumeration, see unit_decode)
+    G.Plog = h->Plog;
+    G.shard = h->shard;
+    G.logB = h->logB;
+    G.recv = h->recv;
+    G.cross = 0;
+    G.cbit = 0;
+    G.Pulog = h->Plog;
+    G.q = h->shard;
+    if (h->Plog && g) {
+        const uint32_t gbits = ilog2(G.G), top0 = gbits - h->Plog;
+        for (uint32_t l = 0; l < g; ++l)
+            if (G.gr_pos[l] >= top0) {
+                G.cross += 1;
+                G.cbit = G.gr_pos[l] - top0;
+            }
+        if (G.cross == 1) {
+            G.Pulog = h->Plog - 1;
+            G.q = ((h->shard >> (G.cbit + 1)) << G.cbit) | (h->shard & ((1u << G.cbit) - 1));
+        }
+    }
+    G.logBu = ilog2(G.nb) - G.Pulog;
+    {
+        const uint64_t Bu = 1ull << G.logBu, Pu = 1ull << G.Pulog;
+        if (G.Pulog == 0) {
+            G.nU_strict = G.nb * (G.nb - 1) / 2;
+            G.nU_loose = G.nb * (G.nb + 1) / 2;
+        } else if (G.q == 0) {
+            G.nU_strict = Pu * (Bu * (Bu - 1) / 2);
+            G.nU_loose = Pu * (Bu * (Bu + 1) / 2);
+        } else {
+            G.nU_strict = G.nU_loose = (Pu / 2) * Bu * Bu;
+        }
+    }
     if (g == 0) {
         G.offdiag = 0;
-        G.nU_units = G.G * (G.G + 1) / 2;
+        G.nU_units = h->count >> (2 * h->m);  // local tiles
         G.nD_units = 0;
     } else {
         G.offdiag = 1;
-        G.nU_units = G.nb * (G.nb - 1) / 2;
-        G.nD_units = G.nb;
+        G.nU_units = G.nU_strict;
+        G.nD_units = G.q == 0 ? G.nb : 0;
     }
     const uint32_t M = G.M;
     const uint64_t unit_elems = (uint64_t)NT * M * M;
@@ -1720,7 +1892,7 @@ void plan_gather(Geo& G) {
     G.logU = 0;
     G.stage_elems = (NT * G.TS + 7) & ~7u;
     G.stages = 3;
-    G.nG_items = (G.nb * (G.nb - 1) / 2) << (2 * G.log_nsb_side);
+    G.nG_items = G.nU_strict << (2 * G.log_nsb_side);
 }
 
 int sm_count(int device) {
@@ -1738,6 +1910,10 @@ int sm_count(int device) {
 
 template <int K, int MODE, int NS>
 int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+    if (G0.cross > 1)
+        return set_err(HS_ERR_UNSUPPORTED, "operation couples more than one cross-shard qubit");
+    if (G0.cross == 1 && !h->recv)
+        return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the partner shard first");
     Geo G = G0;
     if (MODE != M_KRAUS && G.g >= 2 && G.slabs > 1) {
         // units of 16 / 64 stored tiles: sub-block gather kernel for the off-diagonal units,
@@ -1780,7 +1956,7 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
     if (pipe && G.g >= 1 && G.slabs == 1) {
         // whole-unit items: the pipeline handles the diagonal base pairs as well
         G.pipe_diag = 1;
-        G.nU_units = G.nb * (G.nb + 1) / 2;
+        G.nU_units = G.nU_loose;
         G.nU_items = (G.nU_units + G.U - 1) / G.U;
         G.nD_items = 0;
     }
@@ -1910,7 +2086,7 @@ int hs_device_count(int* out) {
     return HS_OK;
 }
 
-int hs_state_create(int n, int m, int device, hs_state** out) {
+int hs_state_create_sharded(int n, int m, int device, int nshards, int shard, hs_state** out) {
     if (!out)
         return set_err(HS_ERR_INVALID, "null out");
     *out = nullptr;
@@ -1920,6 +2096,11 @@ int hs_state_create(int n, int m, int device, hs_state** out) {
         return set_err(HS_ERR_INVALID, "tile exponent must be in [0, n + 2]");
     if (m > 5)
         return set_err(HS_ERR_UNSUPPORTED, "this build supports tile exponents m <= 5");
+    const uint64_t Gt = (1ull << n) >= (1ull << m) ? (1ull << n) >> m : 1;
+    if (nshards < 1 || (nshards & (nshards - 1)) || (uint64_t)nshards > Gt)
+        return set_err(HS_ERR_INVALID, "shard count must be a power of two <= tiles per grid row");
+    if (shard < 0 || shard >= nshards)
+        return set_err(HS_ERR_RANGE, "shard index out of range");
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev)
@@ -1932,7 +2113,14 @@ int hs_state_create(int n, int m, int device, hs_state** out) {
     h->N = 1ull << n;
     h->M = 1ull << m;
     h->G = h->N >= h->M ? h->N / h->M : 1;
-    h->count = h->G * (h->G + 1) / 2 * h->M * h->M;
+    h->Plog = ilog2((uint64_t)nshards);
+    h->shard = (uint32_t)shard;
+    h->logB = ilog2(h->G) - h->Plog;
+    {
+        const uint64_t B = 1ull << h->logB, P = (uint64_t)nshards;
+        const uint64_t tiles = shard == 0 ? P * (B * (B + 1) / 2) : (P / 2) * B * B;
+        h->count = tiles * h->M * h->M;
+    }
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         delete h;
@@ -1962,6 +2150,10 @@ int hs_state_create(int n, int m, int device, hs_state** out) {
     return HS_OK;
 }
 
+int hs_state_create(int n, int m, int device, hs_state** out) {
+    return hs_state_create_sharded(n, m, device, 1, 0, out);
+}
+
 int hs_state_free(hs_state* h) {
     if (!h)
         return HS_OK;
@@ -1970,6 +2162,9 @@ int hs_state_free(hs_state* h) {
     cudaFree(h->d);
     cudaFree(h->red);
     cudaFree(h->kraus);
+    cudaFree(h->recv);
+    if (h->comm && nccl().CommDestroy)
+        nccl().CommDestroy((ncclComm_t)h->comm);
     if (h->own_stream)
         cudaStreamDestroy(h->stream);
     delete h;
@@ -1987,6 +2182,135 @@ int hs_state_info(const hs_state* h, int* n, int* m, uint64_t* count, uint64_t* 
         *count = h->count;
     if (grid)
         *grid = h->G;
+    return HS_OK;
+}
+
+int hs_state_shard_info(const hs_state* h, int* nshards, int* shard, uint64_t* block_rows) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (nshards)
+        *nshards = 1 << h->Plog;
+    if (shard)
+        *shard = (int)h->shard;
+    if (block_rows)
+        *block_rows = 1ull << h->logB;
+    return HS_OK;
+}
+
+int hs_op_partner(const hs_state* h, int k, const uint32_t* targets, int* partner) {
+    if (!h || !targets || !partner || k < 1 || k > 3)
+        return set_err(HS_ERR_INVALID, "bad arguments");
+    *partner = -1;
+    if (!h->Plog)
+        return HS_OK;
+    const uint32_t gbits = ilog2(h->G), top0 = h->m + gbits - h->Plog;  // qubit index of the lowest top bit
+    int found = -1;
+    for (int i = 0; i < k; ++i) {
+        if (targets[i] >= (uint32_t)h->n)
+            return set_err(HS_ERR_RANGE, "target qubit out of range");
+        if (targets[i] >= top0) {
+            if (found >= 0)
+                return set_err(HS_ERR_UNSUPPORTED, "operation couples more than one cross-shard qubit");
+            found = (int)(targets[i] - top0);
+        }
+    }
+    if (found >= 0)
+        *partner = (int)(h->shard ^ (1u << found));
+    return HS_OK;
+}
+
+int hs_state_recv_alloc(hs_state* h) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (h->recv)
+        return HS_OK;
+    DeviceGuard dg(h->device);
+    const uint64_t cnt = shard_count_of(h, 0);  // the largest shard
+    cudaError_t e = cudaMalloc(&h->recv, cnt * sizeof(double2));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        h->recv = nullptr;
+        return set_err(HS_ERR_NOMEM, std::string("cudaMalloc exchange buffer: ") + cudaGetErrorString(e));
+    }
+    h->recv_count = cnt;
+    return HS_OK;
+}
+
+// In-process / single-node exchange: recv <- peer payload (device or peer copy, stream-ordered).
+int hs_state_exchange_from(hs_state* h, const hs_state* peer) {
+    if (!h || !peer)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (peer->Plog != h->Plog || peer->n != h->n || peer->m != h->m)
+        return set_err(HS_ERR_INVALID, "peer is not a shard of the same operator");
+    int rc = hs_state_recv_alloc(h);
+    if (rc)
+        return rc;
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaStreamSynchronize(peer->stream));
+    if (peer->device == h->device)
+        CUDA_TRY(cudaMemcpyAsync(h->recv, peer->d, peer->count * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
+    else
+        CUDA_TRY(cudaMemcpyPeerAsync(h->recv, h->device, peer->d, peer->device, peer->count * sizeof(double2),
+                                     h->stream));
+    return HS_OK;
+}
+
+int hs_nccl_unique_id(void* id128) {
+    if (!id128)
+        return set_err(HS_ERR_INVALID, "null out");
+    NcclApi& api = nccl();
+    if (!api.GetUniqueId)
+        return set_err(HS_ERR_UNSUPPORTED, "libnccl.so.2 not available");
+    ncclUniqueId id;
+    const ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess)
+        return set_err(HS_ERR_CUDA, std::string("ncclGetUniqueId: ") + api.GetErrorString(r));
+    std::memcpy(id128, &id, sizeof(id));
+    return HS_OK;
+}
+
+int hs_state_comm_init(hs_state* h, const void* id128, int nranks, int rank) {
+    if (!h || !id128)
+        return set_err(HS_ERR_INVALID, "null argument");
+    if (nranks != (1 << h->Plog) || rank != (int)h->shard)
+        return set_err(HS_ERR_INVALID, "communicator ranks must be the shards (rank == shard)");
+    NcclApi& api = nccl();
+    if (!api.CommInitRank)
+        return set_err(HS_ERR_UNSUPPORTED, "libnccl.so.2 not available");
+    DeviceGuard dg(h->device);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm;
+    const ncclResult_t r = api.CommInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess)
+        return set_err(HS_ERR_CUDA, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+    h->comm = comm;
+    return HS_OK;
+}
+
+// NCCL pairwise exchange over NVLink: send the whole local shard, receive the partner's into recv.
+int hs_state_exchange(hs_state* h, int partner) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (!h->comm)
+        return set_err(HS_ERR_INVALID, "no communicator: call hs_state_comm_init");
+    if (partner < 0 || partner >= (1 << h->Plog) || partner == (int)h->shard)
+        return set_err(HS_ERR_RANGE, "bad partner shard");
+    int rc = hs_state_recv_alloc(h);
+    if (rc)
+        return rc;
+    NcclApi& api = nccl();
+    DeviceGuard dg(h->device);
+    const uint64_t pc = shard_count_of(h, (uint32_t)partner);
+    ncclComm_t comm = (ncclComm_t)h->comm;
+    ncclResult_t r = api.GroupStart();
+    if (r == ncclSuccess)
+        r = api.Send(h->d, h->count * 2, ncclDouble, partner, comm, h->stream);
+    if (r == ncclSuccess)
+        r = api.Recv(h->recv, pc * 2, ncclDouble, partner, comm, h->stream);
+    const ncclResult_t r2 = api.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return set_err(HS_ERR_CUDA, std::string("NCCL exchange: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
     return HS_OK;
 }
 
@@ -2375,8 +2699,11 @@ static int reduce(const hs_state* a, const hs_state* b, int kind, double* out) {
     DeviceGuard dg(a->device);
     if (b != a)
         CUDA_TRY(cudaStreamSynchronize(b->stream));
-    const uint64_t ntiles = a->G * (a->G + 1) / 2;
-    reduce_kernel<<<RED_BLOCKS, NTHR, 0, a->stream>>>(a->d, b->d, ntiles, (uint32_t)a->m, kind, a->red);
+    if (a->Plog != b->Plog || a->shard != b->shard)
+        return set_err(HS_ERR_INVALID, "expectation: operands are different shards");
+    const uint64_t ntiles = a->count >> (2 * a->m);
+    reduce_kernel<<<RED_BLOCKS, NTHR, 0, a->stream>>>(a->d, b->d, ntiles, (uint32_t)a->m, kind, a->red,
+                                                       SD{a->Plog, a->logB, a->shard});
     finish_kernel<<<1, 32, 0, a->stream>>>(a->red, RED_BLOCKS, kind, a->red + 2 * RED_BLOCKS);
     g_launches.fetch_add(2, std::memory_order_relaxed);
     CUDA_TRY(cudaGetLastError());
@@ -2386,6 +2713,13 @@ static int reduce(const hs_state* a, const hs_state* b, int kind, double* out) {
 }
 
 int hs_expectation(const hs_state* rho, const hs_state* obs, double* out) { return reduce(obs, rho, 0, out); }
+// Linear partial sums of one shard (kind 0: tr(rho O) part, 1: squared Frobenius part, 2: trace part);
+// the operator's value is the sum over shards.
+int hs_reduce_partial(const hs_state* a, const hs_state* b, int kind, double* out) {
+    if (kind < 0 || kind > 2)
+        return set_err(HS_ERR_INVALID, "bad reduction kind");
+    return reduce(a, b ? b : a, kind, out);
+}
 int hs_frobenius(const hs_state* h, double* out) {
     int rc = reduce(h, h, 1, out);
     if (!rc)
@@ -2404,7 +2738,8 @@ int hs_state_fill_mixture(hs_state* h, int rank, const double* psi) {
     CUDA_TRY(cudaMalloc(&dpsi, bytes));
     CUDA_TRY(cudaMemcpyAsync(dpsi, psi, bytes, cudaMemcpyHostToDevice, h->stream));
     const double inv = 1.0 / rank;
-    fill_mixture_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, dpsi, rank, inv);
+    fill_mixture_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, dpsi, rank, inv,
+                                                          SD{h->Plog, h->logB, h->shard});
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     cudaStreamSynchronize(h->stream);
@@ -2433,7 +2768,8 @@ int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uin
         CUDA_TRY(cudaMemcpyAsync(dn, ny, count * 4, cudaMemcpyHostToDevice, h->stream));
     }
     PauliArgs pa{dx, dz, dn, dc, count};
-    fill_pauli_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, pa);
+    fill_pauli_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, pa,
+                                                        SD{h->Plog, h->logB, h->shard});
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     cudaStreamSynchronize(h->stream);
@@ -2453,7 +2789,7 @@ int hs_state_distance_mixture(const hs_state* h, int rank, const double* psi, do
     CUDA_TRY(cudaMalloc(&dpsi, bytes));
     CUDA_TRY(cudaMemcpyAsync(dpsi, psi, bytes, cudaMemcpyHostToDevice, h->stream));
     dist_mixture_kernel<<<RED_BLOCKS, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, dpsi, rank,
-                                                             1.0 / rank, h->red);
+                                                             1.0 / rank, h->red, SD{h->Plog, h->logB, h->shard});
     g_launches.fetch_add(1, std::memory_order_relaxed);
     std::vector<double> part(RED_BLOCKS);
     cudaError_t e = cudaGetLastError();

@@ -61,10 +61,13 @@ class TiledHermitian:
 
     default_tile_exp = 5
 
-    def __init__(self, n_qubits: int, tile_exp: int = 5, device: int = 0):
+    def __init__(self, n_qubits: int, tile_exp: int = 5, device: int = 0, nshards: int = 1, shard: int = 0):
+        """nshards > 1: this object holds shard `shard` of the operator (multigpu.py)."""
         L = nat.engine()
         h = ctypes.c_void_p()
-        nat.check(L.hs_state_create(n_qubits, tile_exp, device, ctypes.byref(h)), "TiledHermitian")
+        nat.check(L.hs_state_create_sharded(n_qubits, tile_exp, device, nshards, shard, ctypes.byref(h)),
+                  "TiledHermitian")
+        self.nshards, self.shard = nshards, shard
         self._h = h
         self._n, self._m = n_qubits, tile_exp
         cnt, grid = ctypes.c_uint64(), ctypes.c_uint64()
