@@ -211,6 +211,7 @@ struct ApplyPlan {
     KernelPath path = KernelPath::dense_generic;
     ActiveQubits targets;
     SubcaseCounters subcases;
+    std::uint64_t touched_bytes = 0;  // HBM bytes the launch reads + writes (algorithmic); extension
 };
 
 ApplyPlan apply(TiledHermitian& h, const ChannelSpec& spec, std::span<const std::uint32_t> targets,

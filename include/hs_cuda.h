@@ -85,6 +85,8 @@ typedef struct hs_plan {
 typedef struct hs_state hs_state;
 
 const char* hs_last_error(void);
+/* Calling thread: fill hs_plan.subcases (host-side enumeration for k = 2) or not (default 1). */
+int hs_set_plan_subcases(int enable);
 const char* hs_version(void);
 int hs_device_count(int* out);
 

@@ -68,6 +68,7 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_version", ctypes.c_char_p, [])
     _sig(L, "hs_device_count", i, [c_int_p])
     _sig(L, "hs_launch_count", u64, [])
+    _sig(L, "hs_set_plan_subcases", i, [i])
     _sig(L, "hs_state_create", i, [i, i, i, pp])
     _sig(L, "hs_state_free", i, [vp])
     _sig(L, "hs_state_info", i, [vp, c_int_p, c_int_p, c_u64_p, c_u64_p])

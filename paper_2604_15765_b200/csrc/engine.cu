@@ -55,6 +55,7 @@ constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, 
 enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5 };
 
 thread_local std::string g_err;
+thread_local bool g_plan_subcases = true;  // hs_set_plan_subcases
 std::atomic<uint64_t> g_launches{0};
 
 int set_err(int code, const std::string& msg) {
@@ -2056,7 +2057,8 @@ int finish_plan(hs_state* h, const Geo& G, int k, const uint32_t* t, int path, h
     plan->grid_bits = (int)G.g;
     plan->launches = (G.nD_items + G.nU_items) ? 1 : 0;
     plan->touched_bytes = touched;
-    count_subcases(h, G, plan->subcases);
+    if (g_plan_subcases)
+        count_subcases(h, G, plan->subcases);
     return HS_OK;
 }
 
@@ -2076,6 +2078,10 @@ int generic_path(const Geo& G) {
 extern "C" {
 
 const char* hs_last_error(void) { return g_err.c_str(); }
+int hs_set_plan_subcases(int enable) {
+    g_plan_subcases = enable != 0;
+    return HS_OK;
+}
 const char* hs_version(void) { return "hermsim_b200 0.1 (sm_100a)"; }
 uint64_t hs_launch_count(void) { return g_launches.load(); }
 

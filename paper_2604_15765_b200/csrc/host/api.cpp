@@ -227,30 +227,39 @@ ApplyPlan apply_on_handle(hs_state* hs, const ChannelSpec& spec, std::span<const
     ApplyPlan plan;
     plan.targets = bc.qubits;
     hs_plan p{};
-    hs_plan* pp = opts.count_subcases ? &p : nullptr;
+    hs_plan* pp = &p;
+    hs_set_plan_subcases(opts.count_subcases ? 1 : 0);
+    struct Restore {
+        ~Restore() { hs_set_plan_subcases(1); }
+    } restore;
     if (opts.allow_native) {
         switch (spec.kind) {
         case GateKind::pauli_x:
             check(hs_apply_pauli(hs, tq[0], 0, pp), "apply");
             plan.path = KernelPath::native_pauli_x;
+            plan.touched_bytes = p.touched_bytes;
             return plan;
         case GateKind::pauli_y:
             check(hs_apply_pauli(hs, tq[0], 1, pp), "apply");
             plan.path = KernelPath::native_pauli_y;
+            plan.touched_bytes = p.touched_bytes;
             return plan;
         case GateKind::diagonal_phase:
             check(hs_apply_diagonal_phase(hs, tq[0], dptr(bc.phases.data()), pp), "apply");
             plan.path = KernelPath::native_phase;
+            plan.touched_bytes = p.touched_bytes;
             return plan;
         case GateKind::hadamard:
             check(hs_apply_hadamard(hs, tq[0], pp), "apply");
             plan.path = KernelPath::native_hadamard;
+            plan.touched_bytes = p.touched_bytes;
             return plan;
         case GateKind::permutation:
             if (bc.perm.size() != (std::size_t{1} << k))
                 throw std::invalid_argument("apply_permutation: bad permutation table size");
             check(hs_apply_permutation(hs, k, bc.perm.data(), tq, pp), "apply");
             plan.path = KernelPath::native_permutation;
+            plan.touched_bytes = p.touched_bytes;
             return plan;
         case GateKind::generic_kraus:
             break;
@@ -278,8 +287,9 @@ ApplyPlan apply_on_handle(hs_state* hs, const ChannelSpec& spec, std::span<const
     for (int i = 0; i < k; ++i)
         grid += tq[i] >= m;
     plan.path = grid == 0 ? KernelPath::tiled_intra : grid == k ? KernelPath::tiled_cross : KernelPath::tiled_mixed;
-    if (pp && (k <= 2) && grid > 0)
+    if (opts.count_subcases && (k <= 2) && grid > 0)
         plan.subcases = counters(p);
+    plan.touched_bytes = p.touched_bytes;
     return plan;
 }
 

@@ -210,6 +210,7 @@ int hb_apply(hs_state* h, const hb_channel* ch, const uint32_t* targets, int nta
             plan->subcases[0] = p.subcases.cross_tile;
             plan->subcases[1] = p.subcases.cross_tile_adj;
             plan->subcases[2] = p.subcases.cross_tile_diag;
+            plan->touched_bytes = p.touched_bytes;
         }
         return HS_OK;
     });

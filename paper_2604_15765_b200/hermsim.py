@@ -307,6 +307,7 @@ class ApplyPlan:
     path: str
     targets: tuple
     subcases: tuple = field(default=(0, 0, 0))
+    touched_bytes: int = 0  # HBM bytes read + written by the launch (extension of the reference plan)
 
 
 def apply(h: TiledHermitian, spec: ChannelSpec, targets, opts: ApplyOptions | None = None) -> ApplyPlan:
@@ -316,7 +317,8 @@ def apply(h: TiledHermitian, spec: ChannelSpec, targets, opts: ApplyOptions | No
     plan = nat.HsPlan()
     nat.check(nat.engine().hb_apply(h.handle, spec._c, tgp, len(tg), 1 if opts.allow_native else 0,
                                     1 if opts.count_subcases else 0, ctypes.byref(plan)), "apply", facade=True)
-    return ApplyPlan(KERNEL_PATHS[plan.path], tuple(plan.targets[: plan.k]), tuple(plan.subcases))
+    return ApplyPlan(KERNEL_PATHS[plan.path], tuple(plan.targets[: plan.k]), tuple(plan.subcases),
+                     int(plan.touched_bytes))
 
 
 def expectation(rho: TiledHermitian, obs: TiledHermitian) -> float:
