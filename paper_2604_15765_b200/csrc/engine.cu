@@ -107,8 +107,12 @@ struct Geo {
     uint32_t stage_elems; // elements per stage buffer
     uint16_t cdir[64], cadj[64];  // component offsets from the unit base (direct / adjoint orientation)
     uint8_t ttr[64];              // logical tile (R * NG + C) of each component
+    uint32_t A;                   // logical tiles staged per unit (monomials skip untouched ones)
+    uint8_t slot[64];             // logical tile -> staging slot within its unit
     uint32_t diag_map;            // transform walks 8x8 position blocks diagonally
     uint32_t pipe_diag;           // pipeline also owns the diagonal units (whole-tile items)
+    uint32_t groups;              // > 0: an item is (unit, tile group) of a tile permutation
+    uint64_t gmask[16];           // logical tiles of each group
     uint32_t PD;                  // row pitch of a direct logical tile in shared memory
     uint32_t logical;             // adjoint tiles staged transposed (logical layout, gather kernel)
     // gather kernel (square sub-blocks of S0 x S0 positions, g >= 2)
@@ -139,6 +143,10 @@ struct Coef {
     uint8_t cyc[64];
     uint8_t cyc_off[66];
     uint32_t ncyc;
+    // tile permutations (every target a grid bit): cycles grouped into <= 4-tile item groups;
+    // group g owns cycles [gcyc_off[g], gcyc_off[g + 1])
+    uint8_t gcyc_off[17];
+    uint32_t ngroups;
 };
 
 uint32_t pdep(uint32_t v, uint32_t mask) {
@@ -837,7 +845,8 @@ constexpr int MAX_STAGES = 4;
 // Fills the item's logical-tile table: stored tile index | F_ADJ / F_SKIP / F_BAD.
 template <int MODE>
 __device__ __forceinline__ void item_tiles(const Geo& G, uint64_t item, uint64_t* gt, uint32_t lane) {
-    const uint64_t u0 = (item >> G.logSlabs) << G.logU;
+    const uint32_t grp = G.groups ? (uint32_t)(item % G.groups) : 0;
+    const uint64_t u0 = G.groups ? item / G.groups : (item >> G.logSlabs) << G.logU;
     const uint32_t ntt = G.U << G.logNT, NGm = (1u << G.logNG) - 1;
     for (uint32_t i = lane; i < ntt; i += 32) {
         const uint32_t uu = i >> G.logNT, lt = i & ((1u << G.logNT) - 1);
@@ -858,7 +867,7 @@ __device__ __forceinline__ void item_tiles(const Geo& G, uint64_t item, uint64_t
             if (tbi == tbj && (lt >> G.logNG) < (lt & NGm))
                 ent |= F_NOSTORE;
         }
-        if (MODE == M_MONO && !((G.active >> lt) & 1ull))
+        if (MODE == M_MONO && (!((G.active >> lt) & 1ull) || (G.groups && !((G.gmask[grp] >> lt) & 1ull))))
             ent |= F_SKIP;
         gt[i] = ent;
     }
@@ -879,7 +888,8 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
             if ((ent & (F_BAD | F_SKIP)) || (STORE && (ent & F_NOSTORE)))
                 continue;
             const uint64_t gbase = (ent & F_MASK) << (2 * G.logM);
-            const uint32_t tsm = sbase + tt * G.TS * 16u;
+            const uint32_t tsm =
+                sbase + ((tt >> G.logNT) * G.A + G.slot[tt & ((1u << G.logNT) - 1)]) * G.TS * 16u;
             if (STORE)
                 bulk_s2g(st + gbase, tsm, bytes);
             else
@@ -892,7 +902,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
         if ((ent & (F_BAD | F_SKIP)) || (STORE && (ent & F_NOSTORE)))
             continue;
         const uint64_t gbase = (ent & F_MASK) << (2 * G.logM);
-        const uint32_t tsm = sbase + tt * G.TS * 16u;
+        const uint32_t tsm = sbase + ((tt >> G.logNT) * G.A + G.slot[tt & ((1u << G.logNT) - 1)]) * G.TS * 16u;
         const double2* src = (ent & F_REMOTE) ? G.recv : st;
         if (!(ent & F_ADJ)) {
             for (uint32_t r = lane; r < G.nruns; r += 32) {
@@ -963,7 +973,7 @@ __device__ __forceinline__ CBlk cblk(const Geo& G, const Tabs& T, const uint64_t
     }
     const uint32_t xs = T.xb[xbi], y = T.yb[ybi];
     CBlk c;
-    c.ub = (uu << G.logNT) * G.TS;
+    c.ub = uu * G.A * G.TS;
     c.d0 = xs * G.PD + y;
     c.a0 = G.logical ? c.d0 : y * G.SRp + xs;
     c.am = G.g ? am_tab[uu] : 0ull;
@@ -987,7 +997,7 @@ __device__ __forceinline__ void stc(double2* sb, uint32_t a, bool cj, double2 v)
 
 template <int K, int MODE, int NS, int NC = NCONS>
 __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const Coef<NS>& cf, const uint64_t* am,
-                                             uint32_t nvalid_units, double2* sb) {
+                                             uint32_t nvalid_units, double2* sb, uint32_t grp = 0) {
     constexpr int D = 1 << K;
     const int tid = threadIdx.x;
     const uint32_t nblk = G.U << (G.logNxb + G.logNyb);
@@ -1104,10 +1114,11 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
         }
     } else if constexpr (MODE == M_MONO) {
         // in-place cycles of the component map; untouched components cost nothing
-        const uint32_t nc = cf.ncyc;
+        const uint32_t cbeg = G.groups ? cf.gcyc_off[grp] : 0;
+        const uint32_t nc = G.groups ? cf.gcyc_off[grp + 1] - cbeg : cf.ncyc;
         const uint32_t items = nblk * nc;
         for (uint32_t w = tid; w < items; w += NC) {
-            const uint32_t b = (w & lomask) | (((w >> lo) / nc) << lo), ci = (w >> lo) % nc;
+            const uint32_t b = (w & lomask) | (((w >> lo) / nc) << lo), ci = cbeg + (w >> lo) % nc;
             uint32_t uu;
             const CBlk c = cblk(G, T, am, b, uu);
             if (uu >= nvalid_units)
@@ -1250,10 +1261,11 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
         const uint32_t s = (uint32_t)(i % S);
         double2* sb = ring + (size_t)s * G.stage_elems;
         const uint64_t item = blockIdx.x + i * gridDim.x;
-        const uint64_t u0 = (item >> G.logSlabs) << G.logU;
+        const uint32_t grp = G.groups ? (uint32_t)(item % G.groups) : 0;
+        const uint64_t u0 = G.groups ? item / G.groups : (item >> G.logSlabs) << G.logU;
         const uint32_t nvalid = G.nU_units - u0 < G.U ? (uint32_t)(G.nU_units - u0) : G.U;
         mbar_wait(&full[s], (uint32_t)((i / S) & 1));
-        pipe_compute<K, MODE, NS>(G, T, cf, am[s], nvalid, sb);
+        pipe_compute<K, MODE, NS>(G, T, cf, am[s], nvalid, sb, grp);
         fence_async_smem();
         __syncwarp();
         if (lane == 0)
@@ -1833,10 +1845,101 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
             G.cdir[i] = (uint16_t)((R * NG + C) * G.TS + xs * M + y);
             G.cadj[i] = (uint16_t)((R * NG + C) * G.TS + y * G.SRp + xs);
         }
+    G.A = NT;
+    for (uint32_t t = 0; t < 64; ++t)
+        G.slot[t] = (uint8_t)t;
     G.stage_elems = ((G.U << G.logNT) * G.TS + 7) & ~7u;
     const uint32_t budget = 200u * 1024u / 16u;  // elements of shared memory for the ring
     G.stages = std::min<uint32_t>(MAX_STAGES, budget / G.stage_elems);
     (void)extra_buffers;
+}
+
+// Tile permutations (all targets are grid bits, kin == 0): every component is a whole logical tile,
+// so each unit splits into independent groups of <= 4 tiles closed under the permutation's cycles
+// (G.gmask, host-built).  Whole stored tiles are staged (one 16 KiB bulk copy each); a tile's slot is
+// its rank within its group, so one component-offset table serves every group.
+void plan_grouped(Geo& G) {
+    const uint32_t M = G.M, NT = 1u << G.logNT;
+    G.SR = M;
+    G.logSR = G.logM;
+    G.slabs = 1;
+    G.logSlabs = 0;
+    G.U = 1;
+    G.logU = 0;
+    for (uint32_t i = 0; i < 32; ++i) {
+        G.xdep[i] = (uint8_t)(i < M ? i : 0);
+        G.xb_tab[i] = G.yb_tab[i] = (uint8_t)(i < M ? i : 0);
+    }
+    G.sdep[0] = 0;
+    G.nruns = 1;
+    G.run_xs[0] = 0;
+    G.run_len[0] = (uint8_t)M;
+    G.nxb = G.nyb = M;
+    G.logNxb = G.logNyb = G.logM;
+    for (uint32_t r = 0; r < 8; ++r)
+        G.xs_in[r] = G.y_in[r] = 0;
+    G.SRp = M;
+    G.PD = M;
+    G.logical = 0;
+    G.TS = M * M;
+    uint32_t A = 1;
+    for (uint32_t gi = 0; gi < G.groups; ++gi) {
+        uint32_t r = 0;
+        for (uint32_t t = 0; t < NT; ++t)
+            if ((G.gmask[gi] >> t) & 1ull)
+                G.slot[t] = (uint8_t)r++;
+        A = std::max(A, r);
+    }
+    G.A = A;
+    const uint32_t D = G.D, NG = 1u << G.g;
+    for (uint32_t rho = 0; rho < D; ++rho)
+        for (uint32_t gam = 0; gam < D; ++gam) {
+            const uint32_t i = rho * D + gam;
+            G.ttr[i] = (uint8_t)(rho * NG + gam);
+            G.cdir[i] = G.cadj[i] = (uint16_t)(G.slot[G.ttr[i]] * G.TS);
+        }
+    G.diag_map = (M >= 8) ? 1 : 0;
+    // diagonal units alias logical (R, C) and (C, R) across groups: they stay on the wedge path
+    G.pipe_diag = 0;
+    G.nU_units = G.nU_strict;
+    G.nU_items = G.nU_units * G.groups;
+    G.stage_elems = (A * G.TS + 7) & ~7u;
+    const uint32_t budget = 200u * 1024u / 16u;
+    G.stages = std::min<uint32_t>(MAX_STAGES, budget / G.stage_elems);
+}
+
+// Monomials leave whole logical tiles untouched (a phase on a grid qubit: half of them): stage only
+// the active ones, packed, and put more units in an item so each item still moves ~64 KiB.
+void compact_pipe(Geo& G) {
+    const uint32_t NT = 1u << G.logNT;
+    const uint64_t all = NT >= 64 ? ~0ull : ((1ull << NT) - 1);
+    if ((G.active & all) == all || G.SR != G.M)
+        return;
+    uint32_t A = 0;
+    for (uint32_t t = 0; t < NT; ++t)
+        G.slot[t] = (G.active >> t) & 1ull ? (uint8_t)A++ : 0;
+    if (A == 0)
+        return;
+    G.A = A;
+    const uint32_t kinm = (1u << G.kin) - 1, D = G.D;
+    for (uint32_t rho = 0; rho < D; ++rho)
+        for (uint32_t gam = 0; gam < D; ++gam) {
+            const uint32_t i = rho * D + gam, sl = G.slot[G.ttr[i]];
+            const uint32_t xs = G.xs_in[rho & kinm], y = G.y_in[gam & kinm];
+            G.cdir[i] = (uint16_t)(sl * G.TS + xs * G.M + y);
+            G.cadj[i] = (uint16_t)(sl * G.TS + y * G.SRp + xs);
+        }
+    const uint64_t unit_elems = (uint64_t)A * G.M * G.M;
+    uint32_t U = 1;
+    while ((uint64_t)(2 * U) * unit_elems <= CAP_WHOLE && (2 * U) * NT <= MAX_TT && 2 * U <= MAX_UA)
+        U *= 2;
+    G.U = U;
+    G.logU = ilog2(U);
+    G.nU_items = (G.nU_units + U - 1) / U;
+    G.nxb = G.M >> G.kin;  // unchanged block structure; only the unit count per item moves
+    G.stage_elems = ((uint32_t)(U * unit_elems) + 7) & ~7u;
+    const uint32_t budget = 200u * 1024u / 16u;
+    G.stages = std::min<uint32_t>(MAX_STAGES, budget / G.stage_elems);
 }
 
 size_t smem_bytes(const Geo& G, int buffers) {
@@ -1916,6 +2019,41 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
     if (G0.cross == 1 && !h->recv)
         return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the partner shard first");
     Geo G = G0;
+    if (MODE == M_MONO && G.groups) {
+        // tile permutation on >= 2 grid bits: whole-tile pipeline, items = (unit, cycle group);
+        // diagonal units through the slab kernel's wedge path
+        cudaError_t e;
+        if (G.nD_items) {
+            Geo Gs = G;
+            Gs.nU_items = 0;
+            Gs.Epad = 0;
+            const size_t smem = smem_bytes(Gs, buffers);
+            auto kd = conj_kernel<K, MODE, NS>;
+            e = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+            kd<<<(unsigned)G.nD_items, NTHR, smem, h->stream>>>(Gs, cf, ka, h->d);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            e = cudaGetLastError();
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
+        }
+        plan_grouped(G);
+        const size_t smem = (size_t)G.stages * G.stage_elems * sizeof(double2);
+        auto kern = pipe_kernel<K, MODE, NS>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess)
+            return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(pipe): ") + cudaGetErrorString(e));
+        if (G.nU_items) {
+            const uint64_t grid = std::min<uint64_t>(G.nU_items, (uint64_t)sm_count(h->device));
+            kern<<<(unsigned)grid, NTHR_PIPE, smem, h->stream>>>(G, cf, h->d);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            e = cudaGetLastError();
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("pipe_kernel launch: ") + cudaGetErrorString(e));
+        }
+        return HS_OK;
+    }
     if (MODE != M_KRAUS && G.g >= 2 && G.slabs > 1) {
         // units of 16 / 64 stored tiles: sub-block gather kernel for the off-diagonal units,
         // the slab kernel's wedge path for the diagonal ones
@@ -1961,6 +2099,8 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         G.nU_items = (G.nU_units + G.U - 1) / G.U;
         G.nD_items = 0;
     }
+    if (pipe)
+        compact_pipe(G);
     cudaError_t e;
     // slab kernel: diagonal units (path D) and, when the pipeline does not apply, path U too
     const uint64_t nU_slab = pipe ? 0 : G.nU_items;
@@ -2644,6 +2784,44 @@ int hs_apply_monomial(hs_state* h, int k, const uint32_t* perm, const double* di
                 active |= 1ull << (R * NG + C);
         }
     G.active = active;
+    G.groups = 0;
+    cf.ngroups = 0;
+    if (G.kin == 0 && G.g >= 2 && G.M >= 2) {
+        // a tile permutation: pack the tile cycles into groups of <= 4 tiles (component index ==
+        // logical tile index when every target is a grid bit)
+        uint32_t ng = 0, fill = 0;
+        uint64_t mask = 0;
+        bool ok = true;
+        cf.gcyc_off[0] = 0;
+        for (uint32_t ci = 0; ci < cf.ncyc && ok; ++ci) {
+            const uint32_t len = cf.cyc_off[ci + 1] - cf.cyc_off[ci];
+            if (len > 4) {
+                ok = false;
+                break;
+            }
+            if (fill + len > 4) {
+                G.gmask[ng] = mask;
+                cf.gcyc_off[++ng] = (uint8_t)ci;
+                fill = 0;
+                mask = 0;
+                if (ng >= 16) {
+                    ok = false;
+                    break;
+                }
+            }
+            for (uint32_t j = 0; j < len; ++j)
+                mask |= 1ull << cf.cyc[cf.cyc_off[ci] + j];
+            fill += len;
+        }
+        if (ok && fill) {
+            G.gmask[ng] = mask;
+            cf.gcyc_off[++ng] = (uint8_t)cf.ncyc;
+        }
+        if (ok && ng >= 1 && ng <= 16) {
+            G.groups = ng;
+            cf.ngroups = ng;
+        }
+    }
     KrausArgs ka{nullptr, 0};
     if (active != 0) {
         if (k == 1)
