@@ -19,8 +19,10 @@ stored).  A step = one pass of the 32 channel applications.
 * cpu_baseline  the reference library itself (oracle/_ref/libhermsim_ref.so, built from
              /root/reference) timed on this host on a bounded sample of the same workload.
 * --impl reference  times that reference CPU path alone, all host threads (rank 0 only).
-For N > 1 (torchrun) every rank runs an independent replica (the path shards only for states that
-do not fit one GPU), so scaling is weak.
+For N > 1 (torchrun) every rank runs an independent replica of the config (weak scaling) -- except
+with --shard (the default for c4, the sharded n = 17 config): the operator is partitioned into N XOR-
+block shards, one per GPU, cross-shard ops exchange over NCCL inside the engine, and the whole job
+processes one operator (strong scaling; value = ops of the operator per second).
 """
 from __future__ import annotations
 
@@ -280,6 +282,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--shard", dest="shard", action="store_true", default=None,
+                    help="partition the operator over the N ranks (default for c4 when N > 1)")
+    ap.add_argument("--replicas", dest="shard", action="store_false", help="N independent replicas")
     args = ap.parse_args()
 
     from paper_2604_15765_b200 import harness as HS
@@ -333,14 +338,23 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     L = nat.engine()
 
     seed = HS.SEEDS[cfg]
-    st = H.TiledHermitian(n, m, device=local)
-    S = st.element_count() * 16
+    sharded = world > 1 and (args.shard if args.shard is not None else cfg == "c4")
+    if sharded:
+        from paper_2604_15765_b200.multigpu import DistributedShard
+        dshard = DistributedShard(n, m, device=local)
+        st = dshard.state
+        apply_op = dshard.apply
+    else:
+        st = H.TiledHermitian(n, m, device=local)
+        apply_op = lambda spec, tg, o: H.apply(st, spec, tg, o)  # noqa: E731
+    S = st.element_count() * 16  # this rank's stored bytes
     psi = None
     strings = None
     if cfg == "c3":
         strings = HS.pauli_strings(n, 64, seed)
         st.fill_pauli_sum(*strings)
-        rho = H.TiledHermitian(n, m, device=local)
+        drho = DistributedShard(n, m, device=local) if sharded else None
+        rho = drho.state if sharded else H.TiledHermitian(n, m, device=local)
         psi = HS.rank_psi(n, seed + 1, 4)
         rho.fill_mixture(psi)
     else:
@@ -360,7 +374,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
         for i, (spec, tg, _) in enumerate(ops):
             if record:
                 L.hs_event_record(ev[2 + 2 * i], st.handle)
-            plan = H.apply(st, spec, tg, opts)
+            plan = apply_op(spec, tg, opts)
             if collect:
                 touched[i] = plan.touched_bytes
             if record:
@@ -394,7 +408,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     dist_barrier(world)
     total_ms = dist_max(total_ms, world)
     ms_per_step = total_ms / args.steps
-    value = world * nops * args.steps / (total_ms / 1e3)
+    value = (1 if sharded else world) * nops * args.steps / (total_ms / 1e3)
 
     # roofline of the dominant kernel (conj_kernel): bytes per launch / mean launch time
     peak, peak_src = load_peaks()
@@ -407,7 +421,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     traffic, traffic_src = load_traffic(cfg)
     result = {}
     if cfg == "c3":
-        result["tr_rho_O"] = H.expectation(rho, st)
+        result["tr_rho_O"] = drho.reduce(dshard, 0) if sharded else H.expectation(rho, st)
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -429,7 +443,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
             if s >= 1:
                 e_ms.append(float(x.value))
         e2e_ms = dist_max(float(np.mean(e_ms)), world)
-        e2e = {"value": world * nops / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": S,
+        e2e = {"value": (1 if sharded else world) * nops / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": S,
                "d2h_bytes_per_step": S, "ms_per_step": e2e_ms, "steps": len(e_ms),
                "path": "hb_apply via paper_2604_15765_b200.hermsim.apply + hs_state_upload/download_async"}
         if rank == 0 and world == 1 and not args.no_cpu:
@@ -448,10 +462,13 @@ def ours_arm(args, cfg, n, m, world, rank, local):
         return 0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded rank-4 rho / Pauli-sum O of BASELINE.json shapes)",
         "config": {"workload": WORKLOADS[cfg], "config": cfg, "n": n, "m": m, "ops_per_step": nops,
-                   "stored_bytes": S, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "stored_bytes_per_rank": S,
+                   "parallelism": (f"sharded x{world} (XOR blocks, NCCL group exchange)" if sharded else
+                                   f"replicas x{world}" if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2 (state %.2f GB vs 126 MB L2); no flush needed" % (S / 1e9)},
         "achieved_hbm_gbs": sum(touched) * args.steps / (total_ms / 1e3) / 1e9,
         "touched_bytes_per_step": sum(touched),

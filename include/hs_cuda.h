@@ -163,19 +163,25 @@ int hs_state_distance_mixture(const hs_state* h, int rank, const double* psi, do
  * Shard s of P holds the stored tiles (ti >= tj) with (ti >> logB) ^ (tj >> logB) == s, B = G / P:
  * shard 0 the P diagonal blocks (triangular), shard s != 0 the P/2 rectangular blocks (a, a ^ s),
  * a > a ^ s.  P = 1 is exactly the reference layout.  Operations whose targets avoid the top
- * log2(P) qubits are shard-local; an operation with one top target pairs shard s with
- * s ^ 2^c: each side needs the partner's payload in its exchange buffer (hs_state_exchange over
- * NCCL, or hs_state_exchange_from for shards in one process), computes every shared unit and
- * stores only its own tiles.  More than one top target: HS_ERR_UNSUPPORTED. */
+ * log2(P) qubits are shard-local; an operation whose targets include top qubits c1.. (mask
+ * 2^c1 | ..) couples the group of shards s ^ span(mask): every member needs the others' payloads
+ * in its exchange slots (hs_state_exchange_group over NCCL, or hs_state_exchange_group_from per
+ * peer for shards in one process), computes every unit of the group and stores only its own
+ * tiles.  One top target = a pairwise butterfly step (partner s ^ 2^c). */
 int hs_state_create_sharded(int n, int m, int device, int nshards, int shard, hs_state** out);
 int hs_state_shard_info(const hs_state* h, int* nshards, int* shard, uint64_t* block_rows);
 /* partner shard of an operation on `targets` (any order), -1 when shard-local */
-int hs_op_partner(const hs_state* h, int k, const uint32_t* targets, int* partner);
-int hs_state_recv_alloc(hs_state* h);
-int hs_state_exchange_from(hs_state* h, const hs_state* peer);  /* recv <- peer payload (device/peer copy) */
+int hs_op_partner(const hs_state* h, int k, const uint32_t* targets, int* partner); /* one top target */
+/* group mask of an operation (0 = shard-local) */
+int hs_op_group(const hs_state* h, int k, const uint32_t* targets, uint32_t* mask);
+int hs_state_recv_alloc(hs_state* h);                       /* one exchange slot */
+int hs_state_recv_reserve(hs_state* h, int slots);          /* 2^popcount(mask) - 1 slots, <= 7 */
+int hs_state_exchange_from(hs_state* h, const hs_state* peer);  /* pair: slot <- peer payload (device/peer copy) */
+int hs_state_exchange_group_from(hs_state* h, const hs_state* peer, uint32_t mask);  /* peer's slot of the group */
 int hs_nccl_unique_id(void* id128);                               /* ncclUniqueId (128 bytes) */
 int hs_state_comm_init(hs_state* h, const void* id128, int nranks, int rank);  /* rank == shard */
 int hs_state_exchange(hs_state* h, int partner);                  /* NCCL send/recv, stream-ordered */
+int hs_state_exchange_group(hs_state* h, uint32_t mask);          /* NCCL, every other member of the group */
 /* linear partial sums of one shard: kind 0 tr(rho O), 1 squared Frobenius, 2 trace (sum over shards) */
 int hs_reduce_partial(const hs_state* a, const hs_state* b, int kind, double* out);
 

@@ -120,9 +120,11 @@ struct Geo {
     uint64_t nG_items;
     // sharding (XOR blocks over the top Plog tile-index bits; Plog == 0: the reference layout)
     uint32_t Plog, shard, logB;   // 2^Plog shards, this shard, 2^logB tile rows per block
-    uint32_t cross, cbit;         // the op has a target on top bit cbit: shard <-> shard ^ 2^cbit
+    uint32_t cross, cmask;        // top targets: shard s works with the group s ^ span(cmask) of 2^cross shards
+    uint32_t cb[3];               // shard bits of cmask, ascending (slot = those bits of own ^ shard, minus 1)
+    uint64_t recv_tiles;          // tiles per exchange slot
     uint32_t q, Pulog, logBu;     // local units: group q over 2^Pulog blocks of 2^logBu grid bases
-    const double2* recv;          // partner shard payload (cross ops)
+    const double2* recv;          // group members' payloads, slot j at recv + j * recv_tiles tiles
     uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
 };
 
@@ -283,8 +285,13 @@ __device__ __forceinline__ uint64_t tile_entry(const Geo& G, uint64_t tr, uint64
     uint64_t ent = shard_index(G.Plog, G.logB, hi, lo, own);
     if (adj)
         ent |= F_ADJ;
-    if (own != G.shard)
-        ent |= F_REMOTE | F_NOSTORE;
+    if (own != G.shard) {
+        const uint32_t d = own ^ G.shard;
+        uint32_t slot = 0;
+        for (uint32_t i = 0; i < G.cross; ++i)
+            slot |= ((d >> G.cb[i]) & 1u) << i;
+        ent = (ent + (uint64_t)(slot - 1) * G.recv_tiles) | F_REMOTE | F_NOSTORE;
+    }
     return ent;
 }
 // local unit u -> grid base pair (tbi, tbj); strict: off-diagonal units only
@@ -1606,8 +1613,10 @@ struct hs_state {
     size_t kraus_cap = 0;
     // sharding (XOR blocks): 2^Plog shards of 2^logB tile rows per block; this is shard `shard`
     uint32_t Plog = 0, logB = 0, shard = 0;
-    double2* recv = nullptr;  // partner shard payload for cross-shard operations
-    uint64_t recv_count = 0;
+    double2* recv = nullptr;  // group members' payloads for cross-shard operations (slots)
+    uint64_t recv_count = 0;  // elements per slot (the largest shard)
+    uint32_t recv_slots = 0;  // allocated slots
+    uint32_t recv_mask = 0;   // shard-bit mask of the last exchange (which slots hold whom)
     void* comm = nullptr;     // ncclComm_t
 };
 
@@ -1711,20 +1720,24 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
     G.logB = h->logB;
     G.recv = h->recv;
     G.cross = 0;
-    G.cbit = 0;
+    G.cmask = 0;
+    G.cb[0] = G.cb[1] = G.cb[2] = 0;
+    G.recv_tiles = h->recv_count >> (2 * h->m);
     G.Pulog = h->Plog;
     G.q = h->shard;
     if (h->Plog && g) {
         const uint32_t gbits = ilog2(G.G), top0 = gbits - h->Plog;
-        for (uint32_t l = 0; l < g; ++l)
+        for (uint32_t l = 0; l < g; ++l)  // gr_pos ascending
             if (G.gr_pos[l] >= top0) {
-                G.cross += 1;
-                G.cbit = G.gr_pos[l] - top0;
+                G.cb[G.cross++] = G.gr_pos[l] - top0;
+                G.cmask |= 1u << (G.gr_pos[l] - top0);
             }
-        if (G.cross == 1) {
-            G.Pulog = h->Plog - 1;
-            G.q = ((h->shard >> (G.cbit + 1)) << G.cbit) | (h->shard & ((1u << G.cbit) - 1));
-        }
+        // the group's units: the shard index with the cross bits deleted (highest first)
+        G.Pulog = h->Plog - G.cross;
+        uint32_t q = h->shard;
+        for (int i = (int)G.cross - 1; i >= 0; --i)
+            q = ((q >> (G.cb[i] + 1)) << G.cb[i]) | (q & ((1u << G.cb[i]) - 1));
+        G.q = q;
     }
     G.logBu = ilog2(G.nb) - G.Pulog;
     {
@@ -2014,10 +2027,8 @@ int sm_count(int device) {
 
 template <int K, int MODE, int NS>
 int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
-    if (G0.cross > 1)
-        return set_err(HS_ERR_UNSUPPORTED, "operation couples more than one cross-shard qubit");
-    if (G0.cross == 1 && !h->recv)
-        return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the partner shard first");
+    if (G0.cross && (!h->recv || h->recv_slots < (1u << G0.cross) - 1 || h->recv_mask != G0.cmask))
+        return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the group's shards first");
     Geo G = G0;
     if (MODE == M_MONO && G.groups) {
         // tile permutation on >= 2 grid bits: whole-tile pipeline, items = (unit, cycle group);
@@ -2196,7 +2207,8 @@ int finish_plan(hs_state* h, const Geo& G, int k, const uint32_t* t, int path, h
         plan->targets[i] = t[i];
     plan->grid_bits = (int)G.g;
     plan->launches = (G.nD_items + G.nU_items) ? 1 : 0;
-    plan->touched_bytes = touched;
+    // a cross-shard op also reads the 2^cross - 1 exchanged payloads of its group (about one shard each)
+    plan->touched_bytes = G.cross ? touched / 2 * ((1ull << G.cross) + 1) : touched;
     if (g_plan_subcases)
         count_subcases(h, G, plan->subcases);
     return HS_OK;
@@ -2343,62 +2355,108 @@ int hs_state_shard_info(const hs_state* h, int* nshards, int* shard, uint64_t* b
     return HS_OK;
 }
 
-int hs_op_partner(const hs_state* h, int k, const uint32_t* targets, int* partner) {
-    if (!h || !targets || !partner || k < 1 || k > 3)
+namespace {
+// the op's cross-shard mask: shard bit c set when a target is the c-th top qubit
+int op_group_mask(const hs_state* h, int k, const uint32_t* targets, uint32_t* mask) {
+    if (!h || !targets || !mask || k < 1 || k > 3)
         return set_err(HS_ERR_INVALID, "bad arguments");
-    *partner = -1;
+    *mask = 0;
+    for (int i = 0; i < k; ++i)
+        if (targets[i] >= (uint32_t)h->n)
+            return set_err(HS_ERR_RANGE, "target qubit out of range");
     if (!h->Plog)
         return HS_OK;
     const uint32_t gbits = ilog2(h->G), top0 = h->m + gbits - h->Plog;  // qubit index of the lowest top bit
-    int found = -1;
-    for (int i = 0; i < k; ++i) {
-        if (targets[i] >= (uint32_t)h->n)
-            return set_err(HS_ERR_RANGE, "target qubit out of range");
-        if (targets[i] >= top0) {
-            if (found >= 0)
-                return set_err(HS_ERR_UNSUPPORTED, "operation couples more than one cross-shard qubit");
-            found = (int)(targets[i] - top0);
-        }
-    }
-    if (found >= 0)
-        *partner = (int)(h->shard ^ (1u << found));
+    for (int i = 0; i < k; ++i)
+        if (targets[i] >= top0)
+            *mask |= 1u << (targets[i] - top0);
+    return HS_OK;
+}
+// slot of group member `shard ^ d` in the exchange buffer (the bits of d under mask, packed, minus 1)
+uint32_t group_slot(uint32_t d, uint32_t mask) {
+    uint32_t slot = 0, i = 0;
+    for (uint32_t b = 0; b < 32; ++b)
+        if (mask >> b & 1u)
+            slot |= ((d >> b) & 1u) << i++;
+    return slot - 1;
+}
+}  // namespace
+
+int hs_op_group(const hs_state* h, int k, const uint32_t* targets, uint32_t* mask) {
+    return op_group_mask(h, k, targets, mask);
+}
+
+int hs_op_partner(const hs_state* h, int k, const uint32_t* targets, int* partner) {
+    if (!partner)
+        return set_err(HS_ERR_INVALID, "bad arguments");
+    *partner = -1;
+    uint32_t mask = 0;
+    int rc = op_group_mask(h, k, targets, &mask);
+    if (rc)
+        return rc;
+    if (mask & (mask - 1))
+        return set_err(HS_ERR_UNSUPPORTED, "operation couples more than one cross-shard qubit: use hs_op_group");
+    if (mask)
+        *partner = (int)(h->shard ^ mask);
     return HS_OK;
 }
 
-int hs_state_recv_alloc(hs_state* h) {
-    if (!h)
-        return set_err(HS_ERR_INVALID, "null state");
-    if (h->recv)
+int hs_state_recv_reserve(hs_state* h, int slots) {
+    if (!h || slots < 1 || slots > 7)
+        return set_err(HS_ERR_INVALID, "bad arguments");
+    if (h->recv && h->recv_slots >= (uint32_t)slots)
         return HS_OK;
     DeviceGuard dg(h->device);
+    if (h->recv) {
+        cudaStreamSynchronize(h->stream);
+        cudaFree(h->recv);
+        h->recv = nullptr;
+        h->recv_slots = 0;
+        h->recv_mask = 0;
+    }
     const uint64_t cnt = shard_count_of(h, 0);  // the largest shard
-    cudaError_t e = cudaMalloc(&h->recv, cnt * sizeof(double2));
+    cudaError_t e = cudaMalloc(&h->recv, (uint64_t)slots * cnt * sizeof(double2));
     if (e != cudaSuccess) {
         cudaGetLastError();
         h->recv = nullptr;
         return set_err(HS_ERR_NOMEM, std::string("cudaMalloc exchange buffer: ") + cudaGetErrorString(e));
     }
     h->recv_count = cnt;
+    h->recv_slots = (uint32_t)slots;
     return HS_OK;
 }
 
-// In-process / single-node exchange: recv <- peer payload (device or peer copy, stream-ordered).
-int hs_state_exchange_from(hs_state* h, const hs_state* peer) {
+int hs_state_recv_alloc(hs_state* h) { return hs_state_recv_reserve(h, 1); }
+
+// In-process / single-node exchange: slot of `peer` (group `mask`) <- peer payload (device or peer
+// copy, stream-ordered).  Call once per other member of the group before the operation.
+int hs_state_exchange_group_from(hs_state* h, const hs_state* peer, uint32_t mask) {
     if (!h || !peer)
         return set_err(HS_ERR_INVALID, "null state");
     if (peer->Plog != h->Plog || peer->n != h->n || peer->m != h->m)
         return set_err(HS_ERR_INVALID, "peer is not a shard of the same operator");
-    int rc = hs_state_recv_alloc(h);
+    const uint32_t d = peer->shard ^ h->shard;
+    if (!d || (d & ~mask) || mask >> h->Plog)
+        return set_err(HS_ERR_INVALID, "peer is not another member of the group");
+    const int nbits = __builtin_popcount(mask);
+    int rc = hs_state_recv_reserve(h, (1 << nbits) - 1);
     if (rc)
         return rc;
     DeviceGuard dg(h->device);
+    double2* dst = h->recv + (uint64_t)group_slot(d, mask) * h->recv_count;
     CUDA_TRY(cudaStreamSynchronize(peer->stream));
     if (peer->device == h->device)
-        CUDA_TRY(cudaMemcpyAsync(h->recv, peer->d, peer->count * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
+        CUDA_TRY(cudaMemcpyAsync(dst, peer->d, peer->count * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
     else
-        CUDA_TRY(cudaMemcpyPeerAsync(h->recv, h->device, peer->d, peer->device, peer->count * sizeof(double2),
-                                     h->stream));
+        CUDA_TRY(cudaMemcpyPeerAsync(dst, h->device, peer->d, peer->device, peer->count * sizeof(double2), h->stream));
+    h->recv_mask = mask;
     return HS_OK;
+}
+
+int hs_state_exchange_from(hs_state* h, const hs_state* peer) {
+    if (!h || !peer)
+        return set_err(HS_ERR_INVALID, "null state");
+    return hs_state_exchange_group_from(h, peer, peer->shard ^ h->shard);
 }
 
 int hs_nccl_unique_id(void* id128) {
@@ -2434,30 +2492,47 @@ int hs_state_comm_init(hs_state* h, const void* id128, int nranks, int rank) {
     return HS_OK;
 }
 
-// NCCL pairwise exchange over NVLink: send the whole local shard, receive the partner's into recv.
-int hs_state_exchange(hs_state* h, int partner) {
+// NCCL exchange over NVLink within the op's group (shards s ^ span(mask)): send the whole local shard
+// to every other member and receive theirs into the exchange slots; one grouped call, stream-ordered.
+// One top target = a pairwise butterfly step.
+int hs_state_exchange_group(hs_state* h, uint32_t mask) {
     if (!h)
         return set_err(HS_ERR_INVALID, "null state");
     if (!h->comm)
         return set_err(HS_ERR_INVALID, "no communicator: call hs_state_comm_init");
-    if (partner < 0 || partner >= (1 << h->Plog) || partner == (int)h->shard)
-        return set_err(HS_ERR_RANGE, "bad partner shard");
-    int rc = hs_state_recv_alloc(h);
+    if (!mask || mask >> h->Plog || __builtin_popcount(mask) > 3)
+        return set_err(HS_ERR_RANGE, "bad group mask");
+    const int nbits = __builtin_popcount(mask);
+    int rc = hs_state_recv_reserve(h, (1 << nbits) - 1);
     if (rc)
         return rc;
     NcclApi& api = nccl();
     DeviceGuard dg(h->device);
-    const uint64_t pc = shard_count_of(h, (uint32_t)partner);
     ncclComm_t comm = (ncclComm_t)h->comm;
     ncclResult_t r = api.GroupStart();
-    if (r == ncclSuccess)
-        r = api.Send(h->d, h->count * 2, ncclDouble, partner, comm, h->stream);
-    if (r == ncclSuccess)
-        r = api.Recv(h->recv, pc * 2, ncclDouble, partner, comm, h->stream);
+    for (uint32_t d = 1; d < (1u << h->Plog) && r == ncclSuccess; ++d) {
+        if (d & ~mask)
+            continue;
+        const int peer = (int)(h->shard ^ d);
+        const uint64_t pc = shard_count_of(h, (uint32_t)peer);
+        r = api.Send(h->d, h->count * 2, ncclDouble, peer, comm, h->stream);
+        if (r == ncclSuccess)
+            r = api.Recv(h->recv + (uint64_t)group_slot(d, mask) * h->recv_count, pc * 2, ncclDouble, peer, comm,
+                         h->stream);
+    }
     const ncclResult_t r2 = api.GroupEnd();
     if (r != ncclSuccess || r2 != ncclSuccess)
         return set_err(HS_ERR_CUDA, std::string("NCCL exchange: ") + api.GetErrorString(r != ncclSuccess ? r : r2));
+    h->recv_mask = mask;
     return HS_OK;
+}
+
+int hs_state_exchange(hs_state* h, int partner) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (partner < 0 || partner >= (1 << h->Plog) || partner == (int)h->shard)
+        return set_err(HS_ERR_RANGE, "bad partner shard");
+    return hs_state_exchange_group(h, (uint32_t)partner ^ h->shard);
 }
 
 int hs_state_upload_range(hs_state* h, const double* host, uint64_t offset, uint64_t count) {

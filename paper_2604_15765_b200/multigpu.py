@@ -8,8 +8,9 @@ and its hermitian mirror on the same shard, and P = 1 is exactly the reference's
 * Operations whose targets avoid the top p qubits touch only one shard's tiles: no communication.
 * An operation with one target among the top p qubits (bit c) pairs shard s with s ^ 2^c: both sides
   exchange their whole shard (NCCL send/recv over NVLink, one pairwise butterfly step), compute every
-  unit they share and store only their own tiles.  Every other collective is a scalar sum
-  (expectation values).
+  unit they share and store only their own tiles.  With t top targets (mask of their shard bits) the
+  group s ^ span(mask) of 2^t shards exchanges all-to-all inside the group the same way (a CX on two
+  top qubits: 4 shards).  Every other collective is a scalar sum (expectation values).
 
 ``ShardLayout`` is the host-side mirror of the engine's addressing (planning, scatter/gather, tests);
 ``ShardGroup`` drives P shards from one process (one GPU or several, exchange by device/peer copies);
@@ -82,15 +83,29 @@ class ShardLayout:
         a = ((blk >> h) << (h + 1)) | (1 << h) | (blk & ((1 << h) - 1))
         return a * B + v // B, (a ^ s) * B + v % B
 
+    def group_mask(self, targets) -> int:
+        """Shard-bit mask of an operation's top targets (0: shard-local)."""
+        if self.P == 1:
+            return 0
+        mask = 0
+        for q in targets:
+            if q >= self.top0:
+                mask |= 1 << (q - self.top0)
+        return mask
+
+    def group(self, shard: int, targets) -> list[int]:
+        """The shards an operation couples with `shard` (itself first): shard ^ span(mask)."""
+        mask = self.group_mask(targets)
+        return [shard ^ d for d in range(1 << self.p) if not d & ~mask]
+
     def partner(self, shard: int, targets) -> int:
-        """Partner shard of an operation on `targets` (-1: shard-local); more than one top target
-        raises (the engine returns HS_ERR_UNSUPPORTED)."""
-        tops = [q - self.top0 for q in targets if q >= self.top0]
-        if self.P == 1 or not tops:
+        """Partner shard of an operation with one top target (-1: shard-local)."""
+        mask = self.group_mask(targets)
+        if not mask:
             return -1
-        if len(tops) > 1:
-            raise NotImplementedError("operation couples more than one cross-shard qubit")
-        return shard ^ (1 << tops[0])
+        if mask & (mask - 1):
+            raise ValueError("operation couples more than two shards: use group()")
+        return shard ^ mask
 
     def tile_slices(self, s: int):
         """[(global tile index, local tile index)] of shard s, in local order."""
@@ -127,6 +142,14 @@ def op_partner(st: H.TiledHermitian, targets) -> int:
     return out.value
 
 
+def op_group(st: H.TiledHermitian, targets) -> int:
+    tg = np.ascontiguousarray(targets, np.uint32)
+    out = ctypes.c_uint32()
+    nat.check(nat.engine().hs_op_group(st.handle, len(tg), tg.ctypes.data_as(nat.c_u32_p), ctypes.byref(out)),
+              "op_group")
+    return out.value
+
+
 def reduce_partial(a: H.TiledHermitian, b: H.TiledHermitian | None, kind: int) -> float:
     out = ctypes.c_double()
     nat.check(nat.engine().hs_reduce_partial(a.handle, (b or a).handle, kind, ctypes.byref(out)), "reduce")
@@ -144,11 +167,13 @@ class ShardGroup:
     def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
         """hermsim.apply on every shard; exchanges first when the op crosses shards."""
         opts = opts or H.ApplyOptions(count_subcases=False)
-        partners = [op_partner(st, targets) for st in self.shards]
-        if partners[0] >= 0:
+        mask = op_group(self.shards[0], targets)
+        if mask:
             # all exchanges read the pre-op payloads, then every shard updates its own tiles
             for s, st in enumerate(self.shards):
-                nat.check(nat.engine().hs_state_exchange_from(st.handle, self.shards[partners[s]].handle), "exchange")
+                for peer in self.layout.group(s, targets)[1:]:
+                    nat.check(nat.engine().hs_state_exchange_group_from(st.handle, self.shards[peer].handle, mask),
+                              "exchange")
             for st in self.shards:
                 st.synchronize()
         plans = [H.apply(st, spec, targets, opts) for st in self.shards]
@@ -204,9 +229,9 @@ class DistributedShard:
 
     def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
         opts = opts or H.ApplyOptions(count_subcases=False)
-        partner = op_partner(self.state, targets)
-        if partner >= 0:
-            nat.check(nat.engine().hs_state_exchange(self.state.handle, partner), "exchange")
+        mask = op_group(self.state, targets)
+        if mask:
+            nat.check(nat.engine().hs_state_exchange_group(self.state.handle, mask), "exchange")
         return H.apply(self.state, spec, targets, opts)
 
     def reduce(self, other: "DistributedShard | None", kind: int) -> float:

@@ -39,8 +39,21 @@ def test_partner_plan():
     assert L.top0 == 8
     assert L.partner(3, [0]) == -1 and L.partner(3, [7, 2]) == -1
     assert L.partner(3, [8]) == 2 and L.partner(3, [9]) == 1 and L.partner(3, [10, 1]) == 7
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(ValueError):
         L.partner(0, [8, 9])
+    # two or three top targets couple the group s ^ span(mask)
+    assert L.group_mask([9, 8]) == 3 and L.group_mask([10, 3, 8]) == 5 and L.group_mask([1, 2]) == 0
+    assert L.group(3, [9, 8]) == [3, 2, 1, 0] and L.group(6, [10, 2, 8]) == [6, 7, 2, 3]
+    assert L.group(5, [10, 9, 8]) == [5 ^ d for d in range(8)]
+    # a k = 2 unit on two top qubits spans exactly its group of four shards
+    for ti in range(0, 64, 5):
+        for tj in range(ti + 1):
+            if (ti | tj) >> 3 & 3:
+                continue
+            sh = {L.shard_of(max(a, b), min(a, b)) for a in (ti, ti | 8, ti | 16, ti | 24)
+                  for b in (tj, tj | 8, tj | 16, tj | 24)}
+            s0 = min(sh)
+            assert sh == {s0 ^ d for d in range(4)}
     # a k = 1 cross unit spans exactly the pair (s, s ^ 2^c) (SURVEY 8e XOR-block property)
     for c, q in ((0, 8), (1, 9), (2, 10)):
         ap = q - 5

@@ -7,6 +7,15 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+def _kraus2(HS):
+    """Rank-2 k = 2 channel: sqrt(0.9) U, sqrt(0.1) V (CPTP)."""
+    return np.stack([np.sqrt(0.9) * HS.haar(2, 11), np.sqrt(0.1) * HS.haar(2, 12)])
+
+
+def _kraus3(HS):
+    return np.stack([np.sqrt(0.7) * HS.haar(3, 13), np.sqrt(0.3) * HS.haar(3, 14)])
+
+
 def _ops(H, HS, n):
     u2, u3 = HS.haar(2, 5), HS.haar(3, 6)
     top = n - 1
@@ -17,6 +26,11 @@ def _ops(H, HS, n):
         (H.make_generic("u2", u2), [top, 5]), (H.make_generic("u2", u2), [2, top - 1]),
         (H.make_generic("u3", u3), [top, 4, 0]), (H.make_generic("u3", u3), [6, 5, 8]),
         (H.native_gate("y"), [top]), (H.native_gate("swap"), [top - 2, 1]), (H.depolarising(0.02), [5]),
+        # several top targets: the group of 4 (8) shards exchanges all-to-all
+        (H.native_gate("cnot"), [top, top - 1]), (H.native_gate("cnot"), [top - 2, top]),
+        (H.make_generic("u2", u2), [top - 1, top - 2]), (H.native_gate("swap"), [top, top - 2]),
+        (H.make_generic("u3", u3), [top, top - 1, 2]), (H.make_generic("u3", u3), [top - 2, top, top - 1]),
+        (H.make_generic("k2", _kraus2(HS)), [top, top - 1]), (H.make_generic("k3", _kraus3(HS)), [2, top, top - 2]),
     ]
 
 
@@ -33,8 +47,6 @@ def test_sharded_bit_identical(n, P):
     assert np.array_equal(grp.download_full().view(np.uint64), ref.download().view(np.uint64))
     opts = H.ApplyOptions(count_subcases=False)
     for spec, tg in _ops(H, HS, n):
-        if len([q for q in tg if q >= grp.layout.top0]) > 1:
-            continue
         H.apply(ref, spec, tg, opts)
         grp.apply(spec, tg)
         got, want = grp.download_full(), ref.download()
@@ -48,9 +60,16 @@ def test_sharded_bit_identical(n, P):
     assert abs(grp.expectation(obs) - H.expectation(ref, obs_ref)) < 1e-13
 
 
-def test_two_top_targets_refused():
+def test_group_exchange_required():
+    """A cross-shard operation without the group's payloads is refused, not computed wrongly."""
     from paper_2604_15765_b200 import hermsim as H
+    from paper_2604_15765_b200 import _native as nat
     from paper_2604_15765_b200.multigpu import ShardGroup
     grp = ShardGroup(10, 5, 4)
-    with pytest.raises(NotImplementedError):
-        grp.apply(H.native_gate("cnot"), [9, 8])
+    st = grp.shards[1]
+    with pytest.raises((ValueError, nat.NativeError)):
+        H.apply(st, H.native_gate("cnot"), [9, 8])
+    # exchanging for a one-bit group does not license a two-bit op
+    nat.check(nat.engine().hs_state_exchange_group_from(st.handle, grp.shards[0].handle, 1))
+    with pytest.raises((ValueError, nat.NativeError)):
+        H.apply(st, H.native_gate("cnot"), [9, 8])
