@@ -115,6 +115,7 @@ struct Geo {
     uint64_t gmask[16];           // logical tiles of each group
     uint32_t PD;                  // row pitch of a direct logical tile in shared memory
     uint32_t logical;             // adjoint tiles staged transposed (logical layout, gather kernel)
+    uint8_t tsk[64];              // gather: per-logical-tile skew of the staging slot (bank spread for DMMA)
     // gather kernel (square sub-blocks of S0 x S0 positions, g >= 2)
     uint32_t S0, logS0, nsb_side, log_nsb_side;
     uint64_t nG_items;
@@ -133,6 +134,7 @@ struct Tabs {
     uint8_t xdep[32], xb[32], yb[32], xs_rin[32], xs_base[32], y_cin[32], y_base[32], xs_in[8], y_in[8];
     uint16_t cdir[64], cadj[64];  // component offsets (copied from Geo: indexed per thread)
     uint8_t ttr[64];
+    uint8_t tsk[64];
 };
 
 template <int NS>
@@ -1295,6 +1297,83 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// k = 3 direct form L B L^dagger on the FP64 tensor path (mma.sync m8n8k4 f64): one warp per 8x8
+// block, 16 DMMA per block (4 real products per complex product, two k = 4 chunks, two stages) in
+// place of 1024 DFMA.  The contraction index k of each chunk j is permuted to k = 2c + j (c = lane
+// & 3): the stage-1 accumulator fragment (row lane >> 2, columns 2c, 2c + 1) is then exactly the
+// stage-2 A fragment of chunks 0 and 1, so no data moves between lanes.  Lane (g = lane >> 2, c)
+// loads B[2c + j][g] and stores Z[g][2c + j].  (B200: DMMA and DFMA share the FP64 pipe at
+// ~37 TFLOP/s, tools/fp64_probe.cu; DMMA issues 8x fewer instructions.)
+__device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+// per-lane constant fragments of the transform (loaded once per kernel: the lane-dependent
+// coefficient index would serialise the constant-cache reads if repeated per item)
+struct DmmaFrag {
+    double lr[2], li[2], nli[2];
+    uint32_t old[2], ost[2];  // staging offsets of the loaded / stored components (from the block base)
+    uint32_t tld[2], tst[2];  // their logical tiles (adjoint mask bits)
+};
+template <int NS>
+__device__ __forceinline__ DmmaFrag dmma_frag(const Tabs& T, const Coef<NS>& cf) {
+    DmmaFrag f;
+    const uint32_t lane = threadIdx.x & 31, gq = lane >> 2, cq = lane & 3;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const double2 l = cf.s[gq * 8 + 2 * cq + j];
+        f.lr[j] = l.x;
+        f.li[j] = l.y;
+        f.nli[j] = -l.y;
+        const uint32_t il = (2 * cq + j) * 8 + gq, is = gq * 8 + 2 * cq + j;
+        f.old[j] = T.cdir[il];
+        f.ost[j] = T.cdir[is];
+        f.tld[j] = T.ttr[il];
+        f.tst[j] = T.ttr[is];
+    }
+    return f;
+}
+template <int NC>
+__device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
+                                             double2* sb) {
+    const uint32_t warp = threadIdx.x >> 5;
+    const bool cld0 = (am >> f.tld[0]) & 1ull, cld1 = (am >> f.tld[1]) & 1ull;
+    const bool cst0 = (am >> f.tst[0]) & 1ull, cst1 = (am >> f.tst[1]) & 1ull;
+    const uint32_t nblk = G.nxb << G.logNyb, ymask = G.nyb - 1;
+#pragma unroll 2
+    for (uint32_t b = warp; b < nblk; b += NC / 32) {
+        const uint32_t base = T.xb[b >> G.logNyb] * G.PD + T.yb[b & ymask];
+        double2 v0 = sb[base + f.old[0]], v1 = sb[base + f.old[1]];
+        if (cld0)
+            v0.y = -v0.y;
+        if (cld1)
+            v1.y = -v1.y;
+        // stage 1: Y = L B
+        double yr0 = 0.0, yr1 = 0.0, yi0 = 0.0, yi1 = 0.0;
+        dmma_acc(yr0, yr1, f.lr[0], v0.x);
+        dmma_acc(yr0, yr1, f.lr[1], v1.x);
+        dmma_acc(yr0, yr1, f.nli[0], v0.y);
+        dmma_acc(yr0, yr1, f.nli[1], v1.y);
+        dmma_acc(yi0, yi1, f.lr[0], v0.y);
+        dmma_acc(yi0, yi1, f.lr[1], v1.y);
+        dmma_acc(yi0, yi1, f.li[0], v0.x);
+        dmma_acc(yi0, yi1, f.li[1], v1.x);
+        // stage 2: Z = Y L^dagger; B fragment of chunk j = conj(L[g][2c + j])
+        double zr0 = 0.0, zr1 = 0.0, zi0 = 0.0, zi1 = 0.0;
+        dmma_acc(zr0, zr1, yr0, f.lr[0]);
+        dmma_acc(zr0, zr1, yr1, f.lr[1]);
+        dmma_acc(zr0, zr1, yi0, f.li[0]);
+        dmma_acc(zr0, zr1, yi1, f.li[1]);
+        dmma_acc(zi0, zi1, yr0, f.nli[0]);
+        dmma_acc(zi0, zi1, yr1, f.nli[1]);
+        dmma_acc(zi0, zi1, yi0, f.lr[0]);
+        dmma_acc(zi0, zi1, yi1, f.lr[1]);
+        sb[base + f.ost[0]] = make_double2(zr0, cst0 ? -zi0 : zi0);
+        sb[base + f.ost[1]] = make_double2(zr1, cst1 ? -zi1 : zi1);
+    }
+}
+
 template <int K, int MODE, int NS, int NC>
 __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     extern __shared__ __align__(128) double2 ring[];
@@ -1315,9 +1394,10 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
         T.cdir[tid] = G.cdir[tid];
         T.cadj[tid] = G.cadj[tid];
         T.ttr[tid] = G.ttr[tid];
+        T.tsk[tid] = G.tsk[tid];
     }
     const uint64_t nItems = G.nG_items;
-    const uint32_t S = G.stages;
+    constexpr uint32_t S = 3;  // plan_gather: three stages
     const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const uint32_t NT = 1u << G.logNT, NGm = (1u << G.logNG) - 1;
     const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
@@ -1371,10 +1451,13 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
                 continue;
             const bool adj = (ent & F_ADJ) != 0;
             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
-            cp_async16(base + (tt * G.TS + (adj ? sm_a : sm_d)) * 16u, ((ent & F_REMOTE) ? G.recv : st) + g);
+            cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, ((ent & F_REMOTE) ? G.recv : st) + g);
         }
     };
     __syncthreads();
+    DmmaFrag fr;
+    if constexpr (K == 3 && MODE == M_DIRECT)
+        fr = dmma_frag(T, cf);
     for (uint32_t j = 0; j + 1 < S; ++j) {
         if (j < nlocal)
             prep(j, j % S);
@@ -1390,7 +1473,10 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
         cp_async_wait<1>();  // S = 3: all but the most recent group (item i + 1) have landed
         __syncthreads();
         double2* sb = ring + (size_t)s * G.stage_elems;
-        pipe_compute<K, MODE, NS, NC>(G, T, cf, am[s], 1, sb);
+        if constexpr (K == 3 && MODE == M_DIRECT)
+            dmma_direct3<NC>(G, T, fr, am[s][0], sb);
+        else
+            pipe_compute<K, MODE, NS, NC>(G, T, cf, am[s], 1, sb);
         __syncthreads();
         // write back along stored rows (adjoint components are already in stored, conjugated form)
         {
@@ -1401,7 +1487,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
                 if (ent & (F_SKIP | F_NOSTORE))
                     continue;
                 const bool adj = (ent & F_ADJ) != 0;
-                st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + (adj ? sm_a : sm_d)];
+                st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
             }
         }
         const uint64_t j = i + S - 1;
@@ -1962,7 +2048,7 @@ size_t smem_bytes(const Geo& G, int buffers) {
 
 
 // Geometry of the gather kernel for an operation whose units do not fit whole (g >= 2).
-void plan_gather(Geo& G) {
+void plan_gather(Geo& G, bool dmma = false) {
     const uint32_t M = G.M, g = G.g, NT = 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -1998,16 +2084,60 @@ void plan_gather(Geo& G) {
     G.logical = 1;
     G.TS = S0 * (S0 + 1);
     const uint32_t D = G.D, kinm = (1u << kin) - 1;
-    for (uint32_t rho = 0; rho < D; ++rho)
-        for (uint32_t gam = 0; gam < D; ++gam) {
-            const uint32_t R = rho >> kin, C = gam >> kin, i = rho * D + gam;
-            G.ttr[i] = (uint8_t)(R * NG + C);
-            G.cdir[i] = G.cadj[i] = (uint16_t)((R * NG + C) * G.TS + G.xs_in[rho & kinm] * G.PD + G.y_in[gam & kinm]);
-        }
+    for (uint32_t t = 0; t < 64; ++t)
+        G.tsk[t] = 0;
+    auto tables = [&]() {
+        for (uint32_t rho = 0; rho < D; ++rho)
+            for (uint32_t gam = 0; gam < D; ++gam) {
+                const uint32_t R = rho >> kin, C = gam >> kin, i = rho * D + gam, t = R * NG + C;
+                G.ttr[i] = (uint8_t)t;
+                G.cdir[i] = G.cadj[i] =
+                    (uint16_t)(t * G.TS + G.tsk[t] + G.xs_in[rho & kinm] * G.PD + G.y_in[gam & kinm]);
+            }
+    };
+    tables();
+    uint32_t extra = 0;
+    if (dmma && D == 8) {
+        // the DMMA transform's lane patterns (load B[2c+j][g], store Z[g][2c+j]) hit 16-byte bank
+        // groups (addr mod 8) by component offset: pick a tile pitch and per-tile-row skew that
+        // spread every quarter-warp over 8 groups
+        const uint32_t TS0 = G.TS;
+        uint32_t best = ~0u, bestE = 0, bestS = 0;
+        for (uint32_t e = 0; e < 8; ++e)
+            for (uint32_t sk = 0; sk < 8; ++sk) {
+                G.TS = TS0 + e;
+                for (uint32_t t = 0; t < NT; ++t)
+                    G.tsk[t] = (uint8_t)((sk * (t >> g)) & 7u);
+                tables();
+                uint32_t cost = 0;
+                for (int pat = 0; pat < 2; ++pat)
+                    for (uint32_t j = 0; j < 2; ++j)
+                        for (uint32_t ph = 0; ph < 4; ++ph) {
+                            uint32_t cnt[8] = {0}, mx = 0;
+                            for (uint32_t l = 8 * ph; l < 8 * ph + 8; ++l) {
+                                const uint32_t gq = l >> 2, cq = l & 3;
+                                const uint32_t i = pat ? gq * 8 + 2 * cq + j : (2 * cq + j) * 8 + gq;
+                                mx = std::max(mx, ++cnt[G.cdir[i] & 7u]);
+                            }
+                            cost += mx;
+                        }
+                cost = cost * 64 + e + sk;  // ties: the smallest footprint
+                if (cost < best) {
+                    best = cost;
+                    bestE = e;
+                    bestS = sk;
+                }
+            }
+        G.TS = TS0 + bestE;
+        for (uint32_t t = 0; t < NT; ++t)
+            G.tsk[t] = (uint8_t)((bestS * (t >> g)) & 7u);
+        tables();
+        extra = 7;
+    }
     G.diag_map = (G.nxb >= 8 && G.nyb >= 8) ? 1 : 0;
     G.U = 1;
     G.logU = 0;
-    G.stage_elems = (NT * G.TS + 7) & ~7u;
+    G.stage_elems = (NT * G.TS + extra + 7) & ~7u;
     G.stages = 3;
     G.nG_items = G.nU_strict << (2 * G.log_nsb_side);
 }
@@ -2085,10 +2215,11 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
                 return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
         }
         Geo Gg = G;
-        plan_gather(Gg);
+        constexpr bool dmma = K == 3 && MODE == M_DIRECT;
+        plan_gather(Gg, dmma);
         if (Gg.nG_items) {
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
-            constexpr int NC = K == 3 ? 256 : NCONS;  // k = 3 blocks need the registers
+            constexpr int NC = dmma ? NCONS : K == 3 ? 256 : NCONS;  // DFMA k = 3 blocks need the registers
             auto kern = gather_kernel<K, MODE, NS, NC>;
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess)
