@@ -127,6 +127,7 @@ struct Geo {
     uint32_t q, Pulog, logBu;     // local units: group q over 2^Pulog blocks of 2^logBu grid bases
     const double2* recv;          // group members' payloads, slot j at recv + j * recv_tiles tiles
     uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
+    uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): bit 0 skips the gather transform
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
@@ -1006,9 +1007,10 @@ __device__ __forceinline__ void stc(double2* sb, uint32_t a, bool cj, double2 v)
 
 template <int K, int MODE, int NS, int NC = NCONS>
 __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const Coef<NS>& cf, const uint64_t* am,
-                                             uint32_t nvalid_units, double2* sb, uint32_t grp = 0) {
+                                             uint32_t nvalid_units, double2* sb, uint32_t grp = 0, int tidv = -1,
+                                             uint32_t barid = 1) {
     constexpr int D = 1 << K;
-    const int tid = threadIdx.x;
+    const int tid = tidv >= 0 ? tidv : (int)threadIdx.x;
     const uint32_t nblk = G.U << (G.logNxb + G.logNyb);
     const uint32_t lo = G.diag_map ? 3u : G.logNyb, lomask = (1u << lo) - 1;
     if constexpr (MODE == M_S1 || MODE == M_HAD) {
@@ -1095,7 +1097,7 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                 stc(sb, a[q], (cjm >> q) & 1u, acc);
             }
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(NC) : "memory");  // consumer warps only
+        asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NC) : "memory");  // consumer warps only
         for (uint32_t w = tid; w < items; w += NC) {  // out = L Y, column by column
             const uint32_t b = (w & lomask) | (((w >> lo) / D) << lo), gam = (w >> lo) % D;
             uint32_t uu;
@@ -1336,8 +1338,7 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Tabs& T, const Coef<NS>& cf)
 }
 template <int NC>
 __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
-                                             double2* sb) {
-    const uint32_t warp = threadIdx.x >> 5;
+                                             double2* sb, uint32_t warp) {
     const bool cld0 = (am >> f.tld[0]) & 1ull, cld1 = (am >> f.tld[1]) & 1ull;
     const bool cst0 = (am >> f.tst[0]) & 1ull, cst1 = (am >> f.tst[1]) & 1ull;
     const uint32_t nblk = G.nxb << G.logNyb, ymask = G.nyb - 1;
@@ -1374,13 +1375,21 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
     }
 }
 
+// Two ping-pong groups of NC / 2 threads: group (i & 1) transforms and writes back local item i,
+// then loads item i + 3 (the other group's) into the stage it just freed.  One group's FP64 tensor
+// work overlaps the other's HBM traffic.  Stage s's `full` mbarrier completes when every thread of
+// the loading group has arrived twice: once on release (tile tables written) and once, via
+// cp.async.mbarrier.arrive.noinc, when its copies have landed.
 template <int K, int MODE, int NS, int NC>
 __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
+    constexpr uint32_t NH = NC / 2;  // threads per group
+    constexpr uint32_t S = 3;        // stages (plan_gather)
     extern __shared__ __align__(128) double2 ring[];
-    __shared__ uint64_t gt[MAX_STAGES][64];
-    __shared__ uint64_t am[MAX_STAGES][1];
+    __shared__ uint64_t gt[S][64];
+    __shared__ uint64_t am[S][1];
+    __shared__ __align__(8) uint64_t full[S];
     __shared__ Tabs T;
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x, grp = tid / NH, gtid = tid % NH;
     if (tid < 32) {
         T.xdep[tid] = G.xdep[tid];
         T.xb[tid] = G.xb_tab[tid];
@@ -1396,43 +1405,23 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
         T.ttr[tid] = G.ttr[tid];
         T.tsk[tid] = G.tsk[tid];
     }
+    if (tid == 0)
+        for (uint32_t q = 0; q < S; ++q)
+            mbar_init(&full[q], 2 * NH);
     const uint64_t nItems = G.nG_items;
-    constexpr uint32_t S = 3;  // plan_gather: three stages
     const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     const uint32_t NT = 1u << G.logNT, NGm = (1u << G.logNG) - 1;
     const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
-    // NC is a multiple of S0^2: every element this thread moves sits at the same sub-block
-    // position (i, jj) in stored order, in tiles tt = tid / S0^2 + k * NC / S0^2
-    const uint32_t r = tid & ((1u << logT) - 1), i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
-    const uint32_t tt0 = tid >> logT, ttstep = NC >> logT;
+    // NH is a multiple of S0^2: every element this thread moves sits at the same sub-block
+    // position (i, jj) in stored order, in tiles tt = gtid / S0^2 + k * NH / S0^2
+    const uint32_t r = gtid & ((1u << logT) - 1), i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
+    const uint32_t tt0 = gtid >> logT, ttstep = NH >> logT;
     const uint32_t sm_d = i0 * P + j0, sm_a = j0 * P + i0;  // logical slot, direct / adjoint
     const uint32_t nsbm = (1u << (2 * G.log_nsb_side)) - 1;
+    const uint32_t barid = 1 + grp;
+    auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NH) : "memory"); };
 
     auto item_of = [&](uint64_t j) { return blockIdx.x + j * gridDim.x; };
-    auto prep = [&](uint64_t j, uint32_t s) {
-        const uint64_t u = item_of(j) >> (2 * G.log_nsb_side);
-        if (tid < NT) {
-            uint64_t tbi, tbj;
-            unit_decode(G, u, true, tbi, tbj);
-            const uint64_t tr = ins_bits(tbi, tid >> G.logNG, G.gr_pos, G.g);
-            const uint64_t tc = ins_bits(tbj, tid & NGm, G.gr_pos, G.g);
-            uint64_t ent = tile_entry(G, tr, tc);
-            if (MODE == M_MONO && !((G.active >> tid) & 1ull))
-                ent |= F_SKIP;
-            gt[s][tid] = ent;
-        }
-    };
-    auto mask_of = [&](uint32_t s) {
-        if (tid < 32) {
-            unsigned long long m = 0;
-            for (uint32_t t = tid; t < NT; t += 32)
-                m |= (unsigned long long)((gt[s][t] & F_ADJ) != 0) << t;
-            for (int o = 16; o; o >>= 1)
-                m |= __shfl_xor_sync(0xffffffffu, m, o);
-            if (tid == 0)
-                am[s][0] = m;
-        }
-    };
     // global offsets (within a tile) of this thread's sub-block position, direct / adjoint
     auto offsets = [&](uint64_t item, uint32_t& od, uint32_t& oa) {
         const uint32_t sb = (uint32_t)(item & nsbm);
@@ -1440,8 +1429,30 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
         od = ((x0 | T.xdep[i0]) << G.logM) + (y0 | T.xdep[j0]);
         oa = ((y0 | T.xdep[i0]) << G.logM) + (x0 | T.xdep[j0]);
     };
-    auto issue = [&](uint64_t j) {
+    // this group loads item j into stage j % S (tile table, adjoint mask, copies, arrivals)
+    auto load = [&](uint64_t j) {
         const uint32_t s = (uint32_t)(j % S);
+        const uint64_t u = item_of(j) >> (2 * G.log_nsb_side);
+        if (gtid < NT) {
+            uint64_t tbi, tbj;
+            unit_decode(G, u, true, tbi, tbj);
+            const uint64_t tr = ins_bits(tbi, gtid >> G.logNG, G.gr_pos, G.g);
+            const uint64_t tc = ins_bits(tbj, gtid & NGm, G.gr_pos, G.g);
+            uint64_t ent = tile_entry(G, tr, tc);
+            if (MODE == M_MONO && !((G.active >> gtid) & 1ull))
+                ent |= F_SKIP;
+            gt[s][gtid] = ent;
+        }
+        gbar();
+        if (gtid < 32) {
+            unsigned long long m = 0;
+            for (uint32_t t = gtid; t < NT; t += 32)
+                m |= (unsigned long long)((gt[s][t] & F_ADJ) != 0) << t;
+            for (int o = 16; o; o >>= 1)
+                m |= __shfl_xor_sync(0xffffffffu, m, o);
+            if (gtid == 0)
+                am[s][0] = m;
+        }
         uint32_t od, oa;
         offsets(item_of(j), od, oa);
         const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
@@ -1453,31 +1464,27 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
             cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, ((ent & F_REMOTE) ? G.recv : st) + g);
         }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        mbar_arrive(&full[s]);
     };
     __syncthreads();
     DmmaFrag fr;
     if constexpr (K == 3 && MODE == M_DIRECT)
         fr = dmma_frag(T, cf);
-    for (uint32_t j = 0; j + 1 < S; ++j) {
-        if (j < nlocal)
-            prep(j, j % S);
-        __syncthreads();
-        if (j < nlocal) {
-            mask_of(j % S);
-            issue(j);
-        }
-        cp_async_commit();
-    }
-    for (uint64_t i = 0; i < nlocal; ++i) {
+    for (uint64_t j = 0; j < S && j < nlocal; ++j)  // item j is loaded by group (j + 1) & 1
+        if (((j + 1) & 1) == grp)
+            load(j);
+    for (uint64_t i = grp; i < nlocal; i += 2) {
         const uint32_t s = (uint32_t)(i % S);
-        cp_async_wait<1>();  // S = 3: all but the most recent group (item i + 1) have landed
-        __syncthreads();
+        mbar_wait(&full[s], (uint32_t)((i / S) & 1));
         double2* sb = ring + (size_t)s * G.stage_elems;
-        if constexpr (K == 3 && MODE == M_DIRECT)
-            dmma_direct3<NC>(G, T, fr, am[s][0], sb);
-        else
-            pipe_compute<K, MODE, NS, NC>(G, T, cf, am[s], 1, sb);
-        __syncthreads();
+        if (!(G.dbg & 1u)) {
+            if constexpr (K == 3 && MODE == M_DIRECT)
+                dmma_direct3<NH>(G, T, fr, am[s][0], sb, gtid >> 5);
+            else
+                pipe_compute<K, MODE, NS, NH>(G, T, cf, am[s], 1, sb, 0, (int)gtid, barid);
+        }
+        gbar();
         // write back along stored rows (adjoint components are already in stored, conjugated form)
         {
             uint32_t od, oa;
@@ -1490,15 +1497,9 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
                 st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
             }
         }
-        const uint64_t j = i + S - 1;
-        if (j < nlocal)
-            prep(j, (uint32_t)(j % S));
-        __syncthreads();
-        if (j < nlocal) {
-            mask_of((uint32_t)(j % S));
-            issue(j);
-        }
-        cp_async_commit();
+        gbar();
+        if (i + S < nlocal)
+            load(i + S);
     }
     cp_async_wait<0>();
 }
@@ -2217,9 +2218,13 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         Geo Gg = G;
         constexpr bool dmma = K == 3 && MODE == M_DIRECT;
         plan_gather(Gg, dmma);
+        {
+            static const char* dbg = getenv("HS_DEBUG_FLAGS");
+            Gg.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
+        }
         if (Gg.nG_items) {
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
-            constexpr int NC = dmma ? NCONS : K == 3 ? 256 : NCONS;  // DFMA k = 3 blocks need the registers
+            constexpr int NC = 512;  // two groups of 256 (a multiple of the S0^2 positions of an item)
             auto kern = gather_kernel<K, MODE, NS, NC>;
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess)
