@@ -127,7 +127,7 @@ struct Geo {
     uint32_t q, Pulog, logBu;     // local units: group q over 2^Pulog blocks of 2^logBu grid bases
     const double2* recv;          // group members' payloads, slot j at recv + j * recv_tiles tiles
     uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
-    uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): bit 0 skips the gather transform
+    uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): gather bit 0 skips the transform, bit 1 the loads, bit 2 the stores
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
@@ -1306,15 +1306,22 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // stage-2 A fragment of chunks 0 and 1, so no data moves between lanes.  Lane (g = lane >> 2, c)
 // loads B[2c + j][g] and stores Z[g][2c + j].  (B200: DMMA and DFMA share the FP64 pipe at
 // ~37 TFLOP/s, tools/fp64_probe.cu; DMMA issues 8x fewer instructions.)
+// (not volatile: a pure function of its operands, so the compiler may interleave independent chains)
 __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+// conjugation flag applied as a sign-bit flip on the integer pipe (a DADD negation would compete
+// with the DMMA for the FP64 pipe)
+__device__ __forceinline__ double flip_sign(double x, uint32_t m) {
+    return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
 }
 // per-lane constant fragments of the transform (loaded once per kernel: the lane-dependent
 // coefficient index would serialise the constant-cache reads if repeated per item)
 struct DmmaFrag {
     double lr[2], li[2], nli[2];
+    double ls[2], ld[2];      // Lr + Li (stage 1, 3M) and Pr + Pi = Lr - Li (stage 2, 3M)
     uint32_t old[2], ost[2];  // staging offsets of the loaded / stored components (from the block base)
     uint32_t tld[2], tst[2];  // their logical tiles (adjoint mask bits)
 };
@@ -1328,6 +1335,8 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Tabs& T, const Coef<NS>& cf)
         f.lr[j] = l.x;
         f.li[j] = l.y;
         f.nli[j] = -l.y;
+        f.ls[j] = l.x + l.y;
+        f.ld[j] = l.x - l.y;
         const uint32_t il = (2 * cq + j) * 8 + gq, is = gq * 8 + 2 * cq + j;
         f.old[j] = T.cdir[il];
         f.ost[j] = T.cdir[is];
@@ -1339,47 +1348,67 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Tabs& T, const Coef<NS>& cf)
 template <int NC>
 __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
                                              double2* sb, uint32_t warp) {
-    const bool cld0 = (am >> f.tld[0]) & 1ull, cld1 = (am >> f.tld[1]) & 1ull;
-    const bool cst0 = (am >> f.tst[0]) & 1ull, cst1 = (am >> f.tst[1]) & 1ull;
+    const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
+    const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
     const uint32_t nblk = G.nxb << G.logNyb, ymask = G.nyb - 1;
-#pragma unroll 2
-    for (uint32_t b = warp; b < nblk; b += NC / 32) {
-        const uint32_t base = T.xb[b >> G.logNyb] * G.PD + T.yb[b & ymask];
-        double2 v0 = sb[base + f.old[0]], v1 = sb[base + f.old[1]];
-        if (cld0)
-            v0.y = -v0.y;
-        if (cld1)
-            v1.y = -v1.y;
-        // stage 1: Y = L B
-        double yr0 = 0.0, yr1 = 0.0, yi0 = 0.0, yi1 = 0.0;
-        dmma_acc(yr0, yr1, f.lr[0], v0.x);
-        dmma_acc(yr0, yr1, f.lr[1], v1.x);
-        dmma_acc(yr0, yr1, f.nli[0], v0.y);
-        dmma_acc(yr0, yr1, f.nli[1], v1.y);
-        dmma_acc(yi0, yi1, f.lr[0], v0.y);
-        dmma_acc(yi0, yi1, f.lr[1], v1.y);
-        dmma_acc(yi0, yi1, f.li[0], v0.x);
-        dmma_acc(yi0, yi1, f.li[1], v1.x);
-        // stage 2: Z = Y L^dagger; B fragment of chunk j = conj(L[g][2c + j])
-        double zr0 = 0.0, zr1 = 0.0, zi0 = 0.0, zi1 = 0.0;
-        dmma_acc(zr0, zr1, yr0, f.lr[0]);
-        dmma_acc(zr0, zr1, yr1, f.lr[1]);
-        dmma_acc(zr0, zr1, yi0, f.li[0]);
-        dmma_acc(zr0, zr1, yi1, f.li[1]);
-        dmma_acc(zi0, zi1, yr0, f.nli[0]);
-        dmma_acc(zi0, zi1, yr1, f.nli[1]);
-        dmma_acc(zi0, zi1, yi0, f.lr[0]);
-        dmma_acc(zi0, zi1, yi1, f.lr[1]);
-        sb[base + f.ost[0]] = make_double2(zr0, cst0 ? -zi0 : zi0);
-        sb[base + f.ost[1]] = make_double2(zr1, cst1 ? -zi1 : zi1);
+    // two blocks per pass: four independent accumulator chains per stage keep the FP64 tensor
+    // pipe fed (nblk = 64 is a multiple of 2 * NC / 32)
+    for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32)) {
+        uint32_t base[2];
+        double2 v0[2], v1[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t bq = b + q * (NC / 32);
+            base[q] = T.xb[bq >> G.logNyb] * G.PD + T.yb[bq & ymask];
+            v0[q] = sb[base[q] + f.old[0]];
+            v1[q] = sb[base[q] + f.old[1]];
+            v0[q].y = flip_sign(v0[q].y, cld0);
+            v1[q].y = flip_sign(v1[q].y, cld1);
+        }
+        // 3M form (Gauss): three real products per complex product.  Stage 1: Y = L B with
+        // T1 = Lr Br, T2 = Li Bi, T3 = (Lr + Li)(Br + Bi); Yr = T1 - T2, Yi = T3 - T1 - T2
+        double yr0[2], yr1[2], yi0[2], yi1[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            double t1a = 0.0, t1b = 0.0, t2a = 0.0, t2b = 0.0, t3a = 0.0, t3b = 0.0;
+            const double s0 = v0[q].x + v0[q].y, s1 = v1[q].x + v1[q].y;
+            dmma_acc(t1a, t1b, f.lr[0], v0[q].x);
+            dmma_acc(t2a, t2b, f.li[0], v0[q].y);
+            dmma_acc(t3a, t3b, f.ls[0], s0);
+            dmma_acc(t1a, t1b, f.lr[1], v1[q].x);
+            dmma_acc(t2a, t2b, f.li[1], v1[q].y);
+            dmma_acc(t3a, t3b, f.ls[1], s1);
+            yr0[q] = t1a - t2a;
+            yr1[q] = t1b - t2b;
+            yi0[q] = t3a - t1a - t2a;
+            yi1[q] = t3b - t1b - t2b;
+        }
+        // stage 2: Z = Y P, P = L^dagger (B fragment of chunk j: P[2c + j][g] = conj(L[g][2c + j]));
+        // U1 = Yr Pr, U2 = Yi Pi, U3 = (Yr + Yi)(Pr + Pi); Zr = U1 - U2, Zi = U3 - U1 - U2
+        double zr0[2], zr1[2], zi0[2], zi1[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
+            const double s0 = yr0[q] + yi0[q], s1 = yr1[q] + yi1[q];
+            dmma_acc(u1a, u1b, yr0[q], f.lr[0]);
+            dmma_acc(u2a, u2b, yi0[q], f.nli[0]);
+            dmma_acc(u3a, u3b, s0, f.ld[0]);
+            dmma_acc(u1a, u1b, yr1[q], f.lr[1]);
+            dmma_acc(u2a, u2b, yi1[q], f.nli[1]);
+            dmma_acc(u3a, u3b, s1, f.ld[1]);
+            zr0[q] = u1a - u2a;
+            zr1[q] = u1b - u2b;
+            zi0[q] = u3a - u1a - u2a;
+            zi1[q] = u3b - u1b - u2b;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            sb[base[q] + f.ost[0]] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
+            sb[base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
+        }
     }
 }
 
-// Two ping-pong groups of NC / 2 threads: group (i & 1) transforms and writes back local item i,
-// then loads item i + 3 (the other group's) into the stage it just freed.  One group's FP64 tensor
-// work overlaps the other's HBM traffic.  Stage s's `full` mbarrier completes when every thread of
-// the loading group has arrived twice: once on release (tile tables written) and once, via
-// cp.async.mbarrier.arrive.noinc, when its copies have landed.
 template <int K, int MODE, int NS, int NC>
 __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     constexpr uint32_t NH = NC / 2;  // threads per group
@@ -1414,20 +1443,26 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
     const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
     // NH is a multiple of S0^2: every element this thread moves sits at the same sub-block
     // position (i, jj) in stored order, in tiles tt = gtid / S0^2 + k * NH / S0^2
-    const uint32_t r = gtid & ((1u << logT) - 1), i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
-    const uint32_t tt0 = gtid >> logT, ttstep = NH >> logT;
-    const uint32_t sm_d = i0 * P + j0, sm_a = j0 * P + i0;  // logical slot, direct / adjoint
+    // positions moved by this thread: npos = max(1, S0^2 / NH) sub-block positions
+    // r = (gtid mod S0^2) + q * NH, each in tiles tt = tt0 + k * ttstep
+    const uint32_t T2 = 1u << logT;
+    const uint32_t npos = T2 > NH ? T2 / NH : 1u;
+    const uint32_t tt0 = T2 > NH ? 0u : gtid >> logT, ttstep = T2 > NH ? 1u : NH >> logT;
     const uint32_t nsbm = (1u << (2 * G.log_nsb_side)) - 1;
     const uint32_t barid = 1 + grp;
     auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NH) : "memory"); };
 
     auto item_of = [&](uint64_t j) { return blockIdx.x + j * gridDim.x; };
-    // global offsets (within a tile) of this thread's sub-block position, direct / adjoint
-    auto offsets = [&](uint64_t item, uint32_t& od, uint32_t& oa) {
+    // global offsets (within a tile) of this thread's q-th sub-block position, direct / adjoint,
+    // and its logical staging slot (direct / adjoint placement)
+    auto offsets = [&](uint64_t item, uint32_t q, uint32_t& od, uint32_t& oa, uint32_t& sm_d, uint32_t& sm_a) {
+        const uint32_t r = (gtid & (T2 - 1)) + q * NH, i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
         const uint32_t sb = (uint32_t)(item & nsbm);
         const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
         od = ((x0 | T.xdep[i0]) << G.logM) + (y0 | T.xdep[j0]);
         oa = ((y0 | T.xdep[i0]) << G.logM) + (x0 | T.xdep[j0]);
+        sm_d = i0 * P + j0;
+        sm_a = j0 * P + i0;
     };
     // this group loads item j into stage j % S (tile table, adjoint mask, copies, arrivals)
     auto load = [&](uint64_t j) {
@@ -1453,16 +1488,19 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
             if (gtid == 0)
                 am[s][0] = m;
         }
-        uint32_t od, oa;
-        offsets(item_of(j), od, oa);
         const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
-        for (uint32_t tt = tt0; tt < NT; tt += ttstep) {
-            const uint64_t ent = gt[s][tt];
-            if (ent & F_SKIP)
-                continue;
-            const bool adj = (ent & F_ADJ) != 0;
-            const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
-            cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, ((ent & F_REMOTE) ? G.recv : st) + g);
+        for (uint32_t q = 0; q < npos; ++q) {
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(j), q, od, oa, sm_d, sm_a);
+            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 2u); tt += ttstep) {
+                const uint64_t ent = gt[s][tt];
+                if (ent & F_SKIP)
+                    continue;
+                const bool adj = (ent & F_ADJ) != 0;
+                const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
+                cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u,
+                           ((ent & F_REMOTE) ? G.recv : st) + g);
+            }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
         mbar_arrive(&full[s]);
@@ -1486,10 +1524,10 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
         }
         gbar();
         // write back along stored rows (adjoint components are already in stored, conjugated form)
-        {
-            uint32_t od, oa;
-            offsets(item_of(i), od, oa);
-            for (uint32_t tt = tt0; tt < NT; tt += ttstep) {
+        for (uint32_t q = 0; q < npos; ++q) {
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(i), q, od, oa, sm_d, sm_a);
+            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 4u); tt += ttstep) {
                 const uint64_t ent = gt[s][tt];
                 if (ent & (F_SKIP | F_NOSTORE))
                     continue;
@@ -2196,9 +2234,10 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         }
         return HS_OK;
     }
-    if (MODE != M_KRAUS && G.g >= 2 && G.slabs > 1) {
-        // units of 16 / 64 stored tiles: sub-block gather kernel for the off-diagonal units,
-        // the slab kernel's wedge path for the diagonal ones
+    if (MODE != M_KRAUS && ((G.g >= 2 && G.slabs > 1) || (K == 3 && MODE == M_DIRECT && G.g == 1))) {
+        // units of 16 / 64 stored tiles (and k = 3 unitaries on one grid bit, whose 4-tile units
+        // are whole gather items for the FP64 tensor transform): sub-block gather kernel for the
+        // off-diagonal units, the slab kernel's wedge path for the diagonal ones
         cudaError_t e;
         if (G.nD_items) {
             Geo Gs = G;

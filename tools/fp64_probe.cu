@@ -49,6 +49,26 @@ __global__ void dmma_kernel(double* out, double s) {
         out[0] = r;
 }
 
+template <int CH>
+__global__ void dmma_chains_kernel(double* out, double s) {
+    double acc[CH][2];
+#pragma unroll
+    for (int i = 0; i < CH; ++i)
+        acc[i][0] = acc[i][1] = threadIdx.x * 1e-3 + i;
+    const double a = s, b = 1.0 - s;
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+            dmma(acc[i], a, b);
+    }
+    double r = 0;
+#pragma unroll
+    for (int i = 0; i < CH; ++i)
+        r += acc[i][0] + acc[i][1];
+    if (r == 12345.0)
+        out[0] = r;
+}
+
 __global__ void mixed_kernel(double* out, double s) {
     double acc[4][2];
     double v[8];
@@ -118,6 +138,24 @@ int main() {
                threads, fl_dfma / ms / 1e9, fl_dmma / ms2 / 1e9, fl_mix / ms3 / 1e9,
                2.0 * 256 * 4 * ITERS * (double)blocks * threads / 32 / ms3 / 1e9,
                2.0 * 8 * ITERS * (double)blocks * threads / ms3 / 1e9);
+    }
+    // DMMA rate vs resident warps per SM and independent accumulator chains per warp
+    for (int warps : {4, 8, 16, 32}) {
+        auto run = [&](auto kern, int ch) {
+            float ms;
+            kern<<<sms, warps * 32>>>(out, 0.999);
+            cudaEventRecord(e0);
+            kern<<<sms, warps * 32>>>(out, 0.999);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double fl = 2.0 * 256 * ch * ITERS * (double)sms * warps;
+            printf("  warps/SM=%d chains=%d: DMMA %.2f TFLOP/s\n", warps, ch, fl / ms / 1e9);
+        };
+        run(dmma_chains_kernel<1>, 1);
+        run(dmma_chains_kernel<2>, 2);
+        run(dmma_chains_kernel<4>, 4);
+        run(dmma_chains_kernel<8>, 8);
     }
     cudaError_t e = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(e));
