@@ -1351,14 +1351,16 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
     const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
     const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
     const uint32_t nblk = G.nxb << G.logNyb, ymask = G.nyb - 1;
-    // two blocks per pass: four independent accumulator chains per stage keep the FP64 tensor
-    // pipe fed (nblk = 64 is a multiple of 2 * NC / 32)
+    // two blocks per pass: independent accumulator chains keep the FP64 tensor pipe fed (small
+    // tiles, m < 5, have fewer blocks than warps: the second block of a pass may be absent and is
+    // then computed on a copy of the first and not stored)
     for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32)) {
         uint32_t base[2];
         double2 v0[2], v1[2];
+        const bool two = b + NC / 32 < nblk;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-            const uint32_t bq = b + q * (NC / 32);
+            const uint32_t bq = (q && two) ? b + NC / 32 : b;
             base[q] = T.xb[bq >> G.logNyb] * G.PD + T.yb[bq & ymask];
             v0[q] = sb[base[q] + f.old[0]];
             v1[q] = sb[base[q] + f.old[1]];
@@ -1403,6 +1405,8 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
+            if (q && !two)
+                break;
             sb[base[q] + f.ost[0]] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
             sb[base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
         }
