@@ -1413,6 +1413,7 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
     }
 }
 
+__device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group
 template <int K, int MODE, int NS, int NC>
 __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     constexpr uint32_t NH = NC / 2;  // threads per group
@@ -1516,9 +1517,13 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
     for (uint64_t j = 0; j < S && j < nlocal; ++j)  // item j is loaded by group (j + 1) & 1
         if (((j + 1) & 1) == grp)
             load(j);
+    const bool prof = (G.dbg & 16u) && gtid == 0;  // phase timing (diagnostics): wait / transform / write-back / load
+    long long ph[4] = {0, 0, 0, 0};
     for (uint64_t i = grp; i < nlocal; i += 2) {
         const uint32_t s = (uint32_t)(i % S);
+        long long t0 = prof ? clock64() : 0;
         mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+        long long t1 = prof ? clock64() : 0;
         double2* sb = ring + (size_t)s * G.stage_elems;
         if (!(G.dbg & 1u)) {
             if constexpr (K == 3 && MODE == M_DIRECT)
@@ -1527,6 +1532,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
                 pipe_compute<K, MODE, NS, NH>(G, T, cf, am[s], 1, sb, 0, (int)gtid, barid);
         }
         gbar();
+        long long t2 = prof ? clock64() : 0;
         // write back along stored rows (adjoint components are already in stored, conjugated form)
         for (uint32_t q = 0; q < npos; ++q) {
             uint32_t od, oa, sm_d, sm_a;
@@ -1540,9 +1546,20 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
             }
         }
         gbar();
+        long long t3 = prof ? clock64() : 0;
         if (i + S < nlocal)
             load(i + S);
+        if (prof) {
+            const long long t4 = clock64();
+            ph[0] += t1 - t0;
+            ph[1] += t2 - t1;
+            ph[2] += t3 - t2;
+            ph[3] += t4 - t3;
+        }
     }
+    if (prof)
+        for (int q = 0; q < 4; ++q)
+            atomicAdd(&g_phase_cycles[grp * 4 + q], (unsigned long long)ph[q]);
     cp_async_wait<0>();
 }
 
@@ -3271,3 +3288,14 @@ int hs_event_elapsed_ms(void* start, void* stop, float* ms) {
 }
 
 }  // extern "C"
+
+// Diagnostics: gather-kernel phase cycles summed over CTAs (HS_DEBUG_FLAGS bit 4), read and reset.
+extern "C" int hs_debug_phase_cycles(unsigned long long* out8) {
+    if (!out8)
+        return set_err(HS_ERR_INVALID, "null out");
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(out8, g_phase_cycles, 8 * sizeof(unsigned long long)));
+    unsigned long long z[8] = {0};
+    CUDA_TRY(cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)));
+    return HS_OK;
+}
