@@ -1563,6 +1563,147 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
     cp_async_wait<0>();
 }
 
+// Warp-specialised gather for the k = 3 tensor-core transform: 8 transform warps and 16 copy warps
+// (768 threads).  The copy warps write back item i as soon as the transform warps release its stage
+// (`done`), then load item i + 3 into it (`full`, cp.async tracked by the mbarrier); the transform
+// warps only wait for data and run DMMA.  The 16 copy warps keep twice the memory-instruction
+// parallelism of a ping-pong group, and the transform never waits for its own write-back or loads.
+// (Register-staged loads in place of cp.async were 1.6x slower here.)
+template <int NS>
+__global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
+    constexpr uint32_t NCW = 256, NMW = 512, S = 3;
+    extern __shared__ __align__(128) double2 ring[];
+    __shared__ uint64_t gt[S][64];
+    __shared__ uint64_t am[S][1];
+    __shared__ __align__(8) uint64_t full[S], done[S];
+    __shared__ Tabs T;
+    const uint32_t tid = threadIdx.x;
+    if (tid < 32) {
+        T.xdep[tid] = G.xdep[tid];
+        T.xb[tid] = G.xb_tab[tid];
+        T.yb[tid] = G.yb_tab[tid];
+        if (tid < 8) {
+            T.xs_in[tid] = G.xs_in[tid];
+            T.y_in[tid] = G.y_in[tid];
+        }
+    }
+    if (tid < 64) {
+        T.cdir[tid] = G.cdir[tid];
+        T.cadj[tid] = G.cadj[tid];
+        T.ttr[tid] = G.ttr[tid];
+        T.tsk[tid] = G.tsk[tid];
+    }
+    if (tid == 0)
+        for (uint32_t q = 0; q < S; ++q) {
+            mbar_init(&full[q], 2 * NMW);
+            mbar_init(&done[q], NCW);
+        }
+    const uint64_t nItems = G.nG_items;
+    const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto item_of = [&](uint64_t j) { return blockIdx.x + j * gridDim.x; };
+    __syncthreads();
+    if (tid < NCW) {
+        // ---- transform warps
+        const DmmaFrag fr = dmma_frag(T, cf);
+        for (uint64_t i = 0; i < nlocal; ++i) {
+            const uint32_t s = (uint32_t)(i % S);
+            mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+            if (!(G.dbg & 1u))
+                dmma_direct3<NCW>(G, T, fr, am[s][0], ring + (size_t)s * G.stage_elems, tid >> 5);
+            mbar_arrive(&done[s]);
+        }
+        return;
+    }
+    // ---- copy warps
+    const uint32_t mtid = tid - NCW;
+    const uint32_t NT = 1u << G.logNT, NGm = (1u << G.logNG) - 1;
+    const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
+    const uint32_t T2 = 1u << logT;
+    const uint32_t npos = T2 > NMW ? T2 / NMW : 1u;
+    const uint32_t tt0 = T2 > NMW ? 0u : mtid >> logT, ttstep = T2 > NMW ? 1u : NMW >> logT;
+    const uint32_t nsbm = (1u << (2 * G.log_nsb_side)) - 1;
+    auto mbar_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NMW) : "memory"); };
+    auto offsets = [&](uint64_t item, uint32_t q, uint32_t& od, uint32_t& oa, uint32_t& sm_d, uint32_t& sm_a) {
+        const uint32_t r = (mtid & (T2 - 1)) + q * NMW, i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
+        const uint32_t sb = (uint32_t)(item & nsbm);
+        const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
+        od = ((x0 | T.xdep[i0]) << G.logM) + (y0 | T.xdep[j0]);
+        oa = ((y0 | T.xdep[i0]) << G.logM) + (x0 | T.xdep[j0]);
+        sm_d = i0 * P + j0;
+        sm_a = j0 * P + i0;
+    };
+    auto load = [&](uint64_t j) {
+        const uint32_t s = (uint32_t)(j % S);
+        if (mtid < NT) {
+            uint64_t tbi, tbj;
+            unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), true, tbi, tbj);
+            const uint64_t tr = ins_bits(tbi, mtid >> G.logNG, G.gr_pos, G.g);
+            const uint64_t tc = ins_bits(tbj, mtid & NGm, G.gr_pos, G.g);
+            gt[s][mtid] = tile_entry(G, tr, tc);
+        }
+        mbar_sync();
+        if (mtid < 32) {
+            unsigned long long m = 0;
+            for (uint32_t t = mtid; t < NT; t += 32)
+                m |= (unsigned long long)((gt[s][t] & F_ADJ) != 0) << t;
+            for (int o = 16; o; o >>= 1)
+                m |= __shfl_xor_sync(0xffffffffu, m, o);
+            if (mtid == 0)
+                am[s][0] = m;
+        }
+        const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
+        for (uint32_t q = 0; q < npos; ++q) {
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(j), q, od, oa, sm_d, sm_a);
+            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 2u); tt += ttstep) {
+                const uint64_t ent = gt[s][tt];
+                const bool adj = (ent & F_ADJ) != 0;
+                const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
+                cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u,
+                           ((ent & F_REMOTE) ? G.recv : st) + g);
+            }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        mbar_arrive(&full[s]);
+    };
+    const bool prof = (G.dbg & 16u) && mtid == 0;
+    long long ph[4] = {0, 0, 0, 0};
+    for (uint64_t j = 0; j < S && j < nlocal; ++j)
+        load(j);
+    for (uint64_t i = 0; i < nlocal; ++i) {
+        const uint32_t s = (uint32_t)(i % S);
+        const long long t0 = prof ? clock64() : 0;
+        mbar_wait(&done[s], (uint32_t)((i / S) & 1));
+        const long long t1 = prof ? clock64() : 0;
+        const double2* sb = ring + (size_t)s * G.stage_elems;
+        for (uint32_t q = 0; q < npos; ++q) {
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(i), q, od, oa, sm_d, sm_a);
+            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 4u); tt += ttstep) {
+                const uint64_t ent = gt[s][tt];
+                if (ent & F_NOSTORE)
+                    continue;
+                const bool adj = (ent & F_ADJ) != 0;
+                st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+            }
+        }
+        mbar_sync();  // every write-back read of stage s (and of gt[s]) is done
+        const long long t2 = prof ? clock64() : 0;
+        if (i + S < nlocal)
+            load(i + S);
+        if (prof) {
+            const long long t3 = clock64();
+            ph[0] += t1 - t0;
+            ph[2] += t2 - t1;
+            ph[3] += t3 - t2;
+        }
+    }
+    if (prof)
+        for (int q = 0; q < 4; ++q)
+            atomicAdd(&g_phase_cycles[q], (unsigned long long)ph[q]);
+    cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------------- reductions
 // Per-CTA partial sums over a contiguous tile range, fixed order, then a single-CTA
 // ordered sum: deterministic for a given grid (SPEC.md observables: fixed-order reduction).
@@ -2284,6 +2425,21 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         }
         if (Gg.nG_items) {
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
+            if constexpr (dmma) {
+                if (!(Gg.dbg & 32u)) {  // warp-specialised variant (bit 5: the ping-pong kernel instead)
+                    auto kw = gather_ws_kernel<NS>;
+                    e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                    if (e != cudaSuccess)
+                        return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
+                    const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
+                    kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d);
+                    g_launches.fetch_add(1, std::memory_order_relaxed);
+                    e = cudaGetLastError();
+                    if (e != cudaSuccess)
+                        return set_err(HS_ERR_CUDA, std::string("gather_ws_kernel launch: ") + cudaGetErrorString(e));
+                    return HS_OK;
+                }
+            }
             constexpr int NC = 512;  // two groups of 256 (a multiple of the S0^2 positions of an item)
             auto kern = gather_kernel<K, MODE, NS, NC>;
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
