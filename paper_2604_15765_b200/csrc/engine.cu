@@ -1573,8 +1573,8 @@ template <int NS>
 __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     constexpr uint32_t NCW = 256, NMW = 512, S = 3;
     extern __shared__ __align__(128) double2 ring[];
-    __shared__ uint64_t gt[S][64];
-    __shared__ uint64_t am[S][1];
+    __shared__ uint64_t gt[S + 1][64];  // tile tables by item % (S + 1): built one item ahead
+    __shared__ uint64_t am[S + 1][1];
     __shared__ __align__(8) uint64_t full[S], done[S];
     __shared__ Tabs T;
     const uint32_t tid = threadIdx.x;
@@ -1609,7 +1609,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
             if (!(G.dbg & 1u))
-                dmma_direct3<NCW>(G, T, fr, am[s][0], ring + (size_t)s * G.stage_elems, tid >> 5);
+                dmma_direct3<NCW>(G, T, fr, am[i % (S + 1)][0], ring + (size_t)s * G.stage_elems, tid >> 5);
             mbar_arrive(&done[s]);
         }
         return;
@@ -1632,31 +1632,34 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         sm_d = i0 * P + j0;
         sm_a = j0 * P + i0;
     };
-    auto load = [&](uint64_t j) {
-        const uint32_t s = (uint32_t)(j % S);
-        if (mtid < NT) {
-            uint64_t tbi, tbj;
-            unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), true, tbi, tbj);
-            const uint64_t tr = ins_bits(tbi, mtid >> G.logNG, G.gr_pos, G.g);
-            const uint64_t tc = ins_bits(tbj, mtid & NGm, G.gr_pos, G.g);
-            gt[s][mtid] = tile_entry(G, tr, tc);
+    // tile table and adjoint mask of item j, by the first copy warp alone (lanes take tiles lane,
+    // lane + 32) into slot j % (S + 1), which no stage in flight uses
+    auto tables = [&](uint64_t j) {
+        const uint32_t ts = (uint32_t)(j % (S + 1));
+        uint64_t tbi, tbj;
+        unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), true, tbi, tbj);
+        unsigned long long m = 0;
+        for (uint32_t t = mtid; t < NT; t += 32) {
+            const uint64_t tr = ins_bits(tbi, t >> G.logNG, G.gr_pos, G.g);
+            const uint64_t tc = ins_bits(tbj, t & NGm, G.gr_pos, G.g);
+            const uint64_t ent = tile_entry(G, tr, tc);
+            gt[ts][t] = ent;
+            m |= (unsigned long long)((ent & F_ADJ) != 0) << t;
         }
-        mbar_sync();
-        if (mtid < 32) {
-            unsigned long long m = 0;
-            for (uint32_t t = mtid; t < NT; t += 32)
-                m |= (unsigned long long)((gt[s][t] & F_ADJ) != 0) << t;
-            for (int o = 16; o; o >>= 1)
-                m |= __shfl_xor_sync(0xffffffffu, m, o);
-            if (mtid == 0)
-                am[s][0] = m;
-        }
+        for (int o = 16; o; o >>= 1)
+            m |= __shfl_xor_sync(0xffffffffu, m, o);
+        if (mtid == 0)
+            am[ts][0] = m;
+    };
+    // cp.async of item j into stage j % S (its table is visible: a copy-warp barrier separates them)
+    auto issue = [&](uint64_t j) {
+        const uint32_t s = (uint32_t)(j % S), ts = (uint32_t)(j % (S + 1));
         const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
         for (uint32_t q = 0; q < npos; ++q) {
             uint32_t od, oa, sm_d, sm_a;
             offsets(item_of(j), q, od, oa, sm_d, sm_a);
             for (uint32_t tt = tt0; tt < NT && !(G.dbg & 2u); tt += ttstep) {
-                const uint64_t ent = gt[s][tt];
+                const uint64_t ent = gt[ts][tt];
                 const bool adj = (ent & F_ADJ) != 0;
                 const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
                 cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u,
@@ -1668,29 +1671,36 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     };
     const bool prof = (G.dbg & 16u) && mtid == 0;
     long long ph[4] = {0, 0, 0, 0};
+    if (mtid < 32)
+        for (uint64_t j = 0; j < S && j < nlocal; ++j)
+            tables(j);
+    mbar_sync();
     for (uint64_t j = 0; j < S && j < nlocal; ++j)
-        load(j);
+        issue(j);
     for (uint64_t i = 0; i < nlocal; ++i) {
-        const uint32_t s = (uint32_t)(i % S);
+        const uint32_t s = (uint32_t)(i % S), ts = (uint32_t)(i % (S + 1));
         const long long t0 = prof ? clock64() : 0;
         mbar_wait(&done[s], (uint32_t)((i / S) & 1));
         const long long t1 = prof ? clock64() : 0;
+        const bool more = i + S < nlocal;
+        if (more && mtid < 32)
+            tables(i + S);
         const double2* sb = ring + (size_t)s * G.stage_elems;
         for (uint32_t q = 0; q < npos; ++q) {
             uint32_t od, oa, sm_d, sm_a;
             offsets(item_of(i), q, od, oa, sm_d, sm_a);
             for (uint32_t tt = tt0; tt < NT && !(G.dbg & 4u); tt += ttstep) {
-                const uint64_t ent = gt[s][tt];
+                const uint64_t ent = gt[ts][tt];
                 if (ent & F_NOSTORE)
                     continue;
                 const bool adj = (ent & F_ADJ) != 0;
                 st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
             }
         }
-        mbar_sync();  // every write-back read of stage s (and of gt[s]) is done
+        mbar_sync();  // every write-back read of stage s is done; the next table is visible
         const long long t2 = prof ? clock64() : 0;
-        if (i + S < nlocal)
-            load(i + S);
+        if (more)
+            issue(i + S);
         if (prof) {
             const long long t3 = clock64();
             ph[0] += t1 - t0;
