@@ -128,6 +128,7 @@ struct Geo {
     const double2* recv;          // group members' payloads, slot j at recv + j * recv_tiles tiles
     uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
     uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): gather bit 0 skips the transform, bit 1 the loads, bit 2 the stores
+    uint32_t rev;                 // sweep the items in reverse order (alternates per launch: L2 reuse)
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
@@ -296,6 +297,13 @@ __device__ __forceinline__ uint64_t tile_entry(const Geo& G, uint64_t tr, uint64
         ent = (ent + (uint64_t)(slot - 1) * G.recv_tiles) | F_REMOTE | F_NOSTORE;
     }
     return ent;
+}
+// Item j of this CTA (persistent kernels: items blockIdx + j * gridDim).  Consecutive operations
+// sweep the state in opposite directions, so the lines the previous operation wrote last (still in
+// the 126 MB L2) are read first: an L2-sized state (n = 12: 135 MB) is then largely served from L2.
+__device__ __forceinline__ uint64_t sweep_item(const Geo& G, uint64_t n_items, uint64_t j) {
+    const uint64_t it = blockIdx.x + j * gridDim.x;
+    return G.rev ? n_items - 1 - it : it;
 }
 // local unit u -> grid base pair (tbi, tbj); strict: off-diagonal units only
 __device__ __forceinline__ void unit_decode(const Geo& G, uint64_t u, bool strict, uint64_t& tbi, uint64_t& tbj) {
@@ -1229,7 +1237,7 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
         for (uint64_t j = p; j < nlocal + S; j += S) {
             uint32_t bytes = 0;
             if (j < nlocal) {  // metadata of item j, prepared before the stage is free
-                item_tiles<MODE>(G, blockIdx.x + j * gridDim.x, gn, lane);
+                item_tiles<MODE>(G, sweep_item(G, nItems, j), gn, lane);
                 __syncwarp();
                 uint32_t cnt = 0;
                 for (uint32_t t = lane; t < ntt; t += 32)
@@ -1241,7 +1249,7 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
             if (j >= S) {
                 const uint64_t jj = j - S;
                 mbar_wait(&done[p], (uint32_t)((jj / S) & 1));
-                item_copies<true>(G, T, blockIdx.x + jj * gridDim.x, gt[p], sb, st, nullptr, lane);
+                item_copies<true>(G, T, sweep_item(G, nItems, jj), gt[p], sb, st, nullptr, lane);
                 bulk_commit();
             }
             if (j < nlocal) {
@@ -1261,7 +1269,7 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
                 if (lane == 0)
                     mbar_arrive_expect(&full[p], bytes);
                 __syncwarp();
-                item_copies<false>(G, T, blockIdx.x + j * gridDim.x, gt[p], sb, st, &full[p], lane);
+                item_copies<false>(G, T, sweep_item(G, nItems, j), gt[p], sb, st, &full[p], lane);
             }
         }
         bulk_wait_all();
@@ -1271,7 +1279,7 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
     for (uint64_t i = 0; i < nlocal; ++i) {
         const uint32_t s = (uint32_t)(i % S);
         double2* sb = ring + (size_t)s * G.stage_elems;
-        const uint64_t item = blockIdx.x + i * gridDim.x;
+        const uint64_t item = sweep_item(G, nItems, i);
         const uint32_t grp = G.groups ? (uint32_t)(item % G.groups) : 0;
         const uint64_t u0 = G.groups ? item / G.groups : (item >> G.logSlabs) << G.logU;
         const uint32_t nvalid = G.nU_units - u0 < G.U ? (uint32_t)(G.nU_units - u0) : G.U;
@@ -1457,7 +1465,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
     const uint32_t barid = 1 + grp;
     auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NH) : "memory"); };
 
-    auto item_of = [&](uint64_t j) { return blockIdx.x + j * gridDim.x; };
+    auto item_of = [&](uint64_t j) { return sweep_item(G, nItems, j); };
     // global offsets (within a tile) of this thread's q-th sub-block position, direct / adjoint,
     // and its logical staging slot (direct / adjoint placement)
     auto offsets = [&](uint64_t item, uint32_t q, uint32_t& od, uint32_t& oa, uint32_t& sm_d, uint32_t& sm_a) {
@@ -1600,7 +1608,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         }
     const uint64_t nItems = G.nG_items;
     const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    auto item_of = [&](uint64_t j) { return blockIdx.x + j * gridDim.x; };
+    auto item_of = [&](uint64_t j) { return sweep_item(G, nItems, j); };
     __syncthreads();
     if (tid < NCW) {
         // ---- transform warps
@@ -1912,6 +1920,7 @@ struct hs_state {
     uint32_t Plog = 0, logB = 0, shard = 0;
     double2* recv = nullptr;  // group members' payloads for cross-shard operations (slots)
     uint64_t recv_count = 0;  // elements per slot (the largest shard)
+    uint64_t sweeps = 0;      // launches so far (alternating sweep direction)
     uint32_t recv_slots = 0;  // allocated slots
     uint32_t recv_mask = 0;   // shard-bit mask of the last exchange (which slots hold whom)
     void* comm = nullptr;     // ncclComm_t
@@ -2371,6 +2380,8 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
     if (G0.cross && (!h->recv || h->recv_slots < (1u << G0.cross) - 1 || h->recv_mask != G0.cmask))
         return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the group's shards first");
     Geo G = G0;
+    G.rev = (uint32_t)(h->sweeps++ & 1u);
+    G.dbg = 0;
     if (MODE == M_MONO && G.groups) {
         // tile permutation on >= 2 grid bits: whole-tile pipeline, items = (unit, cycle group);
         // diagonal units through the slab kernel's wedge path

@@ -69,6 +69,31 @@ __global__ void dmma_chains_kernel(double* out, double s) {
         out[0] = r;
 }
 
+// distinct A/B operands per chain (as in the 3M transform: every DMMA reads its own registers)
+template <int CH>
+__global__ void dmma_distinct_kernel(double* out, double s) {
+    double acc[CH][2], a[CH], b[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+        acc[i][0] = acc[i][1] = threadIdx.x * 1e-3 + i;
+        a[i] = s + i * 1e-3;
+        b[i] = 1.0 - s - i * 1e-3;
+    }
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            dmma(acc[i], a[i], b[(i + it) % CH]);
+            a[i] = acc[i][1];
+        }
+    }
+    double r = 0;
+#pragma unroll
+    for (int i = 0; i < CH; ++i)
+        r += acc[i][0] + acc[i][1];
+    if (r == 12345.0)
+        out[0] = r;
+}
+
 __global__ void mixed_kernel(double* out, double s) {
     double acc[4][2];
     double v[8];
@@ -156,6 +181,9 @@ int main() {
         run(dmma_chains_kernel<2>, 2);
         run(dmma_chains_kernel<4>, 4);
         run(dmma_chains_kernel<8>, 8);
+        printf("  distinct operands:\n");
+        run(dmma_distinct_kernel<2>, 2);
+        run(dmma_distinct_kernel<6>, 6);
     }
     cudaError_t e = cudaGetLastError();
     printf("status: %s\n", cudaGetErrorString(e));
