@@ -1333,32 +1333,51 @@ struct DmmaFrag {
     uint32_t old[2], ost[2];  // staging offsets of the loaded / stored components (from the block base)
     uint32_t tld[2], tst[2];  // their logical tiles (adjoint mask bits)
 };
-template <int NS>
-__device__ __forceinline__ DmmaFrag dmma_frag(const Tabs& T, const Coef<NS>& cf) {
+// k = 3: the 8 x 8 block itself.  k = 2: four 4 x 4 blocks (2X + R1, 2Y + C1) as the quadrants of
+// one 8 x 8 matrix M, transformed by I2 (x) L: (I2 (x) L) M (I2 (x) L)^dagger applies L . L^dagger to
+// every quadrant, so one tensor-core transform serves four k = 2 blocks (kin = 0: quadrant
+// offsets are R1 * PD + C1, folded into the component offsets).
+template <int K, int NS>
+__device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const Coef<NS>& cf) {
     DmmaFrag f;
     const uint32_t lane = threadIdx.x & 31, gq = lane >> 2, cq = lane & 3;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        const double2 l = cf.s[gq * 8 + 2 * cq + j];
+        const uint32_t c8 = 2 * cq + j;
+        double2 l;
+        if constexpr (K == 3)
+            l = cf.s[gq * 8 + c8];
+        else
+            l = (gq >> 2) == (c8 >> 2) ? cf.s[(gq & 3) * 4 + (c8 & 3)] : make_double2(0.0, 0.0);
         f.lr[j] = l.x;
         f.li[j] = l.y;
         f.nli[j] = -l.y;
         f.ls[j] = l.x + l.y;
         f.ld[j] = l.x - l.y;
-        const uint32_t il = (2 * cq + j) * 8 + gq, is = gq * 8 + 2 * cq + j;
-        f.old[j] = T.cdir[il];
-        f.ost[j] = T.cdir[is];
-        f.tld[j] = T.ttr[il];
-        f.tst[j] = T.ttr[is];
+        if constexpr (K == 3) {
+            const uint32_t il = c8 * 8 + gq, is = gq * 8 + c8;
+            f.old[j] = T.cdir[il];
+            f.ost[j] = T.cdir[is];
+            f.tld[j] = T.ttr[il];
+            f.tst[j] = T.ttr[is];
+        } else {
+            // load component (row c8, column gq), store component (row gq, column c8) of M
+            const uint32_t il = (c8 & 3) * 4 + (gq & 3), is = (gq & 3) * 4 + (c8 & 3);
+            f.old[j] = T.cdir[il] + (c8 >> 2) * G.PD + (gq >> 2);
+            f.ost[j] = T.cdir[is] + (gq >> 2) * G.PD + (c8 >> 2);
+            f.tld[j] = T.ttr[il];
+            f.tst[j] = T.ttr[is];
+        }
     }
     return f;
 }
-template <int NC>
+template <int NC, int K = 3>
 __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
                                              double2* sb, uint32_t warp) {
+    constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
     const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
     const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
-    const uint32_t nblk = G.nxb << G.logNyb, ymask = G.nyb - 1;
+    const uint32_t logNy = G.logNyb - sh, nblk = (G.nxb >> sh) << logNy, ymask = (G.nyb >> sh) - 1;
     // two blocks per pass: independent accumulator chains keep the FP64 tensor pipe fed (small
     // tiles, m < 5, have fewer blocks than warps: the second block of a pass may be absent and is
     // then computed on a copy of the first and not stored)
@@ -1369,7 +1388,7 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const uint32_t bq = (q && two) ? b + NC / 32 : b;
-            base[q] = T.xb[bq >> G.logNyb] * G.PD + T.yb[bq & ymask];
+            base[q] = T.xb[(bq >> logNy) << sh] * G.PD + T.yb[(bq & ymask) << sh];
             v0[q] = sb[base[q] + f.old[0]];
             v1[q] = sb[base[q] + f.old[1]];
             v0[q].y = flip_sign(v0[q].y, cld0);
@@ -1521,7 +1540,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
     __syncthreads();
     DmmaFrag fr;
     if constexpr (K == 3 && MODE == M_DIRECT)
-        fr = dmma_frag(T, cf);
+        fr = dmma_frag<3>(G, T, cf);
     for (uint64_t j = 0; j < S && j < nlocal; ++j)  // item j is loaded by group (j + 1) & 1
         if (((j + 1) & 1) == grp)
             load(j);
@@ -1577,7 +1596,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
 // warps only wait for data and run DMMA.  The 16 copy warps keep twice the memory-instruction
 // parallelism of a ping-pong group, and the transform never waits for its own write-back or loads.
 // (Register-staged loads in place of cp.async were 1.6x slower here.)
-template <int NS>
+template <int K, int NS>
 __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     constexpr uint32_t NCW = 256, NMW = 512, S = 3;
     extern __shared__ __align__(128) double2 ring[];
@@ -1612,12 +1631,12 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     __syncthreads();
     if (tid < NCW) {
         // ---- transform warps
-        const DmmaFrag fr = dmma_frag(T, cf);
+        const DmmaFrag fr = dmma_frag<K>(G, T, cf);
         for (uint64_t i = 0; i < nlocal; ++i) {
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
             if (!(G.dbg & 1u))
-                dmma_direct3<NCW>(G, T, fr, am[i % (S + 1)][0], ring + (size_t)s * G.stage_elems, tid >> 5);
+                dmma_direct3<NCW, K>(G, T, fr, am[i % (S + 1)][0], ring + (size_t)s * G.stage_elems, tid >> 5);
             mbar_arrive(&done[s]);
         }
         return;
@@ -2446,9 +2465,11 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         }
         if (Gg.nG_items) {
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
-            if constexpr (dmma) {
-                if (!(Gg.dbg & 32u)) {  // warp-specialised variant (bit 5: the ping-pong kernel instead)
-                    auto kw = gather_ws_kernel<NS>;
+            // tensor-core transform in the warp-specialised kernel (bit 5: the ping-pong kernel instead);
+            // k = 2 pairs blocks two by two in each direction
+            if constexpr (K == 3 ? dmma : (K == 2 && MODE == M_DIRECT)) {
+                if (!(Gg.dbg & 32u) && (K == 3 || (Gg.nxb >= 2 && Gg.nyb >= 2 && Gg.kin == 0))) {
+                    auto kw = gather_ws_kernel<K, NS>;
                     e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     if (e != cudaSuccess)
                         return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
