@@ -1649,6 +1649,8 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     const uint32_t npos = T2 > NMW ? T2 / NMW : 1u;
     const uint32_t tt0 = T2 > NMW ? 0u : mtid >> logT, ttstep = T2 > NMW ? 1u : NMW >> logT;
     const uint32_t nsbm = (1u << (2 * G.log_nsb_side)) - 1;
+    const bool fast = npos == 1 && (NT << logT) == 8 * NMW;  // every thread moves 8 tiles at one position
+    const bool fast2 = npos == 2 && NT == 4;                  // or 4 tiles at two positions (whole-tile units)
     auto mbar_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NMW) : "memory"); };
     auto offsets = [&](uint64_t item, uint32_t q, uint32_t& od, uint32_t& oa, uint32_t& sm_d, uint32_t& sm_a) {
         const uint32_t r = (mtid & (T2 - 1)) + q * NMW, i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
@@ -1682,15 +1684,34 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     auto issue = [&](uint64_t j) {
         const uint32_t s = (uint32_t)(j % S), ts = (uint32_t)(j % (S + 1));
         const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
-        for (uint32_t q = 0; q < npos; ++q) {
+        auto one = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
+            const uint64_t ent = gt[ts][tt];
+            const bool adj = (ent & F_ADJ) != 0;
+            const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
+            cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, ((ent & F_REMOTE) ? G.recv : st) + g);
+        };
+        if (G.dbg & 2u) {
+        } else if (fast) {  // 8 tiles at one position: unrolled, table reads hoisted
             uint32_t od, oa, sm_d, sm_a;
-            offsets(item_of(j), q, od, oa, sm_d, sm_a);
-            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 2u); tt += ttstep) {
-                const uint64_t ent = gt[ts][tt];
-                const bool adj = (ent & F_ADJ) != 0;
-                const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
-                cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u,
-                           ((ent & F_REMOTE) ? G.recv : st) + g);
+            offsets(item_of(j), 0, od, oa, sm_d, sm_a);
+#pragma unroll
+            for (uint32_t e = 0; e < 8; ++e)
+                one(tt0 + e * ttstep, od, oa, sm_d, sm_a);
+        } else if (fast2) {
+#pragma unroll
+            for (uint32_t q = 0; q < 2; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(j), q, od, oa, sm_d, sm_a);
+#pragma unroll
+                for (uint32_t tt = 0; tt < 4; ++tt)
+                    one(tt, od, oa, sm_d, sm_a);
+            }
+        } else {
+            for (uint32_t q = 0; q < npos; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(j), q, od, oa, sm_d, sm_a);
+                for (uint32_t tt = tt0; tt < NT; tt += ttstep)
+                    one(tt, od, oa, sm_d, sm_a);
             }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
@@ -1713,15 +1734,35 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         if (more && mtid < 32)
             tables(i + S);
         const double2* sb = ring + (size_t)s * G.stage_elems;
-        for (uint32_t q = 0; q < npos; ++q) {
+        auto wb = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
+            const uint64_t ent = gt[ts][tt];
+            if (ent & F_NOSTORE)
+                return;
+            const bool adj = (ent & F_ADJ) != 0;
+            st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+        };
+        if (G.dbg & 4u) {
+        } else if (fast) {
             uint32_t od, oa, sm_d, sm_a;
-            offsets(item_of(i), q, od, oa, sm_d, sm_a);
-            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 4u); tt += ttstep) {
-                const uint64_t ent = gt[ts][tt];
-                if (ent & F_NOSTORE)
-                    continue;
-                const bool adj = (ent & F_ADJ) != 0;
-                st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+            offsets(item_of(i), 0, od, oa, sm_d, sm_a);
+#pragma unroll
+            for (uint32_t e = 0; e < 8; ++e)
+                wb(tt0 + e * ttstep, od, oa, sm_d, sm_a);
+        } else if (fast2) {
+#pragma unroll
+            for (uint32_t q = 0; q < 2; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(i), q, od, oa, sm_d, sm_a);
+#pragma unroll
+                for (uint32_t tt = 0; tt < 4; ++tt)
+                    wb(tt, od, oa, sm_d, sm_a);
+            }
+        } else {
+            for (uint32_t q = 0; q < npos; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(i), q, od, oa, sm_d, sm_a);
+                for (uint32_t tt = tt0; tt < NT; tt += ttstep)
+                    wb(tt, od, oa, sm_d, sm_a);
             }
         }
         mbar_sync();  // every write-back read of stage s is done; the next table is visible
