@@ -307,23 +307,25 @@ def reference_arm(args, cfg, n, m, world):
     from paper_2604_15765_b200 import harness as HS
     threads = os.cpu_count() or 1
     seed = HS.SEEDS[cfg]
+    nc = cpu_sample_n(cfg, n, m)
     if cfg == "c3":
-        payload = HS.pauli_payload(n, HS.pauli_strings(n, 64, seed))
+        payload = HS.pauli_payload(nc, HS.pauli_strings(nc, 64, seed))
     else:
-        payload = host_payload(HS, n, m, HS.rank_psi(n, seed, 4), threads=threads)
+        payload = host_payload(HS, nc, m, HS.rank_psi(nc, seed, 4), threads=threads)
     ops_per_step = 2
-    times = run_reference_cpu(cfg, n, m, payload, ops_per_step, args.steps, args.warmup, threads)
+    times = run_reference_cpu(cfg, nc, m, payload, ops_per_step, args.steps, args.warmup, threads)
     del payload
     t = float(np.mean(times))
-    value = ops_per_step / t
+    value = ops_per_step / t / 4.0 ** (n - nc)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
         "config": {"workload": WORKLOADS[cfg], "n": n, "m": m, "ops_per_step": ops_per_step},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{ops_per_step} consecutive ops of {cfg} per step (blocks spread over the sequence) at n={n} through "
-                                   "hermsim::apply (oracle/_ref/libhermsim_ref.so, threads=nproc)"},
+                         "sample": f"{ops_per_step} consecutive ops of {cfg} per step (blocks spread over the sequence) at n={nc} through "
+                                   "hermsim::apply (oracle/_ref/libhermsim_ref.so, threads=nproc)"
+                                   + (f"; host RAM/time-bounded, extrapolated to n={n} by 4^(n-{nc})" if nc != n else "")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -489,26 +491,55 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     return 0
 
 
+def stored_bytes(n: int, m: int = 5) -> int:
+    G = (1 << n) >> m if n >= m else 1
+    M = min(1 << m, 1 << n)
+    return G * (G + 1) // 2 * M * M * 16
+
+
+def cpu_sample_n(cfg: str, n: int, m: int, reserved: int = 0) -> int:
+    """Largest n' <= n whose reference run fits this host's free RAM (where RAM is short,
+    time at the largest feasible n and extrapolate x4 per qubit).  The reference holds its own copy
+    of the payload; its k = 3 path converts through three dense 4^n matrices (kernels.cpp:498-505)."""
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available - reserved
+    except Exception:  # pragma: no cover
+        avail = 32 << 30
+    budget = 0.6 * avail
+    for k in range(n, 4, -1):
+        need = 2.2 * stored_bytes(k, m) + (3 * 16 * (1 << (2 * k)) if cfg == "c3" else 0)
+        # the dense k = 3 path also costs ~4^n time: keep a C3 sample within seconds per op
+        if need <= budget and (cfg != "c3" or k <= 13):
+            return k
+    return 5
+
+
 def cpu_baseline_from(host_view, cfg, n, m, S, psi=None, strings=None):
     """Reference CPU path on a bounded sample (about 10-30 s) of the same workload, rank 0 only."""
     try:
         from paper_2604_15765_b200 import harness as HS
         threads = os.cpu_count() or 1
-        if host_view is not None:
-            payload = np.frombuffer(host_view, dtype=np.complex128)
-            # host_view holds the post-e2e state; rebuild the config input instead
+        nc = cpu_sample_n(cfg, n, m)
         if cfg == "c3":
-            payload = HS.pauli_payload(n, strings if strings is not None else HS.pauli_strings(n, 64, HS.SEEDS[cfg]))
+            payload = HS.pauli_payload(nc, HS.pauli_strings(nc, 64, HS.SEEDS[cfg]) if nc != n or strings is None
+                                       else strings)
         else:
-            payload = host_payload(HS, n, m, psi if psi is not None else HS.rank_psi(n, HS.SEEDS[cfg], 4),
-                                   out=np.frombuffer(host_view, dtype=np.complex128) if host_view is not None else None,
+            use_host = host_view is not None and nc == n  # the pinned e2e buffer holds n-sized payloads
+            payload = host_payload(HS, nc, m, psi if (psi is not None and nc == n) else HS.rank_psi(nc, HS.SEEDS[cfg], 4),
+                                   out=np.frombuffer(host_view, dtype=np.complex128) if use_host else None,
                                    threads=threads)
         ops_per_step = 2
-        times = run_reference_cpu(cfg, n, m, payload, ops_per_step, steps=3, warmup=0, threads=threads, budget_s=30.0)
+        times = run_reference_cpu(cfg, nc, m, payload, ops_per_step, steps=3, warmup=0, threads=threads, budget_s=30.0)
         t = float(np.mean(times))
-        return {"value": ops_per_step / t, "unit": UNIT, "cores": threads, "kind": "reference",
-                "sample": f"{len(times)} x {ops_per_step} consecutive ops of {cfg}, blocks spread over the sequence, at n={n} through "
-                          "hermsim::apply of the compiled reference (oracle/_ref/libhermsim_ref.so), threads=nproc"}
+        scale = 4.0 ** (n - nc)
+        out = {"value": ops_per_step / t / scale, "unit": UNIT, "cores": threads, "kind": "reference",
+               "sample": f"{len(times)} x {ops_per_step} consecutive ops of {cfg}, blocks spread over the sequence, at n={nc} through "
+                         "hermsim::apply of the compiled reference (oracle/_ref/libhermsim_ref.so), threads=nproc"}
+        if nc != n:
+            out["extrapolated_from_n"] = nc
+            out["sample"] += f"; host RAM/time-bounded, extrapolated to n={n} by 4^(n-{nc}) (work grows 4x per qubit)"
+        return out
     except Exception as e:  # the baseline is reported, never fatal
         return {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference", "error": str(e)}
 
