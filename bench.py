@@ -285,6 +285,8 @@ def main():
     ap.add_argument("--shard", dest="shard", action="store_true", default=None,
                     help="partition the operator over the N ranks (default for c4 when N > 1)")
     ap.add_argument("--replicas", dest="shard", action="store_false", help="N independent replicas")
+    ap.add_argument("--fuse", action="store_true",
+                    help="operation fusion (SURVEY 8f): same sequence, fewer passes; value counts the logical ops")
     args = ap.parse_args()
 
     from paper_2604_15765_b200 import harness as HS
@@ -365,14 +367,32 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     ops = build_ops(H, HS, cfg, n)
     nops = len(ops)
     opts = H.ApplyOptions(count_subcases=False)
+    fplan = None
+    if args.fuse:
+        if sharded:
+            raise SystemExit("--fuse runs on single-GPU / replica states")
+        from paper_2604_15765_b200 import fusion
+        fplan = fusion.plan_sequence([(spec, tg) for spec, tg, _ in ops], n, m)
 
-    ev = [ctypes.c_void_p() for _ in range(2 * nops + 2)]
+    npass = fplan.launches if fplan is not None else nops  # timed launch groups per step
+
+    ev = [ctypes.c_void_p() for _ in range(2 * npass + 2)]
     for e in ev:
         nat.check(L.hs_event_create(ctypes.byref(e)))
 
-    touched = [0] * nops  # HBM bytes each op reads + writes (engine plan, algorithmic)
+    touched = [0] * npass  # HBM bytes each op (or fused pass) reads + writes (engine plan, algorithmic)
 
     def step(record=False, collect=False):
+        if fplan is not None:  # fused passes; touched bytes: 2 S per pass (program or composed step)
+            for i, item in enumerate(fplan.items):
+                if record:
+                    L.hs_event_record(ev[2 + 2 * i], st.handle)
+                fusion.execute(st, fusion.Plan([item]), opts)
+                if collect:
+                    touched[i] = 2 * S
+                if record:
+                    L.hs_event_record(ev[3 + 2 * i], st.handle)
+            return
         for i, (spec, tg, _) in enumerate(ops):
             if record:
                 L.hs_event_record(ev[2 + 2 * i], st.handle)
@@ -402,7 +422,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     ms = ctypes.c_float()
     nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(ms)))
     total_ms = float(ms.value)
-    for i in range(nops):
+    for i in range(npass):
         x = ctypes.c_float()
         nat.check(L.hs_event_elapsed_ms(ev[2 + 2 * i], ev[3 + 2 * i], ctypes.byref(x)))
         launch_ms.append(float(x.value))
@@ -415,7 +435,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     # roofline of the dominant kernel (conj_kernel): bytes per launch / mean launch time
     peak, peak_src = load_peaks()
     if not any(touched):
-        touched = [2 * S] * nops
+        touched = [2 * S] * npass
     per_launch_bytes = float(np.mean(touched))
     mean_launch_ms = float(np.mean(launch_ms))
     # bytes-weighted over the step: sum of algorithmic bytes / sum of launch durations
@@ -468,6 +488,9 @@ def ours_arm(args, cfg, n, m, world, rank, local):
         "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded rank-4 rho / Pauli-sum O of BASELINE.json shapes)",
         "config": {"workload": WORKLOADS[cfg], "config": cfg, "n": n, "m": m, "ops_per_step": nops,
+                   "fused": ({"passes_per_step": npass, "note": "operation fusion (SURVEY 8f): value counts the "
+                              "logical operations; reported separately from the per-operation metric"}
+                             if fplan is not None else None),
                    "stored_bytes_per_rank": S,
                    "parallelism": (f"sharded x{world} (XOR blocks, NCCL group exchange)" if sharded else
                                    f"replicas x{world}" if world > 1 else "single GPU"),

@@ -121,6 +121,11 @@ int hs_host_free(void* p);
 /* Kraus channel through its row-stacked transfer matrix (kernels.cpp:27-37): `s` is
  * 4^k x 4^k complex, k in {1, 2}.  plan may be NULL. */
 int hs_apply_transfer(hs_state* h, int k, const double* s_rowstacked, const uint32_t* targets, hs_plan* plan);
+/* Fused program (no reference counterpart: the reference applies one op per pass):
+ * nsteps <= 8 single-qubit steps on in-tile qubits (< m) in ONE pass over the triangle, equal to
+ * applying them in order.  kinds[p]: 0 = row-stacked 4x4 transfer matrix s[16p..16p+15]
+ * (interleaved complex), 1 = Hadamard (s ignored), 2 = diagonal transfer (diagonal of s used). */
+int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s, hs_plan* plan);
 /* Unitary conjugation B -> U B U^dagger per coupled block, direct form; k in {1, 2, 3}. */
 int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* targets, hs_plan* plan);
 /* Generic Kraus set {L_a} (nops matrices 2^k x 2^k), k in {1, 2, 3}. */

@@ -107,6 +107,7 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_state_comm_init", i, [vp, vp, i, i])
     _sig(L, "hs_state_exchange", i, [vp, i])
     _sig(L, "hs_op_group", i, [vp, i, c_u32_p, c_u32_p])
+    _sig(L, "hs_apply_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
     _sig(L, "hs_state_recv_reserve", i, [vp, i])
     _sig(L, "hs_state_exchange_group_from", i, [vp, vp, ctypes.c_uint32])
     _sig(L, "hs_state_exchange_group", i, [vp, ctypes.c_uint32])

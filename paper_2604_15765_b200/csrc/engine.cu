@@ -52,7 +52,7 @@ constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in 
 constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_NOSTORE = 1ull << 60,
                    F_REMOTE = 1ull << 59, F_MASK = (1ull << 56) - 1;
 
-enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5 };
+enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5, M_PROG = 6 };
 
 thread_local std::string g_err;
 thread_local bool g_plan_subcases = true;  // hs_set_plan_subcases
@@ -152,7 +152,10 @@ struct Coef {
     // tile permutations (every target a grid bit): cycles grouped into <= 4-tile item groups;
     // group g owns cycles [gcyc_off[g], gcyc_off[g + 1])
     uint8_t gcyc_off[17];
-    uint32_t ngroups;
+    // fused program (M_PROG): nsteps single-qubit steps on in-tile bits, step p uses s[16p .. 16p+15]
+    uint8_t pbit[16], pkind[16];
+    uint32_t nsteps;
+    uint32_t ngroups;  // tile permutations: number of item groups
 };
 
 uint32_t pdep(uint32_t v, uint32_t mask) {
@@ -1013,6 +1016,40 @@ __device__ __forceinline__ void stc(double2* sb, uint32_t a, bool cj, double2 v)
     sb[a] = v;
 }
 
+// One program step on a quad, row-stacked (h00, h01, h10, h11).  kind: 0 transfer matrix,
+// 1 Hadamard (native.cpp:332-339), 2 diagonal transfer, 3 real transfer coupling only (00, 11) and
+// (01, 10) (depolarising, amplitude damping and their compositions).
+__device__ __forceinline__ void prog_quad(uint32_t kind, const double2* S, double2& v0, double2& v1, double2& v2,
+                                          double2& v3) {
+    double2 w0, w1, w2, w3;
+    if (kind == 1) {
+        const double2 aa = make_double2(v0.x + v1.x, v0.y + v1.y), b2 = make_double2(v0.x - v1.x, v0.y - v1.y);
+        const double2 cc = make_double2(v2.x + v3.x, v2.y + v3.y), dd = make_double2(v2.x - v3.x, v2.y - v3.y);
+        w0 = make_double2(0.5 * (aa.x + cc.x), 0.5 * (aa.y + cc.y));
+        w1 = make_double2(0.5 * (b2.x + dd.x), 0.5 * (b2.y + dd.y));
+        w2 = make_double2(0.5 * (aa.x - cc.x), 0.5 * (aa.y - cc.y));
+        w3 = make_double2(0.5 * (b2.x - dd.x), 0.5 * (b2.y - dd.y));
+    } else if (kind == 2) {
+        w0 = cmul(S[0], v0);
+        w1 = cmul(S[5], v1);
+        w2 = cmul(S[10], v2);
+        w3 = cmul(S[15], v3);
+    } else if (kind == 3) {
+        w0 = make_double2(S[0].x * v0.x + S[3].x * v3.x, S[0].x * v0.y + S[3].x * v3.y);
+        w3 = make_double2(S[12].x * v0.x + S[15].x * v3.x, S[12].x * v0.y + S[15].x * v3.y);
+        w1 = make_double2(S[5].x * v1.x + S[6].x * v2.x, S[5].x * v1.y + S[6].x * v2.y);
+        w2 = make_double2(S[9].x * v1.x + S[10].x * v2.x, S[9].x * v1.y + S[10].x * v2.y);
+    } else {
+        w0 = cmul(S[0], v0); w0 = cfma(S[1], v1, w0); w0 = cfma(S[2], v2, w0); w0 = cfma(S[3], v3, w0);
+        w1 = cmul(S[4], v0); w1 = cfma(S[5], v1, w1); w1 = cfma(S[6], v2, w1); w1 = cfma(S[7], v3, w1);
+        w2 = cmul(S[8], v0); w2 = cfma(S[9], v1, w2); w2 = cfma(S[10], v2, w2); w2 = cfma(S[11], v3, w2);
+        w3 = cmul(S[12], v0); w3 = cfma(S[13], v1, w3); w3 = cfma(S[14], v2, w3); w3 = cfma(S[15], v3, w3);
+    }
+    v0 = w0;
+    v1 = w1;
+    v2 = w2;
+    v3 = w3;
+}
 template <int K, int MODE, int NS, int NC = NCONS>
 __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const Coef<NS>& cf, const uint64_t* am,
                                              uint32_t nvalid_units, double2* sb, uint32_t grp = 0, int tidv = -1,
@@ -1130,6 +1167,32 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                     acc = cfma(cf.s[r * D + t], v[t], acc);
                 stc(sb, a[r], (cjm >> r) & 1u, acc);
             }
+        }
+    } else if constexpr (MODE == M_PROG) {
+        // fused program: single-qubit steps on in-tile bits applied to the staged whole
+        // tiles one after another (one HBM pass for the whole run; the host composes the run's
+        // operations per qubit).  Quads of step p: rows (x, x + 2^a) x columns (y, y + 2^a),
+        // row-stacked (h00, h01, h10, h11) as TransferQuad (kernels.cpp:66-77); consecutive threads
+        // take consecutive quads along a row.
+        const uint32_t lq = G.logM - 1, nq = nvalid_units << (2 * lq), M = G.M;
+        for (uint32_t p = 0; p < cf.nsteps; ++p) {
+            const uint32_t a = cf.pbit[p], sa = 1u << a, lo = sa - 1, kind = cf.pkind[p];
+            const double2* S = cf.s + 16 * p;
+            for (uint32_t q = tid; q < nq; q += NC) {
+                const uint32_t u = q >> (2 * lq), r = q & ((1u << (2 * lq)) - 1);
+                const uint32_t qx = r >> lq, qy = r & ((1u << lq) - 1);
+                const uint32_t x = ((qx & ~lo) << 1) | (qx & lo), y = ((qy & ~lo) << 1) | (qy & lo);
+                const uint32_t b0 = u * G.A * G.TS + x * M + y;
+                const uint32_t b1 = b0 + sa, b2 = b0 + sa * M, b3 = b2 + sa;
+                double2 v0 = sb[b0], v1 = sb[b1], v2 = sb[b2], v3 = sb[b3];
+                prog_quad(kind, S, v0, v1, v2, v3);
+                sb[b0] = v0;
+                sb[b1] = v1;
+                sb[b2] = v2;
+                sb[b3] = v3;
+            }
+            if (p + 1 < cf.nsteps)
+                asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NC) : "memory");  // consumer warps only
         }
     } else if constexpr (MODE == M_MONO) {
         // in-place cycles of the component map; untouched components cost nothing
@@ -3105,6 +3168,38 @@ int hs_apply_transfer(hs_state* h, int k, const double* s, const uint32_t* t, hs
     if (rc)
         return rc;
     return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+}
+
+// Fused program of nsteps (<= 8) single-qubit steps on in-tile qubits (< m), one HBM pass
+// (SURVEY 8f "op fusion": a run of consecutive in-tile single-qubit operations).  kinds[p]: 0 row-
+// stacked 4 x 4 transfer matrix s[16p..16p+15] (interleaved complex), 1 Hadamard, 2 diagonal
+// transfer (s diagonal used).  Equivalent to applying the steps one by one (hs_apply_transfer).
+int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s, hs_plan* plan) {
+    if (!h || nsteps < 1 || nsteps > 16 || !kinds || !bits || !s)
+        return set_err(HS_ERR_INVALID, "bad program");
+    const uint32_t edge = std::min<uint32_t>((uint32_t)h->m, (uint32_t)h->n);
+    for (int p = 0; p < nsteps; ++p) {
+        if (bits[p] >= edge)
+            return set_err(HS_ERR_RANGE, "program steps act on in-tile qubits (< m) only");
+        if (kinds[p] < 0 || kinds[p] > 3)
+            return set_err(HS_ERR_INVALID, "bad program step kind");
+    }
+    DeviceGuard dg(h->device);
+    Geo G;
+    plan_geo(h, 1, bits, G, 1);
+    KrausArgs ka{nullptr, 0};
+    auto* cf = new Coef<256>();
+    std::memcpy(cf->s, s, (size_t)nsteps * 16 * sizeof(double2));
+    for (int p = 0; p < nsteps; ++p) {
+        cf->pbit[p] = (uint8_t)bits[p];
+        cf->pkind[p] = (uint8_t)kinds[p];
+    }
+    cf->nsteps = (uint32_t)nsteps;
+    int rc = launch<1, M_PROG, 256>(h, G, *cf, ka, 1);
+    delete cf;
+    if (rc)
+        return rc;
+    return finish_plan(h, G, 1, bits, HS_PATH_TILED_INTRA, plan, 2 * state_bytes(h));
 }
 
 int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* t, hs_plan* plan) {

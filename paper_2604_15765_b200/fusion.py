@@ -1,0 +1,169 @@
+"""Operation fusion: fewer HBM passes for the same operation sequence.
+
+The reference applies one operation per pass over the tiled triangle (`hermsim::apply`,
+kernels.cpp:510-549). ``apply_sequence`` gives the same result for a whole sequence with fewer passes:
+
+* a run of consecutive single-qubit operations is regrouped per qubit (single-qubit channels on
+  different qubits commute);
+* the operations of each qubit are composed into one transfer matrix S = S_last ... S_first
+  (row-stacked, the engine's `TransferQuad` order, kernels.cpp:66-77);
+* the composed steps of all in-tile qubits (< m) of the run go into ONE pass (`hs_apply_program`):
+  the staged tiles are transformed step after step in shared memory, each step in its cheapest form
+  (Hadamard butterfly, diagonal phase, real (00,11)/(01,10) transfer as for depolarising / amplitude
+  damping and their compositions, or a general transfer matrix);
+* the composed operation of each grid qubit is one pass (native Hadamard when it is a lone H);
+* any other operation (k >= 2) ends the run and is applied as is.
+
+The result equals applying the sequence one operation at a time up to floating-point rounding
+(the composition reorders products); ``tests/test_gpu_fusion.py`` checks it at 1e-12 * ||rho||_F.
+Throughput with fusion is reported separately from the per-operation metric (bench.py --fuse).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from . import hermsim as H
+
+
+def transfer_rowstacked(kraus: np.ndarray) -> np.ndarray:
+    """Row-stacked 4 x 4 transfer matrix of a single-qubit Kraus set: w[r*2+c] = sum S v[r'*2+c'],
+    S[(r, c), (r', c')] = sum_a K_a[r, r'] conj(K_a[c, c']) (H' = sum_a K_a H K_a^dagger)."""
+    k = np.asarray(kraus, np.complex128).reshape(-1, 2, 2)
+    s = np.einsum("arp,acq->rcpq", k, k.conj())
+    return s.reshape(4, 4)
+
+
+@dataclass
+class Step:
+    qubit: int
+    s: np.ndarray            # row-stacked 4 x 4
+    lone_h: bool = False     # exactly one native Hadamard
+    count: int = 1           # operations composed into this step
+
+
+@dataclass
+class Plan:
+    """Launch list of a fused sequence: ("program", [Step]) | ("step", Step) | ("op", spec, targets)."""
+    items: list = field(default_factory=list)
+    ops: int = 0
+
+    @property
+    def launches(self) -> int:
+        return len(self.items)
+
+
+def _single_qubit_s(spec: H.ChannelSpec) -> np.ndarray:
+    return transfer_rowstacked(spec.kraus)
+
+
+def plan_sequence(ops, n: int, m: int = 5) -> Plan:
+    """ops: iterable of (ChannelSpec, targets)."""
+    plan = Plan()
+    edge = min(m, n)  # in-tile qubits
+    run: dict[int, Step] = {}   # grid qubits: composed per qubit
+    order: list[int] = []
+    chains: dict[int, list[Step]] = {}  # in-tile qubits: steps, composed only where it is cheaper
+
+    def flush():
+        intile = [x for q in order if q < edge for x in chains[q]]
+        for i in range(0, len(intile), 16):
+            plan.items.append(("program", intile[i:i + 16]))
+        for q in order:
+            if q >= edge:
+                plan.items.append(("step", run[q]))
+        run.clear()
+        chains.clear()
+        order.clear()
+
+    for spec, targets in ops:
+        targets = list(targets)
+        plan.ops += 1
+        if spec.k != 1 or len(targets) != 1:
+            flush()
+            plan.items.append(("op", spec, targets))
+            continue
+        q = int(targets[0])
+        s = _single_qubit_s(spec)
+        is_h = spec.kind == "hadamard"
+        if q < edge:
+            step = Step(q, s, is_h, 1)
+            ch = chains.setdefault(q, [])
+            if not ch:
+                order.append(q)
+            elif _cost(Step(q, s @ ch[-1].s, False, 2)) <= _cost(ch[-1]) + _cost(step):
+                prev = ch.pop()
+                step = Step(q, s @ prev.s, False, prev.count + 1)
+            ch.append(step)
+            continue
+        if q in run:
+            prev = run[q]
+            run[q] = Step(q, s @ prev.s, False, prev.count + 1)
+        else:
+            run[q] = Step(q, s, is_h, 1)
+            order.append(q)
+    flush()
+    return plan
+
+
+_XPAT = np.zeros((4, 4), bool)
+for _r, _c in ((0, 0), (0, 3), (3, 0), (3, 3), (1, 1), (1, 2), (2, 1), (2, 2)):
+    _XPAT[_r, _c] = True
+
+
+def _kind(step: Step) -> int:
+    """Cheapest kernel form of a step: 1 Hadamard, 2 diagonal, 3 real (00,11)/(01,10), 0 general."""
+    if step.lone_h:
+        return 1
+    s = step.s
+    if not np.any(s - np.diag(np.diag(s))):
+        return 2
+    if not np.any(s.imag) and not np.any(s[~_XPAT]):
+        return 3
+    return 0
+
+
+# relative cost of a program step: one shared-memory round trip of the staged tiles (dominant:
+# measured ~1.4k cycles per 64 KiB item on B200) plus its arithmetic per quad
+_STEP_COST = {1: 0.5, 2: 1.0, 3: 1.0, 0: 4.0}
+
+
+def _cost(step: Step) -> float:
+    return 3.0 + _STEP_COST[_kind(step)]
+
+
+def execute(st: H.TiledHermitian, plan: Plan, opts: H.ApplyOptions | None = None) -> int:
+    """Runs a plan on a state; returns the number of passes (launch groups) issued."""
+    opts = opts or H.ApplyOptions(count_subcases=False)
+    L = nat.engine()
+    for item in plan.items:
+        if item[0] == "program":
+            steps = item[1]
+            kinds = np.array([_kind(x) for x in steps], np.int32)
+            bits = np.array([x.qubit for x in steps], np.uint32)
+            s = np.ascontiguousarray(np.stack([x.s for x in steps]).astype(np.complex128))
+            nat.check(L.hs_apply_program(st.handle, len(steps), kinds.ctypes.data_as(nat.c_i32_p),
+                                         bits.ctypes.data_as(nat.c_u32_p), s.ctypes.data_as(nat.c_double_p), None),
+                      "apply_program")
+        elif item[0] == "step":
+            x = item[1]
+            if x.lone_h:
+                H.apply_hadamard(st, x.qubit)
+            else:
+                H.apply_transfer(st, np.ascontiguousarray(x.s), [x.qubit])
+        else:
+            H.apply(st, item[1], item[2], opts)
+    return plan.launches
+
+
+def apply_sequence(st: H.TiledHermitian, ops, opts: H.ApplyOptions | None = None) -> Plan:
+    """Fused equivalent of `for spec, tg in ops: hermsim.apply(st, spec, tg)`."""
+    plan = plan_sequence(ops, st.qubits(), st.tile_exp())
+    execute(st, plan, opts)
+    return plan
+
+
+_ = ctypes

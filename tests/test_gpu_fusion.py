@@ -1,0 +1,67 @@
+"""Fused sequences (paper_2604_15765_b200/fusion.py) against one-op-at-a-time application
+on the GPU, and the compiled reference on the same inputs: max |delta| <= 1e-12 * ||X||_F."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _seq(H, HS, name, n):
+    if name == "c2":
+        return [(H.depolarising(0.01) if op.kind == "depol" else H.amplitude_damping(0.05), list(op.targets))
+                for op in HS.config_ops("c2", n)]
+    if name == "c0":
+        return [(H.native_gate("h"), list(op.targets)) for op in HS.config_ops("c0", n)]
+    out = []
+    for op in HS.config_ops("c4", n)[: 3 * n + 8]:  # one layer: Rz, H, CX matching, depolarising
+        if op.kind == "rz":
+            out.append((H.native_gate("rz", op.param), list(op.targets)))
+        elif op.kind == "h":
+            out.append((H.native_gate("h"), list(op.targets)))
+        elif op.kind == "cnot":
+            out.append((H.native_gate("cnot"), list(op.targets)))
+        else:
+            out.append((H.depolarising(op.param), list(op.targets)))
+    return out
+
+
+@pytest.mark.parametrize("name,n,m", [("c2", 10, 5), ("c2", 9, 3), ("c0", 9, 5), ("c4", 11, 5), ("c4", 8, 2)])
+def test_fused_equals_sequential(name, n, m):
+    from paper_2604_15765_b200 import fusion
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    psi = HS.rank_psi(n, 11, 4)
+    a, b = H.TiledHermitian(n, m), H.TiledHermitian(n, m)
+    a.fill_mixture(psi)
+    b.fill_mixture(psi)
+    ops = _seq(H, HS, name, n)
+    opts = H.ApplyOptions(count_subcases=False)
+    for spec, tg in ops:
+        H.apply(a, spec, tg, opts)
+    plan = fusion.apply_sequence(b, ops)
+    assert plan.launches < len(ops)
+    want, got = a.download(), b.download()
+    fro = H.frobenius(a)
+    assert np.max(np.abs(got - want)) <= 1e-12 * fro, (name, plan.launches)
+
+
+def test_fused_against_reference(oracle):
+    """The fused C2 pass against the compiled reference applying the same 2n operations."""
+    from paper_2604_15765_b200 import fusion
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    n, m = 10, 5
+    psi = HS.rank_psi(n, 3, 4)
+    want = HS.rho_payload(n, psi, m)
+    ref = oracle.Reference()
+    h = ref.create(n, m, want)
+    for op in HS.config_ops("c2", n):
+        ch = oracle.depolarising(op.param) if op.kind == "depol" else oracle.amplitude_damping(op.param)
+        ref.apply(h, ch, list(op.targets), threads=4)
+    want = ref.view(h).copy()
+    ref.free(h)
+    st = H.TiledHermitian(n, m)
+    st.fill_mixture(psi)
+    fusion.apply_sequence(st, _seq(H, HS, "c2", n))
+    got = st.download()
+    assert oracle.rel_max_err(got, want, oracle.Oracle().frobenius(want, n, m)) <= 1e-12

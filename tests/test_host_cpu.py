@@ -175,3 +175,30 @@ def test_bench_reference_arm_contract():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_fusion_plan_counts():
+    """Fusion planner (host only): C2 at n = 16 -> one in-tile program + one pass per grid qubit;
+    C4's Rz/H run -> one program + one pass per grid qubit; k >= 2 ops end a run."""
+    from paper_2604_15765_b200 import fusion
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    dep, amp = H.depolarising(0.01), H.amplitude_damping(0.05)
+    ops = [(dep if op.kind == "depol" else amp, list(op.targets)) for op in HS.config_ops("c2", 16)]
+    plan = fusion.plan_sequence(ops, 16, 5)
+    assert plan.ops == 32 and plan.launches == 12
+    assert plan.items[0][0] == "program" and [s.qubit for s in plan.items[0][1]] == [0, 1, 2, 3, 4]
+    assert [fusion._kind(s) for s in plan.items[0][1]] == [3] * 5  # depolarising o amplitude damping
+    assert all(it[0] == "step" and it[1].count == 2 for it in plan.items[1:])
+    h, cx = H.native_gate("h"), H.native_gate("cnot")
+    seq = [(H.native_gate("rz", 0.3), [q]) for q in range(8)] + [(h, [q]) for q in range(8)] + [(cx, [7, 1])] + [(h, [6])]
+    plan = fusion.plan_sequence(seq, 8, 5)
+    kinds = [it[0] for it in plan.items]
+    assert kinds == ["program", "step", "step", "step", "op", "step"]
+    assert plan.items[-1][1].lone_h
+    # H o Rz: one general transfer step per qubit (a step's shared-memory round trip dominates)
+    assert [fusion._kind(s) for s in plan.items[0][1]] == [0] * 5
+    # composition order: S(second) @ S(first)
+    s_rz = fusion.transfer_rowstacked(H.native_gate("rz", 0.3).kraus)
+    s_h = fusion.transfer_rowstacked(h.kraus)
+    assert np.allclose(plan.items[1][1].s, s_h @ s_rz)
