@@ -1,3 +1,4 @@
+# gpurun recipe: smoke, GPU tests, all bench configs, C3 launch list and ncu capture of the top kernel
 set -x
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
