@@ -121,8 +121,9 @@ struct Geo {
     uint64_t nG_items;
     // sharding (XOR blocks over the top Plog tile-index bits; Plog == 0: the reference layout)
     uint32_t Plog, shard, logB;   // 2^Plog shards, this shard, 2^logB tile rows per block
-    uint32_t cross, cmask;        // top targets: shard s works with the group s ^ span(cmask) of 2^cross shards
-    uint32_t cb[3];               // shard bits of cmask, ascending (slot = those bits of own ^ shard, minus 1)
+    uint32_t cross, cmask;        // top targets: `cross` of them, shard bits cb[]; cmask: the shard bits whose
+    uint32_t cb[3];               // remote tiles the op reads (all top targets, or only the moving ones)
+    uint32_t xmask, nx, xb[3];    // exchange-slot layout (recv_mask): slot = pext(own ^ shard, xmask) - 1
     uint64_t recv_tiles;          // tiles per exchange slot
     uint32_t q, Pulog, logBu;     // local units: group q over 2^Pulog blocks of 2^logBu grid bases
     const double2* recv;          // group members' payloads, slot j at recv + j * recv_tiles tiles
@@ -294,9 +295,11 @@ __device__ __forceinline__ uint64_t tile_entry(const Geo& G, uint64_t tr, uint64
         ent |= F_ADJ;
     if (own != G.shard) {
         const uint32_t d = own ^ G.shard;
+        if (d & ~G.cmask)  // a shard the op never reads from (stationary top target): not staged
+            return ent | F_REMOTE | F_NOSTORE | F_SKIP;
         uint32_t slot = 0;
-        for (uint32_t i = 0; i < G.cross; ++i)
-            slot |= ((d >> G.cb[i]) & 1u) << i;
+        for (uint32_t i = 0; i < G.nx; ++i)
+            slot |= ((d >> G.xb[i]) & 1u) << i;
         ent = (ent + (uint64_t)(slot - 1) * G.recv_tiles) | F_REMOTE | F_NOSTORE;
     }
     return ent;
@@ -742,10 +745,12 @@ __device__ void path_d(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
         double2 v;
         if (R >= C) {
             const uint64_t ent = tile_entry(G, trow[R], trow[C]);
-            v = ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)x << logM) + y];
+            v = (ent & F_SKIP) ? make_double2(0.0, 0.0)
+                               : ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)x << logM) + y];
         } else {
             const uint64_t ent = tile_entry(G, trow[C], trow[R]);
-            v = ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)y << logM) + x];
+            v = (ent & F_SKIP) ? make_double2(0.0, 0.0)
+                               : ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)y << logM) + x];
             v.y = -v.y;
         }
         if (!one)
@@ -2151,6 +2156,8 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
     G.cross = 0;
     G.cmask = 0;
     G.cb[0] = G.cb[1] = G.cb[2] = 0;
+    G.xmask = G.nx = 0;
+    G.xb[0] = G.xb[1] = G.xb[2] = 0;
     G.recv_tiles = h->recv_count >> (2 * h->m);
     G.Pulog = h->Plog;
     G.q = h->shard;
@@ -2500,9 +2507,17 @@ int sm_count(int device) {
 
 template <int K, int MODE, int NS>
 int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
-    if (G0.cross && (!h->recv || h->recv_slots < (1u << G0.cross) - 1 || h->recv_mask != G0.cmask))
+    if (G0.cmask && (!h->recv || (G0.cmask & ~h->recv_mask) ||
+                     h->recv_slots < (1u << __builtin_popcount(h->recv_mask)) - 1))
         return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the group's shards first");
     Geo G = G0;
+    if (G.cmask) {  // exchange-slot layout of the last exchange (it may cover more bits than needed)
+        G.xmask = h->recv_mask;
+        G.nx = 0;
+        for (uint32_t b = 0; b < 32 && G.nx < 3; ++b)
+            if (G.xmask >> b & 1u)
+                G.xb[G.nx++] = b;
+    }
     G.rev = (uint32_t)(h->sweeps++ & 1u);
     G.dbg = 0;
     if (MODE == M_MONO && G.groups) {
@@ -2706,7 +2721,7 @@ int finish_plan(hs_state* h, const Geo& G, int k, const uint32_t* t, int path, h
     plan->grid_bits = (int)G.g;
     plan->launches = (G.nD_items + G.nU_items) ? 1 : 0;
     // a cross-shard op also reads the 2^cross - 1 exchanged payloads of its group (about one shard each)
-    plan->touched_bytes = G.cross ? touched / 2 * ((1ull << G.cross) + 1) : touched;
+    plan->touched_bytes = G.cmask ? touched / 2 * ((1ull << __builtin_popcount(G.cmask)) + 1) : touched;
     if (g_plan_subcases)
         count_subcases(h, G, plan->subcases);
     return HS_OK;
@@ -3327,6 +3342,22 @@ int hs_apply_monomial(hs_state* h, int k, const uint32_t* perm, const double* di
     DeviceGuard dg(h->device);
     Geo G;
     plan_geo(h, k, t, G, 1);
+    // a monomial moves elements only along the local bits its permutation flips: remote tiles that
+    // differ in a stationary top target (a diagonal phase, a control) are never read, so those
+    // shards need no exchange (multigpu.op_mask mirrors this)
+    {
+        uint32_t moving = 0;
+        for (uint32_t x = 0; x < D; ++x)
+            moving |= x ^ p[x];
+        if (G.cmask) {
+            const uint32_t top0 = h->m + ilog2(h->G) - h->Plog;
+            uint32_t need = 0;
+            for (int l = 0; l < k; ++l)
+                if (t[l] >= top0 && (moving >> l & 1u))
+                    need |= 1u << (t[l] - top0);
+            G.cmask = need;
+        }
+    }
     Coef<64> cf{};
     const double2* dg2 = reinterpret_cast<const double2*>(diag);
     // U = P Dg with P|x> = |p[x]>: (U B U^dag)(r, c) = d[pinv r] conj(d[pinv c]) B(pinv r, pinv c).

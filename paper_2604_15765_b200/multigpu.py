@@ -142,6 +142,28 @@ def op_partner(st: H.TiledHermitian, targets) -> int:
     return out.value
 
 
+def moving_qubits(spec: H.ChannelSpec, targets) -> set:
+    """Target qubits whose bit an operation changes: none for a diagonal phase, the permuted bits of
+    a permutation (a CX moves only its target), every target otherwise.  Stationary top targets need
+    no exchange (the engine skips those remote tiles, hs_apply_monomial)."""
+    targets = [int(q) for q in targets]
+    if spec.kind == "diagonal_phase":
+        return set()
+    if spec.kind == "permutation":
+        perm = spec.perm
+        if perm is not None:
+            k, mv = len(targets), 0
+            for x, px in enumerate(perm):
+                mv |= x ^ int(px)
+            return {targets[i] for i in range(k) if mv >> (k - 1 - i) & 1}  # first-listed = MSB
+    return set(targets)
+
+
+def op_mask(layout: ShardLayout, spec: H.ChannelSpec, targets) -> int:
+    """Shard-bit mask of the group an operation must exchange with (0: shard-local)."""
+    return layout.group_mask(sorted(moving_qubits(spec, targets)))
+
+
 def op_group(st: H.TiledHermitian, targets) -> int:
     tg = np.ascontiguousarray(targets, np.uint32)
     out = ctypes.c_uint32()
@@ -167,11 +189,11 @@ class ShardGroup:
     def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
         """hermsim.apply on every shard; exchanges first when the op crosses shards."""
         opts = opts or H.ApplyOptions(count_subcases=False)
-        mask = op_group(self.shards[0], targets)
+        mask = op_mask(self.layout, spec, targets)
         if mask:
             # all exchanges read the pre-op payloads, then every shard updates its own tiles
             for s, st in enumerate(self.shards):
-                for peer in self.layout.group(s, targets)[1:]:
+                for peer in [s ^ d for d in range(1, self.P) if not d & ~mask]:
                     nat.check(nat.engine().hs_state_exchange_group_from(st.handle, self.shards[peer].handle, mask),
                               "exchange")
             for st in self.shards:
@@ -229,7 +251,7 @@ class DistributedShard:
 
     def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
         opts = opts or H.ApplyOptions(count_subcases=False)
-        mask = op_group(self.state, targets)
+        mask = op_mask(self.layout, spec, targets)
         if mask:
             nat.check(nat.engine().hs_state_exchange_group(self.state.handle, mask), "exchange")
         return H.apply(self.state, spec, targets, opts)

@@ -131,3 +131,17 @@ def test_two_rank_gloo_sharded_channels(oracle, orc):
     for ci, a in seq:
         orc.apply(want, n, 5, chans[ci][1], [a])
     assert oracle.rel_max_err(got, want, orc.frobenius(want, n, 5)) <= 1e-13
+
+
+def test_exchange_mask_moving_bits():
+    """Only qubits an op moves need the partner's tiles: a phase never, a CX only its target."""
+    from paper_2604_15765_b200 import hermsim as H
+    from paper_2604_15765_b200.multigpu import ShardLayout, moving_qubits, op_mask
+    L = ShardLayout(11, 5, 8)  # top qubits 8, 9, 10 -> shard bits 0, 1, 2
+    cx, rz, h, sw = H.native_gate("cnot"), H.native_gate("rz", 0.4), H.native_gate("h"), H.native_gate("swap")
+    assert moving_qubits(rz, [10]) == set() and op_mask(L, rz, [10]) == 0
+    assert moving_qubits(cx, [10, 3]) == {3} and op_mask(L, cx, [10, 3]) == 0      # control on a top qubit
+    assert moving_qubits(cx, [3, 10]) == {10} and op_mask(L, cx, [3, 10]) == 4     # target on a top qubit
+    assert op_mask(L, cx, [10, 9]) == 2 and op_mask(L, sw, [10, 9]) == 6
+    assert op_mask(L, h, [9]) == 2 and op_mask(L, H.native_gate("toffoli"), [10, 9, 8]) == 1
+    assert op_mask(L, H.depolarising(0.1), [8]) == 1

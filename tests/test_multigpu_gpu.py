@@ -31,6 +31,10 @@ def _ops(H, HS, n):
         (H.make_generic("u2", u2), [top - 1, top - 2]), (H.native_gate("swap"), [top, top - 2]),
         (H.make_generic("u3", u3), [top, top - 1, 2]), (H.make_generic("u3", u3), [top - 2, top, top - 1]),
         (H.make_generic("k2", _kraus2(HS)), [top, top - 1]), (H.make_generic("k3", _kraus3(HS)), [2, top, top - 2]),
+        # stationary top targets: no exchange (phase; CX / Toffoli controls)
+        (H.native_gate("rz", 0.9), [top - 1]), (H.native_gate("cnot"), [top, top - 1]),
+        (H.native_gate("cnot"), [top - 2, 4]), (H.native_gate("toffoli"), [top, top - 2, 1]),
+        (H.native_gate("toffoli"), [top, top - 1, top - 2]), (H.native_gate("z"), [top]),
     ]
 
 
@@ -69,7 +73,9 @@ def test_group_exchange_required():
     st = grp.shards[1]
     with pytest.raises((ValueError, nat.NativeError)):
         H.apply(st, H.native_gate("cnot"), [9, 8])
-    # exchanging for a one-bit group does not license a two-bit op
+    # a one-bit exchange licenses an op that moves only that bit (CX target 8, control 9 stationary)
+    # but not one that moves both (SWAP)
     nat.check(nat.engine().hs_state_exchange_group_from(st.handle, grp.shards[0].handle, 1))
+    H.apply(st, H.native_gate("cnot"), [9, 8])
     with pytest.raises((ValueError, nat.NativeError)):
-        H.apply(st, H.native_gate("cnot"), [9, 8])
+        H.apply(st, H.native_gate("swap"), [9, 8])
