@@ -165,13 +165,31 @@ class TiledHermitian {
     std::vector<cplx> to_host() const;
     void synchronize() const;
     hs_state* handle() const { return h_; }
+    // takes ownership of an engine state (hs_state_load, ...)
+    static TiledHermitian adopt(hs_state* h);
 
   private:
+    TiledHermitian() = default;
     hs_state* h_ = nullptr;
     int n_ = 0, m_ = 0;
     std::uint64_t grid_ = 0;
     std::size_t count_ = 0;
 };
+
+// ------------------------------------------------------------- file I/O (storage_io.hpp)
+// OHRM container (magic, version 1, format tag, n, m, payload), tiled format, streamed between
+// HBM and the file.  Errors: IoError with the reference's kinds (storage_io.hpp:11-20).
+enum class IoErrorKind { bad_magic, bad_version, bad_header, truncated, length_mismatch, io_failure };
+class IoError : public std::runtime_error {
+  public:
+    IoError(IoErrorKind kind, const std::string& what) : std::runtime_error(what), kind_(kind) {}
+    IoErrorKind kind() const { return kind_; }
+
+  private:
+    IoErrorKind kind_;
+};
+void save(const TiledHermitian& h, const std::string& path);
+TiledHermitian load(const std::string& path, int device = 0);
 
 // ----------------------------------------------------------------- kernels (kernels.hpp)
 enum class KernelPath : std::uint8_t {

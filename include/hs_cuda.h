@@ -53,7 +53,8 @@ enum hs_status {
     HS_ERR_RANGE = -2,       /* std::out_of_range in the reference */
     HS_ERR_CUDA = -3,        /* CUDA runtime failure (incl. missing device) */
     HS_ERR_NOMEM = -4,       /* device allocation failed */
-    HS_ERR_UNSUPPORTED = -5  /* valid request this build does not implement */
+    HS_ERR_UNSUPPORTED = -5, /* valid request this build does not implement */
+    HS_ERR_IO = -6           /* hermsim::IoError (storage_io.hpp:11-20); message starts with the IoErrorKind */
 };
 
 /* KernelPath (include/hermsim/kernels.hpp:12-24); same numbering. */
@@ -105,6 +106,10 @@ int hs_state_upload_async(hs_state* h, const double* host, uint64_t count);
 int hs_state_download_async(const hs_state* h, double* host, uint64_t count);
 /* Partial copies of `count` complex elements starting at element `offset`. */
 int hs_state_upload_range(hs_state* h, const double* host, uint64_t offset, uint64_t count);
+/* OHRM container (hermsim::save / load, storage_io.cpp:34-118; tiled format), streamed between
+ * HBM and the file through pinned buffers. */
+int hs_state_save(const hs_state* h, const char* path);
+int hs_state_load(const char* path, int device, hs_state** out);
 int hs_state_download_range(const hs_state* h, double* host, uint64_t offset, uint64_t count);
 int hs_state_copy(hs_state* dst, const hs_state* src);
 int hs_state_zero(hs_state* h);

@@ -262,6 +262,9 @@ class Reference:
         L.ref_tile_offset.argtypes = [ctypes.c_uint64] * 3
         L.ref_random_hermitian.restype = ctypes.c_void_p
         L.ref_random_hermitian.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
+        L.ref_save.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+        L.ref_load.restype = ctypes.c_void_p
+        L.ref_load.argtypes = [ctypes.c_char_p]
 
     # -- state handles -------------------------------------------------------------------
     def create(self, n: int, m: int = 5, payload: np.ndarray | None = None):
@@ -279,6 +282,16 @@ class Reference:
 
     def free(self, h):
         self.lib.ref_free(h)
+
+    def save(self, h, path: str):
+        if self.lib.ref_save(h, path.encode()):
+            raise IOError(self.lib.ref_last_error().decode())
+
+    def load(self, path: str):
+        h = self.lib.ref_load(path.encode())
+        if not h:
+            raise IOError(self.lib.ref_last_error().decode())
+        return h
 
     def random_hermitian(self, n, seed, m=5):
         h = self.lib.ref_random_hermitian(n, seed, 2, m)

@@ -8,6 +8,7 @@
 //   hermsim::native_gate / depolarising / make_generic / dual_channel (channel.hpp:54-92)
 //   hermsim::gaussian_entry, footprint_bytes, to_dense (storage.hpp:129-154)
 //   hermsim::insert_bits / tile_offset       (bit_index.hpp:40-83)
+//   hermsim::save / load                     (storage_io.hpp:22-29)
 // Errors are caught and reported as negative return codes (the reference throws).
 #include <cstdint>
 #include <cstring>
@@ -19,6 +20,7 @@
 #include "hermsim/channel.hpp"
 #include "hermsim/kernels.hpp"
 #include "hermsim/storage.hpp"
+#include "hermsim/storage_io.hpp"
 
 using namespace hermsim;
 
@@ -66,6 +68,25 @@ void* ref_dense_create(int n) {
 }
 
 void ref_free(void* h) { delete static_cast<MatrixHandle*>(h); }
+
+// hermsim::save / load (storage_io.cpp:34-118): the OHRM container.
+int ref_save(void* h, const char* path) {
+    try {
+        save(*static_cast<MatrixHandle*>(h), std::string(path));
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+void* ref_load(const char* path) {
+    try {
+        return new MatrixHandle(load(std::string(path)));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
 
 double* ref_payload(void* h) { return reinterpret_cast<double*>(static_cast<MatrixHandle*>(h)->payload()); }
 

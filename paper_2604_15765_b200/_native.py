@@ -39,6 +39,16 @@ class HsPlan(ctypes.Structure):
     ]
 
 
+class IoError(RuntimeError):
+    """hermsim::IoError (storage_io.hpp:11-20): `kind` is the IoErrorKind name."""
+
+    def __init__(self, text: str):
+        super().__init__(text)
+        tail = text.split(": ", 1)[-1] if ": " in text else text
+        self.kind = next((k for k in ("bad_magic", "bad_version", "bad_header", "truncated", "length_mismatch",
+                                      "io_failure") if k in tail), "io_failure")
+
+
 class NativeError(RuntimeError):
     pass
 
@@ -108,6 +118,8 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_state_exchange", i, [vp, i])
     _sig(L, "hs_op_group", i, [vp, i, c_u32_p, c_u32_p])
     _sig(L, "hs_apply_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
+    _sig(L, "hs_state_save", i, [vp, ctypes.c_char_p])
+    _sig(L, "hs_state_load", i, [ctypes.c_char_p, i, pp])
     _sig(L, "hs_state_recv_reserve", i, [vp, i])
     _sig(L, "hs_state_exchange_group_from", i, [vp, vp, ctypes.c_uint32])
     _sig(L, "hs_state_exchange_group", i, [vp, ctypes.c_uint32])
@@ -172,4 +184,6 @@ def check(rc: int, where: str = "", facade: bool = False) -> None:
         raise MemoryError(text)
     if rc == -5:
         raise NotImplementedError(text)
+    if rc == -6:
+        raise IoError(text)
     raise NativeError(text)

@@ -3664,3 +3664,167 @@ extern "C" int hs_debug_phase_cycles(unsigned long long* out8) {
     CUDA_TRY(cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)));
     return HS_OK;
 }
+
+// ---------------------------------------------------------------------- OHRM save / load
+// The reference's container (storage_io.cpp:34-118, storage_io.hpp:22-29): magic "OHRM", version
+// u32 = 1, format tag u8 (tiled = 2, types.hpp:15), n u8, m u8, five reserved zero bytes, then the
+// payload as little-endian (re, im) binary64 pairs in native element order.  The payload streams
+// between HBM and the file through two pinned 64 MiB buffers (copy of chunk i+1 overlaps the write /
+// read of chunk i), so a 137 GB n = 17 operator never needs host RAM.  Error messages carry the
+// reference's IoErrorKind names.
+namespace {
+constexpr uint64_t IO_CHUNK = 64ull << 20;  // bytes
+struct PinnedPair {
+    void* b[2] = {nullptr, nullptr};
+    ~PinnedPair() {
+        for (void* p : b)
+            if (p)
+                cudaFreeHost(p);
+    }
+};
+}  // namespace
+
+int hs_state_save(const hs_state* h, const char* path) {
+    if (!h || !path)
+        return set_err(HS_ERR_INVALID, "null argument");
+    if (h->Plog)
+        return set_err(HS_ERR_UNSUPPORTED, "save: sharded operators are saved shard by shard (download_full)");
+    FILE* f = std::fopen(path, "wb");
+    if (!f)
+        return set_err(HS_ERR_IO, std::string("io_failure: save: cannot open ") + path);
+    unsigned char hdr[16] = {'O', 'H', 'R', 'M', 1, 0, 0, 0, 2, (unsigned char)h->n, (unsigned char)h->m, 0, 0, 0, 0, 0};
+    bool ok = std::fwrite(hdr, 1, 16, f) == 16;
+    DeviceGuard dg(h->device);
+    PinnedPair pp;
+    const uint64_t total = h->count * sizeof(double2);
+    for (int i = 0; i < 2 && ok; ++i)
+        if (cudaHostAlloc(&pp.b[i], IO_CHUNK, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            std::fclose(f);
+            return set_err(HS_ERR_NOMEM, "save: pinned staging buffer");
+        }
+    cudaEvent_t ev[2];
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    const char* src = reinterpret_cast<const char*>(h->d);
+    uint64_t off = 0, prev = 0;
+    int cur = 0;
+    bool pending = false;
+    uint64_t prev_len = 0;
+    while (ok && (off < total || pending)) {
+        const uint64_t len = std::min<uint64_t>(IO_CHUNK, total - off);
+        if (off < total) {
+            if (cudaMemcpyAsync(pp.b[cur], src + off, len, cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) {
+                ok = false;
+                break;
+            }
+            cudaEventRecord(ev[cur], h->stream);
+        }
+        if (pending) {  // write the previous chunk while this one copies
+            cudaEventSynchronize(ev[cur ^ 1]);
+            ok = std::fwrite(pp.b[cur ^ 1], 1, prev_len, f) == prev_len;
+        }
+        pending = off < total;
+        prev = off;
+        prev_len = len;
+        off += len;
+        cur ^= 1;
+    }
+    (void)prev;
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    ok = (std::fclose(f) == 0) && ok;
+    if (cudaGetLastError() != cudaSuccess)
+        return set_err(HS_ERR_CUDA, "save: device copy failed");
+    if (!ok)
+        return set_err(HS_ERR_IO, "io_failure: save: stream write failed");
+    return HS_OK;
+}
+
+int hs_state_load(const char* path, int device, hs_state** out) {
+    if (!path || !out)
+        return set_err(HS_ERR_INVALID, "null argument");
+    *out = nullptr;
+    FILE* f = std::fopen(path, "rb");
+    if (!f)
+        return set_err(HS_ERR_IO, std::string("io_failure: load: cannot open ") + path);
+    unsigned char hdr[16];
+    auto fail = [&](int code, const char* msg) {
+        std::fclose(f);
+        return set_err(code, msg);
+    };
+    if (std::fread(hdr, 1, 16, f) != 16)
+        return fail(HS_ERR_IO, "truncated: load: header truncated");
+    if (std::memcmp(hdr, "OHRM", 4) != 0)
+        return fail(HS_ERR_IO, "bad_magic: load: bad magic bytes");
+    const uint32_t ver = hdr[4] | (hdr[5] << 8) | (hdr[6] << 16) | ((uint32_t)hdr[7] << 24);
+    if (ver != 1)
+        return fail(HS_ERR_IO, "bad_version: load: unsupported version");
+    const int tag = hdr[8], n = hdr[9], m = hdr[10];
+    if (tag > 2)
+        return fail(HS_ERR_IO, "bad_header: load: unknown format tag");
+    if (n < 1 || n > 30)
+        return fail(HS_ERR_IO, "bad_header: load: qubit count out of range");
+    if (tag != 2 && m != 0)
+        return fail(HS_ERR_IO, "bad_header: load: tile exponent set for non-tiled format");
+    if (tag == 2 && (m < 0 || m > n + 2))
+        return fail(HS_ERR_IO, "bad_header: load: tile exponent out of range");
+    if (tag != 2)
+        return fail(HS_ERR_UNSUPPORTED, "load: dense / packed payloads are not device formats (tiled only)");
+    hs_state* h = nullptr;
+    int rc = hs_state_create(n, m, device, &h);
+    if (rc) {
+        std::fclose(f);
+        return rc;
+    }
+    DeviceGuard dg(h->device);
+    PinnedPair pp;
+    for (int i = 0; i < 2; ++i)
+        if (cudaHostAlloc(&pp.b[i], IO_CHUNK, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            hs_state_free(h);
+            return fail(HS_ERR_NOMEM, "load: pinned staging buffer");
+        }
+    const uint64_t total = h->count * sizeof(double2);
+    char* dst = reinterpret_cast<char*>(h->d);
+    uint64_t off = 0;
+    int cur = 0;
+    cudaEvent_t ev[2];
+    cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+    bool used[2] = {false, false};
+    bool ok = true;
+    while (off < total) {
+        const uint64_t len = std::min<uint64_t>(IO_CHUNK, total - off);
+        if (used[cur])
+            cudaEventSynchronize(ev[cur]);  // the buffer's previous upload has left it
+        if (std::fread(pp.b[cur], 1, len, f) != len) {
+            ok = false;
+            break;
+        }
+        cudaMemcpyAsync(dst + off, pp.b[cur], len, cudaMemcpyHostToDevice, h->stream);
+        cudaEventRecord(ev[cur], h->stream);
+        used[cur] = true;
+        off += len;
+        cur ^= 1;
+    }
+    cudaStreamSynchronize(h->stream);
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    if (!ok) {
+        hs_state_free(h);
+        return fail(HS_ERR_IO, "truncated: load: payload truncated");
+    }
+    char probe;
+    if (std::fread(&probe, 1, 1, f) != 0) {
+        hs_state_free(h);
+        return fail(HS_ERR_IO, "length_mismatch: load: trailing bytes after payload");
+    }
+    std::fclose(f);
+    if (cudaGetLastError() != cudaSuccess) {
+        hs_state_free(h);
+        return set_err(HS_ERR_CUDA, "load: device copy failed");
+    }
+    *out = h;
+    return HS_OK;
+}

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "hermsim_b200/hermsim.hpp"
 
@@ -20,6 +21,18 @@ namespace {
         throw std::invalid_argument(msg);
     if (rc == HS_ERR_RANGE)
         throw std::out_of_range(msg);
+    if (rc == HS_ERR_IO) {
+        const std::string e = hs_last_error();
+        IoErrorKind kind = IoErrorKind::io_failure;
+        const std::pair<const char*, IoErrorKind> names[] = {
+            {"bad_magic", IoErrorKind::bad_magic}, {"bad_version", IoErrorKind::bad_version},
+            {"bad_header", IoErrorKind::bad_header}, {"truncated", IoErrorKind::truncated},
+            {"length_mismatch", IoErrorKind::length_mismatch}};
+        for (const auto& [name, k] : names)
+            if (e.rfind(name, 0) == 0)
+                kind = k;
+        throw IoError(kind, msg);
+    }
     throw std::runtime_error(msg);
 }
 
@@ -122,6 +135,27 @@ TiledHermitian& TiledHermitian::operator=(TiledHermitian&& o) noexcept {
         o.h_ = nullptr;
     }
     return *this;
+}
+
+TiledHermitian TiledHermitian::adopt(hs_state* h) {
+    TiledHermitian t;
+    int n = 0, m = 0;
+    std::uint64_t count = 0, grid = 0;
+    check(hs_state_info(h, &n, &m, &count, &grid), "TiledHermitian");
+    t.h_ = h;
+    t.n_ = n;
+    t.m_ = m;
+    t.count_ = count;
+    t.grid_ = grid;
+    return t;
+}
+
+void save(const TiledHermitian& h, const std::string& path) { check(hs_state_save(h.handle(), path.c_str()), "save"); }
+
+TiledHermitian load(const std::string& path, int device) {
+    hs_state* h = nullptr;
+    check(hs_state_load(path.c_str(), device, &h), "load");
+    return TiledHermitian::adopt(h);
 }
 
 void TiledHermitian::upload(const cplx* payload) { check(hs_state_upload(h_, dptr(payload), count_), "upload"); }

@@ -23,6 +23,7 @@ for ``std::out_of_range``.  There is no CPU path: every operation runs the CUDA 
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -155,6 +156,26 @@ class TiledHermitian:
         nat.check(nat.engine().hs_state_distance_mixture(self.handle, psi.shape[0], _dp(psi), ctypes.byref(out)),
                   "distance_to_mixture")
         return out.value
+
+    def save(self, path: str) -> None:
+        """hermsim::save (storage_io.cpp:34-56): OHRM container, tiled format."""
+        nat.check(nat.engine().hs_state_save(self.handle, os.fsencode(path)), "save")
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "TiledHermitian":
+        """hermsim::load (storage_io.cpp:58-118) of a tiled OHRM file into HBM."""
+        h = ctypes.c_void_p()
+        nat.check(nat.engine().hs_state_load(os.fsencode(path), device, ctypes.byref(h)), "load")
+        self = cls.__new__(cls)
+        L = nat.engine()
+        n, m = ctypes.c_int(), ctypes.c_int()
+        cnt, grid = ctypes.c_uint64(), ctypes.c_uint64()
+        nat.check(L.hs_state_info(h, ctypes.byref(n), ctypes.byref(m), ctypes.byref(cnt), ctypes.byref(grid)))
+        self.nshards, self.shard, self._h = 1, 0, h
+        self._n, self._m = n.value, m.value
+        self._count, self._grid = int(cnt.value), int(grid.value)
+        self.device = device
+        return self
 
     def free(self) -> None:
         if getattr(self, "_h", None) is not None:

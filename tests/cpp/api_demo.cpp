@@ -3,6 +3,8 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <stdexcept>
 #include <vector>
 
@@ -55,6 +57,21 @@ int main() {
     TiledHermitian copy = rho;  // deep device copy
     if (std::fabs(trace(copy) - 1.0) > 1e-12)
         return 8;
+    // checkpoint / resume through the reference's OHRM container (storage_io.hpp:22-29)
+    const char* path = std::getenv("API_DEMO_OHRM");
+    if (path) {
+        save(rho, path);
+        TiledHermitian back = load(path);
+        if (std::fabs(expectation(back, zz) - e) > 0.0 || back.qubits() != n)
+            return 9;
+        try {
+            load(std::string(path) + ".missing");
+            return 10;
+        } catch (const IoError& err) {
+            if (err.kind() != IoErrorKind::io_failure)
+                return 11;
+        }
+    }
     std::printf("api_demo ok: <Z0 Z8> = %.15f\n", e);
     return 0;
 }

@@ -24,6 +24,7 @@ def test_cpp_api_compiles(tmp_path):
 
 @pytest.mark.gpu
 def test_cpp_api_runs(tmp_path):
-    out = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120)
+    env = dict(os.environ, API_DEMO_OHRM=str(tmp_path / "rho.ohrm"))
+    out = subprocess.run([_build(tmp_path)], capture_output=True, text=True, timeout=120, env=env)
     assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
     assert "api_demo ok" in out.stdout

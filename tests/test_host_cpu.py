@@ -202,3 +202,30 @@ def test_fusion_plan_counts():
     s_rz = fusion.transfer_rowstacked(H.native_gate("rz", 0.3).kraus)
     s_h = fusion.transfer_rowstacked(h.kraus)
     assert np.allclose(plan.items[1][1].s, s_h @ s_rz)
+
+
+def test_ohrm_header_validation_without_device(tmp_path):
+    """hs_state_load validates the OHRM header (storage_io.cpp:58-83) before touching a device:
+    each malformed header fails with the reference's IoErrorKind."""
+    from paper_2604_15765_b200 import _native as nat
+    from paper_2604_15765_b200 import hermsim as H
+
+    def hdr(magic=b"OHRM", ver=1, tag=2, n=6, m=3):
+        return magic + ver.to_bytes(4, "little") + bytes([tag, n, m, 0, 0, 0, 0, 0])
+
+    cases = [(hdr(magic=b"OHRX"), "bad_magic"), (hdr(ver=2), "bad_version"), (hdr(tag=3), "bad_header"),
+             (hdr(n=0), "bad_header"), (hdr(n=31), "bad_header"), (hdr(m=9), "bad_header"),
+             (hdr(tag=0, m=1), "bad_header"), (b"OHRM\x01\x00", "truncated")]
+    for i, (data, kind) in enumerate(cases):
+        p = tmp_path / f"h{i}.ohrm"
+        p.write_bytes(data)
+        with pytest.raises(nat.IoError) as ei:
+            H.TiledHermitian.load(str(p))
+        assert ei.value.kind == kind, (data, str(ei.value))
+    with pytest.raises(nat.IoError) as ei:
+        H.TiledHermitian.load(str(tmp_path / "missing.ohrm"))
+    assert ei.value.kind == "io_failure"
+    p = tmp_path / "dense.ohrm"
+    p.write_bytes(hdr(tag=0, m=0))
+    with pytest.raises(NotImplementedError):  # dense / packed are not device formats
+        H.TiledHermitian.load(str(p))
