@@ -156,6 +156,9 @@ struct Coef {
     // fused program (M_PROG): nsteps single-qubit steps on in-tile bits, step p uses s[16p .. 16p+15]
     uint8_t pbit[16], pkind[16];
     uint32_t nsteps;
+    // k = 1 transfer matrix that couples only (00, 11) and (01, 10) (depolarising, amplitude
+    // damping, dephasing, ...): w = S v reads only class-consistent components
+    uint32_t xpat;
     uint32_t ngroups;  // tile permutations: number of item groups
 };
 
@@ -354,6 +357,12 @@ __device__ __forceinline__ void xf_quad(double2* sm, uint32_t base, const uint16
         w1 = make_double2(0.5 * (b.x + d.x), 0.5 * (b.y + d.y));
         w2 = make_double2(0.5 * (a.x - c.x), 0.5 * (a.y - c.y));
         w3 = make_double2(0.5 * (b.x - d.x), 0.5 * (b.y - d.y));
+    } else if (cf.xpat) {
+        const double2* s = cf.s;
+        w0 = cfma(s[3], v3, cmul(s[0], v0));
+        w3 = cfma(s[15], v3, cmul(s[12], v0));
+        w1 = cfma(s[6], v2, cmul(s[5], v1));
+        w2 = cfma(s[10], v2, cmul(s[9], v1));
     } else {
         const double2* s = cf.s;
         w0 = cmul(s[0], v0); w0 = cfma(s[1], v1, w0); w0 = cfma(s[2], v2, w0); w0 = cfma(s[3], v3, w0);
@@ -1082,6 +1091,12 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                 w1 = make_double2(0.5 * (bb.x + d.x), 0.5 * (bb.y + d.y));
                 w2 = make_double2(0.5 * (a.x - cc.x), 0.5 * (a.y - cc.y));
                 w3 = make_double2(0.5 * (bb.x - d.x), 0.5 * (bb.y - d.y));
+            } else if (c16.xpat) {  // TransferQuad with only (00, 11) / (01, 10) couplings
+                const double2* s = c16.s;
+                w0 = cfma(s[3], v3, cmul(s[0], v0));
+                w3 = cfma(s[15], v3, cmul(s[12], v0));
+                w1 = cfma(s[6], v2, cmul(s[5], v1));
+                w2 = cfma(s[10], v2, cmul(s[9], v1));
             } else {  // TransferQuad (kernels.cpp:66-77)
                 const double2* s = c16.s;
                 w0 = cmul(s[0], v0); w0 = cfma(s[1], v1, w0); w0 = cfma(s[2], v2, w0); w0 = cfma(s[3], v3, w0);
@@ -3173,6 +3188,17 @@ int hs_apply_transfer(hs_state* h, int k, const double* s, const uint32_t* t, hs
     if (k == 1) {
         Coef<16> cf{};
         std::memcpy(cf.s, s, sizeof(cf.s));
+        // (00, 11) and (01, 10) are the two shard classes of a cross-shard quad (T00, T11 on one
+        // shard, T01, T10 on the partner): a transfer matrix without couplings between
+        // them needs no exchange, and the quad reads only class-consistent components
+        bool xp = true;
+        for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c)
+                if (((r == 0 || r == 3) != (c == 0 || c == 3)) && (s[2 * (4 * r + c)] != 0.0 || s[2 * (4 * r + c) + 1] != 0.0))
+                    xp = false;
+        cf.xpat = xp ? 1u : 0u;
+        if (xp)
+            G.cmask = 0;
         rc = launch<1, M_S1, 16>(h, G, cf, ka, 1);
     } else {
         auto* cf = new Coef<256>();

@@ -159,8 +159,22 @@ def moving_qubits(spec: H.ChannelSpec, targets) -> set:
     return set(targets)
 
 
+def xpattern(spec: H.ChannelSpec) -> bool:
+    """A single-qubit channel whose transfer matrix couples only (00, 11) and (01, 10): the two
+    shard classes of a cross-shard quad, so it needs no exchange (depolarising,
+    amplitude damping, dephasing; the engine's hs_apply_transfer applies the same test)."""
+    if spec.k != 1 or spec.kind not in ("generic_kraus",):
+        return False
+    from .fusion import transfer_rowstacked
+    s = transfer_rowstacked(spec.kraus)
+    cls = np.array([0, 1, 1, 0])
+    return not np.any(s[cls[:, None] != cls[None, :]])
+
+
 def op_mask(layout: ShardLayout, spec: H.ChannelSpec, targets) -> int:
     """Shard-bit mask of the group an operation must exchange with (0: shard-local)."""
+    if xpattern(spec):
+        return 0
     return layout.group_mask(sorted(moving_qubits(spec, targets)))
 
 

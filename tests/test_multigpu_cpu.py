@@ -144,4 +144,7 @@ def test_exchange_mask_moving_bits():
     assert moving_qubits(cx, [3, 10]) == {10} and op_mask(L, cx, [3, 10]) == 4     # target on a top qubit
     assert op_mask(L, cx, [10, 9]) == 2 and op_mask(L, sw, [10, 9]) == 6
     assert op_mask(L, h, [9]) == 2 and op_mask(L, H.native_gate("toffoli"), [10, 9, 8]) == 1
-    assert op_mask(L, H.depolarising(0.1), [8]) == 1
+    assert op_mask(L, H.depolarising(0.1), [8]) == 0  # (00,11)/(01,10) couplings only: shard-local
+    assert op_mask(L, H.amplitude_damping(0.2), [9]) == 0
+    k = np.stack([np.eye(2) * np.sqrt(0.9), np.sqrt(0.1) * np.array([[1, 1], [1, -1]]) / np.sqrt(2)])
+    assert op_mask(L, H.make_generic("mix_h", k), [9]) == 2  # couples the classes: exchange

@@ -134,7 +134,7 @@ def test_four_rank_group_exchange():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert exchanged == [1, 3, 3, 2, 3, 0, 0, 0]
+    assert exchanged == [1, 3, 3, 0, 3, 0, 0, 0]  # depolarising keeps both shard classes: local
     # the whole matrix, one operation at a time
     from paper_2604_15765_b200.multigpu import ShardLayout
     L = ShardLayout(n, m, 1)
@@ -157,6 +157,7 @@ def test_protocol_detects_missing_exchange():
     full = HS.rho_payload(n, HS.rank_psi(n, 7, 4), m)
     mine = L.scatter(full)[1]
     for spec, tg, needs in ((H.native_gate("cnot"), [3, 7], True), (H.native_gate("cnot"), [7, 3], False),
-                            (H.native_gate("rz", 0.3), [6], False), (H.depolarising(0.2), [6], True)):
+                            (H.native_gate("rz", 0.3), [6], False), (H.depolarising(0.2), [6], False),
+                            (H.native_gate("h"), [6], True)):
         d = apply_kraus(_tiles_to_dense(L, {1: mine}, n, m), n, spec.kraus, tg)
         assert np.isnan(_own_tiles(L, 1, d, m)).any() == needs, (spec.name, tg)
