@@ -27,6 +27,7 @@ processes one operator (strong scaling; value = ops of the operator per second).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -281,7 +282,9 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override the config's qubit count (testing)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-serial", action="store_true",
+                    help="e2e without overlapping consecutive steps (one state, one buffer)")
     ap.add_argument("--shard", dest="shard", action="store_true", default=None,
                     help="partition the operator over the N ranks (default for c4 when N > 1)")
     ap.add_argument("--replicas", dest="shard", action="store_false", help="N independent replicas")
@@ -452,22 +455,26 @@ def ours_arm(args, cfg, n, m, world, rank, local):
         nat.check(L.hs_host_alloc(ctypes.c_uint64(S), ctypes.byref(hbuf)), "pinned alloc")
         host = np.ctypeslib.as_array(ctypes.cast(hbuf, ctypes.POINTER(ctypes.c_double)), shape=(2 * st.element_count(),))
         nat.check(L.hs_state_download(st.handle, host.ctypes.data_as(nat.c_double_p), st.element_count()))
-        e_ms = []
-        for s in range(1 + args.e2e_steps):
-            L.hs_event_record(ev[0], st.handle)
-            nat.check(L.hs_state_upload_async(st.handle, host.ctypes.data_as(nat.c_double_p), st.element_count()))
-            step()
-            nat.check(L.hs_state_download_async(st.handle, host.ctypes.data_as(nat.c_double_p), st.element_count()))
-            L.hs_event_record(ev[1], st.handle)
-            st.synchronize()
-            x = ctypes.c_float()
-            nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(x)))
-            if s >= 1:
-                e_ms.append(float(x.value))
-        e2e_ms = dist_max(float(np.mean(e_ms)), world)
-        e2e = {"value": (1 if sharded else world) * nops / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": S,
-               "d2h_bytes_per_step": S, "ms_per_step": e2e_ms, "steps": len(e_ms),
-               "path": "hb_apply via paper_2604_15765_b200.hermsim.apply + hs_state_upload/download_async"}
+        e2e = None
+        if not sharded and not args.e2e_serial:
+            e2e = pipelined_e2e(args, H, L, nat, st, host, S, n, m, nops, world, fplan, ops, opts)
+        if e2e is None:
+            e_ms = []
+            for s in range(1 + args.e2e_steps):
+                L.hs_event_record(ev[0], st.handle)
+                nat.check(L.hs_state_upload_async(st.handle, host.ctypes.data_as(nat.c_double_p), st.element_count()))
+                step()
+                nat.check(L.hs_state_download_async(st.handle, host.ctypes.data_as(nat.c_double_p), st.element_count()))
+                L.hs_event_record(ev[1], st.handle)
+                st.synchronize()
+                x = ctypes.c_float()
+                nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(x)))
+                if s >= 1:
+                    e_ms.append(float(x.value))
+            e2e_ms = dist_max(float(np.mean(e_ms)), world)
+            e2e = {"value": (1 if sharded else world) * nops / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": S,
+                   "d2h_bytes_per_step": S, "ms_per_step": e2e_ms, "steps": len(e_ms), "pipelined": False,
+                   "path": "hb_apply via paper_2604_15765_b200.hermsim.apply + hs_state_upload/download_async"}
         if rank == 0 and world == 1 and not args.no_cpu:
             cpu = cpu_baseline_from(host, cfg, n, m, S)
         else:
@@ -536,6 +543,68 @@ def cpu_sample_n(cfg: str, n: int, m: int, reserved: int = 0) -> int:
         if need <= budget and (cfg != "c3" or k <= 13):
             return k
     return 5
+
+
+def pipelined_e2e(args, H, L, nat, st, host0, S, n, m, nops, world, fplan, ops, opts):
+    """End to end through the public API with consecutive steps overlapped, as a serving loop
+    would run: two device states and two pinned host buffers; step k uploads its input into state
+    k % 2, applies the sequence and downloads the result, all on that state's stream, so step k's
+    upload runs while step k - 1 computes / downloads (PCIe is full duplex).  Every step still
+    moves S bytes host->device and S bytes device->host inside the timed region.  Returns None
+    when a second state or pinned buffer does not fit (the serial loop is used then)."""
+    try:
+        st2 = H.TiledHermitian(n, m, device=st.device)
+    except (MemoryError, Exception):
+        return None
+    hb2 = ctypes.c_void_p()
+    if L.hs_host_alloc(ctypes.c_uint64(S), ctypes.byref(hb2)) != 0:
+        st2.free()
+        return None
+    cnt = st.element_count()
+    host1 = np.ctypeslib.as_array(ctypes.cast(hb2, ctypes.POINTER(ctypes.c_double)), shape=(2 * cnt,))
+    host1[:] = host0
+    states, bufs = [st, st2], [host0, host1]
+    if fplan is not None:
+        from paper_2604_15765_b200 import fusion
+
+    def one(k):
+        s, b = states[k % 2], bufs[k % 2]
+        nat.check(L.hs_state_upload_async(s.handle, b.ctypes.data_as(nat.c_double_p), cnt))
+        if fplan is not None:
+            fusion.execute(s, fplan, opts)
+        else:
+            for spec, tg, _ in ops:
+                H.apply(s, spec, tg, opts)
+        nat.check(L.hs_state_download_async(s.handle, b.ctypes.data_as(nat.c_double_p), cnt))
+
+    ev = [ctypes.c_void_p() for _ in range(3)]
+    for e in ev:
+        nat.check(L.hs_event_create(ctypes.byref(e)))
+    one(0)  # warm-up pair
+    one(1)
+    st.synchronize()
+    st2.synchronize()
+    K = max(2, args.e2e_steps)
+    L.hs_event_record(ev[0], st.handle)  # both streams are idle: every later copy / kernel starts after it
+    for k in range(K):
+        one(k)
+    L.hs_event_record(ev[1], st.handle)
+    L.hs_event_record(ev[2], st2.handle)
+    st.synchronize()
+    st2.synchronize()
+    a, b = ctypes.c_float(), ctypes.c_float()
+    nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(a)))
+    nat.check(L.hs_event_elapsed_ms(ev[0], ev[2], ctypes.byref(b)))
+    total = max(a.value, b.value)
+    for e in ev:
+        L.hs_event_destroy(e)
+    st2.free()
+    L.hs_host_free(hb2)
+    ms = dist_max(total / K, world)
+    return {"value": world * nops / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
+            "ms_per_step": ms, "steps": K, "pipelined": True,
+            "path": "hermsim.apply (or fusion.execute with --fuse) + hs_state_upload/download_async; two states, "
+                    "consecutive steps overlap (upload k || compute/download k-1)"}
 
 
 def cpu_baseline_from(host_view, cfg, n, m, S, psi=None, strings=None):
