@@ -11,7 +11,9 @@ kernels.cpp:510-549). ``apply_sequence`` gives the same result for a whole seque
   the staged tiles are transformed step after step in shared memory, each step in its cheapest form
   (Hadamard butterfly, diagonal phase, real (00,11)/(01,10) transfer as for depolarising / amplitude
   damping and their compositions, or a general transfer matrix);
-* the composed operation of each grid qubit is one pass (native Hadamard when it is a lone H);
+* the composed operations of two grid qubits share one pass when both are unitary (U_a (x) U_b, a
+  2-qubit unitary on two grid bits: the tensor-core gather); otherwise each grid qubit's composed
+  operation is one pass (native Hadamard when it is a lone H);
 * any other operation (k >= 2) ends the run and is applied as is.
 
 The result equals applying the sequence one operation at a time up to floating-point rounding
@@ -43,6 +45,7 @@ class Step:
     s: np.ndarray            # row-stacked 4 x 4
     lone_h: bool = False     # exactly one native Hadamard
     count: int = 1           # operations composed into this step
+    u: np.ndarray | None = None  # 2 x 2 unitary when every composed operation is one (S = conj(U) (x) U)
 
 
 @dataclass
@@ -60,7 +63,15 @@ def _single_qubit_s(spec: H.ChannelSpec) -> np.ndarray:
     return transfer_rowstacked(spec.kraus)
 
 
-def plan_sequence(ops, n: int, m: int = 5) -> Plan:
+def _unitary_of(spec: H.ChannelSpec) -> np.ndarray | None:
+    k = spec.kraus
+    if k.shape[0] != 1:
+        return None
+    u = k[0]
+    return u if np.allclose(u @ u.conj().T, np.eye(2), atol=1e-14) else None
+
+
+def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True) -> Plan:
     """ops: iterable of (ChannelSpec, targets)."""
     plan = Plan()
     edge = min(m, n)  # in-tile qubits
@@ -72,9 +83,24 @@ def plan_sequence(ops, n: int, m: int = 5) -> Plan:
         intile = [x for q in order if q < edge for x in chains[q]]
         for i in range(0, len(intile), 16):
             plan.items.append(("program", intile[i:i + 16]))
+        # grid qubits: two unitary steps share one pass as the 2-qubit unitary U_a (x) U_b (the
+        # tensor-core gather, k = 2 on two grid bits); others are one pass each
+        pend = None
         for q in order:
-            if q >= edge:
-                plan.items.append(("step", run[q]))
+            if q < edge:
+                continue
+            st = run[q]
+            if pair_unitaries and st.u is not None:
+                if pend is None:
+                    pend = st
+                    continue
+                u2 = np.kron(pend.u, st.u)  # first-listed target (pend) is the most significant bit
+                plan.items.append(("op", H.make_generic("fused_u2", u2), [pend.qubit, st.qubit]))
+                pend = None
+                continue
+            plan.items.append(("step", st))
+        if pend is not None:
+            plan.items.append(("step", pend))
         run.clear()
         chains.clear()
         order.clear()
@@ -99,11 +125,13 @@ def plan_sequence(ops, n: int, m: int = 5) -> Plan:
                 step = Step(q, s @ prev.s, False, prev.count + 1)
             ch.append(step)
             continue
+        u = _unitary_of(spec)
         if q in run:
             prev = run[q]
-            run[q] = Step(q, s @ prev.s, False, prev.count + 1)
+            uu = u @ prev.u if (u is not None and prev.u is not None) else None
+            run[q] = Step(q, s @ prev.s, False, prev.count + 1, uu)
         else:
-            run[q] = Step(q, s, is_h, 1)
+            run[q] = Step(q, s, is_h, 1, u)
             order.append(q)
     flush()
     return plan

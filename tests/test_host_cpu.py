@@ -192,9 +192,13 @@ def test_fusion_plan_counts():
     assert all(it[0] == "step" and it[1].count == 2 for it in plan.items[1:])
     h, cx = H.native_gate("h"), H.native_gate("cnot")
     seq = [(H.native_gate("rz", 0.3), [q]) for q in range(8)] + [(h, [q]) for q in range(8)] + [(cx, [7, 1])] + [(h, [6])]
-    plan = fusion.plan_sequence(seq, 8, 5)
+    plan = fusion.plan_sequence(seq, 8, 5, pair_unitaries=False)
     kinds = [it[0] for it in plan.items]
     assert kinds == ["program", "step", "step", "step", "op", "step"]
+    paired = fusion.plan_sequence(seq, 8, 5)  # grid qubits 5, 6 share a pass as H Rz (x) H Rz
+    assert [it[0] for it in paired.items] == ["program", "op", "step", "op", "step"]
+    assert paired.items[1][2] == [5, 6] and paired.items[1][1].k == 2
+    assert paired.items[2][1].qubit == 7 and paired.items[-1][1].lone_h
     assert plan.items[-1][1].lone_h
     # H o Rz: one general transfer step per qubit (a step's shared-memory round trip dominates)
     assert [fusion._kind(s) for s in plan.items[0][1]] == [0] * 5
