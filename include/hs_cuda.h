@@ -131,6 +131,11 @@ int hs_apply_transfer(hs_state* h, int k, const double* s_rowstacked, const uint
  * applying them in order.  kinds[p]: 0 = row-stacked 4x4 transfer matrix s[16p..16p+15]
  * (interleaved complex), 1 = Hadamard (s ignored), 2 = diagonal transfer (diagonal of s used). */
 int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s, hs_plan* plan);
+/* Fused grid program: one step on each of 2 or 3 distinct grid qubits (>= m) in ONE pass over the
+ * triangle (the units of those grid bits are gathered and the steps applied one after another).
+ * Single-GPU states, m = 5. */
+int hs_apply_grid_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s,
+                          hs_plan* plan);
 /* Unitary conjugation B -> U B U^dagger per coupled block, direct form; k in {1, 2, 3}. */
 int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* targets, hs_plan* plan);
 /* Generic Kraus set {L_a} (nops matrices 2^k x 2^k), k in {1, 2, 3}. */

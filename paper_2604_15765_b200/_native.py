@@ -118,6 +118,7 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_state_exchange", i, [vp, i])
     _sig(L, "hs_op_group", i, [vp, i, c_u32_p, c_u32_p])
     _sig(L, "hs_apply_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
+    _sig(L, "hs_apply_grid_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
     _sig(L, "hs_state_save", i, [vp, ctypes.c_char_p])
     _sig(L, "hs_state_load", i, [ctypes.c_char_p, i, pp])
     _sig(L, "hs_state_recv_reserve", i, [vp, i])

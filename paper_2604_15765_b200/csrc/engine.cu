@@ -129,6 +129,7 @@ struct Geo {
     const double2* recv;          // group members' payloads, slot j at recv + j * recv_tiles tiles
     uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
     uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): gather bit 0 skips the transform, bit 1 the loads, bit 2 the stores
+    uint32_t ws_diag;             // gather_ws: units include the diagonal base pairs (grid programs)
     uint32_t rev;                 // sweep the items in reverse order (alternates per launch: L2 reuse)
 };
 
@@ -1679,7 +1680,45 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
 // warps only wait for data and run DMMA.  The 16 copy warps keep twice the memory-instruction
 // parallelism of a ping-pong group, and the transform never waits for its own write-back or loads.
 // (Register-staged loads in place of cp.async were 1.6x slower here.)
-template <int K, int NS>
+// One k = 1 step of a grid program on the staged logical tiles (MODE == M_PROG in gather_ws_kernel):
+// quads of logical tiles (R, C), (R, C | e), (R | e, C), (R | e, C | e) at every staged position,
+// e = 2^l for the step's grid bit l; adjoint tiles are staged transposed and conjugated on the fly.
+template <uint32_t NCW, int NS>
+__device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, const Coef<NS>& cf, uint32_t p,
+                                               uint64_t am, double2* sb, uint32_t tid) {
+    const uint32_t g = G.g, NG = 1u << g, e = 1u << cf.pbit[p], lo = e - 1;
+    const uint32_t S0 = G.S0, P = S0 + 1, npos = S0 * S0, lp = 2 * G.logS0;
+    const uint32_t nq = (NG / 2) * (NG / 2) * npos;
+    const double2* S = cf.s + 16 * p;
+    const uint32_t kind = cf.pkind[p];
+    for (uint32_t q = tid; q < nq; q += NCW) {
+        const uint32_t tq = q >> lp, pos = q & (npos - 1), i = pos >> G.logS0, j = pos & (S0 - 1);
+        const uint32_t rr = tq >> (g - 1), cc = tq & ((NG >> 1) - 1);
+        const uint32_t R0 = ((rr & ~lo) << 1) | (rr & lo), C0 = ((cc & ~lo) << 1) | (cc & lo);
+        const uint32_t t0 = R0 * NG + C0, t1 = R0 * NG + (C0 | e), t2 = (R0 | e) * NG + C0, t3 = t2 + e;
+        const uint32_t off = i * P + j;
+        const uint32_t a0 = t0 * G.TS + T.tsk[t0] + off, a1 = t1 * G.TS + T.tsk[t1] + off;
+        const uint32_t a2 = t2 * G.TS + T.tsk[t2] + off, a3 = t3 * G.TS + T.tsk[t3] + off;
+        const uint32_t f0 = (uint32_t)((am >> t0) & 1ull) << 31, f1 = (uint32_t)((am >> t1) & 1ull) << 31;
+        const uint32_t f2 = (uint32_t)((am >> t2) & 1ull) << 31, f3 = (uint32_t)((am >> t3) & 1ull) << 31;
+        double2 v0 = sb[a0], v1 = sb[a1], v2 = sb[a2], v3 = sb[a3];
+        v0.y = flip_sign(v0.y, f0);
+        v1.y = flip_sign(v1.y, f1);
+        v2.y = flip_sign(v2.y, f2);
+        v3.y = flip_sign(v3.y, f3);
+        prog_quad(kind, S, v0, v1, v2, v3);
+        v0.y = flip_sign(v0.y, f0);
+        v1.y = flip_sign(v1.y, f1);
+        v2.y = flip_sign(v2.y, f2);
+        v3.y = flip_sign(v3.y, f3);
+        sb[a0] = v0;
+        sb[a1] = v1;
+        sb[a2] = v2;
+        sb[a3] = v3;
+    }
+}
+
+template <int K, int NS, int MODE = M_DIRECT>
 __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     constexpr uint32_t NCW = 256, NMW = 512, S = 3;
     extern __shared__ __align__(128) double2 ring[];
@@ -1714,12 +1753,22 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     __syncthreads();
     if (tid < NCW) {
         // ---- transform warps
-        const DmmaFrag fr = dmma_frag<K>(G, T, cf);
+        DmmaFrag fr;
+        if constexpr (MODE == M_DIRECT)
+            fr = dmma_frag<K>(G, T, cf);
         for (uint64_t i = 0; i < nlocal; ++i) {
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
-            if (!(G.dbg & 1u))
-                dmma_direct3<NCW, K>(G, T, fr, am[i % (S + 1)][0], ring + (size_t)s * G.stage_elems, tid >> 5);
+            double2* sb = ring + (size_t)s * G.stage_elems;
+            if constexpr (MODE == M_DIRECT) {
+                if (!(G.dbg & 1u))
+                    dmma_direct3<NCW, K>(G, T, fr, am[i % (S + 1)][0], sb, tid >> 5);
+            } else {
+                for (uint32_t p = 0; p < cf.nsteps; ++p) {
+                    grid_prog_step<NCW>(G, T, cf, p, am[i % (S + 1)][0], sb, tid);
+                    asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+                }
+            }
             mbar_arrive(&done[s]);
         }
         return;
@@ -1749,12 +1798,14 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     auto tables = [&](uint64_t j) {
         const uint32_t ts = (uint32_t)(j % (S + 1));
         uint64_t tbi, tbj;
-        unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), true, tbi, tbj);
+        unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), !G.ws_diag, tbi, tbj);
         unsigned long long m = 0;
         for (uint32_t t = mtid; t < NT; t += 32) {
             const uint64_t tr = ins_bits(tbi, t >> G.logNG, G.gr_pos, G.g);
             const uint64_t tc = ins_bits(tbj, t & NGm, G.gr_pos, G.g);
-            const uint64_t ent = tile_entry(G, tr, tc);
+            uint64_t ent = tile_entry(G, tr, tc);
+            if (tbi == tbj && (t >> G.logNG) < (t & NGm))
+                ent |= F_NOSTORE;  // aliases stored (C, R) of the same diagonal unit: read-only copy
             gt[ts][t] = ent;
             m |= (unsigned long long)((ent & F_ADJ) != 0) << t;
         }
@@ -2575,7 +2626,7 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         // are whole gather items for the FP64 tensor transform): sub-block gather kernel for the
         // off-diagonal units, the slab kernel's wedge path for the diagonal ones
         cudaError_t e;
-        if (G.nD_items) {
+        if (G.nD_items && MODE != M_PROG) {  // grid programs: diagonal units inside the gather
             Geo Gs = G;
             Gs.nU_items = 0;
             Gs.Epad = 0;
@@ -2596,6 +2647,24 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         {
             static const char* dbg = getenv("HS_DEBUG_FLAGS");
             Gg.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
+        }
+        if constexpr (MODE == M_PROG) {
+            // grid program: every unit including the diagonal ones (logical (R, C), R < C, of a
+            // diagonal unit is a read-only staged copy of stored (C, R), never written back)
+            Gg.ws_diag = 1;
+            Gg.nG_items = Gg.nU_loose << (2 * Gg.log_nsb_side);
+            const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
+            auto kw = gather_ws_kernel<K, NS, M_PROG>;
+            e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
+            const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
+            kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            e = cudaGetLastError();
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("gather_ws_kernel launch: ") + cudaGetErrorString(e));
+            return HS_OK;
         }
         if (Gg.nG_items) {
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
@@ -3241,6 +3310,50 @@ int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* 
     if (rc)
         return rc;
     return finish_plan(h, G, 1, bits, HS_PATH_TILED_INTRA, plan, 2 * state_bytes(h));
+}
+
+// Fused grid program: one k = 1 step on each of nsteps (<= 3) distinct grid qubits
+// (>= m), applied in ONE pass: the units of the g = nsteps grid bits are gathered (warp-specialised
+// gather) and the steps run one after another on the staged logical tiles.  kinds / s as for
+// hs_apply_program.  Single-GPU states only (a cross-shard step would need its own exchange).
+int hs_apply_grid_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s,
+                          hs_plan* plan) {
+    if (!h || nsteps < 2 || nsteps > 3 || !kinds || !bits || !s)
+        return set_err(HS_ERR_INVALID, "bad grid program (2 or 3 steps; one step: hs_apply_transfer)");
+    if (h->Plog)
+        return set_err(HS_ERR_UNSUPPORTED, "grid programs run on single-GPU states");
+    uint32_t t[3];
+    for (int p = 0; p < nsteps; ++p) {
+        if (bits[p] < (uint32_t)h->m || bits[p] >= (uint32_t)h->n)
+            return set_err(HS_ERR_RANGE, "grid program steps act on grid qubits (>= m) only");
+        if (kinds[p] < 0 || kinds[p] > 3)
+            return set_err(HS_ERR_INVALID, "bad program step kind");
+        for (int q = 0; q < p; ++q)
+            if (bits[q] == bits[p])
+                return set_err(HS_ERR_INVALID, "grid program: one step per qubit");
+        t[p] = bits[p];
+    }
+    std::sort(t, t + nsteps);
+    if (h->m != 5 || ((uint64_t)1 << (2 * nsteps)) * 1024 < 4096)
+        return set_err(HS_ERR_UNSUPPORTED, "grid programs need 32 x 32 tiles");
+    DeviceGuard dg(h->device);
+    Geo G;
+    plan_geo(h, nsteps, t, G, 1);
+    auto* cf = new Coef<64>();
+    for (int p = 0; p < nsteps; ++p) {
+        std::memcpy(cf->s + 16 * p, s + 32 * p, 16 * sizeof(double2));
+        uint32_t l = 0;
+        while (t[l] != bits[p])
+            ++l;
+        cf->pbit[p] = (uint8_t)l;  // local grid bit of the step
+        cf->pkind[p] = (uint8_t)kinds[p];
+    }
+    cf->nsteps = (uint32_t)nsteps;
+    int rc = launch<3, M_PROG, 64>(h, G, *cf, KrausArgs{nullptr, 0}, 1);
+    delete cf;
+    if (rc)
+        return rc;
+    return finish_plan(h, G, nsteps, t, HS_PATH_TILED_CROSS, plan, 2 * state_bytes(h));
 }
 
 int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* t, hs_plan* plan) {

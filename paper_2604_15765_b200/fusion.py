@@ -11,9 +11,9 @@ kernels.cpp:510-549). ``apply_sequence`` gives the same result for a whole seque
   the staged tiles are transformed step after step in shared memory, each step in its cheapest form
   (Hadamard butterfly, diagonal phase, real (00,11)/(01,10) transfer as for depolarising / amplitude
   damping and their compositions, or a general transfer matrix);
-* the composed operations of two grid qubits share one pass when both are unitary (U_a (x) U_b, a
-  2-qubit unitary on two grid bits: the tensor-core gather); otherwise each grid qubit's composed
-  operation is one pass (native Hadamard when it is a lone H);
+* the composed operations of up to three grid qubits share one pass (`hs_apply_grid_program`: the
+  units of those grid bits are gathered and the steps applied one after another; m = 5); without
+  grid programs, two unitary grid steps share a pass as U_a (x) U_b (tensor-core gather);
 * any other operation (k >= 2) ends the run and is applied as is.
 
 The result equals applying the sequence one operation at a time up to floating-point rounding
@@ -71,7 +71,7 @@ def _unitary_of(spec: H.ChannelSpec) -> np.ndarray | None:
     return u if np.allclose(u @ u.conj().T, np.eye(2), atol=1e-14) else None
 
 
-def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True) -> Plan:
+def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_groups: int = 3) -> Plan:
     """ops: iterable of (ChannelSpec, targets)."""
     plan = Plan()
     edge = min(m, n)  # in-tile qubits
@@ -83,6 +83,21 @@ def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True) -> Plan:
         intile = [x for q in order if q < edge for x in chains[q]]
         for i in range(0, len(intile), 16):
             plan.items.append(("program", intile[i:i + 16]))
+        grid = [run[q] for q in order if q >= edge]
+        if grid_groups > 1 and m == 5:
+            # grid qubits three (two) at a time in one gathered pass (hs_apply_grid_program)
+            i = 0
+            while i < len(grid):
+                grp = grid[i:i + grid_groups]
+                if len(grp) == 1:
+                    plan.items.append(("step", grp[0]))
+                else:
+                    plan.items.append(("gprogram", grp))
+                i += grid_groups
+            run.clear()
+            chains.clear()
+            order.clear()
+            return
         # grid qubits: two unitary steps share one pass as the 2-qubit unitary U_a (x) U_b (the
         # tensor-core gather, k = 2 on two grid bits); others are one pass each
         pend = None
@@ -176,6 +191,14 @@ def execute(st: H.TiledHermitian, plan: Plan, opts: H.ApplyOptions | None = None
             nat.check(L.hs_apply_program(st.handle, len(steps), kinds.ctypes.data_as(nat.c_i32_p),
                                          bits.ctypes.data_as(nat.c_u32_p), s.ctypes.data_as(nat.c_double_p), None),
                       "apply_program")
+        elif item[0] == "gprogram":
+            steps = item[1]
+            kinds = np.array([_kind(x) for x in steps], np.int32)
+            bits = np.array([x.qubit for x in steps], np.uint32)
+            s = np.ascontiguousarray(np.stack([x.s for x in steps]).astype(np.complex128))
+            nat.check(L.hs_apply_grid_program(st.handle, len(steps), kinds.ctypes.data_as(nat.c_i32_p),
+                                              bits.ctypes.data_as(nat.c_u32_p), s.ctypes.data_as(nat.c_double_p),
+                                              None), "apply_grid_program")
         elif item[0] == "step":
             x = item[1]
             if x.lone_h:

@@ -185,17 +185,20 @@ def test_fusion_plan_counts():
     from paper_2604_15765_b200 import hermsim as H
     dep, amp = H.depolarising(0.01), H.amplitude_damping(0.05)
     ops = [(dep if op.kind == "depol" else amp, list(op.targets)) for op in HS.config_ops("c2", 16)]
-    plan = fusion.plan_sequence(ops, 16, 5)
+    plan = fusion.plan_sequence(ops, 16, 5, grid_groups=1)
     assert plan.ops == 32 and plan.launches == 12
     assert plan.items[0][0] == "program" and [s.qubit for s in plan.items[0][1]] == [0, 1, 2, 3, 4]
     assert [fusion._kind(s) for s in plan.items[0][1]] == [3] * 5  # depolarising o amplitude damping
     assert all(it[0] == "step" and it[1].count == 2 for it in plan.items[1:])
     h, cx = H.native_gate("h"), H.native_gate("cnot")
     seq = [(H.native_gate("rz", 0.3), [q]) for q in range(8)] + [(h, [q]) for q in range(8)] + [(cx, [7, 1])] + [(h, [6])]
-    plan = fusion.plan_sequence(seq, 8, 5, pair_unitaries=False)
+    plan = fusion.plan_sequence(seq, 8, 5, pair_unitaries=False, grid_groups=1)
     kinds = [it[0] for it in plan.items]
     assert kinds == ["program", "step", "step", "step", "op", "step"]
-    paired = fusion.plan_sequence(seq, 8, 5)  # grid qubits 5, 6 share a pass as H Rz (x) H Rz
+    grouped = fusion.plan_sequence(ops, 16, 5)  # C2: grid qubits three at a time
+    assert [it[0] for it in grouped.items] == ["program"] + ["gprogram"] * 3 + ["gprogram"]
+    assert [len(it[1]) for it in grouped.items[1:]] == [3, 3, 3, 2]
+    paired = fusion.plan_sequence(seq, 8, 5, grid_groups=1)  # grid qubits 5, 6 share a pass as H Rz (x) H Rz
     assert [it[0] for it in paired.items] == ["program", "op", "step", "op", "step"]
     assert paired.items[1][2] == [5, 6] and paired.items[1][1].k == 2
     assert paired.items[2][1].qubit == 7 and paired.items[-1][1].lone_h
