@@ -1793,26 +1793,26 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         sm_d = i0 * P + j0;
         sm_a = j0 * P + i0;
     };
-    // tile table and adjoint mask of item j, by the first copy warp alone (lanes take tiles lane,
-    // lane + 32) into slot j % (S + 1), which no stage in flight uses
-    auto tables = [&](uint64_t j) {
+    // tile table and adjoint mask of item j, by the first two copy warps (one logical tile per
+    // lane) into slot j % (S + 1), which no stage in flight uses
+    auto tables = [&](uint64_t j) {  // copy warps 0 and 1: one logical tile per lane (NT <= 64)
         const uint32_t ts = (uint32_t)(j % (S + 1));
         uint64_t tbi, tbj;
         unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), !G.ws_diag, tbi, tbj);
-        unsigned long long m = 0;
-        for (uint32_t t = mtid; t < NT; t += 32) {
+        const uint32_t t = mtid;
+        bool adj = false;
+        if (t < NT) {
             const uint64_t tr = ins_bits(tbi, t >> G.logNG, G.gr_pos, G.g);
             const uint64_t tc = ins_bits(tbj, t & NGm, G.gr_pos, G.g);
             uint64_t ent = tile_entry(G, tr, tc);
             if (tbi == tbj && (t >> G.logNG) < (t & NGm))
                 ent |= F_NOSTORE;  // aliases stored (C, R) of the same diagonal unit: read-only copy
             gt[ts][t] = ent;
-            m |= (unsigned long long)((ent & F_ADJ) != 0) << t;
+            adj = (ent & F_ADJ) != 0;
         }
-        for (int o = 16; o; o >>= 1)
-            m |= __shfl_xor_sync(0xffffffffu, m, o);
-        if (mtid == 0)
-            am[ts][0] = m;
+        const unsigned bal = __ballot_sync(0xffffffffu, adj);
+        if ((mtid & 31) == 0)
+            reinterpret_cast<uint32_t*>(&am[ts][0])[mtid >> 5] = bal;  // little endian: tiles 0-31, 32-63
     };
     // cp.async of item j into stage j % S (its table is visible: a copy-warp barrier separates them)
     auto issue = [&](uint64_t j) {
@@ -1853,7 +1853,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     };
     const bool prof = (G.dbg & 16u) && mtid == 0;
     long long ph[4] = {0, 0, 0, 0};
-    if (mtid < 32)
+    if (mtid < 64)
         for (uint64_t j = 0; j < S && j < nlocal; ++j)
             tables(j);
     mbar_sync();
@@ -1865,7 +1865,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         mbar_wait(&done[s], (uint32_t)((i / S) & 1));
         const long long t1 = prof ? clock64() : 0;
         const bool more = i + S < nlocal;
-        if (more && mtid < 32)
+        if (more && mtid < 64)
             tables(i + S);
         const double2* sb = ring + (size_t)s * G.stage_elems;
         auto wb = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
