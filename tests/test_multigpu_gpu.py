@@ -38,7 +38,7 @@ def _ops(H, HS, n):
     ]
 
 
-@pytest.mark.parametrize("n,P", [(9, 2), (10, 4), (11, 8), (10, 2)])
+@pytest.mark.parametrize("n,P", [(9, 2), (10, 4), (11, 8), (10, 2), (13, 8), (13, 4)])
 def test_sharded_bit_identical(n, P):
     from paper_2604_15765_b200 import harness as HS
     from paper_2604_15765_b200 import hermsim as H
