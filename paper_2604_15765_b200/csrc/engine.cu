@@ -124,9 +124,9 @@ struct Geo {
     uint32_t cross, cmask;        // top targets: `cross` of them, shard bits cb[]; cmask: the shard bits whose
     uint32_t cb[3];               // remote tiles the op reads (all top targets, or only the moving ones)
     uint32_t xmask, nx, xb[3];    // exchange-slot layout (recv_mask): slot = pext(own ^ shard, xmask) - 1
-    uint64_t recv_tiles;          // tiles per exchange slot
+    double2* out;                 // where stores go: the state itself, or (peer mode) the next buffer
     uint32_t q, Pulog, logBu;     // local units: group q over 2^Pulog blocks of 2^logBu grid bases
-    const double2* recv;          // group members' payloads, slot j at recv + j * recv_tiles tiles
+    const double2* rbase[7];      // remote tiles of group slot j: exchange buffer slot j, or the peer's payload
     uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
     uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): gather bit 0 skips the transform, bit 1 the loads, bit 2 the stores
     uint32_t ws_diag;             // gather_ws: units include the diagonal base pairs (grid programs)
@@ -289,6 +289,10 @@ __device__ __forceinline__ void shard_decode(uint32_t Plog, uint32_t logB, uint3
         tj = (uint64_t)b * B + (v & (B - 1));
     }
 }
+// base pointer of the payload an entry's tile lives in (own state or the group slot's source)
+__device__ __forceinline__ const double2* tile_base(const Geo& G, uint64_t ent, const double2* st) {
+    return (ent & F_REMOTE) ? G.rbase[(ent >> 56) & 7u] : st;
+}
 // (stored-tile index | F_ADJ | F_REMOTE) of logical tile (tr, tc) for this operation's shard
 __device__ __forceinline__ uint64_t tile_entry(const Geo& G, uint64_t tr, uint64_t tc) {
     const bool adj = tr < tc;
@@ -304,7 +308,7 @@ __device__ __forceinline__ uint64_t tile_entry(const Geo& G, uint64_t tr, uint64
         uint32_t slot = 0;
         for (uint32_t i = 0; i < G.nx; ++i)
             slot |= ((d >> G.xb[i]) & 1u) << i;
-        ent = (ent + (uint64_t)(slot - 1) * G.recv_tiles) | F_REMOTE | F_NOSTORE;
+        ent |= F_REMOTE | F_NOSTORE | ((uint64_t)(slot - 1) << 56);  // bits 56-58: the slot
     }
     return ent;
 }
@@ -630,7 +634,7 @@ __device__ void path_u(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
                         xs = l & SRm;
                         src = tb + ((uint64_t)y << G.logM) + (x0 | T.xdep[xs]);
                     }
-                    v[j] = ldg2(((ent & F_REMOTE) ? G.recv : st) + src);
+                    v[j] = ldg2(tile_base(G, ent, st) + src);
                     if (ent & F_ADJ)
                         v[j].y = -v[j].y;
                     dst[j] = (tt * G.SR + xs) * Mp + y;
@@ -699,7 +703,7 @@ __device__ void path_u(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
             }
             if (adj)
                 w.y = -w.y;
-            st[dstg] = w;
+            G.out[dstg] = w;
         }
     }
 }
@@ -756,11 +760,11 @@ __device__ void path_d(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
         if (R >= C) {
             const uint64_t ent = tile_entry(G, trow[R], trow[C]);
             v = (ent & F_SKIP) ? make_double2(0.0, 0.0)
-                               : ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)x << logM) + y];
+                               : tile_base(G, ent, st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)x << logM) + y];
         } else {
             const uint64_t ent = tile_entry(G, trow[C], trow[R]);
             v = (ent & F_SKIP) ? make_double2(0.0, 0.0)
-                               : ((ent & F_REMOTE) ? G.recv : st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)y << logM) + x];
+                               : tile_base(G, ent, st)[((ent & F_MASK) << (2 * logM)) + ((uint64_t)y << logM) + x];
             v.y = -v.y;
         }
         if (!one)
@@ -793,13 +797,13 @@ __device__ void path_d(const Geo& G, const Tabs& T, const Coef<NS>& cf, const Kr
             continue;  // the partner shard stores this tile
         const uint64_t t0 = (ent & F_MASK) << (2 * logM);
         if (R > C) {
-            st[t0 + ((uint64_t)x << logM) + y] = w;
+            G.out[t0 + ((uint64_t)x << logM) + y] = w;
         } else if (R < C) {
-            st[t0 + ((uint64_t)y << logM) + x] = cconj(w);
+            G.out[t0 + ((uint64_t)y << logM) + x] = cconj(w);
         } else {
-            st[t0 + ((uint64_t)x << logM) + y] = w;
+            G.out[t0 + ((uint64_t)x << logM) + y] = w;
             if (x != y)
-                st[t0 + ((uint64_t)y << logM) + x] = cconj(w);
+                G.out[t0 + ((uint64_t)y << logM) + x] = cconj(w);
         }
     }
 }
@@ -927,9 +931,9 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
             const uint32_t tsm =
                 sbase + ((tt >> G.logNT) * G.A + G.slot[tt & ((1u << G.logNT) - 1)]) * G.TS * 16u;
             if (STORE)
-                bulk_s2g(st + gbase, tsm, bytes);
+                bulk_s2g(G.out + gbase, tsm, bytes);
             else
-                bulk_g2s(tsm, ((ent & F_REMOTE) ? G.recv : st) + gbase, bytes, bar);
+                bulk_g2s(tsm, tile_base(G, ent, st) + gbase, bytes, bar);
         }
         return;
     }
@@ -939,7 +943,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
             continue;
         const uint64_t gbase = (ent & F_MASK) << (2 * G.logM);
         const uint32_t tsm = sbase + ((tt >> G.logNT) * G.A + G.slot[tt & ((1u << G.logNT) - 1)]) * G.TS * 16u;
-        const double2* src = (ent & F_REMOTE) ? G.recv : st;
+        const double2* src = tile_base(G, ent, st);
         if (!(ent & F_ADJ)) {
             for (uint32_t r = lane; r < G.nruns; r += 32) {
                 const uint32_t xs0 = G.run_xs[r], len = G.run_len[r];
@@ -947,7 +951,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
                 const uint32_t s = tsm + ((xs0 << G.logM) << 4);
                 const uint32_t bytes = (len << G.logM) << 4;
                 if (STORE)
-                    bulk_s2g(st + g, s, bytes);
+                    bulk_s2g(G.out + g, s, bytes);
                 else
                     bulk_g2s(s, src + g, bytes, bar);
             }
@@ -959,7 +963,7 @@ __device__ __forceinline__ void item_copies(const Geo& G, const Tabs& T, uint64_
                 const uint64_t g = gbase + ((uint64_t)y << G.logM) + (x0 | T.xdep[xs0]);
                 const uint32_t s = tsm + ((y * G.SRp + xs0) << 4);
                 if (STORE)
-                    bulk_s2g(st + g, s, len << 4);
+                    bulk_s2g(G.out + g, s, len << 4);
                 else
                     bulk_g2s(s, src + g, len << 4, bar);
             }
@@ -1615,7 +1619,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
                 const bool adj = (ent & F_ADJ) != 0;
                 const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
                 cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u,
-                           ((ent & F_REMOTE) ? G.recv : st) + g);
+                           tile_base(G, ent, st) + g);
             }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
@@ -1653,7 +1657,7 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
                 if (ent & (F_SKIP | F_NOSTORE))
                     continue;
                 const bool adj = (ent & F_ADJ) != 0;
-                st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+                G.out[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
             }
         }
         gbar();
@@ -1822,7 +1826,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint64_t ent = gt[ts][tt];
             const bool adj = (ent & F_ADJ) != 0;
             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
-            cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, ((ent & F_REMOTE) ? G.recv : st) + g);
+            cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, tile_base(G, ent, st) + g);
         };
         if (G.dbg & 2u) {
         } else if (fast) {  // 8 tiles at one position: unrolled, table reads hoisted
@@ -1873,7 +1877,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             if (ent & F_NOSTORE)
                 return;
             const bool adj = (ent & F_ADJ) != 0;
-            st[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+            G.out[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
         };
         if (G.dbg & 4u) {
         } else if (fast) {
@@ -2218,13 +2222,12 @@ void plan_geo(const hs_state* h, int k, const uint32_t* t, Geo& G, uint32_t extr
     G.Plog = h->Plog;
     G.shard = h->shard;
     G.logB = h->logB;
-    G.recv = h->recv;
+    G.out = h->d;
     G.cross = 0;
     G.cmask = 0;
     G.cb[0] = G.cb[1] = G.cb[2] = 0;
     G.xmask = G.nx = 0;
     G.xb[0] = G.xb[1] = G.xb[2] = 0;
-    G.recv_tiles = h->recv_count >> (2 * h->m);
     G.Pulog = h->Plog;
     G.q = h->shard;
     if (h->Plog && g) {
@@ -2583,6 +2586,8 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         for (uint32_t b = 0; b < 32 && G.nx < 3; ++b)
             if (G.xmask >> b & 1u)
                 G.xb[G.nx++] = b;
+        for (uint32_t j = 0; j < 7; ++j)
+            G.rbase[j] = j < h->recv_slots ? h->recv + (uint64_t)j * h->recv_count : nullptr;
     }
     G.rev = (uint32_t)(h->sweeps++ & 1u);
     G.dbg = 0;
