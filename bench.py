@@ -21,7 +21,8 @@ stored).  A step = one pass of the 32 channel applications.
 * --impl reference  times that reference CPU path alone, all host threads (rank 0 only).
 For N > 1 (torchrun) every rank runs an independent replica of the config (weak scaling) -- except
 with --shard (the default for c4, the sharded n = 17 config): the operator is partitioned into N XOR-
-block shards, one per GPU, cross-shard ops exchange over NCCL inside the engine, and the whole job
+block shards, one per GPU; a cross-shard op's kernels read the group members' tiles in place over
+NVLink (peer mode, CUDA IPC) or, with --exchange, after an NCCL group exchange; the whole job
 processes one operator (strong scaling; value = ops of the operator per second).
 """
 from __future__ import annotations
@@ -288,6 +289,9 @@ def main():
     ap.add_argument("--shard", dest="shard", action="store_true", default=None,
                     help="partition the operator over the N ranks (default for c4 when N > 1)")
     ap.add_argument("--replicas", dest="shard", action="store_false", help="N independent replicas")
+    ap.add_argument("--exchange", action="store_true",
+                    help="sharded: NCCL exchange of the group's shards before a cross-shard op (default: peer mode, "
+                         "the op's kernels read the members' tiles in place over NVLink)")
     ap.add_argument("--fuse", action="store_true",
                     help="operation fusion (SURVEY 8f): same sequence, fewer passes; value counts the logical ops")
     args = ap.parse_args()
@@ -348,7 +352,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     sharded = world > 1 and (args.shard if args.shard is not None else cfg == "c4")
     if sharded:
         from paper_2604_15765_b200.multigpu import DistributedShard
-        dshard = DistributedShard(n, m, device=local)
+        dshard = DistributedShard(n, m, device=local, peer=not args.exchange)
         st = dshard.state
         apply_op = dshard.apply
     else:
@@ -360,7 +364,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     if cfg == "c3":
         strings = HS.pauli_strings(n, 64, seed)
         st.fill_pauli_sum(*strings)
-        drho = DistributedShard(n, m, device=local) if sharded else None
+        drho = DistributedShard(n, m, device=local, peer=not args.exchange) if sharded else None
         rho = drho.state if sharded else H.TiledHermitian(n, m, device=local)
         psi = HS.rank_psi(n, seed + 1, 4)
         rho.fill_mixture(psi)
@@ -499,7 +503,8 @@ def ours_arm(args, cfg, n, m, world, rank, local):
                               "logical operations; reported separately from the per-operation metric"}
                              if fplan is not None else None),
                    "stored_bytes_per_rank": S,
-                   "parallelism": (f"sharded x{world} (XOR blocks, NCCL group exchange)" if sharded else
+                   "parallelism": (f"sharded x{world} (XOR blocks, " + ("NCCL group exchange" if args.exchange else
+                                   "peer-memory reads fused into the op kernels") + ")" if sharded else
                                    f"replicas x{world}" if world > 1 else "single GPU"),
                    "l2": "inputs larger than L2 (state %.2f GB vs 126 MB L2); no flush needed" % (S / 1e9)},
         "achieved_hbm_gbs": sum(touched) * args.steps / (total_ms / 1e3) / 1e9,

@@ -197,6 +197,19 @@ int hs_nccl_unique_id(void* id128);                               /* ncclUniqueI
 int hs_state_comm_init(hs_state* h, const void* id128, int nranks, int rank);  /* rank == shard */
 int hs_state_exchange(hs_state* h, int partner);                  /* NCCL send/recv, stream-ordered */
 int hs_state_exchange_group(hs_state* h, uint32_t mask);          /* NCCL, every other member of the group */
+/* Peer mode: cross-shard operations read the group members' payloads in place (peer memory over
+ * NVLink via CUDA IPC / peer access, or the same device) inside their own kernels and write this
+ * shard's result into its second buffer, which becomes current -- no exchange buffer.  The caller
+ * must order operations across shards: before a cross-shard operation, every group member has
+ * finished its previous ones (barrier). */
+int hs_state_peer_enable(hs_state* h);                                   /* allocates the second buffer */
+int hs_state_peer_buffers(const hs_state* h, void** b0, void** b1);      /* this shard's two buffers */
+int hs_state_set_peer(hs_state* h, int shard, const void* b0, const void* b1);  /* a member's two buffers */
+int hs_state_peer_flip(const hs_state* h, int* flip);                   /* index of the current buffer */
+int hs_ipc_handles(const hs_state* h, void* out128);                     /* cudaIpcMemHandle of both buffers */
+int hs_ipc_open(const void* handle64, int device, void** ptr);
+int hs_ipc_close(void* ptr, int device);
+int hs_peer_access(int device, int peer_device);
 /* linear partial sums of one shard: kind 0 tr(rho O), 1 squared Frobenius, 2 trace (sum over shards) */
 int hs_reduce_partial(const hs_state* a, const hs_state* b, int kind, double* out);
 

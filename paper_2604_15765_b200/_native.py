@@ -119,6 +119,14 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_op_group", i, [vp, i, c_u32_p, c_u32_p])
     _sig(L, "hs_apply_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
     _sig(L, "hs_apply_grid_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
+    _sig(L, "hs_state_peer_enable", i, [vp])
+    _sig(L, "hs_state_peer_buffers", i, [vp, pp, pp])
+    _sig(L, "hs_state_set_peer", i, [vp, i, vp, vp])
+    _sig(L, "hs_state_peer_flip", i, [vp, c_int_p])
+    _sig(L, "hs_ipc_handles", i, [vp, vp])
+    _sig(L, "hs_ipc_open", i, [vp, i, pp])
+    _sig(L, "hs_ipc_close", i, [vp, i])
+    _sig(L, "hs_peer_access", i, [i, i])
     _sig(L, "hs_state_save", i, [vp, ctypes.c_char_p])
     _sig(L, "hs_state_load", i, [ctypes.c_char_p, i, pp])
     _sig(L, "hs_state_recv_reserve", i, [vp, i])

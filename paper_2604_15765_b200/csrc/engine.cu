@@ -2122,6 +2122,12 @@ struct hs_state {
     uint32_t recv_slots = 0;  // allocated slots
     uint32_t recv_mask = 0;   // shard-bit mask of the last exchange (which slots hold whom)
     void* comm = nullptr;     // ncclComm_t
+    // peer mode: cross-shard operations read the group members' payloads in place (peer memory over
+    // NVLink, or the same device) and write this shard's result out of place into the other buffer
+    bool peer_mode = false;
+    double2* buf[2] = {nullptr, nullptr};     // this shard's two payload buffers (buf[flip] is current)
+    uint32_t flip = 0;
+    const double2* peer_buf[64][2] = {};       // peers' buffers, valid on this device
 };
 
 namespace {
@@ -2575,12 +2581,39 @@ int sm_count(int device) {
 }
 
 template <int K, int MODE, int NS>
-int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
-    if (G0.cmask && (!h->recv || (G0.cmask & ~h->recv_mask) ||
-                     h->recv_slots < (1u << __builtin_popcount(h->recv_mask)) - 1))
+int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+    const bool peer = G0.cmask && h->peer_mode;
+    if (peer) {
+        for (uint32_t d = 1; d < 32; ++d)
+            if (!(d & ~G0.cmask) && !h->peer_buf[h->shard ^ d][h->flip])
+                return set_err(HS_ERR_INVALID, "peer mode: a group member's buffers are not registered");
+    } else if (G0.cmask && (!h->recv || (G0.cmask & ~h->recv_mask) ||
+                            h->recv_slots < (1u << __builtin_popcount(h->recv_mask)) - 1))
         return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the group's shards first");
     Geo G = G0;
-    if (G.cmask) {  // exchange-slot layout of the last exchange (it may cover more bits than needed)
+    if (peer) {
+        // read the group members' current payloads where they lie, write ours into the other
+        // buffer (the members read our current one concurrently); slots follow the op's own mask
+        G.xmask = G.cmask;
+        G.nx = 0;
+        for (uint32_t b = 0; b < 32 && G.nx < 3; ++b)
+            if (G.xmask >> b & 1u)
+                G.xb[G.nx++] = b;
+        for (uint32_t j = 0; j < 7; ++j)
+            G.rbase[j] = nullptr;
+        for (uint32_t d = 1; d < 32; ++d) {
+            if (d & ~G.cmask)
+                continue;
+            uint32_t slot = 0, i = 0;
+            for (uint32_t b = 0; b < 32; ++b)
+                if (G.cmask >> b & 1u)
+                    slot |= ((d >> b) & 1u) << i++;
+            G.rbase[slot - 1] = h->peer_buf[h->shard ^ d][h->flip];
+        }
+        G.out = h->buf[h->flip ^ 1];
+        if (MODE == M_MONO || MODE == M_KRAUS)  // tiles a monomial leaves untouched must carry over
+            CUDA_TRY(cudaMemcpyAsync(G.out, h->d, h->count * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
+    } else if (G.cmask) {  // exchange-slot layout of the last exchange (it may cover more bits than needed)
         G.xmask = h->recv_mask;
         G.nx = 0;
         for (uint32_t b = 0; b < 32 && G.nx < 3; ++b)
@@ -2752,6 +2785,17 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
     return HS_OK;
 }
 
+// One operation's kernels.  Peer mode: the result went to the other buffer, which becomes current.
+template <int K, int MODE, int NS>
+int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+    const int rc = launch_impl<K, MODE, NS>(h, G0, cf, ka, buffers);
+    if (rc == HS_OK && G0.cmask && h->peer_mode) {
+        h->flip ^= 1u;
+        h->d = h->buf[h->flip];
+    }
+    return rc;
+}
+
 // Subcase counters (SubcaseCounters, kernels.hpp:29-41) for the cross/mixed engines: A = unit
 // whose logical tiles are all stored directly, B = some logical tile is an adjoint, C =
 // diagonal base pair.  Counted on the host by the closed form (k = 1) or by enumeration.
@@ -2919,7 +2963,12 @@ int hs_state_free(hs_state* h) {
         return HS_OK;
     DeviceGuard dg(h->device);
     cudaStreamSynchronize(h->stream);
-    cudaFree(h->d);
+    if (h->peer_mode) {
+        cudaFree(h->buf[0]);
+        cudaFree(h->buf[1]);
+    } else {
+        cudaFree(h->d);
+    }
     cudaFree(h->red);
     cudaFree(h->kraus);
     cudaFree(h->recv);
@@ -3970,5 +4019,104 @@ int hs_state_load(const char* path, int device, hs_state** out) {
         return set_err(HS_ERR_CUDA, "load: device copy failed");
     }
     *out = h;
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------ peer-memory sharding
+// Peer mode: a cross-shard operation reads the group members' current payloads where
+// they lie -- peer memory over NVLink (CUDA IPC across processes, or peer access in one process) or
+// the same device -- inside the operation's own kernels, and writes this shard's result into its
+// second buffer, which then becomes current.  The collective is the kernel's remote tile reads;
+// nothing is staged through an exchange buffer.  The caller orders operations across shards: before
+// a cross-shard operation every group member must have finished its previous operations (a
+// barrier), because members read each other's current buffers while writing their own other one.
+int hs_state_peer_enable(hs_state* h) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (h->peer_mode)
+        return HS_OK;
+    DeviceGuard dg(h->device);
+    double2* alt = nullptr;
+    cudaError_t e = cudaMalloc(&alt, h->count * sizeof(double2));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(HS_ERR_NOMEM, std::string("peer mode: second payload buffer: ") + cudaGetErrorString(e));
+    }
+    h->buf[0] = h->d;
+    h->buf[1] = alt;
+    h->flip = 0;
+    h->peer_mode = true;
+    return HS_OK;
+}
+
+int hs_state_peer_buffers(const hs_state* h, void** b0, void** b1) {
+    if (!h || !h->peer_mode)
+        return set_err(HS_ERR_INVALID, "peer mode not enabled");
+    if (b0)
+        *b0 = h->buf[0];
+    if (b1)
+        *b1 = h->buf[1];
+    return HS_OK;
+}
+
+int hs_state_set_peer(hs_state* h, int shard, const void* b0, const void* b1) {
+    if (!h || !b0 || !b1)
+        return set_err(HS_ERR_INVALID, "null argument");
+    if (shard < 0 || shard >= (1 << h->Plog) || shard >= 64 || shard == (int)h->shard)
+        return set_err(HS_ERR_RANGE, "bad peer shard");
+    h->peer_buf[shard][0] = static_cast<const double2*>(b0);
+    h->peer_buf[shard][1] = static_cast<const double2*>(b1);
+    return HS_OK;
+}
+
+int hs_state_peer_flip(const hs_state* h, int* flip) {
+    if (!h || !flip)
+        return set_err(HS_ERR_INVALID, "null argument");
+    *flip = (int)h->flip;
+    return HS_OK;
+}
+
+int hs_ipc_handles(const hs_state* h, void* out128) {
+    if (!h || !out128 || !h->peer_mode)
+        return set_err(HS_ERR_INVALID, "peer mode not enabled");
+    DeviceGuard dg(h->device);
+    cudaIpcMemHandle_t a, b;
+    CUDA_TRY(cudaIpcGetMemHandle(&a, h->buf[0]));
+    CUDA_TRY(cudaIpcGetMemHandle(&b, h->buf[1]));
+    std::memcpy(out128, &a, 64);
+    std::memcpy(static_cast<char*>(out128) + 64, &b, 64);
+    return HS_OK;
+}
+
+int hs_ipc_open(const void* handle64, int device, void** ptr) {
+    if (!handle64 || !ptr)
+        return set_err(HS_ERR_INVALID, "null argument");
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, handle64, 64);
+    CUDA_TRY(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess));
+    return HS_OK;
+}
+
+int hs_ipc_close(void* ptr, int device) {
+    if (!ptr)
+        return HS_OK;
+    DeviceGuard dg(device);
+    CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return HS_OK;
+}
+
+int hs_peer_access(int device, int peer_device) {
+    if (device == peer_device)
+        return HS_OK;
+    DeviceGuard dg(device);
+    int can = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&can, device, peer_device));
+    if (!can)
+        return set_err(HS_ERR_UNSUPPORTED, "no peer access between the devices");
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return set_err(HS_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+    cudaGetLastError();
     return HS_OK;
 }

@@ -192,17 +192,44 @@ def reduce_partial(a: H.TiledHermitian, b: H.TiledHermitian | None, kind: int) -
     return out.value
 
 
-class ShardGroup:
-    """P shards of one operator driven from one process (devices: one GPU or a list of GPUs)."""
+def _peer_buffers(st: H.TiledHermitian):
+    b0, b1 = ctypes.c_void_p(), ctypes.c_void_p()
+    nat.check(nat.engine().hs_state_peer_buffers(st.handle, ctypes.byref(b0), ctypes.byref(b1)), "peer buffers")
+    return b0, b1
 
-    def __init__(self, n: int, m: int = 5, nshards: int = 2, devices=(0,)):
+
+class ShardGroup:
+    """P shards of one operator driven from one process (devices: one GPU or a list of GPUs).
+
+    peer=False: a cross-shard op first copies the group members' payloads into exchange slots.
+    peer=True: every shard's kernels read the members' current payloads in place (same device or
+    peer access) and write out of place; a barrier (all shard streams synchronised) precedes each
+    op that touches a top qubit."""
+
+    def __init__(self, n: int, m: int = 5, nshards: int = 2, devices=(0,), peer: bool = False):
         self.layout = ShardLayout(n, m, nshards)
-        self.n, self.m, self.P = n, m, nshards
+        self.n, self.m, self.P, self.peer = n, m, nshards, peer
         self.shards = [_shard_state(n, m, devices[s % len(devices)], nshards, s) for s in range(nshards)]
+        if peer:
+            L = nat.engine()
+            for st in self.shards:
+                nat.check(L.hs_state_peer_enable(st.handle), "peer enable")
+            bufs = [_peer_buffers(st) for st in self.shards]
+            for a, st in enumerate(self.shards):
+                for b, other in enumerate(self.shards):
+                    if a != b:
+                        nat.check(L.hs_peer_access(st.device, other.device), "peer access")
+                        nat.check(L.hs_state_set_peer(st.handle, b, bufs[b][0], bufs[b][1]), "set peer")
 
     def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
         """hermsim.apply on every shard; exchanges first when the op crosses shards."""
         opts = opts or H.ApplyOptions(count_subcases=False)
+        if self.peer:
+            if self.layout.group_mask(targets):  # members read each other: previous ops complete
+                for st in self.shards:
+                    st.synchronize()
+            plans = [H.apply(st, spec, targets, opts) for st in self.shards]
+            return plans[0]
         mask = op_mask(self.layout, spec, targets)
         if mask:
             # all exchanges read the pre-op payloads, then every shard updates its own tiles
@@ -246,15 +273,42 @@ class ShardGroup:
 
 
 class DistributedShard:
-    """This rank's shard of an operator sharded over a torch.distributed job (rank == shard); the
-    cross-shard exchange runs inside the engine over NCCL on the state's stream."""
+    """This rank's shard of an operator sharded over a torch.distributed job (rank == shard).
 
-    def __init__(self, n: int, m: int = 5, device: int | None = None):
+    peer=False: the cross-shard exchange runs inside the engine over NCCL on the state's stream.
+    peer=True: the ranks map each other's two payload buffers (CUDA IPC; peer access over NVLink) and
+    a cross-shard op's kernels read the group members' tiles in place -- the collective is fused
+    into the op; a barrier precedes each op that touches a top qubit."""
+
+    def __init__(self, n: int, m: int = 5, device: int | None = None, peer: bool = False):
         import torch.distributed as dist
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.layout = ShardLayout(n, m, self.world)
         self.device = self.rank if device is None else device
         self.state = _shard_state(n, m, self.device, self.world, self.rank)
+        self.peer = peer
+        self._opened = []
+        if peer:
+            L = nat.engine()
+            nat.check(L.hs_state_peer_enable(self.state.handle), "peer enable")
+            hd = (ctypes.c_char * 128)()
+            nat.check(L.hs_ipc_handles(self.state.handle, hd), "ipc handles")
+            allh = [None] * self.world
+            dist.all_gather_object(allh, (bytes(hd), self.device))
+            for r, (h, dev) in enumerate(allh):
+                if r == self.rank:
+                    continue
+                if dev != self.device:
+                    nat.check(L.hs_peer_access(self.device, dev), "peer access")
+                ptrs = []
+                for half in (h[:64], h[64:]):
+                    p = ctypes.c_void_p()
+                    nat.check(L.hs_ipc_open((ctypes.c_char * 64).from_buffer_copy(half), self.device,
+                                            ctypes.byref(p)), "ipc open")
+                    ptrs.append(p)
+                    self._opened.append(p)
+                nat.check(L.hs_state_set_peer(self.state.handle, r, ptrs[0], ptrs[1]), "set peer")
+            return
         uid = (ctypes.c_char * 128)()
         if self.rank == 0:
             nat.check(nat.engine().hs_nccl_unique_id(uid), "nccl id")
@@ -265,10 +319,24 @@ class DistributedShard:
 
     def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
         opts = opts or H.ApplyOptions(count_subcases=False)
+        if self.peer:
+            if self.layout.group_mask(targets):  # members read each other: previous ops complete
+                import torch.distributed as dist
+                self.state.synchronize()
+                dist.barrier()
+            return H.apply(self.state, spec, targets, opts)
         mask = op_mask(self.layout, spec, targets)
         if mask:
             nat.check(nat.engine().hs_state_exchange_group(self.state.handle, mask), "exchange")
         return H.apply(self.state, spec, targets, opts)
+
+    def close(self):
+        """Unmaps the peers' buffers (peer mode); the state itself is freed with the object."""
+        if self.peer:
+            self.state.synchronize()
+            for p in self._opened:
+                nat.engine().hs_ipc_close(p, self.device)
+            self._opened = []
 
     def reduce(self, other: "DistributedShard | None", kind: int) -> float:
         """Sum over shards of the partial (deterministic: gathered, summed in rank order)."""

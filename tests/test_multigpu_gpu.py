@@ -38,15 +38,16 @@ def _ops(H, HS, n):
     ]
 
 
-@pytest.mark.parametrize("n,P", [(9, 2), (10, 4), (11, 8), (10, 2), (13, 8), (13, 4)])
-def test_sharded_bit_identical(n, P):
+@pytest.mark.parametrize("n,P,peer", [(9, 2, False), (10, 4, False), (11, 8, False), (10, 2, False), (13, 8, False),
+                                      (13, 4, False), (9, 2, True), (10, 4, True), (11, 8, True), (13, 8, True)])
+def test_sharded_bit_identical(n, P, peer):
     from paper_2604_15765_b200 import harness as HS
     from paper_2604_15765_b200 import hermsim as H
     from paper_2604_15765_b200.multigpu import ShardGroup
     psi = HS.rank_psi(n, 42, 4)
     ref = H.TiledHermitian(n)
     ref.fill_mixture(psi)
-    grp = ShardGroup(n, 5, P)
+    grp = ShardGroup(n, 5, P, peer=peer)
     grp.fill_mixture(psi)
     assert np.array_equal(grp.download_full().view(np.uint64), ref.download().view(np.uint64))
     opts = H.ApplyOptions(count_subcases=False)
@@ -79,3 +80,55 @@ def test_group_exchange_required():
     H.apply(st, H.native_gate("cnot"), [9, 8])
     with pytest.raises((ValueError, nat.NativeError)):
         H.apply(st, H.native_gate("swap"), [9, 8])
+
+
+def _ipc_worker(rank, world, port, n, q):
+    import os
+    import sys
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    from paper_2604_15765_b200.multigpu import DistributedShard
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    sh = DistributedShard(n, 5, device=0, peer=True)  # both ranks on GPU 0: CUDA IPC, host barriers
+    sh.state.fill_mixture(HS.rank_psi(n, 42, 4))
+    for spec, tg in _ops(H, HS, n):
+        sh.apply(spec, tg)
+    sh.state.synchronize()
+    dist.barrier()
+    parts = [None] * world
+    dist.all_gather_object(parts, sh.state.download())
+    if rank == 0:
+        q.put(sh.layout.gather(parts))
+    dist.barrier()
+    sh.close()
+    dist.destroy_process_group()
+
+
+def test_peer_mode_across_processes():
+    """Peer mode with CUDA IPC between two processes (two shards on one GPU: the kernels never wait on
+    each other -- ordering is by host barriers) against the single-GPU engine, bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    n, world = 10, 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = H.TiledHermitian(n)
+    ref.fill_mixture(HS.rank_psi(n, 42, 4))
+    opts = H.ApplyOptions(count_subcases=False)
+    for spec, tg in _ops(H, HS, n):
+        H.apply(ref, spec, tg, opts)
+    assert np.array_equal(got.view(np.uint64), ref.download().view(np.uint64))
