@@ -61,6 +61,9 @@ def log(*a):
 
 # ----------------------------------------------------------------------------- distributed
 def dist_setup():
+    """One rank per GPU over NCCL.  BENCH_FUNCTIONAL_ONE_GPU=1 (code-path check only, never a
+    measurement): every rank on GPU 0 with a gloo group -- the sharded peer mode then orders the
+    ranks by host barriers, so no kernel waits on another."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -68,8 +71,13 @@ def dist_setup():
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BENCH_FUNCTIONAL_ONE_GPU") == "1":
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -78,7 +86,7 @@ def dist_max(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if dist.get_backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -280,7 +288,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--n", type=int, default=None, help="override the config's qubit count (testing)")
+    ap.add_argument("--qubits", "--n", dest="n", type=int, default=None, help="override the config's qubit count (testing)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
