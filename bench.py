@@ -300,6 +300,8 @@ def main():
     ap.add_argument("--exchange", action="store_true",
                     help="sharded: NCCL exchange of the group's shards before a cross-shard op (default: peer mode, "
                          "the op's kernels read the members' tiles in place over NVLink)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one step as a CUDA graph after the warm-up and replay it (hermsim.capture)")
     ap.add_argument("--fuse", action="store_true",
                     help="operation fusion (SURVEY 8f): same sequence, fewer passes; value counts the logical ops")
     args = ap.parse_args()
@@ -420,6 +422,17 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     for w in range(args.warmup):
         step(collect=(w == 0))
     st.synchronize()
+    graph = None
+    if args.graph:
+        if sharded:
+            raise SystemExit("--graph runs on single-GPU / replica states")
+        with H.capture(st) as graph:  # per-launch events are not captured: launches share the step time
+            step()
+        plain_step = step
+
+        def step(record=False, collect=False):  # noqa: F811
+            graph.launch()
+        _ = plain_step
     dist_barrier(world)
     clocks = ClockSampler(local)
     clocks.start()
@@ -438,6 +451,9 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(ms)))
     total_ms = float(ms.value)
     for i in range(npass):
+        if graph is not None:
+            launch_ms.append(total_ms / args.steps / npass)
+            continue
         x = ctypes.c_float()
         nat.check(L.hs_event_elapsed_ms(ev[2 + 2 * i], ev[3 + 2 * i], ctypes.byref(x)))
         launch_ms.append(float(x.value))
@@ -510,6 +526,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
                    "fused": ({"passes_per_step": npass, "note": "operation fusion (SURVEY 8f): value counts the "
                               "logical operations; reported separately from the per-operation metric"}
                              if fplan is not None else None),
+                   "cuda_graph": bool(args.graph),
                    "stored_bytes_per_rank": S,
                    "parallelism": (f"sharded x{world} (XOR blocks, " + ("NCCL group exchange" if args.exchange else
                                    "peer-memory reads fused into the op kernels") + ")" if sharded else

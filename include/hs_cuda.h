@@ -213,6 +213,18 @@ int hs_peer_access(int device, int peer_device);
 /* linear partial sums of one shard: kind 0 tr(rho O), 1 squared Frobenius, 2 trace (sum over shards) */
 int hs_reduce_partial(const hs_state* a, const hs_state* b, int kind, double* out);
 
+/* ---- CUDA graphs: capture a sequence of operations on one state, replay it with one launch ----
+ * hs_graph_begin(h); ...apply calls on h...; hs_graph_end(h, &g); hs_graph_launch(g, h) (any
+ * number of times, stream-ordered on h).  The captured kernels bake in the operations' parameters
+ * and the state's payload pointer.  Not for peer-mode states; k = 3 multi-operator Kraus channels
+ * cannot be captured. */
+typedef struct hs_graph hs_graph;
+int hs_graph_begin(hs_state* h);
+int hs_graph_end(hs_state* h, hs_graph** out);
+int hs_graph_launch(const hs_graph* g, hs_state* h);
+int hs_graph_nodes(const hs_graph* g, uint64_t* n);
+int hs_graph_free(hs_graph* g);
+
 /* ---- device timing helpers (CUDA events on the state's stream) ------------------------ */
 int hs_event_create(void** ev);
 int hs_event_destroy(void* ev);

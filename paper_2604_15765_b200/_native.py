@@ -127,6 +127,11 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_ipc_open", i, [vp, i, pp])
     _sig(L, "hs_ipc_close", i, [vp, i])
     _sig(L, "hs_peer_access", i, [i, i])
+    _sig(L, "hs_graph_begin", i, [vp])
+    _sig(L, "hs_graph_end", i, [vp, pp])
+    _sig(L, "hs_graph_launch", i, [vp, vp])
+    _sig(L, "hs_graph_nodes", i, [vp, c_u64_p])
+    _sig(L, "hs_graph_free", i, [vp])
     _sig(L, "hs_state_save", i, [vp, ctypes.c_char_p])
     _sig(L, "hs_state_load", i, [ctypes.c_char_p, i, pp])
     _sig(L, "hs_state_recv_reserve", i, [vp, i])

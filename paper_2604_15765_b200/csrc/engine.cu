@@ -3485,6 +3485,12 @@ int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32
         CUDA_TRY(cudaMalloc(&h->kraus, bytes));
         h->kraus_cap = bytes;
     }
+    {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing(h->stream, &cs));
+        if (cs != cudaStreamCaptureStatusNone)  // the upload of the Kraus set would read host memory at replay
+            return set_err(HS_ERR_UNSUPPORTED, "k = 3 Kraus channels with several operators cannot be captured in a graph");
+    }
     CUDA_TRY(cudaMemcpyAsync(h->kraus, ops, bytes, cudaMemcpyHostToDevice, h->stream));
     Geo G;
     plan_geo(h, k, t, G, 3);
@@ -4118,5 +4124,78 @@ int hs_peer_access(int device, int peer_device) {
     if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
         return set_err(HS_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
     cudaGetLastError();
+    return HS_OK;
+}
+
+// ------------------------------------------------------------------------- CUDA graphs
+// A sequence of operations on one state captured once and replayed: the host-side planning (tables,
+// geometry, dispatch) runs at capture time only, the replay is one cudaGraphLaunch on the state's
+// stream.  For circuits repeated many times and for small states, where launch latency and host
+// dispatch approach the kernel time.  Not for peer-mode states (buffer flips are host state).
+struct hs_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int device = 0;
+};
+
+int hs_graph_begin(hs_state* h) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (h->peer_mode)
+        return set_err(HS_ERR_UNSUPPORTED, "graphs: peer-mode states flip buffers on the host");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    return HS_OK;
+}
+
+int hs_graph_end(hs_state* h, hs_graph** out) {
+    if (!h || !out)
+        return set_err(HS_ERR_INVALID, "null argument");
+    *out = nullptr;
+    DeviceGuard dg(h->device);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(HS_ERR_CUDA, std::string("graph capture failed: ") + cudaGetErrorString(e));
+    }
+    auto* hg = new hs_graph();
+    hg->graph = g;
+    hg->device = h->device;
+    const cudaError_t e2 = cudaGraphInstantiate(&hg->exec, g, 0);
+    if (e2 != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphDestroy(g);
+        delete hg;
+        return set_err(HS_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e2));
+    }
+    *out = hg;
+    return HS_OK;
+}
+
+int hs_graph_launch(const hs_graph* g, hs_state* h) {
+    if (!g || !h)
+        return set_err(HS_ERR_INVALID, "null argument");
+    DeviceGuard dg(h->device);
+    CUDA_TRY(cudaGraphLaunch(g->exec, h->stream));
+    return HS_OK;
+}
+
+int hs_graph_nodes(const hs_graph* g, uint64_t* n) {
+    if (!g || !n)
+        return set_err(HS_ERR_INVALID, "null argument");
+    size_t c = 0;
+    CUDA_TRY(cudaGraphGetNodes(g->graph, nullptr, &c));
+    *n = c;
+    return HS_OK;
+}
+
+int hs_graph_free(hs_graph* g) {
+    if (!g)
+        return HS_OK;
+    DeviceGuard dg(g->device);
+    cudaGraphExecDestroy(g->exec);
+    cudaGraphDestroy(g->graph);
+    delete g;
     return HS_OK;
 }

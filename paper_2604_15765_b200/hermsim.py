@@ -342,6 +342,53 @@ def apply(h: TiledHermitian, spec: ChannelSpec, targets, opts: ApplyOptions | No
                      int(plan.touched_bytes))
 
 
+class Graph:
+    """A captured sequence of operations on one state (CUDA graph); `launch()` replays it on the
+    state's stream.  Build with `capture(state)`:
+
+        with hermsim.capture(rho) as g:
+            for spec, tg in circuit:
+                hermsim.apply(rho, spec, tg)
+        g.launch(); g.launch()
+    """
+
+    def __init__(self, state: TiledHermitian):
+        self.state = state
+        self._g = None
+
+    def __enter__(self):
+        nat.check(nat.engine().hs_graph_begin(self.state.handle), "graph begin")
+        return self
+
+    def __exit__(self, exc_type, exc, tb):
+        g = ctypes.c_void_p()
+        rc = nat.engine().hs_graph_end(self.state.handle, ctypes.byref(g))
+        if exc_type is None:
+            nat.check(rc, "graph end")
+            self._g = g
+        return False
+
+    def nodes(self) -> int:
+        out = ctypes.c_uint64()
+        nat.check(nat.engine().hs_graph_nodes(self._g, ctypes.byref(out)), "graph nodes")
+        return int(out.value)
+
+    def launch(self) -> None:
+        nat.check(nat.engine().hs_graph_launch(self._g, self.state.handle), "graph launch")
+
+    def __del__(self):
+        try:
+            if self._g is not None:
+                nat.engine().hs_graph_free(self._g)
+                self._g = None
+        except Exception:
+            pass
+
+
+def capture(state: TiledHermitian) -> Graph:
+    return Graph(state)
+
+
 def expectation(rho: TiledHermitian, obs: TiledHermitian) -> float:
     """tr(rho O) (strict ti > tj per SPEC.md); deterministic reduction."""
     out = ctypes.c_double()

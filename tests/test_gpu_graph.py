@@ -1,0 +1,44 @@
+"""CUDA-graph capture of an operation sequence (hermsim.capture / hs_graph_*): replaying the graph
+equals applying the sequence again, bit for bit; uncapturable operations fail loudly."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _seq(H, HS, n):
+    return [(H.depolarising(0.02), [0]), (H.amplitude_damping(0.1), [n - 1]), (H.native_gate("h"), [6]),
+            (H.native_gate("cnot"), [n - 1, 2]), (H.make_generic("u2", HS.haar(2, 1)), [7, n - 2]),
+            (H.make_generic("u3", HS.haar(3, 2)), [n - 1, 1, 6]), (H.native_gate("rz", 0.4), [3])]
+
+
+def test_graph_replay_bit_identical():
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    n = 10
+    psi = HS.rank_psi(n, 5, 4)
+    a, b = H.TiledHermitian(n), H.TiledHermitian(n)
+    a.fill_mixture(psi)
+    b.fill_mixture(psi)
+    opts = H.ApplyOptions(count_subcases=False)
+    seq = _seq(H, HS, n)
+    with H.capture(b) as g:  # capture records, does not run
+        for spec, tg in seq:
+            H.apply(b, spec, tg, opts)
+    assert g.nodes() >= len(seq)
+    assert np.array_equal(b.download().view(np.uint64), a.download().view(np.uint64))
+    for _ in range(3):
+        for spec, tg in seq:
+            H.apply(a, spec, tg, opts)
+        g.launch()
+    assert np.array_equal(b.download().view(np.uint64), a.download().view(np.uint64))
+
+
+def test_graph_refuses_uncapturable():
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    st = H.TiledHermitian(9)
+    k3 = H.make_generic("k3", np.stack([np.sqrt(0.5) * HS.haar(3, 3), np.sqrt(0.5) * HS.haar(3, 4)]))
+    with pytest.raises(Exception):
+        with H.capture(st):
+            H.apply(st, k3, [8, 2, 0])
