@@ -139,6 +139,7 @@ struct Tabs {
     uint16_t cdir[64], cadj[64];  // component offsets (copied from Geo: indexed per thread)
     uint8_t ttr[64];
     uint8_t tsk[64];
+    uint8_t slt[64];  // pipe kernel, monomials: staging slot -> logical tile (compacted active tiles)
 };
 
 template <int NS>
@@ -160,6 +161,10 @@ struct Coef {
     // k = 1 transfer matrix that couples only (00, 11) and (01, 10) (depolarising, amplitude
     // damping, dephasing, ...): w = S v reads only class-consistent components
     uint32_t xpat;
+    // monomial that is diagonal (phases only): element-wise scaling fast path; ibit = in-tile
+    // target bits (ascending), nib of them
+    uint32_t diag, nib;
+    uint8_t ibit[3];
     uint32_t ngroups;  // tile permutations: number of item groups
 };
 
@@ -1220,6 +1225,25 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                 asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NC) : "memory");  // consumer warps only
         }
     } else if constexpr (MODE == M_MONO) {
+        if (cf.diag && cf.nib == 0 && !G.groups && G.SR == G.M && !G.logical) {
+            // diagonal phases on grid qubits only: every element of a staged logical tile (R, C)
+            // gets the tile's factor f(R, C) (adjoint tiles, in stored orientation: conj f); the
+            // cycle walk below costs ~8x more instructions per element for this case
+            const uint32_t lMM = 2 * G.logM, D = 1u << K;
+            const uint32_t nel = nvalid_units * G.A << lMM;
+            for (uint32_t e = tid; e < nel; e += NC) {
+                const uint32_t st_ = e >> lMM, uu = st_ / G.A, sl = st_ - uu * G.A;
+                const uint32_t t = T.slt[sl], comp = (t >> G.logNG) * D + (t & ((1u << G.logNG) - 1));
+                if ((cf.fone >> comp) & 1ull)
+                    continue;
+                double2 f = cf.s[comp];
+                if ((am[uu] >> t) & 1ull)
+                    f.y = -f.y;
+                const uint32_t addr = (uu * G.A + sl) * G.TS + (e & ((1u << lMM) - 1));
+                sb[addr] = cmul(f, sb[addr]);
+            }
+            return;
+        }
         // in-place cycles of the component map; untouched components cost nothing
         const uint32_t cbeg = G.groups ? cf.gcyc_off[grp] : 0;
         const uint32_t nc = G.groups ? cf.gcyc_off[grp + 1] - cbeg : cf.ncyc;
@@ -1299,6 +1323,8 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
         T.cdir[tid] = G.cdir[tid];
         T.cadj[tid] = G.cadj[tid];
         T.ttr[tid] = G.ttr[tid];
+        if ((G.active >> tid) & 1ull)
+            T.slt[G.slot[tid]] = (uint8_t)tid;
     }
     if (tid == 0) {
         for (uint32_t s = 0; s < G.stages; ++s) {
@@ -3558,6 +3584,16 @@ int hs_apply_monomial(hs_state* h, int k, const uint32_t* perm, const double* di
         }
     }
     Coef<64> cf{};
+    {
+        bool ident = true;
+        for (uint32_t x = 0; x < D; ++x)
+            ident &= p[x] == x;
+        cf.diag = ident ? 1u : 0u;
+        cf.nib = 0;
+        for (int l = 0; l < k; ++l)  // ascending bound targets: in-tile ones first
+            if (t[l] < (uint32_t)h->m)
+                cf.ibit[cf.nib++] = (uint8_t)t[l];
+    }
     const double2* dg2 = reinterpret_cast<const double2*>(diag);
     // U = P Dg with P|x> = |p[x]>: (U B U^dag)(r, c) = d[pinv r] conj(d[pinv c]) B(pinv r, pinv c).
     // Factor exactly 1 when the two diagonal entries are identical (equal-bit elements stay
