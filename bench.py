@@ -577,28 +577,36 @@ def cpu_sample_n(cfg: str, n: int, m: int, reserved: int = 0) -> int:
 
 def pipelined_e2e(args, H, L, nat, st, host0, S, n, m, nops, world, fplan, ops, opts):
     """End to end through the public API with consecutive steps overlapped, as a serving loop
-    would run: two device states and two pinned host buffers; step k uploads its input into state
-    k % 2, applies the sequence and downloads the result, all on that state's stream, so step k's
-    upload runs while step k - 1 computes / downloads (PCIe is full duplex).  Every step still
-    moves S bytes host->device and S bytes device->host inside the timed region.  Returns None
-    when a second state or pinned buffer does not fit (the serial loop is used then)."""
-    try:
-        st2 = H.TiledHermitian(n, m, device=st.device)
-    except (MemoryError, Exception):
-        return None
-    hb2 = ctypes.c_void_p()
-    if L.hs_host_alloc(ctypes.c_uint64(S), ctypes.byref(hb2)) != 0:
-        st2.free()
-        return None
+    would run: up to three device states and pinned host buffers; step k uploads its input into
+    state k % B, applies the sequence and downloads the result, all on that state's stream, so
+    uploads, compute and downloads of neighbouring steps overlap (PCIe is full duplex: ~91 GB/s
+    both ways together on the box, tools/pcie_probe.cu).  Every step still moves S bytes
+    host->device and S bytes device->host inside the timed region.  Returns None when not even a
+    second state or pinned buffer fits (the serial loop is used then)."""
     cnt = st.element_count()
-    host1 = np.ctypeslib.as_array(ctypes.cast(hb2, ctypes.POINTER(ctypes.c_double)), shape=(2 * cnt,))
-    host1[:] = host0
-    states, bufs = [st, st2], [host0, host1]
+    states, bufs, pinned = [st], [host0], []
+    for _ in range(2):  # triple buffering when HBM and host memory allow
+        try:
+            sx = H.TiledHermitian(n, m, device=st.device)
+        except Exception:
+            break
+        hb = ctypes.c_void_p()
+        if L.hs_host_alloc(ctypes.c_uint64(S), ctypes.byref(hb)) != 0:
+            sx.free()
+            break
+        hx = np.ctypeslib.as_array(ctypes.cast(hb, ctypes.POINTER(ctypes.c_double)), shape=(2 * cnt,))
+        hx[:] = host0
+        states.append(sx)
+        bufs.append(hx)
+        pinned.append(hb)
+    B = len(states)
+    if B < 2:
+        return None
     if fplan is not None:
         from paper_2604_15765_b200 import fusion
 
     def one(k):
-        s, b = states[k % 2], bufs[k % 2]
+        s, b = states[k % B], bufs[k % B]
         nat.check(L.hs_state_upload_async(s.handle, b.ctypes.data_as(nat.c_double_p), cnt))
         if fplan is not None:
             fusion.execute(s, fplan, opts)
@@ -607,34 +615,37 @@ def pipelined_e2e(args, H, L, nat, st, host0, S, n, m, nops, world, fplan, ops, 
                 H.apply(s, spec, tg, opts)
         nat.check(L.hs_state_download_async(s.handle, b.ctypes.data_as(nat.c_double_p), cnt))
 
-    ev = [ctypes.c_void_p() for _ in range(3)]
+    ev = [ctypes.c_void_p() for _ in range(1 + B)]
     for e in ev:
         nat.check(L.hs_event_create(ctypes.byref(e)))
-    one(0)  # warm-up pair
-    one(1)
-    st.synchronize()
-    st2.synchronize()
-    K = max(2, args.e2e_steps)
-    L.hs_event_record(ev[0], st.handle)  # both streams are idle: every later copy / kernel starts after it
+    for k in range(B):  # warm-up round
+        one(k)
+    for s in states:
+        s.synchronize()
+    K = max(2 * B, args.e2e_steps)
+    L.hs_event_record(ev[0], st.handle)  # all streams are idle: every later copy / kernel starts after it
     for k in range(K):
         one(k)
-    L.hs_event_record(ev[1], st.handle)
-    L.hs_event_record(ev[2], st2.handle)
-    st.synchronize()
-    st2.synchronize()
-    a, b = ctypes.c_float(), ctypes.c_float()
-    nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(a)))
-    nat.check(L.hs_event_elapsed_ms(ev[0], ev[2], ctypes.byref(b)))
-    total = max(a.value, b.value)
+    for i, s in enumerate(states):
+        L.hs_event_record(ev[1 + i], s.handle)
+    for s in states:
+        s.synchronize()
+    total = 0.0
+    for i in range(B):
+        x = ctypes.c_float()
+        nat.check(L.hs_event_elapsed_ms(ev[0], ev[1 + i], ctypes.byref(x)))
+        total = max(total, x.value)
     for e in ev:
         L.hs_event_destroy(e)
-    st2.free()
-    L.hs_host_free(hb2)
+    for s in states[1:]:
+        s.free()
+    for hb in pinned:
+        L.hs_host_free(hb)
     ms = dist_max(total / K, world)
     return {"value": world * nops / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
-            "ms_per_step": ms, "steps": K, "pipelined": True,
-            "path": "hermsim.apply (or fusion.execute with --fuse) + hs_state_upload/download_async; two states, "
-                    "consecutive steps overlap (upload k || compute/download k-1)"}
+            "ms_per_step": ms, "steps": K, "pipelined": True, "states_in_flight": B,
+            "path": "hermsim.apply (or fusion.execute with --fuse) + hs_state_upload/download_async; consecutive "
+                    "steps on different states overlap (upload k+1 || compute k || download k-1)"}
 
 
 def cpu_baseline_from(host_view, cfg, n, m, S, psi=None, strings=None):
