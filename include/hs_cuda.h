@@ -166,6 +166,10 @@ int hs_frobenius(const hs_state* h, double* out);
 int hs_state_fill_mixture(hs_state* h, int rank, const double* psi);
 /* O = sum_s coef_s P_s for Pauli strings with X-mask x[s], Z-mask z[s] (Y sets both) and
  * ny[s] = #Y; bit-identical to hsg_pauli_payload (harness.c). */
+/* hermsim::random_hermitian(n, seed) and basis_projector(n, basis) (storage.cpp:195-239), generated
+ * on the device (counter-based RNG: elements equal the reference's to ~1e-16 relative). */
+int hs_state_fill_random_hermitian(hs_state* h, uint64_t seed);
+int hs_state_fill_basis_projector(hs_state* h, uint64_t basis);
 int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uint64_t* z, const int32_t* ny,
                             const double* coef);
 

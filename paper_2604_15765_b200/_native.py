@@ -127,6 +127,8 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_ipc_open", i, [vp, i, pp])
     _sig(L, "hs_ipc_close", i, [vp, i])
     _sig(L, "hs_peer_access", i, [i, i])
+    _sig(L, "hs_state_fill_random_hermitian", i, [vp, ctypes.c_uint64])
+    _sig(L, "hs_state_fill_basis_projector", i, [vp, ctypes.c_uint64])
     _sig(L, "hs_graph_begin", i, [vp])
     _sig(L, "hs_graph_end", i, [vp, pp])
     _sig(L, "hs_graph_launch", i, [vp, vp])

@@ -2049,6 +2049,50 @@ __global__ void fill_mixture_kernel(double2* st, uint64_t count, uint32_t logM, 
 }
 
 
+// The reference's seeded operators (storage.cpp:22-55,195-239) generated where they live: the
+// counter-based gaussian_entry (splitmix64 + Box-Muller) per element, H = (A + A^dagger) / 2.  The
+// integer stream is exact; CUDA's log / sqrt / sincos may differ from glibc's in the last ulp, so
+// elements agree with the reference to ~1e-16 relative (tests/test_gpu_parity.py).
+__device__ __forceinline__ uint64_t splitmix64_d(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ double2 gaussian_entry_d(uint64_t base, uint64_t counter) {
+    const uint64_t r1 = splitmix64_d(base + 2 * counter), r2 = splitmix64_d(base + 2 * counter + 1);
+    const double u1 = (double)((r1 >> 11) + 1) * 0x1.0p-53;
+    const double u2 = (double)(r2 >> 11) * 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    double sn, cs;
+    sincos(2.0 * 3.141592653589793238462643383279502884 * u2, &sn, &cs);
+    return make_double2(r * cs, r * sn);
+}
+// kind 0: random_hermitian(seed); kind 1: basis_projector(basis = seed)
+__global__ void fill_seeded_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, uint64_t seed, int kind,
+                                   SD sd) {
+    const uint32_t M = 1u << logM;
+    const uint64_t base = splitmix64_d(seed ^ 0xD6E8FEB86659FD93ull);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 v = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            if (kind == 0) {
+                const double2 a = gaussian_entry_d(base, i * N + j), b = gaussian_entry_d(base, j * N + i);
+                v = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+            } else if (i == seed && j == seed) {
+                v.x = 1.0;
+            }
+        }
+        st[e] = v;
+    }
+}
+
 // max_e |st[e] - rho_psi(e)| over the stored payload, rho_psi = (1/rank) sum |psi_i><psi_i| built
 // exactly as fill_mixture_kernel (verification of full-size states without a second copy)
 __global__ void dist_mixture_kernel(const double2* st, uint64_t count, uint32_t logM, uint64_t N, const double2* psi,
@@ -3801,6 +3845,32 @@ int hs_state_fill_mixture(hs_state* h, int rank, const double* psi) {
     cudaFree(dpsi);
     if (e != cudaSuccess)
         return set_err(HS_ERR_CUDA, cudaGetErrorString(e));
+    return HS_OK;
+}
+
+// hermsim::random_hermitian(n, seed, tiled, m) (storage.cpp:195-201) and basis_projector (:230-239)
+// generated on the device into this state (any shard).
+int hs_state_fill_random_hermitian(hs_state* h, uint64_t seed) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    DeviceGuard dg(h->device);
+    fill_seeded_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, seed, 0,
+                                                         SD{h->Plog, h->logB, h->shard});
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CUDA_TRY(cudaGetLastError());
+    return HS_OK;
+}
+
+int hs_state_fill_basis_projector(hs_state* h, uint64_t basis) {
+    if (!h)
+        return set_err(HS_ERR_INVALID, "null state");
+    if (basis >= h->N)
+        return set_err(HS_ERR_RANGE, "basis_projector: basis index out of range");
+    DeviceGuard dg(h->device);
+    fill_seeded_kernel<<<148 * 16, NTHR, 0, h->stream>>>(h->d, h->count, (uint32_t)h->m, h->N, basis, 1,
+                                                         SD{h->Plog, h->logB, h->shard});
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CUDA_TRY(cudaGetLastError());
     return HS_OK;
 }
 

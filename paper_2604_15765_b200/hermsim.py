@@ -157,6 +157,14 @@ class TiledHermitian:
                   "distance_to_mixture")
         return out.value
 
+    def fill_random_hermitian(self, seed: int) -> None:
+        """hermsim::random_hermitian(n, seed, tiled, m) (storage.cpp:195-201), generated on the device."""
+        nat.check(nat.engine().hs_state_fill_random_hermitian(self.handle, seed), "random_hermitian")
+
+    def fill_basis_projector(self, basis: int) -> None:
+        """hermsim::basis_projector(n, basis, tiled, m) (storage.cpp:230-239)."""
+        nat.check(nat.engine().hs_state_fill_basis_projector(self.handle, basis), "basis_projector")
+
     def save(self, path: str) -> None:
         """hermsim::save (storage_io.cpp:34-56): OHRM container, tiled format."""
         nat.check(nat.engine().hs_state_save(self.handle, os.fsencode(path)), "save")

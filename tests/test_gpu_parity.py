@@ -199,3 +199,20 @@ def test_golden_vectors_gpu(H):
         assert err <= (0.0 if exact else TOL), (i, name, rec["targets"], err)
         if len(rec["targets"]) <= 2:
             assert plan.path == rec["path"] and list(plan.subcases) == rec["subcases"], (i, name, plan)
+
+
+def test_device_random_hermitian_matches_reference(H, oracle):
+    """random_hermitian / basis_projector generated on the device against the compiled reference's
+    own generators (storage.cpp:195-239)."""
+    ref = oracle.Reference()
+    for n, m, seed in ((8, 5, 3), (9, 3, 11), (4, 5, 7), (7, 0, 2)):
+        h = ref.random_hermitian(n, seed, m)
+        want = ref.view(h).copy()
+        ref.free(h)
+        st = H.TiledHermitian(n, m)
+        st.fill_random_hermitian(seed)
+        got = st.download()
+        assert np.max(np.abs(got - want)) <= 1e-14 * np.max(np.abs(want)), (n, m)
+        st.fill_basis_projector(5)
+        p = st.download()
+        assert p.sum() == 1.0 and np.count_nonzero(p) == 1
