@@ -191,6 +191,13 @@ class IoError : public std::runtime_error {
 void save(const TiledHermitian& h, const std::string& path);
 TiledHermitian load(const std::string& path, int device = 0);
 
+// ------------------------------------------------------------ generators (storage.hpp:129-154)
+// hermsim::random_hermitian / basis_projector, tiled format, generated on the device
+TiledHermitian random_hermitian(int n, std::uint64_t seed, int tile_exp = TiledHermitian::default_tile_exp,
+                                int device = 0);
+TiledHermitian basis_projector(int n, std::uint64_t basis, int tile_exp = TiledHermitian::default_tile_exp,
+                               int device = 0);
+
 // ----------------------------------------------------------------- kernels (kernels.hpp)
 enum class KernelPath : std::uint8_t {
     dense_generic,

@@ -152,6 +152,18 @@ TiledHermitian TiledHermitian::adopt(hs_state* h) {
 
 void save(const TiledHermitian& h, const std::string& path) { check(hs_state_save(h.handle(), path.c_str()), "save"); }
 
+TiledHermitian random_hermitian(int n, std::uint64_t seed, int tile_exp, int device) {
+    TiledHermitian t(n, tile_exp, device);
+    check(hs_state_fill_random_hermitian(t.handle(), seed), "random_hermitian");
+    return t;
+}
+
+TiledHermitian basis_projector(int n, std::uint64_t basis, int tile_exp, int device) {
+    TiledHermitian t(n, tile_exp, device);
+    check(hs_state_fill_basis_projector(t.handle(), basis), "basis_projector");
+    return t;
+}
+
 TiledHermitian load(const std::string& path, int device) {
     hs_state* h = nullptr;
     check(hs_state_load(path.c_str(), device, &h), "load");

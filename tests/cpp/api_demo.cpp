@@ -72,6 +72,13 @@ int main() {
                 return 11;
         }
     }
+    // generators of the reference's storage API, on the device
+    TiledHermitian proj = basis_projector(n, 0);
+    if (std::fabs(trace(proj) - 1.0) > 0.0 || std::fabs(expectation(proj, zz) - 1.0) > 0.0)
+        return 12;
+    TiledHermitian rh = random_hermitian(n, 42);
+    if (!std::isfinite(trace(rh)))
+        return 13;
     std::printf("api_demo ok: <Z0 Z8> = %.15f\n", e);
     return 0;
 }
