@@ -42,3 +42,24 @@ def test_graph_refuses_uncapturable():
     with pytest.raises(Exception):
         with H.capture(st):
             H.apply(st, k3, [8, 2, 0])
+
+
+def test_graph_of_fused_sequence():
+    """A fused C2-style sequence (in-tile program + grid programs) captured and replayed equals the
+    fused sequence applied again."""
+    from paper_2604_15765_b200 import fusion
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    n = 10
+    psi = HS.rank_psi(n, 8, 4)
+    a, b = H.TiledHermitian(n), H.TiledHermitian(n)
+    a.fill_mixture(psi)
+    b.fill_mixture(psi)
+    ops = [(H.depolarising(0.01), [q]) for q in range(n)] + [(H.amplitude_damping(0.05), [q]) for q in range(n)]
+    plan = fusion.plan_sequence(ops, n, 5)
+    with H.capture(b) as g:
+        fusion.execute(b, plan)
+    for _ in range(2):
+        fusion.execute(a, plan)
+        g.launch()
+    assert np.array_equal(b.download().view(np.uint64), a.download().view(np.uint64))
