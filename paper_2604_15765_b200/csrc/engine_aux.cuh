@@ -1,0 +1,231 @@
+// engine_aux.cuh -- part of engine.cu (one translation unit; included in order).
+// Deterministic reductions (tr(rho O), trace, Frobenius) and device-side input generators.
+#pragma once
+
+namespace {
+// ------------------------------------------------------------------------- reductions
+// Per-CTA partial sums over a contiguous tile range, fixed order, then a single-CTA
+// ordered sum: deterministic for a given grid (SPEC.md observables: fixed-order reduction).
+constexpr int RED_BLOCKS = 1184;  // 8 x 148 SMs
+
+struct SD {  // shard descriptor of a state's local payload
+    uint32_t Plog, logB, shard;
+};
+
+__device__ double block_sum(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = NTHR / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// kind 0: Re<a, b>_F (expectation); kind 1: |a|^2 (frobenius); kind 2: trace (diagonal elements)
+__global__ void __launch_bounds__(NTHR) reduce_kernel(const double2* __restrict__ a, const double2* __restrict__ b,
+                                                      uint64_t ntiles, uint32_t logM, int kind, double* partials, SD sd) {
+    __shared__ double sh[NTHR];
+    const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+    const uint64_t t0 = blockIdx.x * per, t1 = min(ntiles, t0 + per);
+    const uint32_t MM = 1u << (2 * logM), M = 1u << logM;
+    double dsum = 0.0, osum = 0.0;
+    if (t0 < t1) {
+        for (uint64_t t = t0; t < t1; ++t) {
+            uint64_t ti, tj;
+            shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
+            const double2* pa = a + (t << (2 * logM));
+            const double2* pb = b + (t << (2 * logM));
+            double acc = 0.0;
+            if (kind == 2) {
+                if (ti == tj)
+                    for (uint32_t p = threadIdx.x; p < M; p += NTHR)
+                        acc += pa[p * M + p].x;
+            } else {
+                for (uint32_t p = threadIdx.x; p < MM; p += NTHR) {
+                    const double2 x = pa[p], y = pb[p];
+                    acc = fma(x.x, y.x, acc);
+                    acc = fma(x.y, y.y, acc);
+                }
+            }
+            if (ti == tj)
+                dsum += acc;
+            else
+                osum += acc;
+        }
+    }
+    dsum = block_sum(dsum, sh);
+    osum = block_sum(osum, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = dsum;
+        partials[2 * blockIdx.x + 1] = osum;
+    }
+}
+
+__global__ void finish_kernel(const double* partials, int nparts, int kind, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double d = 0.0, o = 0.0;
+        for (int i = 0; i < nparts; ++i) {
+            d += partials[2 * i];
+            o += partials[2 * i + 1];
+        }
+        out[0] = kind == 2 ? d : d + 2.0 * o;
+    }
+}
+
+// ------------------------------------------------------------------------- generators
+// rho(i, j) = (1/rank) sum_a psi_a[i] conj(psi_a[j]) with explicit rounding (no contraction),
+// bit-identical to hsg_rho_payload (harness.c).
+__global__ void fill_mixture_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, const double2* psi,
+                                    int rank, double inv, SD sd) {
+    const uint32_t M = 1u << logM;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 acc = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            for (int a = 0; a < rank; ++a) {
+                const double2 p = psi[(uint64_t)a * N + i], q = psi[(uint64_t)a * N + j];
+                const double re = __dadd_rn(__dmul_rn(p.x, q.x), __dmul_rn(p.y, q.y));
+                const double im = __dsub_rn(__dmul_rn(p.y, q.x), __dmul_rn(p.x, q.y));
+                acc.x = __dadd_rn(acc.x, re);
+                acc.y = __dadd_rn(acc.y, im);
+            }
+            acc.x = __dmul_rn(acc.x, inv);
+            acc.y = __dmul_rn(acc.y, inv);
+        }
+        st[e] = acc;
+    }
+}
+
+
+// The reference's seeded operators (storage.cpp:22-55,195-239) generated where they live: the
+// counter-based gaussian_entry (splitmix64 + Box-Muller) per element, H = (A + A^dagger) / 2.  The
+// integer stream is exact; CUDA's log / sqrt / sincos may differ from glibc's in the last ulp, so
+// elements agree with the reference to ~1e-16 relative (tests/test_gpu_parity.py).
+__device__ __forceinline__ uint64_t splitmix64_d(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ double2 gaussian_entry_d(uint64_t base, uint64_t counter) {
+    const uint64_t r1 = splitmix64_d(base + 2 * counter), r2 = splitmix64_d(base + 2 * counter + 1);
+    const double u1 = (double)((r1 >> 11) + 1) * 0x1.0p-53;
+    const double u2 = (double)(r2 >> 11) * 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    double sn, cs;
+    sincos(2.0 * 3.141592653589793238462643383279502884 * u2, &sn, &cs);
+    return make_double2(r * cs, r * sn);
+}
+// kind 0: random_hermitian(seed); kind 1: basis_projector(basis = seed)
+__global__ void fill_seeded_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, uint64_t seed, int kind,
+                                   SD sd) {
+    const uint32_t M = 1u << logM;
+    const uint64_t base = splitmix64_d(seed ^ 0xD6E8FEB86659FD93ull);
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 v = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            if (kind == 0) {
+                const double2 a = gaussian_entry_d(base, i * N + j), b = gaussian_entry_d(base, j * N + i);
+                v = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+            } else if (i == seed && j == seed) {
+                v.x = 1.0;
+            }
+        }
+        st[e] = v;
+    }
+}
+
+// max_e |st[e] - rho_psi(e)| over the stored payload, rho_psi = (1/rank) sum |psi_i><psi_i| built
+// exactly as fill_mixture_kernel (verification of full-size states without a second copy)
+__global__ void dist_mixture_kernel(const double2* st, uint64_t count, uint32_t logM, uint64_t N, const double2* psi,
+                                    int rank, double inv, double* out, SD sd) {
+    __shared__ double sh[NTHR];
+    const uint32_t M = 1u << logM;
+    double mx = 0.0;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 acc = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            for (int a = 0; a < rank; ++a) {
+                const double2 p = psi[(uint64_t)a * N + i], q = psi[(uint64_t)a * N + j];
+                acc.x = __dadd_rn(acc.x, __dadd_rn(__dmul_rn(p.x, q.x), __dmul_rn(p.y, q.y)));
+                acc.y = __dadd_rn(acc.y, __dsub_rn(__dmul_rn(p.y, q.x), __dmul_rn(p.x, q.y)));
+            }
+            acc.x = __dmul_rn(acc.x, inv);
+            acc.y = __dmul_rn(acc.y, inv);
+        }
+        const double2 v = st[e];
+        mx = fmax(mx, fmax(fabs(v.x - acc.x), fabs(v.y - acc.y)));
+    }
+    sh[threadIdx.x] = mx;
+    __syncthreads();
+    for (int s = NTHR / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+            sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        out[blockIdx.x] = sh[0];
+}
+
+struct PauliArgs {
+    const uint64_t* x;
+    const uint64_t* z;
+    const int32_t* ny;
+    const double* coef;
+    int count;
+};
+
+__global__ void fill_pauli_kernel(double2* st, uint64_t count, uint32_t logM, uint64_t N, PauliArgs pa, SD sd) {
+    const uint32_t M = 1u << logM;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < count;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = e >> (2 * logM);
+        const uint32_t r = (uint32_t)((e >> logM) & (M - 1)), c = (uint32_t)(e & (M - 1));
+        uint64_t ti, tj;
+        shard_decode(sd.Plog, sd.logB, sd.shard, t, ti, tj);
+        const uint64_t i = ti * M + r, j = tj * M + c;
+        double2 acc = make_double2(0.0, 0.0);
+        if (i < N && j < N) {
+            const uint64_t ij = i ^ j;
+            for (int s = 0; s < pa.count; ++s) {
+                if (pa.x[s] != ij)
+                    continue;
+                double v = pa.coef[s];
+                if (__popcll(j & pa.z[s]) & 1)
+                    v = -v;
+                const int ph = pa.ny[s] & 3;  // i^ny
+                if (ph == 0)
+                    acc.x = __dadd_rn(acc.x, v);
+                else if (ph == 1)
+                    acc.y = __dadd_rn(acc.y, v);
+                else if (ph == 2)
+                    acc.x = __dadd_rn(acc.x, -v);
+                else
+                    acc.y = __dadd_rn(acc.y, -v);
+            }
+        }
+        st[e] = acc;
+    }
+}
+}  // namespace

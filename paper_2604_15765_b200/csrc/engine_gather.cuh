@@ -1,0 +1,547 @@
+// engine_gather.cuh -- part of engine.cu (one translation unit; included in order).
+// Gather kernels for units that do not fit whole (g >= 2; k = 3 with g = 1): the ping-pong
+// cp.async gather and the warp-specialised gather with the FP64 tensor-core (DMMA) transforms
+// and grid programs.
+#pragma once
+
+namespace {
+// ------------------------------------------------------------- gather kernel (g >= 2: sub-blocks)
+// Units with >= 2 grid bits couple 16 or 64 stored tiles, too many for whole-tile staging.  An item
+// is then one S0 x S0 sub-block of positions (closed under the in-tile target bits) of every
+// logical tile of a unit (4096 elements, 64 KiB); rows of S0 elements are whole cache lines in
+// both orientations.  All 512 threads gather with cp.async (16 B each, adjoint tiles transposed on
+// the way in, padded pitch S0 + 1), 3-stage software pipeline (commit/wait groups), transform in
+// shared memory, and write back with coalesced st.global along stored rows.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// k = 3 direct form L B L^dagger on the FP64 tensor path (mma.sync m8n8k4 f64): one warp per 8x8
+// block, 16 DMMA per block (4 real products per complex product, two k = 4 chunks, two stages) in
+// place of 1024 DFMA.  The contraction index k of each chunk j is permuted to k = 2c + j (c = lane
+// & 3): the stage-1 accumulator fragment (row lane >> 2, columns 2c, 2c + 1) is then exactly the
+// stage-2 A fragment of chunks 0 and 1, so no data moves between lanes.  Lane (g = lane >> 2, c)
+// loads B[2c + j][g] and stores Z[g][2c + j].  (B200: DMMA and DFMA share the FP64 pipe at
+// ~37 TFLOP/s, tools/fp64_probe.cu; DMMA issues 8x fewer instructions.)
+// (not volatile: a pure function of its operands, so the compiler may interleave independent chains)
+__device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+// conjugation flag applied as a sign-bit flip on the integer pipe (a DADD negation would compete
+// with the DMMA for the FP64 pipe)
+__device__ __forceinline__ double flip_sign(double x, uint32_t m) {
+    return __hiloint2double(__double2hiint(x) ^ (int)m, __double2loint(x));
+}
+// per-lane constant fragments of the transform (loaded once per kernel: the lane-dependent
+// coefficient index would serialise the constant-cache reads if repeated per item)
+struct DmmaFrag {
+    double lr[2], li[2], nli[2];
+    double ls[2], ld[2];      // Lr + Li (stage 1, 3M) and Pr + Pi = Lr - Li (stage 2, 3M)
+    uint32_t old[2], ost[2];  // staging offsets of the loaded / stored components (from the block base)
+    uint32_t tld[2], tst[2];  // their logical tiles (adjoint mask bits)
+};
+// k = 3: the 8 x 8 block itself.  k = 2: four 4 x 4 blocks (2X + R1, 2Y + C1) as the quadrants of
+// one 8 x 8 matrix M, transformed by I2 (x) L: (I2 (x) L) M (I2 (x) L)^dagger applies L . L^dagger to
+// every quadrant, so one tensor-core transform serves four k = 2 blocks (kin = 0: quadrant
+// offsets are R1 * PD + C1, folded into the component offsets).
+template <int K, int NS>
+__device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const Coef<NS>& cf) {
+    DmmaFrag f;
+    const uint32_t lane = threadIdx.x & 31, gq = lane >> 2, cq = lane & 3;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const uint32_t c8 = 2 * cq + j;
+        double2 l;
+        if constexpr (K == 3)
+            l = cf.s[gq * 8 + c8];
+        else
+            l = (gq >> 2) == (c8 >> 2) ? cf.s[(gq & 3) * 4 + (c8 & 3)] : make_double2(0.0, 0.0);
+        f.lr[j] = l.x;
+        f.li[j] = l.y;
+        f.nli[j] = -l.y;
+        f.ls[j] = l.x + l.y;
+        f.ld[j] = l.x - l.y;
+        if constexpr (K == 3) {
+            const uint32_t il = c8 * 8 + gq, is = gq * 8 + c8;
+            f.old[j] = T.cdir[il];
+            f.ost[j] = T.cdir[is];
+            f.tld[j] = T.ttr[il];
+            f.tst[j] = T.ttr[is];
+        } else {
+            // load component (row c8, column gq), store component (row gq, column c8) of M
+            const uint32_t il = (c8 & 3) * 4 + (gq & 3), is = (gq & 3) * 4 + (c8 & 3);
+            f.old[j] = T.cdir[il] + (c8 >> 2) * G.PD + (gq >> 2);
+            f.ost[j] = T.cdir[is] + (gq >> 2) * G.PD + (c8 >> 2);
+            f.tld[j] = T.ttr[il];
+            f.tst[j] = T.ttr[is];
+        }
+    }
+    return f;
+}
+template <int NC, int K = 3>
+__device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
+                                             double2* sb, uint32_t warp) {
+    constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
+    const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
+    const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
+    const uint32_t logNy = G.logNyb - sh, nblk = (G.nxb >> sh) << logNy, ymask = (G.nyb >> sh) - 1;
+    // two blocks per pass: independent accumulator chains keep the FP64 tensor pipe fed (small
+    // tiles, m < 5, have fewer blocks than warps: the second block of a pass may be absent and is
+    // then computed on a copy of the first and not stored)
+    for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32)) {
+        uint32_t base[2];
+        double2 v0[2], v1[2];
+        const bool two = b + NC / 32 < nblk;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const uint32_t bq = (q && two) ? b + NC / 32 : b;
+            base[q] = T.xb[(bq >> logNy) << sh] * G.PD + T.yb[(bq & ymask) << sh];
+            v0[q] = sb[base[q] + f.old[0]];
+            v1[q] = sb[base[q] + f.old[1]];
+            v0[q].y = flip_sign(v0[q].y, cld0);
+            v1[q].y = flip_sign(v1[q].y, cld1);
+        }
+        // 3M form (Gauss): three real products per complex product.  Stage 1: Y = L B with
+        // T1 = Lr Br, T2 = Li Bi, T3 = (Lr + Li)(Br + Bi); Yr = T1 - T2, Yi = T3 - T1 - T2
+        double yr0[2], yr1[2], yi0[2], yi1[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            double t1a = 0.0, t1b = 0.0, t2a = 0.0, t2b = 0.0, t3a = 0.0, t3b = 0.0;
+            const double s0 = v0[q].x + v0[q].y, s1 = v1[q].x + v1[q].y;
+            dmma_acc(t1a, t1b, f.lr[0], v0[q].x);
+            dmma_acc(t2a, t2b, f.li[0], v0[q].y);
+            dmma_acc(t3a, t3b, f.ls[0], s0);
+            dmma_acc(t1a, t1b, f.lr[1], v1[q].x);
+            dmma_acc(t2a, t2b, f.li[1], v1[q].y);
+            dmma_acc(t3a, t3b, f.ls[1], s1);
+            yr0[q] = t1a - t2a;
+            yr1[q] = t1b - t2b;
+            yi0[q] = t3a - t1a - t2a;
+            yi1[q] = t3b - t1b - t2b;
+        }
+        // stage 2: Z = Y P, P = L^dagger (B fragment of chunk j: P[2c + j][g] = conj(L[g][2c + j]));
+        // U1 = Yr Pr, U2 = Yi Pi, U3 = (Yr + Yi)(Pr + Pi); Zr = U1 - U2, Zi = U3 - U1 - U2
+        double zr0[2], zr1[2], zi0[2], zi1[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
+            const double s0 = yr0[q] + yi0[q], s1 = yr1[q] + yi1[q];
+            dmma_acc(u1a, u1b, yr0[q], f.lr[0]);
+            dmma_acc(u2a, u2b, yi0[q], f.nli[0]);
+            dmma_acc(u3a, u3b, s0, f.ld[0]);
+            dmma_acc(u1a, u1b, yr1[q], f.lr[1]);
+            dmma_acc(u2a, u2b, yi1[q], f.nli[1]);
+            dmma_acc(u3a, u3b, s1, f.ld[1]);
+            zr0[q] = u1a - u2a;
+            zr1[q] = u1b - u2b;
+            zi0[q] = u3a - u1a - u2a;
+            zi1[q] = u3b - u1b - u2b;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (q && !two)
+                break;
+            sb[base[q] + f.ost[0]] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
+            sb[base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
+        }
+    }
+}
+
+__device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group
+template <int K, int MODE, int NS, int NC>
+__global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
+    constexpr uint32_t NH = NC / 2;  // threads per group
+    constexpr uint32_t S = 3;        // stages (plan_gather)
+    extern __shared__ __align__(128) double2 ring[];
+    __shared__ uint64_t gt[S][64];
+    __shared__ uint64_t am[S][1];
+    __shared__ __align__(8) uint64_t full[S];
+    __shared__ Tabs T;
+    const uint32_t tid = threadIdx.x, grp = tid / NH, gtid = tid % NH;
+    if (tid < 32) {
+        T.xdep[tid] = G.xdep[tid];
+        T.xb[tid] = G.xb_tab[tid];
+        T.yb[tid] = G.yb_tab[tid];
+        if (tid < 8) {
+            T.xs_in[tid] = G.xs_in[tid];
+            T.y_in[tid] = G.y_in[tid];
+        }
+    }
+    if (tid < 64) {
+        T.cdir[tid] = G.cdir[tid];
+        T.cadj[tid] = G.cadj[tid];
+        T.ttr[tid] = G.ttr[tid];
+        T.tsk[tid] = G.tsk[tid];
+    }
+    if (tid == 0)
+        for (uint32_t q = 0; q < S; ++q)
+            mbar_init(&full[q], 2 * NH);
+    const uint64_t nItems = G.nG_items;
+    const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint32_t NT = 1u << G.logNT, NGm = (1u << G.logNG) - 1;
+    const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
+    // NH is a multiple of S0^2: every element this thread moves sits at the same sub-block
+    // position (i, jj) in stored order, in tiles tt = gtid / S0^2 + k * NH / S0^2
+    // positions moved by this thread: npos = max(1, S0^2 / NH) sub-block positions
+    // r = (gtid mod S0^2) + q * NH, each in tiles tt = tt0 + k * ttstep
+    const uint32_t T2 = 1u << logT;
+    const uint32_t npos = T2 > NH ? T2 / NH : 1u;
+    const uint32_t tt0 = T2 > NH ? 0u : gtid >> logT, ttstep = T2 > NH ? 1u : NH >> logT;
+    const uint32_t nsbm = (1u << (2 * G.log_nsb_side)) - 1;
+    const uint32_t barid = 1 + grp;
+    auto gbar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NH) : "memory"); };
+
+    auto item_of = [&](uint64_t j) { return sweep_item(G, nItems, j); };
+    // global offsets (within a tile) of this thread's q-th sub-block position, direct / adjoint,
+    // and its logical staging slot (direct / adjoint placement)
+    auto offsets = [&](uint64_t item, uint32_t q, uint32_t& od, uint32_t& oa, uint32_t& sm_d, uint32_t& sm_a) {
+        const uint32_t r = (gtid & (T2 - 1)) + q * NH, i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
+        const uint32_t sb = (uint32_t)(item & nsbm);
+        const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
+        od = ((x0 | T.xdep[i0]) << G.logM) + (y0 | T.xdep[j0]);
+        oa = ((y0 | T.xdep[i0]) << G.logM) + (x0 | T.xdep[j0]);
+        sm_d = i0 * P + j0;
+        sm_a = j0 * P + i0;
+    };
+    // this group loads item j into stage j % S (tile table, adjoint mask, copies, arrivals)
+    auto load = [&](uint64_t j) {
+        const uint32_t s = (uint32_t)(j % S);
+        const uint64_t u = item_of(j) >> (2 * G.log_nsb_side);
+        if (gtid < NT) {
+            uint64_t tbi, tbj;
+            unit_decode(G, u, true, tbi, tbj);
+            const uint64_t tr = ins_bits(tbi, gtid >> G.logNG, G.gr_pos, G.g);
+            const uint64_t tc = ins_bits(tbj, gtid & NGm, G.gr_pos, G.g);
+            uint64_t ent = tile_entry(G, tr, tc);
+            if (MODE == M_MONO && !((G.active >> gtid) & 1ull))
+                ent |= F_SKIP;
+            gt[s][gtid] = ent;
+        }
+        gbar();
+        if (gtid < 32) {
+            unsigned long long m = 0;
+            for (uint32_t t = gtid; t < NT; t += 32)
+                m |= (unsigned long long)((gt[s][t] & F_ADJ) != 0) << t;
+            for (int o = 16; o; o >>= 1)
+                m |= __shfl_xor_sync(0xffffffffu, m, o);
+            if (gtid == 0)
+                am[s][0] = m;
+        }
+        const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
+        for (uint32_t q = 0; q < npos; ++q) {
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(j), q, od, oa, sm_d, sm_a);
+            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 2u); tt += ttstep) {
+                const uint64_t ent = gt[s][tt];
+                if (ent & F_SKIP)
+                    continue;
+                const bool adj = (ent & F_ADJ) != 0;
+                const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
+                cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u,
+                           tile_base(G, ent, st) + g);
+            }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        mbar_arrive(&full[s]);
+    };
+    __syncthreads();
+    DmmaFrag fr;
+    if constexpr (K == 3 && MODE == M_DIRECT)
+        fr = dmma_frag<3>(G, T, cf);
+    for (uint64_t j = 0; j < S && j < nlocal; ++j)  // item j is loaded by group (j + 1) & 1
+        if (((j + 1) & 1) == grp)
+            load(j);
+    const bool prof = (G.dbg & 16u) && gtid == 0;  // phase timing (diagnostics): wait / transform / write-back / load
+    long long ph[4] = {0, 0, 0, 0};
+    for (uint64_t i = grp; i < nlocal; i += 2) {
+        const uint32_t s = (uint32_t)(i % S);
+        long long t0 = prof ? clock64() : 0;
+        mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+        long long t1 = prof ? clock64() : 0;
+        double2* sb = ring + (size_t)s * G.stage_elems;
+        if (!(G.dbg & 1u)) {
+            if constexpr (K == 3 && MODE == M_DIRECT)
+                dmma_direct3<NH>(G, T, fr, am[s][0], sb, gtid >> 5);
+            else
+                pipe_compute<K, MODE, NS, NH>(G, T, cf, am[s], 1, sb, 0, (int)gtid, barid);
+        }
+        gbar();
+        long long t2 = prof ? clock64() : 0;
+        // write back along stored rows (adjoint components are already in stored, conjugated form)
+        for (uint32_t q = 0; q < npos; ++q) {
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(i), q, od, oa, sm_d, sm_a);
+            for (uint32_t tt = tt0; tt < NT && !(G.dbg & 4u); tt += ttstep) {
+                const uint64_t ent = gt[s][tt];
+                if (ent & (F_SKIP | F_NOSTORE))
+                    continue;
+                const bool adj = (ent & F_ADJ) != 0;
+                G.out[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+            }
+        }
+        gbar();
+        long long t3 = prof ? clock64() : 0;
+        if (i + S < nlocal)
+            load(i + S);
+        if (prof) {
+            const long long t4 = clock64();
+            ph[0] += t1 - t0;
+            ph[1] += t2 - t1;
+            ph[2] += t3 - t2;
+            ph[3] += t4 - t3;
+        }
+    }
+    if (prof)
+        for (int q = 0; q < 4; ++q)
+            atomicAdd(&g_phase_cycles[grp * 4 + q], (unsigned long long)ph[q]);
+    cp_async_wait<0>();
+}
+
+// Warp-specialised gather for the k = 3 tensor-core transform: 8 transform warps and 16 copy warps
+// (768 threads).  The copy warps write back item i as soon as the transform warps release its stage
+// (`done`), then load item i + 3 into it (`full`, cp.async tracked by the mbarrier); the transform
+// warps only wait for data and run DMMA.  The 16 copy warps keep twice the memory-instruction
+// parallelism of a ping-pong group, and the transform never waits for its own write-back or loads.
+// (Register-staged loads in place of cp.async were 1.6x slower here.)
+// One k = 1 step of a grid program on the staged logical tiles (MODE == M_PROG in gather_ws_kernel):
+// quads of logical tiles (R, C), (R, C | e), (R | e, C), (R | e, C | e) at every staged position,
+// e = 2^l for the step's grid bit l; adjoint tiles are staged transposed and conjugated on the fly.
+template <uint32_t NCW, int NS>
+__device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, const Coef<NS>& cf, uint32_t p,
+                                               uint64_t am, double2* sb, uint32_t tid) {
+    const uint32_t g = G.g, NG = 1u << g, e = 1u << cf.pbit[p], lo = e - 1;
+    const uint32_t S0 = G.S0, P = S0 + 1, npos = S0 * S0, lp = 2 * G.logS0;
+    const uint32_t nq = (NG / 2) * (NG / 2) * npos;
+    const double2* S = cf.s + 16 * p;
+    const uint32_t kind = cf.pkind[p];
+    for (uint32_t q = tid; q < nq; q += NCW) {
+        const uint32_t tq = q >> lp, pos = q & (npos - 1), i = pos >> G.logS0, j = pos & (S0 - 1);
+        const uint32_t rr = tq >> (g - 1), cc = tq & ((NG >> 1) - 1);
+        const uint32_t R0 = ((rr & ~lo) << 1) | (rr & lo), C0 = ((cc & ~lo) << 1) | (cc & lo);
+        const uint32_t t0 = R0 * NG + C0, t1 = R0 * NG + (C0 | e), t2 = (R0 | e) * NG + C0, t3 = t2 + e;
+        const uint32_t off = i * P + j;
+        const uint32_t a0 = t0 * G.TS + T.tsk[t0] + off, a1 = t1 * G.TS + T.tsk[t1] + off;
+        const uint32_t a2 = t2 * G.TS + T.tsk[t2] + off, a3 = t3 * G.TS + T.tsk[t3] + off;
+        const uint32_t f0 = (uint32_t)((am >> t0) & 1ull) << 31, f1 = (uint32_t)((am >> t1) & 1ull) << 31;
+        const uint32_t f2 = (uint32_t)((am >> t2) & 1ull) << 31, f3 = (uint32_t)((am >> t3) & 1ull) << 31;
+        double2 v0 = sb[a0], v1 = sb[a1], v2 = sb[a2], v3 = sb[a3];
+        v0.y = flip_sign(v0.y, f0);
+        v1.y = flip_sign(v1.y, f1);
+        v2.y = flip_sign(v2.y, f2);
+        v3.y = flip_sign(v3.y, f3);
+        prog_quad(kind, S, v0, v1, v2, v3);
+        v0.y = flip_sign(v0.y, f0);
+        v1.y = flip_sign(v1.y, f1);
+        v2.y = flip_sign(v2.y, f2);
+        v3.y = flip_sign(v3.y, f3);
+        sb[a0] = v0;
+        sb[a1] = v1;
+        sb[a2] = v2;
+        sb[a3] = v3;
+    }
+}
+
+template <int K, int NS, int MODE = M_DIRECT>
+__global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
+    constexpr uint32_t NCW = 256, NMW = 512, S = 3;
+    extern __shared__ __align__(128) double2 ring[];
+    __shared__ uint64_t gt[S + 1][64];  // tile tables by item % (S + 1): built one item ahead
+    __shared__ uint64_t am[S + 1][1];
+    __shared__ __align__(8) uint64_t full[S], done[S];
+    __shared__ Tabs T;
+    const uint32_t tid = threadIdx.x;
+    if (tid < 32) {
+        T.xdep[tid] = G.xdep[tid];
+        T.xb[tid] = G.xb_tab[tid];
+        T.yb[tid] = G.yb_tab[tid];
+        if (tid < 8) {
+            T.xs_in[tid] = G.xs_in[tid];
+            T.y_in[tid] = G.y_in[tid];
+        }
+    }
+    if (tid < 64) {
+        T.cdir[tid] = G.cdir[tid];
+        T.cadj[tid] = G.cadj[tid];
+        T.ttr[tid] = G.ttr[tid];
+        T.tsk[tid] = G.tsk[tid];
+    }
+    if (tid == 0)
+        for (uint32_t q = 0; q < S; ++q) {
+            mbar_init(&full[q], 2 * NMW);
+            mbar_init(&done[q], NCW);
+        }
+    const uint64_t nItems = G.nG_items;
+    const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    auto item_of = [&](uint64_t j) { return sweep_item(G, nItems, j); };
+    __syncthreads();
+    if (tid < NCW) {
+        // ---- transform warps
+        DmmaFrag fr;
+        if constexpr (MODE == M_DIRECT)
+            fr = dmma_frag<K>(G, T, cf);
+        for (uint64_t i = 0; i < nlocal; ++i) {
+            const uint32_t s = (uint32_t)(i % S);
+            mbar_wait(&full[s], (uint32_t)((i / S) & 1));
+            double2* sb = ring + (size_t)s * G.stage_elems;
+            if constexpr (MODE == M_DIRECT) {
+                if (!(G.dbg & 1u))
+                    dmma_direct3<NCW, K>(G, T, fr, am[i % (S + 1)][0], sb, tid >> 5);
+            } else {
+                for (uint32_t p = 0; p < cf.nsteps; ++p) {
+                    grid_prog_step<NCW>(G, T, cf, p, am[i % (S + 1)][0], sb, tid);
+                    asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+                }
+            }
+            mbar_arrive(&done[s]);
+        }
+        return;
+    }
+    // ---- copy warps
+    const uint32_t mtid = tid - NCW;
+    const uint32_t NT = 1u << G.logNT, NGm = (1u << G.logNG) - 1;
+    const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
+    const uint32_t T2 = 1u << logT;
+    const uint32_t npos = T2 > NMW ? T2 / NMW : 1u;
+    const uint32_t tt0 = T2 > NMW ? 0u : mtid >> logT, ttstep = T2 > NMW ? 1u : NMW >> logT;
+    const uint32_t nsbm = (1u << (2 * G.log_nsb_side)) - 1;
+    const bool fast = npos == 1 && (NT << logT) == 8 * NMW;  // every thread moves 8 tiles at one position
+    const bool fast2 = npos == 2 && NT == 4;                  // or 4 tiles at two positions (whole-tile units)
+    auto mbar_sync = [&]() { asm volatile("bar.sync 1, %0;" ::"n"(NMW) : "memory"); };
+    auto offsets = [&](uint64_t item, uint32_t q, uint32_t& od, uint32_t& oa, uint32_t& sm_d, uint32_t& sm_a) {
+        const uint32_t r = (mtid & (T2 - 1)) + q * NMW, i0 = r >> G.logS0, j0 = r & (G.S0 - 1);
+        const uint32_t sb = (uint32_t)(item & nsbm);
+        const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
+        od = ((x0 | T.xdep[i0]) << G.logM) + (y0 | T.xdep[j0]);
+        oa = ((y0 | T.xdep[i0]) << G.logM) + (x0 | T.xdep[j0]);
+        sm_d = i0 * P + j0;
+        sm_a = j0 * P + i0;
+    };
+    // tile table and adjoint mask of item j, by the first two copy warps (one logical tile per
+    // lane) into slot j % (S + 1), which no stage in flight uses
+    auto tables = [&](uint64_t j) {  // copy warps 0 and 1: one logical tile per lane (NT <= 64)
+        const uint32_t ts = (uint32_t)(j % (S + 1));
+        uint64_t tbi, tbj;
+        unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), !G.ws_diag, tbi, tbj);
+        const uint32_t t = mtid;
+        bool adj = false;
+        if (t < NT) {
+            const uint64_t tr = ins_bits(tbi, t >> G.logNG, G.gr_pos, G.g);
+            const uint64_t tc = ins_bits(tbj, t & NGm, G.gr_pos, G.g);
+            uint64_t ent = tile_entry(G, tr, tc);
+            if (tbi == tbj && (t >> G.logNG) < (t & NGm))
+                ent |= F_NOSTORE;  // aliases stored (C, R) of the same diagonal unit: read-only copy
+            gt[ts][t] = ent;
+            adj = (ent & F_ADJ) != 0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, adj);
+        if ((mtid & 31) == 0)
+            reinterpret_cast<uint32_t*>(&am[ts][0])[mtid >> 5] = bal;  // little endian: tiles 0-31, 32-63
+    };
+    // cp.async of item j into stage j % S (its table is visible: a copy-warp barrier separates them)
+    auto issue = [&](uint64_t j) {
+        const uint32_t s = (uint32_t)(j % S), ts = (uint32_t)(j % (S + 1));
+        const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
+        auto one = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
+            const uint64_t ent = gt[ts][tt];
+            const bool adj = (ent & F_ADJ) != 0;
+            const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
+            cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, tile_base(G, ent, st) + g);
+        };
+        if (G.dbg & 2u) {
+        } else if (fast) {  // 8 tiles at one position: unrolled, table reads hoisted
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(j), 0, od, oa, sm_d, sm_a);
+#pragma unroll
+            for (uint32_t e = 0; e < 8; ++e)
+                one(tt0 + e * ttstep, od, oa, sm_d, sm_a);
+        } else if (fast2) {
+#pragma unroll
+            for (uint32_t q = 0; q < 2; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(j), q, od, oa, sm_d, sm_a);
+#pragma unroll
+                for (uint32_t tt = 0; tt < 4; ++tt)
+                    one(tt, od, oa, sm_d, sm_a);
+            }
+        } else {
+            for (uint32_t q = 0; q < npos; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(j), q, od, oa, sm_d, sm_a);
+                for (uint32_t tt = tt0; tt < NT; tt += ttstep)
+                    one(tt, od, oa, sm_d, sm_a);
+            }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        mbar_arrive(&full[s]);
+    };
+    const bool prof = (G.dbg & 16u) && mtid == 0;
+    long long ph[4] = {0, 0, 0, 0};
+    if (mtid < 64)
+        for (uint64_t j = 0; j < S && j < nlocal; ++j)
+            tables(j);
+    mbar_sync();
+    for (uint64_t j = 0; j < S && j < nlocal; ++j)
+        issue(j);
+    for (uint64_t i = 0; i < nlocal; ++i) {
+        const uint32_t s = (uint32_t)(i % S), ts = (uint32_t)(i % (S + 1));
+        const long long t0 = prof ? clock64() : 0;
+        mbar_wait(&done[s], (uint32_t)((i / S) & 1));
+        const long long t1 = prof ? clock64() : 0;
+        const bool more = i + S < nlocal;
+        if (more && mtid < 64)
+            tables(i + S);
+        const double2* sb = ring + (size_t)s * G.stage_elems;
+        auto wb = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
+            const uint64_t ent = gt[ts][tt];
+            if (ent & F_NOSTORE)
+                return;
+            const bool adj = (ent & F_ADJ) != 0;
+            G.out[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+        };
+        if (G.dbg & 4u) {
+        } else if (fast) {
+            uint32_t od, oa, sm_d, sm_a;
+            offsets(item_of(i), 0, od, oa, sm_d, sm_a);
+#pragma unroll
+            for (uint32_t e = 0; e < 8; ++e)
+                wb(tt0 + e * ttstep, od, oa, sm_d, sm_a);
+        } else if (fast2) {
+#pragma unroll
+            for (uint32_t q = 0; q < 2; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(i), q, od, oa, sm_d, sm_a);
+#pragma unroll
+                for (uint32_t tt = 0; tt < 4; ++tt)
+                    wb(tt, od, oa, sm_d, sm_a);
+            }
+        } else {
+            for (uint32_t q = 0; q < npos; ++q) {
+                uint32_t od, oa, sm_d, sm_a;
+                offsets(item_of(i), q, od, oa, sm_d, sm_a);
+                for (uint32_t tt = tt0; tt < NT; tt += ttstep)
+                    wb(tt, od, oa, sm_d, sm_a);
+            }
+        }
+        mbar_sync();  // every write-back read of stage s is done; the next table is visible
+        const long long t2 = prof ? clock64() : 0;
+        if (more)
+            issue(i + S);
+        if (prof) {
+            const long long t3 = clock64();
+            ph[0] += t1 - t0;
+            ph[2] += t2 - t1;
+            ph[3] += t3 - t2;
+        }
+    }
+    if (prof)
+        for (int q = 0; q < 4; ++q)
+            atomicAdd(&g_phase_cycles[q], (unsigned long long)ph[q]);
+    cp_async_wait<0>();
+}
+
+}  // namespace
