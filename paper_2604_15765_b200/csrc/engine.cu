@@ -660,7 +660,17 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             // tensor-core transform in the warp-specialised kernel (bit 5: the ping-pong kernel instead);
             // k = 2 pairs blocks two by two in each direction
             if constexpr (K == 3 ? dmma : (K == 2 && MODE == M_DIRECT)) {
-                if (!(Gg.dbg & 32u) && (K == 3 || (Gg.nxb >= 2 && Gg.nyb >= 2 && Gg.kin == 0))) {
+                // k = 2: quadrant blocks (2X + R1, 2Y + C1) sit at a constant offset qstride (the lowest
+                // non-target in-tile bit) in each direction
+                bool quad_ok = K == 3;
+                if (K == 2 && Gg.nxb >= 2 && Gg.nyb >= 2 && Gg.kin <= 1) {
+                    const uint32_t d = Gg.xb_tab[1] - Gg.xb_tab[0];
+                    quad_ok = d == Gg.yb_tab[1] - Gg.yb_tab[0];
+                    for (uint32_t x = 0; quad_ok && 2 * x + 1 < Gg.nxb; ++x)
+                        quad_ok = Gg.xb_tab[2 * x + 1] - Gg.xb_tab[2 * x] == d && Gg.yb_tab[2 * x + 1] - Gg.yb_tab[2 * x] == d;
+                    Gg.qstride = d;
+                }
+                if (!(Gg.dbg & 32u) && quad_ok) {
                     auto kw = gather_ws_kernel<K, NS>;
                     e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
                     if (e != cudaSuccess)

@@ -47,8 +47,8 @@ struct DmmaFrag {
 };
 // k = 3: the 8 x 8 block itself.  k = 2: four 4 x 4 blocks (2X + R1, 2Y + C1) as the quadrants of
 // one 8 x 8 matrix M, transformed by I2 (x) L: (I2 (x) L) M (I2 (x) L)^dagger applies L . L^dagger to
-// every quadrant, so one tensor-core transform serves four k = 2 blocks (kin = 0: quadrant
-// offsets are R1 * PD + C1, folded into the component offsets).
+// every quadrant, so one tensor-core transform serves four k = 2 blocks (quadrant offsets
+// (R1 * PD + C1) * qstride, folded into the component offsets).
 template <int K, int NS>
 __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const Coef<NS>& cf) {
     DmmaFrag f;
@@ -75,8 +75,8 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
         } else {
             // load component (row c8, column gq), store component (row gq, column c8) of M
             const uint32_t il = (c8 & 3) * 4 + (gq & 3), is = (gq & 3) * 4 + (c8 & 3);
-            f.old[j] = T.cdir[il] + (c8 >> 2) * G.PD + (gq >> 2);
-            f.ost[j] = T.cdir[is] + (gq >> 2) * G.PD + (c8 >> 2);
+            f.old[j] = T.cdir[il] + ((c8 >> 2) * G.PD + (gq >> 2)) * G.qstride;
+            f.ost[j] = T.cdir[is] + ((gq >> 2) * G.PD + (c8 >> 2)) * G.qstride;
             f.tld[j] = T.ttr[il];
             f.tst[j] = T.ttr[is];
         }
