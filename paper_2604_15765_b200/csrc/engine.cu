@@ -615,7 +615,49 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
         // are whole gather items for the FP64 tensor transform): sub-block gather kernel for the
         // off-diagonal units, the slab kernel's wedge path for the diagonal ones
         cudaError_t e;
-        if (G.nD_items && MODE != M_PROG) {  // grid programs: diagonal units inside the gather
+        Geo Gg = G;
+        constexpr bool dmma = K == 3 && MODE == M_DIRECT;
+        plan_gather(Gg, dmma);
+        {
+            static const char* dbg = getenv("HS_DEBUG_FLAGS");
+            Gg.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
+        }
+        // the warp-specialised kernel runs grid programs and the tensor-core transforms (bit 5: the
+        // ping-pong kernel instead); k = 2 pairs blocks two by two in each direction, the quadrant
+        // blocks (2X + R1, 2Y + C1) sitting at a constant offset qstride
+        bool ws = MODE == M_PROG;
+        if constexpr (K == 3 ? dmma : (K == 2 && MODE == M_DIRECT)) {
+            bool quad_ok = K == 3;
+            if (K == 2 && Gg.nxb >= 2 && Gg.nyb >= 2 && Gg.kin <= 1) {
+                const uint32_t d = Gg.xb_tab[1] - Gg.xb_tab[0];
+                quad_ok = d == Gg.yb_tab[1] - Gg.yb_tab[0];
+                for (uint32_t x = 0; quad_ok && 2 * x + 1 < Gg.nxb; ++x)
+                    quad_ok = Gg.xb_tab[2 * x + 1] - Gg.xb_tab[2 * x] == d && Gg.yb_tab[2 * x + 1] - Gg.yb_tab[2 * x] == d;
+                Gg.qstride = d;
+            }
+            ws = !(Gg.dbg & 32u) && quad_ok;
+        }
+        if (ws) {
+            // every unit including the diagonal ones: logical (R, C), R < C, of a diagonal unit is a
+            // read-only staged copy of stored (C, R), never written back (no separate wedge launch)
+            Gg.ws_diag = 1;
+            Gg.nG_items = Gg.nU_loose << (2 * Gg.log_nsb_side);
+            const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
+            auto kw = gather_ws_kernel<K, NS, MODE == M_PROG ? M_PROG : M_DIRECT>;
+            e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess)
+                return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
+            const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
+            if (grid) {
+                kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d);
+                g_launches.fetch_add(1, std::memory_order_relaxed);
+                e = cudaGetLastError();
+                if (e != cudaSuccess)
+                    return set_err(HS_ERR_CUDA, std::string("gather_ws_kernel launch: ") + cudaGetErrorString(e));
+            }
+            return HS_OK;
+        }
+        if (G.nD_items) {  // diagonal units: the slab kernel's wedge path
             Geo Gs = G;
             Gs.nU_items = 0;
             Gs.Epad = 0;
@@ -630,60 +672,8 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             if (e != cudaSuccess)
                 return set_err(HS_ERR_CUDA, std::string("conj_kernel launch: ") + cudaGetErrorString(e));
         }
-        Geo Gg = G;
-        constexpr bool dmma = K == 3 && MODE == M_DIRECT;
-        plan_gather(Gg, dmma);
-        {
-            static const char* dbg = getenv("HS_DEBUG_FLAGS");
-            Gg.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
-        }
-        if constexpr (MODE == M_PROG) {
-            // grid program: every unit including the diagonal ones (logical (R, C), R < C, of a
-            // diagonal unit is a read-only staged copy of stored (C, R), never written back)
-            Gg.ws_diag = 1;
-            Gg.nG_items = Gg.nU_loose << (2 * Gg.log_nsb_side);
-            const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
-            auto kw = gather_ws_kernel<K, NS, M_PROG>;
-            e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess)
-                return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
-            const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
-            kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d);
-            g_launches.fetch_add(1, std::memory_order_relaxed);
-            e = cudaGetLastError();
-            if (e != cudaSuccess)
-                return set_err(HS_ERR_CUDA, std::string("gather_ws_kernel launch: ") + cudaGetErrorString(e));
-            return HS_OK;
-        }
         if (Gg.nG_items) {
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
-            // tensor-core transform in the warp-specialised kernel (bit 5: the ping-pong kernel instead);
-            // k = 2 pairs blocks two by two in each direction
-            if constexpr (K == 3 ? dmma : (K == 2 && MODE == M_DIRECT)) {
-                // k = 2: quadrant blocks (2X + R1, 2Y + C1) sit at a constant offset qstride (the lowest
-                // non-target in-tile bit) in each direction
-                bool quad_ok = K == 3;
-                if (K == 2 && Gg.nxb >= 2 && Gg.nyb >= 2 && Gg.kin <= 1) {
-                    const uint32_t d = Gg.xb_tab[1] - Gg.xb_tab[0];
-                    quad_ok = d == Gg.yb_tab[1] - Gg.yb_tab[0];
-                    for (uint32_t x = 0; quad_ok && 2 * x + 1 < Gg.nxb; ++x)
-                        quad_ok = Gg.xb_tab[2 * x + 1] - Gg.xb_tab[2 * x] == d && Gg.yb_tab[2 * x + 1] - Gg.yb_tab[2 * x] == d;
-                    Gg.qstride = d;
-                }
-                if (!(Gg.dbg & 32u) && quad_ok) {
-                    auto kw = gather_ws_kernel<K, NS>;
-                    e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-                    if (e != cudaSuccess)
-                        return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
-                    const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
-                    kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d);
-                    g_launches.fetch_add(1, std::memory_order_relaxed);
-                    e = cudaGetLastError();
-                    if (e != cudaSuccess)
-                        return set_err(HS_ERR_CUDA, std::string("gather_ws_kernel launch: ") + cudaGetErrorString(e));
-                    return HS_OK;
-                }
-            }
             constexpr int NC = 512;  // two groups of 256 (a multiple of the S0^2 positions of an item)
             auto kern = gather_kernel<K, MODE, NS, NC>;
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

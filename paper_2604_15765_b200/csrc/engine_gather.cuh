@@ -433,8 +433,21 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint64_t tr = ins_bits(tbi, t >> G.logNG, G.gr_pos, G.g);
             const uint64_t tc = ins_bits(tbj, t & NGm, G.gr_pos, G.g);
             uint64_t ent = tile_entry(G, tr, tc);
-            if (tbi == tbj && (t >> G.logNG) < (t & NGm))
-                ent |= F_NOSTORE;  // aliases stored (C, R) of the same diagonal unit: read-only copy
+            if (tbi == tbj) {
+                // Diagonal unit: logical (R, C), R < C, aliases stored (C, R) of the same unit, so
+                // sub-block items (a, b) and (b, a) read what the other writes.  Only a >= b runs:
+                // a == b stores R >= C (the block is its own mirror); a > b stores every tile, R < C
+                // through the adjoint write-back and R == C also at the mirrored position.
+                const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
+                const uint32_t a = sb >> G.log_nsb_side, b = sb & ((1u << G.log_nsb_side) - 1);
+                const uint32_t R = t >> G.logNG, C = t & NGm;
+                if (a < b)
+                    ent |= F_SKIP | F_NOSTORE;
+                else if (a == b && R < C)
+                    ent |= F_NOSTORE;
+                else if (a > b && R == C && !(ent & F_NOSTORE))
+                    ent |= F_MIRROR;
+            }
             gt[ts][t] = ent;
             adj = (ent & F_ADJ) != 0;
         }
@@ -448,6 +461,8 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
         auto one = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
             const uint64_t ent = gt[ts][tt];
+            if (ent & F_SKIP)
+                return;
             const bool adj = (ent & F_ADJ) != 0;
             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
             cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, tile_base(G, ent, st) + g);
@@ -501,7 +516,13 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             if (ent & F_NOSTORE)
                 return;
             const bool adj = (ent & F_ADJ) != 0;
-            G.out[((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od)] = sb[tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)];
+            double2* o = G.out + ((ent & F_MASK) << (2 * G.logM));
+            const double2* v = sb + tt * G.TS + T.tsk[tt];
+            o[adj ? oa : od] = v[adj ? sm_a : sm_d];
+            if (ent & F_MIRROR) {
+                const double2 w = v[sm_a];
+                o[oa] = make_double2(w.x, -w.y);
+            }
         };
         if (G.dbg & 4u) {
         } else if (fast) {

@@ -11,7 +11,7 @@ constexpr uint32_t CAPD = 2048;    // same for diagonal-unit items
 constexpr uint32_t CAP_WHOLE = 4096;  // units up to 64 KiB are staged as whole stored tiles
 constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in smem)
 constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_NOSTORE = 1ull << 60,
-                   F_REMOTE = 1ull << 59, F_MASK = (1ull << 56) - 1;
+                   F_REMOTE = 1ull << 59, F_MIRROR = 1ull << 55, F_MASK = (1ull << 55) - 1;
 
 enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5, M_PROG = 6 };
 
