@@ -424,7 +424,9 @@ size_t smem_bytes(const Geo& G, int buffers) {
 
 
 // Geometry of the gather kernel for an operation whose units do not fit whole (g >= 2).
-void plan_gather(Geo& G, bool dmma = false) {
+// bulk: stage sub-block rows with cp.async.bulk when they are contiguous runs of >= 16 elements
+// (tiles keep their stored orientation, adjoint components addressed through cadj).
+void plan_gather(Geo& G, bool dmma = false, bool bulk = false) {
     const uint32_t M = G.M, g = G.g, NT = 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -458,6 +460,7 @@ void plan_gather(Geo& G, bool dmma = false) {
     G.PD = S0 + 1;
     G.SRp = S0 + 1;
     G.logical = 1;
+    G.bulk = bulk && dmma && S0 >= 16 && cmask == S0 - 1;
     G.TS = S0 * (S0 + 1);
     const uint32_t D = G.D, kinm = (1u << kin) - 1;
     for (uint32_t t = 0; t < 64; ++t)
@@ -469,6 +472,8 @@ void plan_gather(Geo& G, bool dmma = false) {
                 G.ttr[i] = (uint8_t)t;
                 G.cdir[i] = G.cadj[i] =
                     (uint16_t)(t * G.TS + G.tsk[t] + G.xs_in[rho & kinm] * G.PD + G.y_in[gam & kinm]);
+                if (G.bulk)  // adjoint tiles in stored orientation: logical (x, y) at row y, column x
+                    G.cadj[i] = (uint16_t)(t * G.TS + G.tsk[t] + G.y_in[gam & kinm] * G.PD + G.xs_in[rho & kinm]);
             }
     };
     tables();
@@ -636,6 +641,12 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
                 Gg.qstride = d;
             }
             ws = !(Gg.dbg & 32u) && quad_ok;
+            if (ws && !(Gg.dbg & 64u)) {  // contiguous sub-block rows: bulk row copies (bit 6: off)
+                const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;
+                plan_gather(Gg, dmma || K == 2, true);
+                Gg.qstride = qs;
+                Gg.dbg = dbgf;
+            }
         }
         if (ws) {
             // every unit including the diagonal ones: logical (R, C), R < C, of a diagonal unit is a
@@ -644,6 +655,9 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             Gg.nG_items = Gg.nU_loose << (2 * Gg.log_nsb_side);
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
             auto kw = gather_ws_kernel<K, NS, MODE == M_PROG ? M_PROG : M_DIRECT>;
+            if constexpr ((K == 3 && MODE == M_DIRECT) || (K == 2 && MODE == M_DIRECT))
+                if (Gg.bulk)
+                    kw = gather_ws_kernel<K, NS, M_DIRECT, true>;
             e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess)
                 return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));

@@ -44,12 +44,13 @@ struct DmmaFrag {
     double ls[2], ld[2];      // Lr + Li (stage 1, 3M) and Pr + Pi = Lr - Li (stage 2, 3M)
     uint32_t old[2], ost[2];  // staging offsets of the loaded / stored components (from the block base)
     uint32_t tld[2], tst[2];  // their logical tiles (adjoint mask bits)
+    uint32_t oldA[2], ostA[2];  // bulk staging: the same components in an adjoint tile (stored orientation)
 };
 // k = 3: the 8 x 8 block itself.  k = 2: four 4 x 4 blocks (2X + R1, 2Y + C1) as the quadrants of
 // one 8 x 8 matrix M, transformed by I2 (x) L: (I2 (x) L) M (I2 (x) L)^dagger applies L . L^dagger to
 // every quadrant, so one tensor-core transform serves four k = 2 blocks (quadrant offsets
 // (R1 * PD + C1) * qstride, folded into the component offsets).
-template <int K, int NS>
+template <int K, int NS, bool BULK = false>
 __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const Coef<NS>& cf) {
     DmmaFrag f;
     const uint32_t lane = threadIdx.x & 31, gq = lane >> 2, cq = lane & 3;
@@ -72,6 +73,10 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
             f.ost[j] = T.cdir[is];
             f.tld[j] = T.ttr[il];
             f.tst[j] = T.ttr[is];
+            if constexpr (BULK) {
+                f.oldA[j] = T.cadj[il];
+                f.ostA[j] = T.cadj[is];
+            }
         } else {
             // load component (row c8, column gq), store component (row gq, column c8) of M
             const uint32_t il = (c8 & 3) * 4 + (gq & 3), is = (gq & 3) * 4 + (c8 & 3);
@@ -79,11 +84,15 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
             f.ost[j] = T.cdir[is] + ((gq >> 2) * G.PD + (c8 >> 2)) * G.qstride;
             f.tld[j] = T.ttr[il];
             f.tst[j] = T.ttr[is];
+            if constexpr (BULK) {  // transposed quadrant offsets in stored orientation
+                f.oldA[j] = T.cadj[il] + ((gq >> 2) * G.PD + (c8 >> 2)) * G.qstride;
+                f.ostA[j] = T.cadj[is] + ((c8 >> 2) * G.PD + (gq >> 2)) * G.qstride;
+            }
         }
     }
     return f;
 }
-template <int NC, int K = 3>
+template <int NC, int K = 3, bool BULK = false>
 __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
                                              double2* sb, uint32_t warp) {
     constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
@@ -94,15 +103,22 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
     // tiles, m < 5, have fewer blocks than warps: the second block of a pass may be absent and is
     // then computed on a copy of the first and not stored)
     for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32)) {
-        uint32_t base[2];
+        uint32_t base[2], baseA[2];
         double2 v0[2], v1[2];
         const bool two = b + NC / 32 < nblk;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const uint32_t bq = (q && two) ? b + NC / 32 : b;
-            base[q] = T.xb[(bq >> logNy) << sh] * G.PD + T.yb[(bq & ymask) << sh];
-            v0[q] = sb[base[q] + f.old[0]];
-            v1[q] = sb[base[q] + f.old[1]];
+            const uint32_t xbv = T.xb[(bq >> logNy) << sh], ybv = T.yb[(bq & ymask) << sh];
+            base[q] = xbv * G.PD + ybv;
+            if constexpr (BULK) {  // adjoint tiles in stored orientation: row y, column x
+                baseA[q] = ybv * G.PD + xbv;
+                v0[q] = sb[cld0 ? baseA[q] + f.oldA[0] : base[q] + f.old[0]];
+                v1[q] = sb[cld1 ? baseA[q] + f.oldA[1] : base[q] + f.old[1]];
+            } else {
+                v0[q] = sb[base[q] + f.old[0]];
+                v1[q] = sb[base[q] + f.old[1]];
+            }
             v0[q].y = flip_sign(v0[q].y, cld0);
             v1[q].y = flip_sign(v1[q].y, cld1);
         }
@@ -146,8 +162,13 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         for (int q = 0; q < 2; ++q) {
             if (q && !two)
                 break;
-            sb[base[q] + f.ost[0]] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
-            sb[base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
+            if constexpr (BULK) {
+                sb[cst0 ? baseA[q] + f.ostA[0] : base[q] + f.ost[0]] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
+                sb[cst1 ? baseA[q] + f.ostA[1] : base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
+            } else {
+                sb[base[q] + f.ost[0]] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
+                sb[base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
+            }
         }
     }
 }
@@ -346,12 +367,18 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
     }
 }
 
-template <int K, int NS, int MODE = M_DIRECT>
+// BULK (G.bulk): sub-block rows are contiguous runs of S0 >= 16 elements; every tile is staged in its
+// stored orientation (pitch S0 + 1) by one cp.async.bulk per row (256 / 512 B, completing on the
+// stage's `full` mbarrier) and written back by one bulk store per row -- no per-element copy
+// instructions.  Adjoint components are addressed through cadj (transposed offsets); the bank
+// groups are the same as in the logical layout since the pitch is 1 mod 8.
+template <int K, int NS, int MODE = M_DIRECT, bool BULK = false>
 __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     constexpr uint32_t NCW = 256, NMW = 512, S = 3;
     extern __shared__ __align__(128) double2 ring[];
     __shared__ uint64_t gt[S + 1][64];  // tile tables by item % (S + 1): built one item ahead
     __shared__ uint64_t am[S + 1][1];
+    __shared__ uint32_t mir[S + 1];     // BULK: the item has mirrored tiles (diagonal unit, a > b)
     __shared__ __align__(8) uint64_t full[S], done[S];
     __shared__ Tabs T;
     const uint32_t tid = threadIdx.x;
@@ -383,20 +410,22 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         // ---- transform warps
         DmmaFrag fr;
         if constexpr (MODE == M_DIRECT)
-            fr = dmma_frag<K>(G, T, cf);
+            fr = dmma_frag<K, NS, BULK>(G, T, cf);
         for (uint64_t i = 0; i < nlocal; ++i) {
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
             double2* sb = ring + (size_t)s * G.stage_elems;
             if constexpr (MODE == M_DIRECT) {
                 if (!(G.dbg & 1u))
-                    dmma_direct3<NCW, K>(G, T, fr, am[i % (S + 1)][0], sb, tid >> 5);
+                    dmma_direct3<NCW, K, BULK>(G, T, fr, am[i % (S + 1)][0], sb, tid >> 5);
             } else {
                 for (uint32_t p = 0; p < cf.nsteps; ++p) {
                     grid_prog_step<NCW>(G, T, cf, p, am[i % (S + 1)][0], sb, tid);
                     asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
                 }
             }
+            if constexpr (BULK)
+                fence_async_smem();  // the bulk stores (async proxy) read what these threads wrote
             mbar_arrive(&done[s]);
         }
         return;
@@ -450,6 +479,10 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             }
             gt[ts][t] = ent;
             adj = (ent & F_ADJ) != 0;
+            if (BULK && t == 0) {
+                const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
+                mir[ts] = tbi == tbj && (sb >> G.log_nsb_side) > (sb & ((1u << G.log_nsb_side) - 1));
+            }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, adj);
         if ((mtid & 31) == 0)
@@ -467,7 +500,27 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
             cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, tile_base(G, ent, st) + g);
         };
-        if (G.dbg & 2u) {
+        if constexpr (BULK) {
+            // one row of one tile per thread: stored rows x0 + r (direct) / y0 + r (adjoint)
+            if (!(G.dbg & 2u) && mtid < (NT << G.logS0)) {
+                const uint32_t t = mtid >> G.logS0, r = mtid & (G.S0 - 1);
+                const uint64_t ent = gt[ts][t];
+                if (!(ent & F_SKIP)) {
+                    const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
+                    const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
+                    const bool adj = (ent & F_ADJ) != 0;
+                    const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
+                                       (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
+                    mbar_arrive_expect(&full[s], G.S0 * 16u);
+                    bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD) * 16u, tile_base(G, ent, st) + g, G.S0 * 16u, &full[s]);
+                    mbar_arrive(&full[s]);
+                    return;
+                }
+            }
+            mbar_arrive(&full[s]);
+            mbar_arrive(&full[s]);
+            return;
+        } else if (G.dbg & 2u) {
         } else if (fast) {  // 8 tiles at one position: unrolled, table reads hoisted
             uint32_t od, oa, sm_d, sm_a;
             offsets(item_of(j), 0, od, oa, sm_d, sm_a);
@@ -524,7 +577,37 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                 o[oa] = make_double2(w.x, -w.y);
             }
         };
-        if (G.dbg & 4u) {
+        if constexpr (BULK) {
+            if (!(G.dbg & 4u)) {
+                if (mtid < (NT << G.logS0)) {
+                    const uint32_t t = mtid >> G.logS0, r = mtid & (G.S0 - 1);
+                    const uint64_t ent = gt[ts][t];
+                    if (!(ent & F_NOSTORE)) {
+                        const uint32_t sbi = (uint32_t)(item_of(i) & nsbm);
+                        const uint32_t x0 = G.sdep[sbi >> G.log_nsb_side], y0 = G.sdep[sbi & ((1u << G.log_nsb_side) - 1)];
+                        const bool adj = (ent & F_ADJ) != 0;
+                        const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
+                                           (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
+                        bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD), G.S0 * 16u);
+                        bulk_commit();
+                    }
+                }
+                if (mir[ts]) {  // diagonal unit, a > b: the R == C tiles also at the mirrored position
+                    for (uint32_t q = 0; q < npos; ++q) {
+                        uint32_t od, oa, sm_d, sm_a;
+                        offsets(item_of(i), q, od, oa, sm_d, sm_a);
+                        for (uint32_t tt = tt0; tt < NT; tt += ttstep) {
+                            const uint64_t ent = gt[ts][tt];
+                            if (ent & F_MIRROR) {
+                                const double2 w = sb[tt * G.TS + T.tsk[tt] + sm_a];
+                                G.out[((ent & F_MASK) << (2 * G.logM)) + oa] = make_double2(w.x, -w.y);
+                            }
+                        }
+                    }
+                }
+                bulk_wait_read0();  // this thread's row has left shared memory
+            }
+        } else if (G.dbg & 4u) {
         } else if (fast) {
             uint32_t od, oa, sm_d, sm_a;
             offsets(item_of(i), 0, od, oa, sm_d, sm_a);
@@ -562,7 +645,10 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     if (prof)
         for (int q = 0; q < 4; ++q)
             atomicAdd(&g_phase_cycles[q], (unsigned long long)ph[q]);
-    cp_async_wait<0>();
+    if constexpr (BULK)
+        bulk_wait_all();
+    else
+        cp_async_wait<0>();
 }
 
 }  // namespace

@@ -1,0 +1,81 @@
+// throughput of the f64 mma.sync shapes on B200 (m8n8k4 vs m16n8k4 / m16n8k8 / m16n8k16)
+#include <cstdio>
+constexpr int ITERS = 4096;
+template <int CH>
+__global__ void k884(double* out, double s) {
+    double acc[CH][2] = {};
+    double a = s * threadIdx.x, b = s + threadIdx.x;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                         : "+d"(acc[i][0]), "+d"(acc[i][1]) : "d"(a), "d"(b));
+    double t = 0; for (int i = 0; i < CH; ++i) t += acc[i][0] + acc[i][1];
+    if (t == 1.2345) out[0] = t;
+}
+template <int CH>
+__global__ void k1684(double* out, double s) {
+    double acc[CH][4] = {};
+    double a0 = s * threadIdx.x, a1 = a0 + 1, b = s + threadIdx.x;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+            asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                         : "+d"(acc[i][0]), "+d"(acc[i][1]), "+d"(acc[i][2]), "+d"(acc[i][3]) : "d"(a0), "d"(a1), "d"(b));
+    double t = 0; for (int i = 0; i < CH; ++i) t += acc[i][0] + acc[i][1] + acc[i][2] + acc[i][3];
+    if (t == 1.2345) out[0] = t;
+}
+template <int CH>
+__global__ void k1688(double* out, double s) {
+    double acc[CH][4] = {};
+    double a0 = s * threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, b0 = s + threadIdx.x, b1 = b0 + 1;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+            asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                         : "+d"(acc[i][0]), "+d"(acc[i][1]), "+d"(acc[i][2]), "+d"(acc[i][3])
+                         : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+    double t = 0; for (int i = 0; i < CH; ++i) t += acc[i][0] + acc[i][1] + acc[i][2] + acc[i][3];
+    if (t == 1.2345) out[0] = t;
+}
+template <int CH>
+__global__ void k16816(double* out, double s) {
+    double acc[CH][4] = {};
+    double a[8], b[4];
+    for (int i = 0; i < 8; ++i) a[i] = s * threadIdx.x + i;
+    for (int i = 0; i < 4; ++i) b[i] = s + threadIdx.x + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i)
+            asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                         : "+d"(acc[i][0]), "+d"(acc[i][1]), "+d"(acc[i][2]), "+d"(acc[i][3])
+                         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                           "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+    double t = 0; for (int i = 0; i < CH; ++i) t += acc[i][0] + acc[i][1] + acc[i][2] + acc[i][3];
+    if (t == 1.2345) out[0] = t;
+}
+template <typename F>
+void run(const char* name, F kern, double fma_per_instr, int ch, int threads) {
+    double* out; cudaMalloc(&out, 8);
+    int blocks = 148 * 2;
+    kern<<<blocks, threads>>>(out, 0.999);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    kern<<<blocks, threads>>>(out, 0.999);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double fl = 2.0 * fma_per_instr * ITERS * ch * (double)blocks * threads / 32;
+    printf("%-10s threads=%4d chains=%d  %.2f TFLOP/s\n", name, threads, ch, fl / ms / 1e9);
+    cudaFree(out);
+}
+int main() {
+    for (int th : {256, 512}) {
+        run("m8n8k4", k884<4>, 256, 4, th);
+        run("m16n8k4", k1684<4>, 512, 4, th);
+        run("m16n8k8", k1688<2>, 1024, 2, th);
+        run("m16n8k8", k1688<4>, 1024, 4, th);
+        run("m16n8k16", k16816<2>, 2048, 2, th);
+        run("m16n8k16", k16816<4>, 2048, 4, th);
+    }
+    printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+}
