@@ -374,7 +374,8 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
 // groups are the same as in the logical layout since the pitch is 1 mod 8.
 template <int K, int NS, int MODE = M_DIRECT, bool BULK = false>
 __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
-    constexpr uint32_t NCW = 256, NMW = 512, S = 3;
+    // bulk rows need few copy instructions: 16 transform warps and 8 copy warps (else 8 and 16)
+    constexpr uint32_t NCW = BULK ? 512 : 256, NMW = BULK ? 256 : 512, S = 3;
     extern __shared__ __align__(128) double2 ring[];
     __shared__ uint64_t gt[S + 1][64];  // tile tables by item % (S + 1): built one item ahead
     __shared__ uint64_t am[S + 1][1];
@@ -502,19 +503,17 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         };
         if constexpr (BULK) {
             // one row of one tile per thread: stored rows x0 + r (direct) / y0 + r (adjoint)
-            if (!(G.dbg & 2u) && mtid < (NT << G.logS0)) {
-                const uint32_t t = mtid >> G.logS0, r = mtid & (G.S0 - 1);
+            const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
+            const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
+            for (uint32_t row = mtid; !(G.dbg & 2u) && row < (NT << G.logS0); row += NMW) {
+                const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
                 const uint64_t ent = gt[ts][t];
                 if (!(ent & F_SKIP)) {
-                    const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
-                    const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
                     const bool adj = (ent & F_ADJ) != 0;
                     const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
                                        (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
-                    mbar_arrive_expect(&full[s], G.S0 * 16u);
+                    mbar_expect(&full[s], G.S0 * 16u);
                     bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD) * 16u, tile_base(G, ent, st) + g, G.S0 * 16u, &full[s]);
-                    mbar_arrive(&full[s]);
-                    return;
                 }
             }
             mbar_arrive(&full[s]);
@@ -579,12 +578,12 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         };
         if constexpr (BULK) {
             if (!(G.dbg & 4u)) {
-                if (mtid < (NT << G.logS0)) {
-                    const uint32_t t = mtid >> G.logS0, r = mtid & (G.S0 - 1);
+                const uint32_t sbi = (uint32_t)(item_of(i) & nsbm);
+                const uint32_t x0 = G.sdep[sbi >> G.log_nsb_side], y0 = G.sdep[sbi & ((1u << G.log_nsb_side) - 1)];
+                for (uint32_t row = mtid; row < (NT << G.logS0); row += NMW) {
+                    const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
                     const uint64_t ent = gt[ts][t];
                     if (!(ent & F_NOSTORE)) {
-                        const uint32_t sbi = (uint32_t)(item_of(i) & nsbm);
-                        const uint32_t x0 = G.sdep[sbi >> G.log_nsb_side], y0 = G.sdep[sbi & ((1u << G.log_nsb_side) - 1)];
                         const bool adj = (ent & F_ADJ) != 0;
                         const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
                                            (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);

@@ -1,5 +1,6 @@
 // throughput of the f64 mma.sync shapes on B200 (m8n8k4 vs m16n8k4 / m16n8k8 / m16n8k16)
 #include <cstdio>
+#include <nvml.h>
 constexpr int ITERS = 4096;
 template <int CH>
 __global__ void k884(double* out, double s) {
@@ -68,6 +69,28 @@ void run(const char* name, F kern, double fma_per_instr, int ch, int threads) {
     printf("%-10s threads=%4d chains=%d  %.2f TFLOP/s\n", name, threads, ch, fl / ms / 1e9);
     cudaFree(out);
 }
+// energy per FMA: run the kernel back to back for ~2 s, NVML total-energy counter around it
+template <typename F>
+void energy(const char* name, F kern, double fma_per_instr, int ch, int threads, nvmlDevice_t dev) {
+    double* out; cudaMalloc(&out, 8);
+    int blocks = 148 * 2;
+    kern<<<blocks, threads>>>(out, 0.999);
+    cudaDeviceSynchronize();
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    unsigned long long j0 = 0, j1 = 0;
+    nvmlDeviceGetTotalEnergyConsumption(dev, &j0);
+    cudaEventRecord(e0);
+    const int reps = 200;
+    for (int r = 0; r < reps; ++r) kern<<<blocks, threads>>>(out, 0.999);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    nvmlDeviceGetTotalEnergyConsumption(dev, &j1);
+    unsigned int clk = 0; nvmlDeviceGetClockInfo(dev, NVML_CLOCK_SM, &clk);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    double fma = fma_per_instr * ITERS * ch * (double)blocks * threads / 32 * reps;
+    printf("%-10s %.2f TFLOP/s  %.0f W  %.2f pJ/FMA  (sm %u MHz, %.0f ms)\n", name, 2 * fma / ms / 1e9,
+           (j1 - j0) / ms, (j1 - j0) * 1e-3 / fma * 1e12, clk, ms);
+    cudaFree(out);
+}
 int main() {
     for (int th : {256, 512}) {
         run("m8n8k4", k884<4>, 256, 4, th);
@@ -77,5 +100,11 @@ int main() {
         run("m16n8k16", k16816<2>, 2048, 2, th);
         run("m16n8k16", k16816<4>, 2048, 4, th);
     }
+    nvmlInit();
+    nvmlDevice_t dev; nvmlDeviceGetHandleByIndex(0, &dev);
+    energy("m8n8k4", k884<4>, 256, 4, 512, dev);
+    energy("m16n8k8", k1688<4>, 1024, 4, 512, dev);
+    energy("m16n8k16", k16816<4>, 2048, 4, 512, dev);
+    energy("m8n8k4", k884<4>, 256, 4, 512, dev);
     printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
