@@ -426,7 +426,7 @@ size_t smem_bytes(const Geo& G, int buffers) {
 // Geometry of the gather kernel for an operation whose units do not fit whole (g >= 2).
 // bulk: stage sub-block rows with cp.async.bulk when they are contiguous runs of >= 16 elements
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
-void plan_gather(Geo& G, bool dmma = false, bool bulk = false) {
+void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0) {
     const uint32_t M = G.M, g = G.g, NT = 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -478,10 +478,31 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false) {
     };
     tables();
     uint32_t extra = 0;
-    if (dmma && D == 8) {
-        // the DMMA transform's lane patterns (load B[2c+j][g], store Z[g][2c+j]) hit 16-byte bank
-        // groups (addr mod 8) by component offset: pick a tile pitch and per-tile-row skew that
-        // spread every quarter-warp over 8 groups
+    if (dmma && (D == 8 || (D == 4 && qstride))) {
+        // the DMMA transform's lane patterns (load B[2c+j][g], store Z[g][2c+j]; k = 2: the 8 x 8
+        // matrix of four quadrant blocks at offset qstride) hit 16-byte bank groups (addr mod 8) by
+        // component offset: pick a tile pitch and per-tile skews that spread every quarter-warp
+        // over 8 groups (the offsets are additive in the block base, so one block decides)
+        auto comp = [&](uint32_t row, uint32_t col) -> uint32_t {
+            if (D == 8)
+                return G.cdir[row * 8 + col];
+            return G.cdir[(row & 3) * 4 + (col & 3)] + ((row >> 2) * G.PD + (col >> 2)) * qstride;
+        };
+        auto cost_of = [&]() {
+            uint32_t cost = 0;
+            for (int pat = 0; pat < 2; ++pat)
+                for (uint32_t j = 0; j < 2; ++j)
+                    for (uint32_t ph = 0; ph < 4; ++ph) {
+                        uint32_t cnt[8] = {0}, mx = 0;
+                        for (uint32_t l = 8 * ph; l < 8 * ph + 8; ++l) {
+                            const uint32_t gq = l >> 2, cq = l & 3;
+                            const uint32_t a = pat ? comp(gq, 2 * cq + j) : comp(2 * cq + j, gq);
+                            mx = std::max(mx, ++cnt[a & 7u]);
+                        }
+                        cost += mx;
+                    }
+            return cost;
+        };
         const uint32_t TS0 = G.TS;
         uint32_t best = ~0u, bestE = 0, bestS = 0;
         for (uint32_t e = 0; e < 8; ++e)
@@ -490,19 +511,7 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false) {
                 for (uint32_t t = 0; t < NT; ++t)
                     G.tsk[t] = (uint8_t)((sk * (t >> g)) & 7u);
                 tables();
-                uint32_t cost = 0;
-                for (int pat = 0; pat < 2; ++pat)
-                    for (uint32_t j = 0; j < 2; ++j)
-                        for (uint32_t ph = 0; ph < 4; ++ph) {
-                            uint32_t cnt[8] = {0}, mx = 0;
-                            for (uint32_t l = 8 * ph; l < 8 * ph + 8; ++l) {
-                                const uint32_t gq = l >> 2, cq = l & 3;
-                                const uint32_t i = pat ? gq * 8 + 2 * cq + j : (2 * cq + j) * 8 + gq;
-                                mx = std::max(mx, ++cnt[G.cdir[i] & 7u]);
-                            }
-                            cost += mx;
-                        }
-                cost = cost * 64 + e + sk;  // ties: the smallest footprint
+                const uint32_t cost = cost_of() * 64 + e + sk;  // ties: the smallest footprint
                 if (cost < best) {
                     best = cost;
                     bestE = e;
@@ -513,6 +522,25 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false) {
         for (uint32_t t = 0; t < NT; ++t)
             G.tsk[t] = (uint8_t)((bestS * (t >> g)) & 7u);
         tables();
+        // then per-tile skews by coordinate descent (a linear skew in the tile row cannot spread
+        // four tile rows x two columns of stride 2 over 8 groups)
+        uint32_t cur = cost_of();
+        for (uint32_t pass = 0; pass < 3 && cur > 16; ++pass)
+            for (uint32_t t = 0; t < NT; ++t) {
+                const uint8_t keep = G.tsk[t];
+                uint8_t bv = keep;
+                for (uint32_t v = 0; v < 8; ++v) {
+                    G.tsk[t] = (uint8_t)v;
+                    tables();
+                    const uint32_t c = cost_of();
+                    if (c < cur) {
+                        cur = c;
+                        bv = (uint8_t)v;
+                    }
+                }
+                G.tsk[t] = bv;
+                tables();
+            }
         extra = 7;
     }
     G.diag_map = (G.nxb >= 8 && G.nyb >= 8) ? 1 : 0;
@@ -643,7 +671,7 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             ws = !(Gg.dbg & 32u) && quad_ok;
             if (ws && !(Gg.dbg & 64u)) {  // contiguous sub-block rows: bulk row copies (bit 6: off)
                 const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;
-                plan_gather(Gg, dmma || K == 2, true);
+                plan_gather(Gg, dmma || K == 2, true, K == 2 ? qs : 0);
                 Gg.qstride = qs;
                 Gg.dbg = dbgf;
             }

@@ -376,10 +376,13 @@ template <int K, int NS, int MODE = M_DIRECT, bool BULK = false>
 __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
     // bulk rows need few copy instructions: 16 transform warps and 8 copy warps (else 8 and 16)
     constexpr uint32_t NCW = BULK ? 512 : 256, NMW = BULK ? 256 : 512, S = 3;
+    // tile tables by item % TSL, built S items ahead (BULK: by two copy groups that may be one item
+    // apart, hence two more slots)
+    constexpr uint32_t TSL = BULK ? S + 3 : S + 1;
     extern __shared__ __align__(128) double2 ring[];
-    __shared__ uint64_t gt[S + 1][64];  // tile tables by item % (S + 1): built one item ahead
-    __shared__ uint64_t am[S + 1][1];
-    __shared__ uint32_t mir[S + 1];     // BULK: the item has mirrored tiles (diagonal unit, a > b)
+    __shared__ uint64_t gt[TSL][64];
+    __shared__ uint64_t am[TSL][1];
+    __shared__ uint32_t mir[TSL];     // BULK: the item has mirrored tiles (diagonal unit, a > b)
     __shared__ __align__(8) uint64_t full[S], done[S];
     __shared__ Tabs T;
     const uint32_t tid = threadIdx.x;
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     }
     if (tid == 0)
         for (uint32_t q = 0; q < S; ++q) {
-            mbar_init(&full[q], 2 * NMW);
+            mbar_init(&full[q], BULK ? NMW : 2 * NMW);  // BULK: one copy group (NMW / 2) loads an item
             mbar_init(&done[q], NCW);
         }
     const uint64_t nItems = G.nG_items;
@@ -418,10 +421,10 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             double2* sb = ring + (size_t)s * G.stage_elems;
             if constexpr (MODE == M_DIRECT) {
                 if (!(G.dbg & 1u))
-                    dmma_direct3<NCW, K, BULK>(G, T, fr, am[i % (S + 1)][0], sb, tid >> 5);
+                    dmma_direct3<NCW, K, BULK>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
             } else {
                 for (uint32_t p = 0; p < cf.nsteps; ++p) {
-                    grid_prog_step<NCW>(G, T, cf, p, am[i % (S + 1)][0], sb, tid);
+                    grid_prog_step<NCW>(G, T, cf, p, am[i % TSL][0], sb, tid);
                     asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
                 }
             }
@@ -452,12 +455,11 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         sm_a = j0 * P + i0;
     };
     // tile table and adjoint mask of item j, by the first two copy warps (one logical tile per
-    // lane) into slot j % (S + 1), which no stage in flight uses
-    auto tables = [&](uint64_t j) {  // copy warps 0 and 1: one logical tile per lane (NT <= 64)
-        const uint32_t ts = (uint32_t)(j % (S + 1));
+    // lane) into slot j % TSL, which no stage in flight uses
+    auto tables = [&](uint64_t j, uint32_t t) {  // threads t < 64 (two warps): one logical tile per lane (NT <= 64)
+        const uint32_t ts = (uint32_t)(j % TSL);
         uint64_t tbi, tbj;
         unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), !G.ws_diag, tbi, tbj);
-        const uint32_t t = mtid;
         bool adj = false;
         if (t < NT) {
             const uint64_t tr = ins_bits(tbi, t >> G.logNG, G.gr_pos, G.g);
@@ -486,12 +488,12 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             }
         }
         const unsigned bal = __ballot_sync(0xffffffffu, adj);
-        if ((mtid & 31) == 0)
-            reinterpret_cast<uint32_t*>(&am[ts][0])[mtid >> 5] = bal;  // little endian: tiles 0-31, 32-63
+        if ((t & 31) == 0)
+            reinterpret_cast<uint32_t*>(&am[ts][0])[t >> 5] = bal;  // little endian: tiles 0-31, 32-63
     };
     // cp.async of item j into stage j % S (its table is visible: a copy-warp barrier separates them)
     auto issue = [&](uint64_t j) {
-        const uint32_t s = (uint32_t)(j % S), ts = (uint32_t)(j % (S + 1));
+        const uint32_t s = (uint32_t)(j % S), ts = (uint32_t)(j % TSL);
         const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
         auto one = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
             const uint64_t ent = gt[ts][tt];
@@ -501,25 +503,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + (adj ? oa : od);
             cp_async16(base + (tt * G.TS + T.tsk[tt] + (adj ? sm_a : sm_d)) * 16u, tile_base(G, ent, st) + g);
         };
-        if constexpr (BULK) {
-            // one row of one tile per thread: stored rows x0 + r (direct) / y0 + r (adjoint)
-            const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
-            const uint32_t x0 = G.sdep[sb >> G.log_nsb_side], y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
-            for (uint32_t row = mtid; !(G.dbg & 2u) && row < (NT << G.logS0); row += NMW) {
-                const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
-                const uint64_t ent = gt[ts][t];
-                if (!(ent & F_SKIP)) {
-                    const bool adj = (ent & F_ADJ) != 0;
-                    const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
-                                       (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
-                    mbar_expect(&full[s], G.S0 * 16u);
-                    bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD) * 16u, tile_base(G, ent, st) + g, G.S0 * 16u, &full[s]);
-                }
-            }
-            mbar_arrive(&full[s]);
-            mbar_arrive(&full[s]);
-            return;
-        } else if (G.dbg & 2u) {
+        if (G.dbg & 2u) {
         } else if (fast) {  // 8 tiles at one position: unrolled, table reads hoisted
             uint32_t od, oa, sm_d, sm_a;
             offsets(item_of(j), 0, od, oa, sm_d, sm_a);
@@ -548,20 +532,100 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     };
     const bool prof = (G.dbg & 16u) && mtid == 0;
     long long ph[4] = {0, 0, 0, 0};
+    if constexpr (BULK) {
+        // Two copy groups of NMW / 2 threads: group (i & 1) writes item i back (one bulk store per
+        // row), waits until its stores have read the stage, and loads item i + S into it.  The other
+        // group's stores of item i + 1 queue behind, so the bulk-copy engine always has work (one
+        // group would leave it idle from the end of its stores to the issue of its loads).
+        constexpr uint32_t NGT = NMW / 2;
+        const uint32_t cg = mtid / NGT, gtid = mtid % NGT;
+        auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(3 + cg), "n"(NGT) : "memory"); };
+        auto rows_of = [&](uint64_t j, uint32_t& x0, uint32_t& y0) {
+            const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
+            x0 = G.sdep[sb >> G.log_nsb_side];
+            y0 = G.sdep[sb & ((1u << G.log_nsb_side) - 1)];
+        };
+        auto bissue = [&](uint64_t j) {  // item j into stage j % S: one bulk copy per stored row
+            const uint32_t s = (uint32_t)(j % S), ts = (uint32_t)(j % TSL);
+            const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
+            uint32_t x0, y0;
+            rows_of(j, x0, y0);
+            for (uint32_t row = gtid; !(G.dbg & 2u) && row < (NT << G.logS0); row += NGT) {
+                const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
+                const uint64_t ent = gt[ts][t];
+                if (!(ent & F_SKIP)) {
+                    const bool adj = (ent & F_ADJ) != 0;
+                    const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
+                                       (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
+                    mbar_expect(&full[s], G.S0 * 16u);
+                    bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD) * 16u, tile_base(G, ent, st) + g, G.S0 * 16u, &full[s]);
+                }
+            }
+            mbar_arrive(&full[s]);
+            mbar_arrive(&full[s]);
+        };
+        for (uint64_t j = 0; j < S && j < nlocal; ++j)  // item j is loaded by group (j + 1) & 1
+            if (((j + 1) & 1) == cg) {
+                if (gtid < 64)
+                    tables(j, gtid);
+                gsync();
+                bissue(j);
+            }
+        for (uint64_t i = cg; i < nlocal; i += 2) {
+            const uint32_t s = (uint32_t)(i % S), ts = (uint32_t)(i % TSL);
+            mbar_wait(&done[s], (uint32_t)((i / S) & 1));
+            const bool more = i + S < nlocal;
+            if (more && gtid < 64)
+                tables(i + S, gtid);
+            const double2* sb = ring + (size_t)s * G.stage_elems;
+            if (!(G.dbg & 4u)) {
+                uint32_t x0, y0;
+                rows_of(i, x0, y0);
+                for (uint32_t row = gtid; row < (NT << G.logS0); row += NGT) {
+                    const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
+                    const uint64_t ent = gt[ts][t];
+                    if (!(ent & F_NOSTORE)) {
+                        const bool adj = (ent & F_ADJ) != 0;
+                        const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
+                                           (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
+                        bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD), G.S0 * 16u);
+                        bulk_commit();
+                    }
+                }
+                if (mir[ts]) {  // diagonal unit, a > b: the R == C tiles also at the mirrored position
+                    for (uint32_t p = gtid; p < (NT << logT); p += NGT) {
+                        const uint32_t tt = p >> logT, rr = p & (T2 - 1), i0 = rr >> G.logS0, j0 = rr & (G.S0 - 1);
+                        const uint64_t ent = gt[ts][tt];
+                        if (ent & F_MIRROR) {  // stored (y0 + i0, x0 + j0) = conj(logical (x0 + j0, y0 + i0))
+                            const double2 w = sb[tt * G.TS + T.tsk[tt] + j0 * P + i0];
+                            G.out[((ent & F_MASK) << (2 * G.logM)) + ((uint64_t)(y0 + i0) << G.logM) + x0 + j0] =
+                                make_double2(w.x, -w.y);
+                        }
+                    }
+                }
+                bulk_wait_read0();  // this thread's rows have left shared memory
+            }
+            gsync();  // the group's stores have read stage s; the table of item i + S is visible
+            if (more)
+                bissue(i + S);
+        }
+        bulk_wait_all();
+        return;
+    }
     if (mtid < 64)
         for (uint64_t j = 0; j < S && j < nlocal; ++j)
-            tables(j);
+            tables(j, mtid);
     mbar_sync();
     for (uint64_t j = 0; j < S && j < nlocal; ++j)
         issue(j);
     for (uint64_t i = 0; i < nlocal; ++i) {
-        const uint32_t s = (uint32_t)(i % S), ts = (uint32_t)(i % (S + 1));
+        const uint32_t s = (uint32_t)(i % S), ts = (uint32_t)(i % TSL);
         const long long t0 = prof ? clock64() : 0;
         mbar_wait(&done[s], (uint32_t)((i / S) & 1));
         const long long t1 = prof ? clock64() : 0;
         const bool more = i + S < nlocal;
         if (more && mtid < 64)
-            tables(i + S);
+            tables(i + S, mtid);
         const double2* sb = ring + (size_t)s * G.stage_elems;
         auto wb = [&](uint32_t tt, uint32_t od, uint32_t oa, uint32_t sm_d, uint32_t sm_a) {
             const uint64_t ent = gt[ts][tt];
@@ -576,37 +640,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                 o[oa] = make_double2(w.x, -w.y);
             }
         };
-        if constexpr (BULK) {
-            if (!(G.dbg & 4u)) {
-                const uint32_t sbi = (uint32_t)(item_of(i) & nsbm);
-                const uint32_t x0 = G.sdep[sbi >> G.log_nsb_side], y0 = G.sdep[sbi & ((1u << G.log_nsb_side) - 1)];
-                for (uint32_t row = mtid; row < (NT << G.logS0); row += NMW) {
-                    const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
-                    const uint64_t ent = gt[ts][t];
-                    if (!(ent & F_NOSTORE)) {
-                        const bool adj = (ent & F_ADJ) != 0;
-                        const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
-                                           (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
-                        bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD), G.S0 * 16u);
-                        bulk_commit();
-                    }
-                }
-                if (mir[ts]) {  // diagonal unit, a > b: the R == C tiles also at the mirrored position
-                    for (uint32_t q = 0; q < npos; ++q) {
-                        uint32_t od, oa, sm_d, sm_a;
-                        offsets(item_of(i), q, od, oa, sm_d, sm_a);
-                        for (uint32_t tt = tt0; tt < NT; tt += ttstep) {
-                            const uint64_t ent = gt[ts][tt];
-                            if (ent & F_MIRROR) {
-                                const double2 w = sb[tt * G.TS + T.tsk[tt] + sm_a];
-                                G.out[((ent & F_MASK) << (2 * G.logM)) + oa] = make_double2(w.x, -w.y);
-                            }
-                        }
-                    }
-                }
-                bulk_wait_read0();  // this thread's row has left shared memory
-            }
-        } else if (G.dbg & 4u) {
+        if (G.dbg & 4u) {
         } else if (fast) {
             uint32_t od, oa, sm_d, sm_a;
             offsets(item_of(i), 0, od, oa, sm_d, sm_a);
@@ -644,10 +678,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     if (prof)
         for (int q = 0; q < 4; ++q)
             atomicAdd(&g_phase_cycles[q], (unsigned long long)ph[q]);
-    if constexpr (BULK)
-        bulk_wait_all();
-    else
-        cp_async_wait<0>();
+    cp_async_wait<0>();
 }
 
 }  // namespace
