@@ -540,6 +540,15 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         constexpr uint32_t NGT = NMW / 2;
         const uint32_t cg = mtid / NGT, gtid = mtid % NGT;
         auto gsync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(3 + cg), "n"(NGT) : "memory"); };
+        // runs: item = NT tiles x S0 rows x rps runs of 2^logRun elements (contiguous in-tile columns)
+        const uint32_t lrr = G.logS0 - G.logRun, rps = 1u << lrr, lrt = G.logS0 + lrr;
+        const uint32_t nruns = NT << lrt, rbytes = 16u << G.logRun;
+        // in-tile offset of run c (sub-block column c) of sub-block row r: stored row x0|xdep[r]
+        // (direct) or y0|xdep[r] (adjoint, stored orientation)
+        auto run_off = [&](bool adj, uint32_t x0, uint32_t y0, uint32_t r, uint32_t c) -> uint64_t {
+            return adj ? ((uint64_t)(y0 | T.xdep[r]) << G.logM) + (x0 | T.xdep[c])
+                       : ((uint64_t)(x0 | T.xdep[r]) << G.logM) + (y0 | T.xdep[c]);
+        };
         auto rows_of = [&](uint64_t j, uint32_t& x0, uint32_t& y0) {
             const uint32_t sb = (uint32_t)(item_of(j) & nsbm);
             x0 = G.sdep[sb >> G.log_nsb_side];
@@ -550,15 +559,14 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
             uint32_t x0, y0;
             rows_of(j, x0, y0);
-            for (uint32_t row = gtid; !(G.dbg & 2u) && row < (NT << G.logS0); row += NGT) {
-                const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
+            for (uint32_t q = gtid; !(G.dbg & 2u) && q < nruns; q += NGT) {
+                const uint32_t t = q >> lrt, r = (q >> lrr) & (G.S0 - 1), c = (q & (rps - 1)) << G.logRun;
                 const uint64_t ent = gt[ts][t];
                 if (!(ent & F_SKIP)) {
                     const bool adj = (ent & F_ADJ) != 0;
-                    const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
-                                       (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
-                    mbar_expect(&full[s], G.S0 * 16u);
-                    bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD) * 16u, tile_base(G, ent, st) + g, G.S0 * 16u, &full[s]);
+                    const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
+                    mbar_expect(&full[s], rbytes);
+                    bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD + c) * 16u, tile_base(G, ent, st) + g, rbytes, &full[s]);
                 }
             }
             mbar_arrive(&full[s]);
@@ -581,14 +589,13 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             if (!(G.dbg & 4u)) {
                 uint32_t x0, y0;
                 rows_of(i, x0, y0);
-                for (uint32_t row = gtid; row < (NT << G.logS0); row += NGT) {
-                    const uint32_t t = row >> G.logS0, r = row & (G.S0 - 1);
+                for (uint32_t q = gtid; q < nruns; q += NGT) {
+                    const uint32_t t = q >> lrt, r = (q >> lrr) & (G.S0 - 1), c = (q & (rps - 1)) << G.logRun;
                     const uint64_t ent = gt[ts][t];
                     if (!(ent & F_NOSTORE)) {
                         const bool adj = (ent & F_ADJ) != 0;
-                        const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) +
-                                           (adj ? ((uint64_t)(y0 + r) << G.logM) + x0 : ((uint64_t)(x0 + r) << G.logM) + y0);
-                        bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD), G.S0 * 16u);
+                        const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
+                        bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD + c), rbytes);
                         bulk_commit();
                     }
                 }
@@ -596,10 +603,10 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                     for (uint32_t p = gtid; p < (NT << logT); p += NGT) {
                         const uint32_t tt = p >> logT, rr = p & (T2 - 1), i0 = rr >> G.logS0, j0 = rr & (G.S0 - 1);
                         const uint64_t ent = gt[ts][tt];
-                        if (ent & F_MIRROR) {  // stored (y0 + i0, x0 + j0) = conj(logical (x0 + j0, y0 + i0))
+                        if (ent & F_MIRROR) {  // stored (y0|i0, x0|j0) = conj(logical (x0|j0, y0|i0))
                             const double2 w = sb[tt * G.TS + T.tsk[tt] + j0 * P + i0];
-                            G.out[((ent & F_MASK) << (2 * G.logM)) + ((uint64_t)(y0 + i0) << G.logM) + x0 + j0] =
-                                make_double2(w.x, -w.y);
+                            G.out[((ent & F_MASK) << (2 * G.logM)) + ((uint64_t)(y0 | T.xdep[i0]) << G.logM) +
+                                  (x0 | T.xdep[j0])] = make_double2(w.x, -w.y);
                         }
                     }
                 }

@@ -93,8 +93,9 @@ struct Geo {
     uint32_t ws_diag;             // gather_ws: units include the diagonal base pairs (grid programs)
     uint32_t qstride;             // gather_ws, k = 2 DMMA: position offset between paired blocks
     uint32_t rev;                 // sweep the items in reverse order (alternates per launch: L2 reuse)
-    uint32_t bulk;                // gather_ws: sub-block rows move as cp.async.bulk rows (S0 >= 16 contiguous
+    uint32_t bulk;                // gather_ws: sub-block rows move as cp.async.bulk runs (>= 8 contiguous
                                   // elements), every tile staged in its STORED orientation (cadj: adjoint offsets)
+    uint32_t logRun;              // bulk: log2 of the run length (contiguous low in-tile bits of the sub-block)
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
