@@ -33,6 +33,7 @@
 // transforms, slab kernel, TMA pipeline), engine_gather.cuh (gather kernels, DMMA transforms, grid
 // programs), engine_aux.cuh (reductions, generators); this file: state, launch planning, C-ABI
 // (include/hs_cuda.h), sharding / exchange, OHRM I/O, CUDA graphs.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -424,9 +425,38 @@ size_t smem_bytes(const Geo& G, int buffers) {
 
 
 // Geometry of the gather kernel for an operation whose units do not fit whole (g >= 2).
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn tensor_map_encoder() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+// The payload as rows of one 32-element tile row (64 doubles, 512 B), boxes of 8 rows x 8 complex
+// elements (128 B: the SWIZZLE_128B span).
+bool encode_tile_map(CUtensorMap* tm, const void* base, uint64_t elems) {
+    const EncodeTiledFn fn = tensor_map_encoder();
+    if (!fn || elems / 32 >= (1ull << 32))
+        return false;
+    cuuint64_t dims[2] = {64, elems / 32};
+    cuuint64_t strides[1] = {512};
+    cuuint32_t box[2] = {16, 8}, estr[2] = {1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // bulk: stage sub-block rows with cp.async.bulk, one copy per run of >= 8 contiguous elements
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
-void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0) {
+void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false) {
     const uint32_t M = G.M, g = G.g, NT = 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -546,10 +576,72 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
             }
         extra = 7;
     }
+    G.tma = 0;
+    const uint32_t nbx = S0 >> 3, bpt = nbx * nbx;
+    if (tma && dmma && D == 8 && !G.bulk && M == 32 && G.logRun >= 3 && (S0 == 8 || S0 == 16) &&
+        ((S0 - 1) & ~xs_tmask) < 8 && (xs_tmask & 7u) == 0 && NT * bpt <= 64) {
+        // 8 x 8 boxes through the tensor map (SWIZZLE_128B): slot = (tile, box) with a swizzle phase
+        // phi (16-B chunk c of box row x lands at c ^ ((x + phi) & 7)).  The DMMA patterns touch the
+        // in-box positions of (block base | component offset) in direct or transposed placement;
+        // pick the phases by coordinate descent over sample blocks and both placements
+        G.tma = 1;
+        const uint32_t nslot = NT * bpt;
+        uint8_t phi[64];
+        for (uint32_t q = 0; q < nslot; ++q) {
+            const uint32_t t = q / bpt, b = q % bpt;
+            phi[q] = (uint8_t)(((t >> g) + (t & (NG - 1)) + (b / nbx) + 2 * (b % nbx)) & 7u);
+        }
+        const uint32_t smp[4][2] = {{0, 0}, {7 & (G.nxb - 1), 5 & (G.nyb - 1)}, {3 & (G.nxb - 1), 6 & (G.nyb - 1)},
+                                    {6 & (G.nxb - 1), 1 & (G.nyb - 1)}};
+        auto tcost = [&]() {
+            uint32_t cost = 0;
+            for (uint32_t sb = 0; sb < 4; ++sb)
+                for (uint32_t ori = 0; ori < 2; ++ori)
+                    for (int pat = 0; pat < 2; ++pat)
+                        for (uint32_t j = 0; j < 2; ++j)
+                            for (uint32_t ph = 0; ph < 4; ++ph) {
+                                uint32_t cnt[8] = {0}, mx = 0;
+                                for (uint32_t l = 8 * ph; l < 8 * ph + 8; ++l) {
+                                    const uint32_t gq = l >> 2, cq = l & 3;
+                                    const uint32_t row = pat ? gq : 2 * cq + j, col = pat ? 2 * cq + j : gq;
+                                    const uint32_t t = G.ttr[row * 8 + col];
+                                    const uint32_t xo = G.xb_tab[smp[sb][0]] | G.xs_in[row & kinm];
+                                    const uint32_t yo = G.yb_tab[smp[sb][1]] | G.y_in[col & kinm];
+                                    const uint32_t xs = ori ? yo : xo, ys = ori ? xo : yo;
+                                    const uint32_t q = t * bpt + (xs >> 3) * nbx + (ys >> 3);
+                                    mx = std::max(mx, ++cnt[((ys & 7u) ^ ((xs + phi[q]) & 7u))]);
+                                }
+                                cost += mx;
+                            }
+            return cost;
+        };
+        uint32_t cur = tcost();
+        for (uint32_t pass = 0; pass < 3 && cur > 128; ++pass)
+            for (uint32_t q = 0; q < nslot; ++q) {
+                uint8_t bv = phi[q];
+                for (uint32_t v = 0; v < 8; ++v) {
+                    phi[q] = (uint8_t)v;
+                    const uint32_t c = tcost();
+                    if (c < cur) {
+                        cur = c;
+                        bv = (uint8_t)v;
+                    }
+                }
+                phi[q] = bv;
+            }
+        // slots in order of phase: box k at k * 1 KiB + phi * 128 B never overlaps box k + 1
+        uint32_t k = 0;
+        for (uint32_t v = 0; v < 8; ++v)
+            for (uint32_t q = 0; q < nslot; ++q)
+                if (phi[q] == v) {
+                    G.cdir[q] = (uint16_t)(k++ * 64 + v * 8);
+                    G.tsk[q] = (uint8_t)v;
+                }
+    }
     G.diag_map = (G.nxb >= 8 && G.nyb >= 8) ? 1 : 0;
     G.U = 1;
     G.logU = 0;
-    G.stage_elems = (NT * G.TS + extra + 7) & ~7u;
+    G.stage_elems = G.tma ? NT * bpt * 64 + 64 : (NT * G.TS + extra + 7) & ~7u;
     G.stages = 3;
     G.nG_items = G.nU_strict << (2 * G.log_nsb_side);
 }
@@ -674,27 +766,40 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             ws = !(Gg.dbg & 32u) && quad_ok;
             if (ws && !(Gg.dbg & 64u)) {  // contiguous sub-block rows: bulk row copies (bit 6: off)
                 const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;
-                plan_gather(Gg, dmma || K == 2, true, K == 2 ? qs : 0);
+                // k = 3 sub-blocks with 128-B rows: tensor-map boxes (bit 8: off); not for ops reading
+                // remote tiles (the maps cover this shard's payload only)
+                const bool tma = K == 3 && !Gg.cmask && !(dbgf & 256u) && Gg.M == 32 && tensor_map_encoder();
+                plan_gather(Gg, dmma || K == 2, true, K == 2 ? qs : 0, tma);
                 Gg.qstride = qs;
                 Gg.dbg = dbgf;
             }
+        }
+        CUtensorMap tin{}, tout{};
+        if (ws && Gg.tma && (!encode_tile_map(&tin, h->d, h->count) || !encode_tile_map(&tout, Gg.out, h->count))) {
+            const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;  // encoding failed: bulk rows / cp.async instead
+            plan_gather(Gg, true, true, 0, false);
+            Gg.qstride = qs;
+            Gg.dbg = dbgf;
         }
         if (ws) {
             // every unit including the diagonal ones: logical (R, C), R < C, of a diagonal unit is a
             // read-only staged copy of stored (C, R), never written back (no separate wedge launch)
             Gg.ws_diag = 1;
             Gg.nG_items = Gg.nU_loose << (2 * Gg.log_nsb_side);
-            const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2);
+            const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2) + (Gg.tma ? 1024 : 0);
             auto kw = gather_ws_kernel<K, NS, MODE == M_PROG ? M_PROG : M_DIRECT>;
             if constexpr ((K == 3 && MODE == M_DIRECT) || (K == 2 && MODE == M_DIRECT))
                 if (Gg.bulk)
                     kw = gather_ws_kernel<K, NS, M_DIRECT, true>;
+            if constexpr (K == 3 && MODE == M_DIRECT)
+                if (Gg.tma)
+                    kw = gather_ws_kernel<K, NS, M_DIRECT, true, true>;
             e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess)
                 return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
             const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
             if (grid) {
-                kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d);
+                kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d, tin, tout);
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 e = cudaGetLastError();
                 if (e != cudaSuccess)

@@ -50,7 +50,20 @@ struct DmmaFrag {
 // one 8 x 8 matrix M, transformed by I2 (x) L: (I2 (x) L) M (I2 (x) L)^dagger applies L . L^dagger to
 // every quadrant, so one tensor-core transform serves four k = 2 blocks (quadrant offsets
 // (R1 * PD + C1) * qstride, folded into the component offsets).
-template <int K, int NS, bool BULK = false>
+// TMA boxes (G.tma): component (sub-block x, y) of tile t sits in the 8 x 8 box (x >> 3, y >> 3) of
+// the tile, stored orientation, SWIZZLE_128B with phase phi (absolute smem address bits 7-9 of the
+// box base): element offset base + xs * 8 + (ys ^ ((xs + phi) & 7)), (xs, ys) the in-box position.
+// Packed per access: base (12 bits) | phi << 12 | in-box x << 15 | in-box y << 18, for a direct and
+// an adjoint (transposed) placement.
+__device__ __forceinline__ uint32_t tma_pack(const Geo& G, const Tabs& T, uint32_t t, uint32_t xo, uint32_t yo) {
+    const uint32_t nbx = G.S0 >> 3, slot = t * nbx * nbx + (xo >> 3) * nbx + (yo >> 3);
+    return T.cdir[slot] | ((uint32_t)T.tsk[slot] << 12) | ((xo & 7u) << 15) | ((yo & 7u) << 18);
+}
+__device__ __forceinline__ uint32_t tma_addr(uint32_t pk, uint32_t xb, uint32_t yb) {
+    const uint32_t xs = xb | ((pk >> 15) & 7u), ys = yb | ((pk >> 18) & 7u);
+    return (pk & 0xfffu) + xs * 8u + (ys ^ ((xs + (pk >> 12)) & 7u));
+}
+template <int K, int NS, bool BULK = false, bool TMAB = false>
 __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const Coef<NS>& cf) {
     DmmaFrag f;
     const uint32_t lane = threadIdx.x & 31, gq = lane >> 2, cq = lane & 3;
@@ -73,7 +86,14 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
             f.ost[j] = T.cdir[is];
             f.tld[j] = T.ttr[il];
             f.tst[j] = T.ttr[is];
-            if constexpr (BULK) {
+            if constexpr (TMAB) {  // component (row, col) offsets xs_in[row], y_in[col] (kin bits)
+                const uint32_t km = (1u << G.kin) - 1;
+                const uint32_t xl = T.xs_in[c8 & km], yl = T.y_in[gq & km], xs = T.xs_in[gq & km], ys = T.y_in[c8 & km];
+                f.old[j] = tma_pack(G, T, T.ttr[il], xl, yl);
+                f.oldA[j] = tma_pack(G, T, T.ttr[il], yl, xl);
+                f.ost[j] = tma_pack(G, T, T.ttr[is], xs, ys);
+                f.ostA[j] = tma_pack(G, T, T.ttr[is], ys, xs);
+            } else if constexpr (BULK) {
                 f.oldA[j] = T.cadj[il];
                 f.ostA[j] = T.cadj[is];
             }
@@ -92,7 +112,7 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
     }
     return f;
 }
-template <int NC, int K = 3, bool BULK = false>
+template <int NC, int K = 3, bool BULK = false, bool TMAB = false>
 __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
                                              double2* sb, uint32_t warp) {
     constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
@@ -111,7 +131,11 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
             const uint32_t bq = (q && two) ? b + NC / 32 : b;
             const uint32_t xbv = T.xb[(bq >> logNy) << sh], ybv = T.yb[(bq & ymask) << sh];
             base[q] = xbv * G.PD + ybv;
-            if constexpr (BULK) {  // adjoint tiles in stored orientation: row y, column x
+            if constexpr (TMAB) {  // swizzled boxes; base / baseA carry the block position
+                base[q] = (xbv << 8) | ybv;
+                v0[q] = sb[cld0 ? tma_addr(f.oldA[0], ybv, xbv) : tma_addr(f.old[0], xbv, ybv)];
+                v1[q] = sb[cld1 ? tma_addr(f.oldA[1], ybv, xbv) : tma_addr(f.old[1], xbv, ybv)];
+            } else if constexpr (BULK) {  // adjoint tiles in stored orientation: row y, column x
                 baseA[q] = ybv * G.PD + xbv;
                 v0[q] = sb[cld0 ? baseA[q] + f.oldA[0] : base[q] + f.old[0]];
                 v1[q] = sb[cld1 ? baseA[q] + f.oldA[1] : base[q] + f.old[1]];
@@ -162,7 +186,11 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         for (int q = 0; q < 2; ++q) {
             if (q && !two)
                 break;
-            if constexpr (BULK) {
+            if constexpr (TMAB) {
+                const uint32_t xbv = base[q] >> 8, ybv = base[q] & 0xffu;
+                sb[cst0 ? tma_addr(f.ostA[0], ybv, xbv) : tma_addr(f.ost[0], xbv, ybv)] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
+                sb[cst1 ? tma_addr(f.ostA[1], ybv, xbv) : tma_addr(f.ost[1], xbv, ybv)] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
+            } else if constexpr (BULK) {
                 sb[cst0 ? baseA[q] + f.ostA[0] : base[q] + f.ost[0]] = make_double2(zr0[q], flip_sign(zi0[q], cst0));
                 sb[cst1 ? baseA[q] + f.ostA[1] : base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
             } else {
@@ -372,14 +400,22 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
 // stage's `full` mbarrier) and written back by one bulk store per row -- no per-element copy
 // instructions.  Adjoint components are addressed through cadj (transposed offsets); the bank
 // groups are the same as in the logical layout since the pitch is 1 mod 8.
-template <int K, int NS, int MODE = M_DIRECT, bool BULK = false>
-__global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
+// TMAB (G.tma, with BULK): items of 8 x 8 sub-block boxes (g = 3, or g = 2 with its in-tile target
+// at bit 4: 128-B rows, too short for row copies) move as 2-D tensor-map copies (one 1 KiB box per
+// tile and box position), SWIZZLE_128B, each box at a 128-B phase of its own (host search) so the
+// DMMA lane patterns spread over the bank groups; same two-copy-group schedule as BULK.
+template <int K, int NS, int MODE = M_DIRECT, bool BULK = false, bool TMAB = false>
+__global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st,
+                                                           const __grid_constant__ CUtensorMap tin,
+                                                           const __grid_constant__ CUtensorMap tout) {
     // bulk rows need few copy instructions: 16 transform warps and 8 copy warps (else 8 and 16)
     constexpr uint32_t NCW = BULK ? 512 : 256, NMW = BULK ? 256 : 512, S = 3;
     // tile tables by item % TSL, built S items ahead (BULK: by two copy groups that may be one item
     // apart, hence two more slots)
     constexpr uint32_t TSL = BULK ? S + 3 : S + 1;
-    extern __shared__ __align__(128) double2 ring[];
+    extern __shared__ __align__(128) double2 ring_raw[];
+    // TMA boxes: stage bases 1 KiB aligned (the swizzle phase follows absolute address bits 7-9)
+    double2* const ring = TMAB ? ring_raw + ((1024u - (smem_u32(ring_raw) & 1023u)) & 1023u) / 16u : ring_raw;
     __shared__ uint64_t gt[TSL][64];
     __shared__ uint64_t am[TSL][1];
     __shared__ uint32_t mir[TSL];     // BULK: the item has mirrored tiles (diagonal unit, a > b)
@@ -414,14 +450,14 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         // ---- transform warps
         DmmaFrag fr;
         if constexpr (MODE == M_DIRECT)
-            fr = dmma_frag<K, NS, BULK>(G, T, cf);
+            fr = dmma_frag<K, NS, BULK, TMAB>(G, T, cf);
         for (uint64_t i = 0; i < nlocal; ++i) {
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
             double2* sb = ring + (size_t)s * G.stage_elems;
             if constexpr (MODE == M_DIRECT) {
                 if (!(G.dbg & 1u))
-                    dmma_direct3<NCW, K, BULK>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
+                    dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
             } else {
                 for (uint32_t p = 0; p < cf.nsteps; ++p) {
                     grid_prog_step<NCW>(G, T, cf, p, am[i % TSL][0], sb, tid);
@@ -543,6 +579,8 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         // runs: item = NT tiles x S0 rows x rps runs of 2^logRun elements (contiguous in-tile columns)
         const uint32_t lrr = G.logS0 - G.logRun, rps = 1u << lrr, lrt = G.logS0 + lrr;
         const uint32_t nruns = NT << lrt, rbytes = 16u << G.logRun;
+        // TMA boxes: nbx x nbx boxes of 8 x 8 per tile (slot t * bpt + bx * nbx + by: base T.cdir, phase T.tsk)
+        const uint32_t nbx = G.S0 >> 3, lnbx = G.logS0 - 3, lbpt = 2 * lnbx, bpt = 1u << lbpt;
         // in-tile offset of run c (sub-block column c) of sub-block row r: stored row x0|xdep[r]
         // (direct) or y0|xdep[r] (adjoint, stored orientation)
         auto run_off = [&](bool adj, uint32_t x0, uint32_t y0, uint32_t r, uint32_t c) -> uint64_t {
@@ -559,14 +597,28 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint32_t base = smem_u32(ring) + s * G.stage_elems * 16u;
             uint32_t x0, y0;
             rows_of(j, x0, y0);
-            for (uint32_t q = gtid; !(G.dbg & 2u) && q < nruns; q += NGT) {
-                const uint32_t t = q >> lrt, r = (q >> lrr) & (G.S0 - 1), c = (q & (rps - 1)) << G.logRun;
-                const uint64_t ent = gt[ts][t];
-                if (!(ent & F_SKIP)) {
-                    const bool adj = (ent & F_ADJ) != 0;
-                    const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
-                    mbar_expect(&full[s], rbytes);
-                    bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD + c) * 16u, tile_base(G, ent, st) + g, rbytes, &full[s]);
+            if constexpr (TMAB) {
+                for (uint32_t q = gtid; !(G.dbg & 2u) && q < (NT << lbpt); q += NGT) {
+                    const uint32_t t = q >> lbpt, bx = (q & (bpt - 1)) >> lnbx, by = q & (nbx - 1);
+                    const uint64_t ent = gt[ts][t];
+                    if (!(ent & F_SKIP)) {
+                        const bool adj = (ent & F_ADJ) != 0;
+                        const uint32_t r0 = (adj ? y0 : x0) | T.xdep[8 * bx], c0 = (adj ? x0 : y0) | T.xdep[8 * by];
+                        mbar_expect(&full[s], 1024u);
+                        tma_load_2d(base + T.cdir[q] * 16u, &tin, 2 * c0, (uint32_t)((ent & F_MASK) << G.logM) + r0, &full[s]);
+                    }
+                }
+            } else {
+                for (uint32_t q = gtid; !(G.dbg & 2u) && q < nruns; q += NGT) {
+                    const uint32_t t = q >> lrt, r = (q >> lrr) & (G.S0 - 1), c = (q & (rps - 1)) << G.logRun;
+                    const uint64_t ent = gt[ts][t];
+                    if (!(ent & F_SKIP)) {
+                        const bool adj = (ent & F_ADJ) != 0;
+                        const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
+                        mbar_expect(&full[s], rbytes);
+                        bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD + c) * 16u, tile_base(G, ent, st) + g, rbytes,
+                                 &full[s]);
+                    }
                 }
             }
             mbar_arrive(&full[s]);
@@ -589,14 +641,27 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             if (!(G.dbg & 4u)) {
                 uint32_t x0, y0;
                 rows_of(i, x0, y0);
-                for (uint32_t q = gtid; q < nruns; q += NGT) {
-                    const uint32_t t = q >> lrt, r = (q >> lrr) & (G.S0 - 1), c = (q & (rps - 1)) << G.logRun;
-                    const uint64_t ent = gt[ts][t];
-                    if (!(ent & F_NOSTORE)) {
-                        const bool adj = (ent & F_ADJ) != 0;
-                        const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
-                        bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD + c), rbytes);
-                        bulk_commit();
+                if constexpr (TMAB) {
+                    for (uint32_t q = gtid; q < (NT << lbpt); q += NGT) {
+                        const uint32_t t = q >> lbpt, bx = (q & (bpt - 1)) >> lnbx, by = q & (nbx - 1);
+                        const uint64_t ent = gt[ts][t];
+                        if (!(ent & F_NOSTORE)) {
+                            const bool adj = (ent & F_ADJ) != 0;
+                            const uint32_t r0 = (adj ? y0 : x0) | T.xdep[8 * bx], c0 = (adj ? x0 : y0) | T.xdep[8 * by];
+                            tma_store_2d(&tout, 2 * c0, (uint32_t)((ent & F_MASK) << G.logM) + r0, smem_u32(sb + T.cdir[q]));
+                            bulk_commit();
+                        }
+                    }
+                } else {
+                    for (uint32_t q = gtid; q < nruns; q += NGT) {
+                        const uint32_t t = q >> lrt, r = (q >> lrr) & (G.S0 - 1), c = (q & (rps - 1)) << G.logRun;
+                        const uint64_t ent = gt[ts][t];
+                        if (!(ent & F_NOSTORE)) {
+                            const bool adj = (ent & F_ADJ) != 0;
+                            const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
+                            bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD + c), rbytes);
+                            bulk_commit();
+                        }
                     }
                 }
                 if (mir[ts]) {  // diagonal unit, a > b: the R == C tiles also at the mirrored position
@@ -604,7 +669,14 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                         const uint32_t tt = p >> logT, rr = p & (T2 - 1), i0 = rr >> G.logS0, j0 = rr & (G.S0 - 1);
                         const uint64_t ent = gt[ts][tt];
                         if (ent & F_MIRROR) {  // stored (y0|i0, x0|j0) = conj(logical (x0|j0, y0|i0))
-                            const double2 w = sb[tt * G.TS + T.tsk[tt] + j0 * P + i0];
+                            uint32_t a;
+                            if constexpr (TMAB) {
+                                const uint32_t sl = (tt << lbpt) + (j0 >> 3) * nbx + (i0 >> 3);
+                                a = T.cdir[sl] + (j0 & 7u) * 8u + ((i0 & 7u) ^ (((j0 & 7u) + T.tsk[sl]) & 7u));
+                            } else {
+                                a = tt * G.TS + T.tsk[tt] + j0 * P + i0;
+                            }
+                            const double2 w = sb[a];
                             G.out[((ent & F_MASK) << (2 * G.logM)) + ((uint64_t)(y0 | T.xdep[i0]) << G.logM) +
                                   (x0 | T.xdep[j0])] = make_double2(w.x, -w.y);
                         }

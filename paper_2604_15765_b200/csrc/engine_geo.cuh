@@ -96,6 +96,8 @@ struct Geo {
     uint32_t bulk;                // gather_ws: sub-block rows move as cp.async.bulk runs (>= 8 contiguous
                                   // elements), every tile staged in its STORED orientation (cadj: adjoint offsets)
     uint32_t logRun;              // bulk: log2 of the run length (contiguous low in-tile bits of the sub-block)
+    uint32_t tma;                 // gather_ws (with bulk groups): 8 x 8 boxes by tensor map, SWIZZLE_128B;
+                                  // cdir[slot] = box base (16-B units, phase included), tsk[slot] = phase
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
