@@ -580,9 +580,11 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
     const uint32_t nbx = S0 >> 3, bpt = nbx * nbx;
     // (preferred to bulk rows where both apply: 64 box copies per item instead of 256 row copies,
     // C3 g = 2 ops 13.5-14.5 ms with rows vs 12.0-12.8 ms with boxes)
-    if (tma && dmma && D == 8 && M == 32 && G.logRun >= 3 && (S0 == 8 || S0 == 16) &&
-        ((S0 - 1) & ~xs_tmask) < 8 && (xs_tmask & 7u) == 0 && NT * bpt <= 64) {
+    G.tq = 1;
+    if (tma && dmma && D == 8 && M == 32 && G.logRun >= 3 && (S0 == 8 || S0 == 16) && NT * bpt <= 64 &&
+        (!(((S0 - 1) & ~xs_tmask) & 8u) || (G.nxb == 8 && G.nyb == 8))) {
         G.bulk = 0;
+        G.tq = (((S0 - 1) & ~xs_tmask) & 8u) ? 4 : 1;  // bit 3 free: it selects the box per block
         // 8 x 8 boxes through the tensor map (SWIZZLE_128B): slot = (tile, box) with a swizzle phase
         // phi (16-B chunk c of box row x lands at c ^ ((x + phi) & 7)).  The DMMA patterns touch the
         // in-box positions of (block base | component offset) in direct or transposed placement;

@@ -88,7 +88,11 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
             f.tst[j] = T.ttr[is];
             if constexpr (TMAB) {  // component (row, col) offsets xs_in[row], y_in[col] (kin bits)
                 const uint32_t km = (1u << G.kin) - 1;
-                const uint32_t xl = T.xs_in[c8 & km], yl = T.y_in[gq & km], xs = T.xs_in[gq & km], ys = T.y_in[c8 & km];
+                // G.tq == 4: this warp's quadrant supplies bit 3 of the block row / column
+                const uint32_t qx = G.tq == 4 ? (((threadIdx.x >> 5) & 3u) >> 1) << 3 : 0u;
+                const uint32_t qy = G.tq == 4 ? ((threadIdx.x >> 5) & 1u) << 3 : 0u;
+                const uint32_t xl = T.xs_in[c8 & km] | qx, yl = T.y_in[gq & km] | qy;
+                const uint32_t xs = T.xs_in[gq & km] | qx, ys = T.y_in[c8 & km] | qy;
                 f.old[j] = tma_pack(G, T, T.ttr[il], xl, yl);
                 f.oldA[j] = tma_pack(G, T, T.ttr[il], yl, xl);
                 f.ost[j] = tma_pack(G, T, T.ttr[is], xs, ys);
@@ -122,16 +126,17 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
     // two blocks per pass: independent accumulator chains keep the FP64 tensor pipe fed (small
     // tiles, m < 5, have fewer blocks than warps: the second block of a pass may be absent and is
     // then computed on a copy of the first and not stored)
-    for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32)) {
+    auto pass = [&](uint32_t b0, uint32_t b1, bool two) {
         uint32_t base[2], baseA[2];
         double2 v0[2], v1[2];
-        const bool two = b + NC / 32 < nblk;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-            const uint32_t bq = (q && two) ? b + NC / 32 : b;
-            const uint32_t xbv = T.xb[(bq >> logNy) << sh], ybv = T.yb[(bq & ymask) << sh];
+            const uint32_t bq = (q && two) ? b1 : b0;
+            uint32_t xbv = T.xb[(bq >> logNy) << sh], ybv = T.yb[(bq & ymask) << sh];
             base[q] = xbv * G.PD + ybv;
-            if constexpr (TMAB) {  // swizzled boxes; base / baseA carry the block position
+            if constexpr (TMAB) {  // swizzled boxes; base carries the in-box block position (the box
+                xbv &= 7u;         // row / column of a quadrant, G.tq == 4, is in the fragment constants)
+                ybv &= 7u;
                 base[q] = (xbv << 8) | ybv;
                 v0[q] = sb[cld0 ? tma_addr(f.oldA[0], ybv, xbv) : tma_addr(f.old[0], xbv, ybv)];
                 v1[q] = sb[cld1 ? tma_addr(f.oldA[1], ybv, xbv) : tma_addr(f.old[1], xbv, ybv)];
@@ -198,7 +203,22 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
                 sb[base[q] + f.ost[1]] = make_double2(zr1[q], flip_sign(zi1[q], cst1));
             }
         }
+    };
+    if (TMAB && G.tq == 4) {
+        // boxes selected by bit 3 of the block position: each warp keeps one quadrant (bit 3 of the
+        // block row and column: block index bits 2 and 5 of 8 x 8 blocks), 16 blocks, NW / 4 warps
+        constexpr uint32_t NWQ = NC / 32 / 4;
+        const uint32_t qd = warp & 3u, wi = warp >> 2;
+        for (uint32_t jb = wi; jb < 16; jb += 2 * NWQ) {
+            const uint32_t j1 = jb + NWQ;
+            const uint32_t b0 = ((((qd >> 1) << 2) | (jb >> 2)) << 3) | ((qd & 1u) << 2) | (jb & 3u);
+            const uint32_t b1 = ((((qd >> 1) << 2) | (j1 >> 2)) << 3) | ((qd & 1u) << 2) | (j1 & 3u);
+            pass(b0, b1, j1 < 16);
+        }
+        return;
     }
+    for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32))
+        pass(b, b + NC / 32, b + NC / 32 < nblk);
 }
 
 __device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group

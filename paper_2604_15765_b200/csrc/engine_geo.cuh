@@ -98,6 +98,7 @@ struct Geo {
     uint32_t logRun;              // bulk: log2 of the run length (contiguous low in-tile bits of the sub-block)
     uint32_t tma;                 // gather_ws (with bulk groups): 8 x 8 boxes by tensor map, SWIZZLE_128B;
                                   // cdir[slot] = box base (16-B units, phase included), tsk[slot] = phase
+    uint32_t tq;                  // tma: 4 when bit 3 of the sub-block is a block-position bit (quadrant per warp)
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
