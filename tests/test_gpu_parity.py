@@ -108,6 +108,40 @@ def test_library_parity(H, HS, oracle, orc, n, m):
     st.free()
 
 
+# Staging modes of the gather kernel for the FP64 tensor-core transforms (engine.cu plan_gather),
+# each hit deterministically at n = 10, m = 5 (units include the diagonal base pairs):
+#   k = 3 on one grid bit          -> bulk rows (whole 32 x 32 tiles)
+#   k = 3 on two grid bits, in-tile target below bit 3 -> TMA boxes, one quadrant per warp
+#   k = 3 on two grid bits, in-tile target at bit 3 / 4 -> TMA boxes, box in the lane constants
+#   k = 3 on three grid bits       -> TMA boxes (one per tile)
+#   k = 2 on two grid bits         -> bulk rows of 256 B (I2 (x) L pairing)
+STAGING_CASES = [
+    (3, (0, 2, 6)), (3, (6, 4, 1)), (3, (1, 6, 8)), (3, (9, 2, 5)), (3, (0, 7, 9)), (3, (3, 6, 8)),
+    (3, (8, 4, 6)), (3, (5, 6, 8)), (3, (9, 7, 5)), (3, (6, 9, 8)), (2, (6, 8)), (2, (9, 5)),
+]
+
+
+@pytest.mark.parametrize("dual", [False, True])
+def test_gather_staging_modes(H, HS, oracle, orc, dual):
+    n, m = 10, 5
+    psi = HS.rank_psi(n, 91, 4)
+    base = HS.rho_payload(n, psi, m)
+    fro = orc.frobenius(base, n, m)
+    st = H.TiledHermitian(n, m)
+    for i, (k, tg) in enumerate(STAGING_CASES):
+        u = _haar(HS, k, 300 + i)
+        spec, och = H.make_generic("u", u), oracle.generic(u)
+        if dual:
+            spec, och = H.dual_channel(spec), oracle.dual(och)
+        want = base.copy()
+        orc.apply(want, n, m, och, list(tg))
+        st.upload(base)
+        H.apply(st, spec, list(tg))
+        err = oracle.rel_max_err(st.download(), want, fro)
+        assert err <= TOL, f"k={k} {tg} dual={dual}: err {err}"
+    st.free()
+
+
 def test_generic_path_without_native(H, HS, oracle, orc):
     """allow_native = false routes native gates through the generic engines (kernels.cpp:515)."""
     n, m = 8, 5
