@@ -456,7 +456,8 @@ bool encode_tile_map(CUtensorMap* tm, const void* base, uint64_t elems) {
 
 // bulk: stage sub-block rows with cp.async.bulk, one copy per run of >= 8 contiguous elements
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
-void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false) {
+void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false,
+                 bool prog = false) {
     const uint32_t M = G.M, g = G.g, NT = 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -581,7 +582,17 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
     // (preferred to bulk rows where both apply: 64 box copies per item instead of 256 row copies,
     // C3 g = 2 ops 13.5-14.5 ms with rows vs 12.0-12.8 ms with boxes)
     G.tq = 1;
-    if (tma && dmma && D == 8 && M == 32 && G.logRun >= 3 && (S0 == 8 || S0 == 16) && NT * bpt <= 64 &&
+    if (tma && prog && M == 32 && G.logRun >= 3 && S0 >= 8 && NT * bpt <= 64) {
+        // grid programs: consecutive threads take consecutive positions of one logical tile, so
+        // any phase is conflict-free in both placements (the in-box chunk y ^ x, resp. x ^ y, is a
+        // bijection along the row): phase 0, boxes packed
+        G.tma = 1;
+        G.bulk = 0;
+        for (uint32_t q = 0; q < NT * bpt; ++q) {
+            G.cdir[q] = (uint16_t)(q * 64);
+            G.tsk[q] = 0;
+        }
+    } else if (tma && dmma && D == 8 && M == 32 && G.logRun >= 3 && (S0 == 8 || S0 == 16) && NT * bpt <= 64 &&
         (!(((S0 - 1) & ~xs_tmask) & 8u) || (G.nxb == 8 && G.nyb == 8))) {
         G.bulk = 0;
         G.tq = (((S0 - 1) & ~xs_tmask) & 8u) ? 4 : 1;  // bit 3 free: it selects the box per block
@@ -755,6 +766,17 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             static const char* dbg = getenv("HS_DEBUG_FLAGS");
             Gg.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
         }
+        // tensor maps of this shard's payload for the TMA-box staging (bit 8: off); not for ops that
+        // read remote tiles (the maps cover the local payload only)
+        CUtensorMap tin{}, tout{};
+        const bool maps = K == 3 && (MODE == M_DIRECT || MODE == M_PROG) && !Gg.cmask && !(Gg.dbg & 256u) &&
+                          Gg.M == 32 && encode_tile_map(&tin, h->d, h->count) &&
+                          encode_tile_map(&tout, Gg.out, h->count);
+        if (MODE == M_PROG && maps && !(Gg.dbg & 64u)) {
+            const uint32_t dbgf = Gg.dbg;
+            plan_gather(Gg, false, false, 0, true, true);
+            Gg.dbg = dbgf;
+        }
         // the warp-specialised kernel runs grid programs and the tensor-core transforms (bit 5: the
         // ping-pong kernel instead); k = 2 pairs blocks two by two in each direction, the quadrant
         // blocks (2X + R1, 2Y + C1) sitting at a constant offset qstride
@@ -773,18 +795,10 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
                 const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;
                 // k = 3 sub-blocks with 128-B rows: tensor-map boxes (bit 8: off); not for ops reading
                 // remote tiles (the maps cover this shard's payload only)
-                const bool tma = K == 3 && !Gg.cmask && !(dbgf & 256u) && Gg.M == 32 && tensor_map_encoder();
-                plan_gather(Gg, dmma || K == 2, true, K == 2 ? qs : 0, tma);
+                plan_gather(Gg, dmma || K == 2, true, K == 2 ? qs : 0, maps);
                 Gg.qstride = qs;
                 Gg.dbg = dbgf;
             }
-        }
-        CUtensorMap tin{}, tout{};
-        if (ws && Gg.tma && (!encode_tile_map(&tin, h->d, h->count) || !encode_tile_map(&tout, Gg.out, h->count))) {
-            const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;  // encoding failed: bulk rows / cp.async instead
-            plan_gather(Gg, true, true, 0, false);
-            Gg.qstride = qs;
-            Gg.dbg = dbgf;
         }
         if (ws) {
             // every unit including the diagonal ones: logical (R, C), R < C, of a diagonal unit is a
@@ -796,6 +810,9 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             if constexpr ((K == 3 && MODE == M_DIRECT) || (K == 2 && MODE == M_DIRECT))
                 if (Gg.bulk)
                     kw = gather_ws_kernel<K, NS, M_DIRECT, true>;
+            if constexpr (K == 3 && MODE == M_PROG)
+                if (Gg.tma)
+                    kw = gather_ws_kernel<K, NS, M_PROG, true, true>;
             if constexpr (K == 3 && MODE == M_DIRECT)
                 if (Gg.tma)
                     kw = gather_ws_kernel<K, NS, M_DIRECT, true, true>;

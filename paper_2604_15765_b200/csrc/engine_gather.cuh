@@ -380,9 +380,15 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
 // One k = 1 step of a grid program on the staged logical tiles (MODE == M_PROG in gather_ws_kernel):
 // quads of logical tiles (R, C), (R, C | e), (R | e, C), (R | e, C | e) at every staged position,
 // e = 2^l for the step's grid bit l; adjoint tiles are staged transposed and conjugated on the fly.
-template <uint32_t NCW, int NS>
+template <uint32_t NCW, int NS, bool TMAB = false>
 __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, const Coef<NS>& cf, uint32_t p,
                                                uint64_t am, double2* sb, uint32_t tid) {
+    // TMA boxes: tiles in stored orientation (adjoint ones transposed), 8 x 8 boxes, phase T.tsk[slot]
+    const uint32_t nbx = G.S0 >> 3, lbpt = 2 * (G.logS0 - 3);
+    auto tma_at = [&](uint32_t t, uint32_t i, uint32_t j, uint32_t f) -> uint32_t {
+        const uint32_t x = f ? j : i, y = f ? i : j, sl = (t << lbpt) + (x >> 3) * nbx + (y >> 3);
+        return T.cdir[sl] + (x & 7u) * 8u + ((y & 7u) ^ ((x + T.tsk[sl]) & 7u));
+    };
     const uint32_t g = G.g, NG = 1u << g, e = 1u << cf.pbit[p], lo = e - 1;
     const uint32_t S0 = G.S0, P = S0 + 1, npos = S0 * S0, lp = 2 * G.logS0;
     const uint32_t nq = (NG / 2) * (NG / 2) * npos;
@@ -393,11 +399,21 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
         const uint32_t rr = tq >> (g - 1), cc = tq & ((NG >> 1) - 1);
         const uint32_t R0 = ((rr & ~lo) << 1) | (rr & lo), C0 = ((cc & ~lo) << 1) | (cc & lo);
         const uint32_t t0 = R0 * NG + C0, t1 = R0 * NG + (C0 | e), t2 = (R0 | e) * NG + C0, t3 = t2 + e;
-        const uint32_t off = i * P + j;
-        const uint32_t a0 = t0 * G.TS + T.tsk[t0] + off, a1 = t1 * G.TS + T.tsk[t1] + off;
-        const uint32_t a2 = t2 * G.TS + T.tsk[t2] + off, a3 = t3 * G.TS + T.tsk[t3] + off;
         const uint32_t f0 = (uint32_t)((am >> t0) & 1ull) << 31, f1 = (uint32_t)((am >> t1) & 1ull) << 31;
         const uint32_t f2 = (uint32_t)((am >> t2) & 1ull) << 31, f3 = (uint32_t)((am >> t3) & 1ull) << 31;
+        uint32_t a0, a1, a2, a3;
+        if constexpr (TMAB) {
+            a0 = tma_at(t0, i, j, f0);
+            a1 = tma_at(t1, i, j, f1);
+            a2 = tma_at(t2, i, j, f2);
+            a3 = tma_at(t3, i, j, f3);
+        } else {
+            const uint32_t off = i * P + j;
+            a0 = t0 * G.TS + T.tsk[t0] + off;
+            a1 = t1 * G.TS + T.tsk[t1] + off;
+            a2 = t2 * G.TS + T.tsk[t2] + off;
+            a3 = t3 * G.TS + T.tsk[t3] + off;
+        }
         double2 v0 = sb[a0], v1 = sb[a1], v2 = sb[a2], v3 = sb[a3];
         v0.y = flip_sign(v0.y, f0);
         v1.y = flip_sign(v1.y, f1);
@@ -480,7 +496,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                     dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
             } else {
                 for (uint32_t p = 0; p < cf.nsteps; ++p) {
-                    grid_prog_step<NCW>(G, T, cf, p, am[i % TSL][0], sb, tid);
+                    grid_prog_step<NCW, NS, TMAB>(G, T, cf, p, am[i % TSL][0], sb, tid);
                     asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
                 }
             }
