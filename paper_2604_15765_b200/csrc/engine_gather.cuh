@@ -40,7 +40,7 @@ __device__ __forceinline__ double flip_sign(double x, uint32_t m) {
 // per-lane constant fragments of the transform (loaded once per kernel: the lane-dependent
 // coefficient index would serialise the constant-cache reads if repeated per item)
 struct DmmaFrag {
-    double lr[2], li[2], nli[2];
+    double lr[2], li[2];
     double ls[2], ld[2];      // Lr + Li (stage 1, 3M) and Pr + Pi = Lr - Li (stage 2, 3M)
     uint32_t old[2], ost[2];  // staging offsets of the loaded / stored components (from the block base)
     uint32_t tld[2], tst[2];  // their logical tiles (adjoint mask bits)
@@ -77,7 +77,6 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
             l = (gq >> 2) == (c8 >> 2) ? cf.s[(gq & 3) * 4 + (c8 & 3)] : make_double2(0.0, 0.0);
         f.lr[j] = l.x;
         f.li[j] = l.y;
-        f.nli[j] = -l.y;
         f.ls[j] = l.x + l.y;
         f.ld[j] = l.x - l.y;
         if constexpr (K == 3) {
@@ -170,22 +169,23 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
             yi1[q] = t3b - t1b - t2b;
         }
         // stage 2: Z = Y P, P = L^dagger (B fragment of chunk j: P[2c + j][g] = conj(L[g][2c + j]));
-        // U1 = Yr Pr, U2 = Yi Pi, U3 = (Yr + Yi)(Pr + Pi); Zr = U1 - U2, Zi = U3 - U1 - U2
+        // U1 = Yr Pr, U2 = Yi Pi, U3 = (Yr + Yi)(Pr + Pi); Zr = U1 - U2, Zi = U3 - U1 - U2.  With
+        // Pi = -Li^T the code accumulates V2 = Yi Li^T = -U2: Zr = U1 + V2, Zi = U3 - U1 + V2
         double zr0[2], zr1[2], zi0[2], zi1[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
             const double s0 = yr0[q] + yi0[q], s1 = yr1[q] + yi1[q];
             dmma_acc(u1a, u1b, yr0[q], f.lr[0]);
-            dmma_acc(u2a, u2b, yi0[q], f.nli[0]);
+            dmma_acc(u2a, u2b, yi0[q], f.li[0]);
             dmma_acc(u3a, u3b, s0, f.ld[0]);
             dmma_acc(u1a, u1b, yr1[q], f.lr[1]);
-            dmma_acc(u2a, u2b, yi1[q], f.nli[1]);
+            dmma_acc(u2a, u2b, yi1[q], f.li[1]);
             dmma_acc(u3a, u3b, s1, f.ld[1]);
-            zr0[q] = u1a - u2a;
-            zr1[q] = u1b - u2b;
-            zi0[q] = u3a - u1a - u2a;
-            zi1[q] = u3b - u1b - u2b;
+            zr0[q] = u1a + u2a;
+            zr1[q] = u1b + u2b;
+            zi0[q] = u3a - u1a + u2a;
+            zi1[q] = u3b - u1b + u2b;
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
