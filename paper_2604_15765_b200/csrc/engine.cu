@@ -754,7 +754,10 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
         }
         return HS_OK;
     }
-    if (MODE != M_KRAUS && ((G.g >= 2 && G.slabs > 1) || (K == 3 && MODE == M_DIRECT && G.g == 1))) {
+    // k = 2 unitaries on one grid bit: the tensor-core gather (bulk rows, two copy groups) when the
+    // I2 (x) L pairing applies (0.83 -> 0.70 ms at n = 14), else the whole-tile pipeline below
+    if (MODE != M_KRAUS && ((G.g >= 2 && G.slabs > 1) || (K == 3 && MODE == M_DIRECT && G.g == 1) ||
+                            (K == 2 && MODE == M_DIRECT && G.g == 1))) {
         // units of 16 / 64 stored tiles (and k = 3 unitaries on one grid bit, whose 4-tile units
         // are whole gather items for the FP64 tensor transform): sub-block gather kernel for the
         // off-diagonal units, the slab kernel's wedge path for the diagonal ones
@@ -829,6 +832,8 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             }
             return HS_OK;
         }
+        if (K == 2 && G.g == 1)
+            goto pipe_path;  // no pairing (or the ping-pong debug switch): whole-tile pipeline
         if (G.nD_items) {  // diagonal units: the slab kernel's wedge path
             Geo Gs = G;
             Gs.nU_items = 0;
@@ -860,6 +865,7 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
         }
         return HS_OK;
     }
+pipe_path:
     const bool pipe = MODE != M_KRAUS && G.stages >= 3 && (G.nU_items > 0 || G.nD_items > 0);
     if (pipe && G.g >= 1 && G.slabs == 1) {
         // whole-unit items: the pipeline handles the diagonal base pairs as well
