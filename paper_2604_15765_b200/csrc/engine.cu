@@ -1564,9 +1564,10 @@ int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* t, hs_
                             make_double2(x.x * y.x + x.y * y.y, x.x * y.y - x.y * y.x);
                     }
         rc = launch<1, M_S1, 16>(h, G, cf, ka, 1);
-    } else if (k == 2 && G.g == 0 && h->m == 5 && (int)h->n - (int)h->m > (int)h->Plog) {
-        // both targets in-tile: run I2 (x) L on (t0, t1, m) -- the lowest grid qubit m, never a shard
-        // bit here, as the most significant local bit -- through the k = 3 tensor-core gather (bulk
+    } else if (k == 2 && G.g == 0 && h->m == 5 && h->n >= h->m + 4) {
+        // both targets in-tile: run I2 (x) L on (t0, t1, m) -- the lowest grid qubit m as the most
+        // significant local bit; never one of the top three qubits, so never a shard bit for up to
+        // 8 shards and the same choice sharded or not -- through the k = 3 tensor-core gather (bulk
         // rows): identical result up to rounding, 0.96 -> ~0.70 ms at n = 14 instead of the
         // scalar two-stage transform of the whole-tile pipeline
         uint32_t t3[3] = {t[0], t[1], (uint32_t)h->m};
@@ -1576,6 +1577,19 @@ int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* t, hs_
         for (int a = 0; a < 8; ++a)
             for (int b = 0; b < 8; ++b)
                 cf.s[a * 8 + b] = (a >> 2) == (b >> 2) ? U[(a & 3) * 4 + (b & 3)] : make_double2(0.0, 0.0);
+        rc = launch<3, M_DIRECT, 64>(h, G3, cf, ka, 1);
+    } else if (k == 2 && G.g == 2 && h->m == 5) {
+        // both targets on grid bits: L (x) I2 on (m - 1, t0, t1) -- the in-tile qubit 4 as the least
+        // significant local bit -- through the k = 3 gather's TMA boxes (5.4 TB/s) instead of the
+        // k = 2 pairing on bulk rows (4.9 TB/s); the extra target is in-tile, so the shards an op
+        // reads are those of its own targets
+        uint32_t t3[3] = {(uint32_t)h->m - 1, t[0], t[1]};
+        Geo G3;
+        plan_geo(h, 3, t3, G3, 1);
+        Coef<64> cf{};
+        for (int a = 0; a < 8; ++a)
+            for (int b = 0; b < 8; ++b)
+                cf.s[a * 8 + b] = (a & 1) == (b & 1) ? U[(a >> 1) * 4 + (b >> 1)] : make_double2(0.0, 0.0);
         rc = launch<3, M_DIRECT, 64>(h, G3, cf, ka, 1);
     } else if (k == 2) {
         Coef<64> cf{};
