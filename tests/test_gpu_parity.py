@@ -114,8 +114,10 @@ def test_library_parity(H, HS, oracle, orc, n, m):
 #   k = 3 on two grid bits, in-tile target below bit 3 -> TMA boxes, one quadrant per warp
 #   k = 3 on two grid bits, in-tile target at bit 3 / 4 -> TMA boxes, box in the lane constants
 #   k = 3 on three grid bits       -> TMA boxes (one per tile)
-#   k = 2 on two grid bits         -> bulk rows of 256 B (I2 (x) L pairing)
+#   k = 3 on in-tile bits only     -> whole-tile pipeline (scalar two-stage transform)
+#   k = 2 on one / two grid bits, or in-tile -> the k = 2 pairing, or promoted to k = 3 (I2 (x) L)
 STAGING_CASES = [
+    (3, (0, 2, 4)), (3, (4, 1, 3)), (2, (1, 3)), (2, (3, 7)),
     (3, (0, 2, 6)), (3, (6, 4, 1)), (3, (1, 6, 8)), (3, (9, 2, 5)), (3, (0, 7, 9)), (3, (3, 6, 8)),
     (3, (8, 4, 6)), (3, (5, 6, 8)), (3, (9, 7, 5)), (3, (6, 9, 8)), (2, (6, 8)), (2, (9, 5)),
 ]
