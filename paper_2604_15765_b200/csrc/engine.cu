@@ -39,6 +39,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
+#include <mutex>
+#include <unordered_map>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -454,6 +457,30 @@ bool encode_tile_map(CUtensorMap* tm, const void* base, uint64_t elems) {
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Bank-spreading searches of plan_gather (skews / swizzle phases) depend only on the shape of an
+// operation (in-tile targets, number of grid targets, sub-block), not on its grid qubits or the
+// state: their results are cached per shape (a search costs up to a few ms of host time, more than
+// a small state's kernel).
+std::mutex g_search_mu;
+std::unordered_map<uint64_t, std::array<uint8_t, 65>> g_search_cache;
+uint64_t search_key(const Geo& G, uint32_t kind, uint32_t qstride) {
+    return (uint64_t)G.in_mask | (uint64_t)G.g << 8 | (uint64_t)G.S0 << 12 | (uint64_t)G.D << 20 |
+           (uint64_t)G.kin << 26 | (uint64_t)qstride << 30 | (uint64_t)G.M << 36 | (uint64_t)G.nxb << 44 |
+           (uint64_t)G.nyb << 51 | (uint64_t)kind << 58;
+}
+bool search_get(uint64_t key, std::array<uint8_t, 65>& out) {
+    std::lock_guard<std::mutex> lk(g_search_mu);
+    auto it = g_search_cache.find(key);
+    if (it == g_search_cache.end())
+        return false;
+    out = it->second;
+    return true;
+}
+void search_put(uint64_t key, const std::array<uint8_t, 65>& v) {
+    std::lock_guard<std::mutex> lk(g_search_mu);
+    g_search_cache[key] = v;
+}
+
 // bulk: stage sub-block rows with cp.async.bulk, one copy per run of >= 8 contiguous elements
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
 void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false,
@@ -538,8 +565,11 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
             return cost;
         };
         const uint32_t TS0 = G.TS;
+        const uint64_t key = search_key(G, 1, qstride);
+        std::array<uint8_t, 65> cached;
+        const bool hit = search_get(key, cached);
         uint32_t best = ~0u, bestE = 0, bestS = 0;
-        for (uint32_t e = 0; e < 8; ++e)
+        for (uint32_t e = 0; e < 8 && !hit; ++e)
             for (uint32_t sk = 0; sk < 8; ++sk) {
                 G.TS = TS0 + e;
                 for (uint32_t t = 0; t < NT; ++t)
@@ -558,7 +588,13 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
         tables();
         // then per-tile skews by coordinate descent (a linear skew in the tile row cannot spread
         // four tile rows x two columns of stride 2 over 8 groups)
-        uint32_t cur = cost_of();
+        if (hit) {
+            G.TS = TS0 + cached[64];
+            for (uint32_t t = 0; t < NT; ++t)
+                G.tsk[t] = cached[t];
+            tables();
+        }
+        uint32_t cur = hit ? 0u : cost_of();
         for (uint32_t pass = 0; pass < 3 && cur > 16; ++pass)
             for (uint32_t t = 0; t < NT; ++t) {
                 const uint8_t keep = G.tsk[t];
@@ -575,6 +611,13 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
                 G.tsk[t] = bv;
                 tables();
             }
+        if (!hit) {
+            std::array<uint8_t, 65> v{};
+            for (uint32_t t = 0; t < NT; ++t)
+                v[t] = G.tsk[t];
+            v[64] = (uint8_t)(G.TS - TS0);
+            search_put(key, v);
+        }
         extra = 7;
     }
     G.tma = 0;
@@ -631,7 +674,13 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
                             }
             return cost;
         };
-        uint32_t cur = tcost();
+        const uint64_t key = search_key(G, 2, G.tq);
+        std::array<uint8_t, 65> cached;
+        const bool hit = search_get(key, cached);
+        if (hit)
+            for (uint32_t q = 0; q < nslot; ++q)
+                phi[q] = cached[q];
+        uint32_t cur = hit ? 0u : tcost();
         for (uint32_t pass = 0; pass < 3 && cur > 128; ++pass)
             for (uint32_t q = 0; q < nslot; ++q) {
                 uint8_t bv = phi[q];
@@ -645,6 +694,12 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
                 }
                 phi[q] = bv;
             }
+        if (!hit) {
+            std::array<uint8_t, 65> v{};
+            for (uint32_t q = 0; q < nslot; ++q)
+                v[q] = phi[q];
+            search_put(key, v);
+        }
         // slots in order of phase: box k at k * 1 KiB + phi * 128 B never overlaps box k + 1
         uint32_t k = 0;
         for (uint32_t v = 0; v < 8; ++v)

@@ -14,7 +14,10 @@ kernels.cpp:510-549). ``apply_sequence`` gives the same result for a whole seque
 * the composed operations of up to three grid qubits share one pass (`hs_apply_grid_program`: the
   units of those grid bits are gathered and the steps applied one after another; m = 5); without
   grid programs, two unitary grid steps share a pass as U_a (x) U_b (tensor-core gather);
-* any other operation (k >= 2) ends the run and is applied as is.
+* any other operation (k >= 2) ends the run; consecutive multi-qubit unitaries on the same qubit
+  set (C1's CX then Haar U on each ordered pair) are composed into one unitary U2 U1 (the second
+  re-indexed to the first's target order, first-listed target = most significant bit,
+  channel.cpp:209-216) and applied in one pass.
 
 The result equals applying the sequence one operation at a time up to floating-point rounding
 (the composition reorders products); ``tests/test_gpu_fusion.py`` checks it at 1e-12 * ||rho||_F.
@@ -71,7 +74,24 @@ def _unitary_of(spec: H.ChannelSpec) -> np.ndarray | None:
     return u if np.allclose(u @ u.conj().T, np.eye(2), atol=1e-14) else None
 
 
-def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_groups: int = 3) -> Plan:
+def reorder_targets(u: np.ndarray, src: list, dst: list) -> np.ndarray:
+    """The k-qubit operator u written for targets `src` (first listed = most significant bit),
+    re-indexed for the same qubits listed as `dst`."""
+    k = len(src)
+    perm = [src.index(q) for q in dst]
+    t = np.asarray(u).reshape((2,) * (2 * k))
+    return t.transpose(perm + [k + p for p in perm]).reshape(1 << k, 1 << k)
+
+
+def _unitary_k(spec: H.ChannelSpec) -> np.ndarray | None:
+    if spec.nops != 1:
+        return None
+    u = spec.kraus[0]
+    return u if np.allclose(u @ u.conj().T, np.eye(u.shape[0]), atol=1e-13) else None
+
+
+def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_groups: int = 3,
+                  compose_multi: bool = True) -> Plan:
     """ops: iterable of (ChannelSpec, targets)."""
     plan = Plan()
     edge = min(m, n)  # in-tile qubits
@@ -125,6 +145,14 @@ def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_gro
         plan.ops += 1
         if spec.k != 1 or len(targets) != 1:
             flush()
+            last = plan.items[-1] if plan.items else None
+            if (compose_multi and last is not None and last[0] == "op" and len(last) == 3
+                    and sorted(last[2]) == sorted(targets)):
+                u1, u2 = _unitary_k(last[1]), _unitary_k(spec)
+                if u1 is not None and u2 is not None:
+                    u = reorder_targets(u2, targets, last[2]) @ u1
+                    plan.items[-1] = ("op", H.make_generic("fused_u", u), last[2])
+                    continue
             plan.items.append(("op", spec, targets))
             continue
         q = int(targets[0])

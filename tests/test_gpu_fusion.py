@@ -12,6 +12,10 @@ def _seq(H, HS, name, n):
                 for op in HS.config_ops("c2", n)]
     if name == "c0":
         return [(H.native_gate("h"), list(op.targets)) for op in HS.config_ops("c0", n)]
+    if name == "c1":  # CX then Haar U4 on ordered pairs: composed per pair, plus a reordered pair
+        out = [(H.native_gate("cnot") if op.kind == "cnot" else H.make_generic("haar", op.matrix), list(op.targets))
+               for op in HS.config_ops("c1", n)][:60]
+        return out + [(H.native_gate("cnot"), [6, 2]), (H.make_generic("haar", HS.haar(2, 9)), [2, 6])]
     out = []
     for op in HS.config_ops("c4", n)[: 3 * n + 8]:  # one layer: Rz, H, CX matching, depolarising
         if op.kind == "rz":
@@ -25,7 +29,8 @@ def _seq(H, HS, name, n):
     return out
 
 
-@pytest.mark.parametrize("name,n,m", [("c2", 10, 5), ("c2", 9, 3), ("c0", 9, 5), ("c4", 11, 5), ("c4", 8, 2)])
+@pytest.mark.parametrize("name,n,m", [("c2", 10, 5), ("c2", 9, 3), ("c0", 9, 5), ("c4", 11, 5), ("c4", 8, 2),
+                                      ("c1", 10, 5), ("c1", 8, 3)])
 def test_fused_equals_sequential(name, n, m):
     from paper_2604_15765_b200 import fusion
     from paper_2604_15765_b200 import harness as HS

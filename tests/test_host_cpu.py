@@ -205,6 +205,19 @@ def test_fusion_plan_counts():
     assert plan.items[-1][1].lone_h
     # H o Rz: one general transfer step per qubit (a step's shared-memory round trip dominates)
     assert [fusion._kind(s) for s in plan.items[0][1]] == [0] * 5
+    # C1: CX then Haar U on each ordered pair -> one composed unitary per pair, U @ CX in the pair's order
+    c1 = [(cx if op.kind == "cnot" else H.make_generic("haar", op.matrix), list(op.targets))
+          for op in HS.config_ops("c1", 14)]
+    p1 = fusion.plan_sequence(c1, 14, 5)
+    assert p1.ops == 364 and p1.launches == 182
+    assert np.allclose(p1.items[0][1].kraus[0], c1[1][0].kraus[0] @ cx.kraus[0]) and p1.items[0][2] == c1[0][1]
+    # a reordered pair: U written for [b, a] is re-indexed to [a, b] first
+    u = HS.haar(2, 9)
+    p2 = fusion.plan_sequence([(cx, [6, 2]), (H.make_generic("u", u), [2, 6])], 8, 5)
+    assert p2.launches == 1
+    assert np.allclose(p2.items[0][1].kraus[0], fusion.reorder_targets(u, [2, 6], [6, 2]) @ cx.kraus[0])
+    assert np.allclose(fusion.reorder_targets(cx.kraus[0], [0, 1], [1, 0]),
+                       np.array([[1, 0, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0], [0, 1, 0, 0]]))
     # composition order: S(second) @ S(first)
     s_rz = fusion.transfer_rowstacked(H.native_gate("rz", 0.3).kraus)
     s_h = fusion.transfer_rowstacked(h.kraus)
