@@ -485,7 +485,7 @@ void search_put(uint64_t key, const std::array<uint8_t, 65>& v) {
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
 void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false,
                  bool prog = false) {
-    const uint32_t M = G.M, g = G.g, NT = 1u << (2 * g), NG = 1u << g, kin = G.kin;
+    const uint32_t M = G.M, g = G.g, NT = G.grp4 ? 4u : 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
     while (NT * (2 * S0) * (2 * S0) <= 4096 && 2 * S0 <= M)
@@ -617,6 +617,11 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
                 v[t] = G.tsk[t];
             v[64] = (uint8_t)(G.TS - TS0);
             search_put(key, v);
+        }
+        if (G.grp4) {  // independent tiles at slot t * TS: one skew (the transform adds t * TS)
+            for (uint32_t t = 1; t < NT; ++t)
+                G.tsk[t] = G.tsk[0];
+            tables();
         }
         extra = 7;
     }
@@ -811,14 +816,22 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
     }
     // k = 2 unitaries on one grid bit: the tensor-core gather (bulk rows, two copy groups) when the
     // I2 (x) L pairing applies (0.83 -> 0.70 ms at n = 14), else the whole-tile pipeline below
+    // k = 3 unitaries on in-tile qubits (m = 5): items of 4 consecutive local tiles through the same
+    // gather (bulk rows, DMMA) instead of the pipeline's scalar two-stage transform
     if (MODE != M_KRAUS && ((G.g >= 2 && G.slabs > 1) || (K == 3 && MODE == M_DIRECT && G.g == 1) ||
-                            (K == 2 && MODE == M_DIRECT && G.g == 1))) {
+                            (K == 2 && MODE == M_DIRECT && G.g == 1) ||
+                            (K == 3 && MODE == M_DIRECT && G.g == 0 && G.M == 32 && G.kin == 3))) {
         // units of 16 / 64 stored tiles (and k = 3 unitaries on one grid bit, whose 4-tile units
         // are whole gather items for the FP64 tensor transform): sub-block gather kernel for the
         // off-diagonal units, the slab kernel's wedge path for the diagonal ones
         cudaError_t e;
         Geo Gg = G;
         constexpr bool dmma = K == 3 && MODE == M_DIRECT;
+        if (G.g == 0) {
+            Gg.grp4 = 1;
+            Gg.logNT = 2;  // four tile slots per item
+            Gg.nloc_tiles = h->count >> 10;
+        }
         plan_gather(Gg, dmma);
         {
             static const char* dbg = getenv("HS_DEBUG_FLAGS");
@@ -862,7 +875,7 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             // every unit including the diagonal ones: logical (R, C), R < C, of a diagonal unit is a
             // read-only staged copy of stored (C, R), never written back (no separate wedge launch)
             Gg.ws_diag = 1;
-            Gg.nG_items = Gg.nU_loose << (2 * Gg.log_nsb_side);
+            Gg.nG_items = Gg.grp4 ? (Gg.nloc_tiles + 3) / 4 : Gg.nU_loose << (2 * Gg.log_nsb_side);
             const size_t smem = (size_t)Gg.stages * Gg.stage_elems * sizeof(double2) + (Gg.tma ? 1024 : 0);
             auto kw = gather_ws_kernel<K, NS, MODE == M_PROG ? M_PROG : M_DIRECT>;
             if constexpr ((K == 3 && MODE == M_DIRECT) || (K == 2 && MODE == M_DIRECT))

@@ -121,7 +121,9 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
     constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
     const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
     const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
-    const uint32_t logNy = G.logNyb - sh, nblk = (G.nxb >> sh) << logNy, ymask = (G.nyb >> sh) - 1;
+    const uint32_t logNy = G.logNyb - sh, ymask = (G.nyb >> sh) - 1;
+    // blocks per tile; G.grp4: an item is 4 independent whole tiles (in-tile k = 3), slot bt at bt * TS
+    const uint32_t lbt = (G.logNxb - sh) + logNy, nblk = (G.grp4 ? 4u : 1u) << lbt;
     // two blocks per pass: independent accumulator chains keep the FP64 tensor pipe fed (small
     // tiles, m < 5, have fewer blocks than warps: the second block of a pass may be absent and is
     // then computed on a copy of the first and not stored)
@@ -130,9 +132,9 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         double2 v0[2], v1[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-            const uint32_t bq = (q && two) ? b1 : b0;
+            const uint32_t bq0 = (q && two) ? b1 : b0, bq = bq0 & ((1u << lbt) - 1);
             uint32_t xbv = T.xb[(bq >> logNy) << sh], ybv = T.yb[(bq & ymask) << sh];
-            base[q] = xbv * G.PD + ybv;
+            base[q] = (bq0 >> lbt) * G.TS + xbv * G.PD + ybv;
             if constexpr (TMAB) {  // swizzled boxes; base carries the in-box block position (the box
                 xbv &= 7u;         // row / column of a quadrant, G.tq == 4, is in the fragment constants)
                 ybv &= 7u;
@@ -531,9 +533,17 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
     auto tables = [&](uint64_t j, uint32_t t) {  // threads t < 64 (two warps): one logical tile per lane (NT <= 64)
         const uint32_t ts = (uint32_t)(j % TSL);
         uint64_t tbi, tbj;
-        unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), !G.ws_diag, tbi, tbj);
+        if (!G.grp4)
+            unit_decode(G, item_of(j) >> (2 * G.log_nsb_side), !G.ws_diag, tbi, tbj);
         bool adj = false;
-        if (t < NT) {
+        if (G.grp4) {  // 4 consecutive local stored tiles, all direct (in-tile operation)
+            if (t < NT) {
+                const uint64_t idx = 4 * (item_of(j) >> (2 * G.log_nsb_side)) + t;
+                gt[ts][t] = idx < G.nloc_tiles ? idx : (F_SKIP | F_NOSTORE);
+                if (BULK && t == 0)
+                    mir[ts] = 0;
+            }
+        } else if (t < NT) {
             const uint64_t tr = ins_bits(tbi, t >> G.logNG, G.gr_pos, G.g);
             const uint64_t tc = ins_bits(tbj, t & NGm, G.gr_pos, G.g);
             uint64_t ent = tile_entry(G, tr, tc);

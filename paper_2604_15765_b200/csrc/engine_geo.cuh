@@ -99,6 +99,8 @@ struct Geo {
     uint32_t tma;                 // gather_ws (with bulk groups): 8 x 8 boxes by tensor map, SWIZZLE_128B;
                                   // cdir[slot] = box base (16-B units, phase included), tsk[slot] = phase
     uint32_t tq;                  // tma: 4 when bit 3 of the sub-block is a block-position bit (quadrant per warp)
+    uint32_t grp4;                // gather_ws, in-tile k = 3: an item is 4 consecutive local stored tiles
+    uint64_t nloc_tiles;          // grp4: local stored tiles
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
