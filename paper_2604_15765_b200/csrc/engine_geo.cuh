@@ -89,7 +89,9 @@ struct Geo {
     uint32_t q, Pulog, logBu;     // local units: group q over 2^Pulog blocks of 2^logBu grid bases
     const double2* rbase[7];      // remote tiles of group slot j: exchange buffer slot j, or the peer's payload
     uint64_t nU_strict, nU_loose; // local off-diagonal units / units including diagonal ones
-    uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): gather bit 0 skips the transform, bit 1 the loads, bit 2 the stores
+    uint32_t dbg;                 // diagnostics (HS_DEBUG_FLAGS): gather bit 0 skips the transform, bit 1 the loads,
+                                  // bit 2 the stores, bit 4 phase timing, bit 5 ping-pong kernel, bit 6 no bulk rows,
+                                  // bit 8 no TMA boxes
     uint32_t ws_diag;             // gather_ws: units include the diagonal base pairs (grid programs)
     uint32_t qstride;             // gather_ws, k = 2 DMMA: position offset between paired blocks
     uint32_t rev;                 // sweep the items in reverse order (alternates per launch: L2 reuse)
