@@ -136,6 +136,10 @@ int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* 
  * Single-GPU states, m = 5. */
 int hs_apply_grid_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s,
                           hs_plan* plan);
+/* CX layer (fusion; no reference counterpart): CX gates on npairs (<= 32) disjoint (control,
+ * target) pairs in ONE in-place pass, bit-identical to applying them one by one
+ * (apply_permutation, native.cpp:433-549).  Single-GPU states. */
+int hs_apply_cx_layer(hs_state* h, int npairs, const uint32_t* controls, const uint32_t* targets, hs_plan* plan);
 /* Unitary conjugation B -> U B U^dagger per coupled block, direct form; k in {1, 2, 3}. */
 int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* targets, hs_plan* plan);
 /* Generic Kraus set {L_a} (nops matrices 2^k x 2^k), k in {1, 2, 3}. */

@@ -119,6 +119,7 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_op_group", i, [vp, i, c_u32_p, c_u32_p])
     _sig(L, "hs_apply_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
     _sig(L, "hs_apply_grid_program", i, [vp, i, c_i32_p, c_u32_p, c_double_p, plan])
+    _sig(L, "hs_apply_cx_layer", i, [vp, i, c_u32_p, c_u32_p, plan])
     _sig(L, "hs_state_peer_enable", i, [vp])
     _sig(L, "hs_state_peer_buffers", i, [vp, pp, pp])
     _sig(L, "hs_state_set_peer", i, [vp, i, vp, vp])

@@ -1563,6 +1563,46 @@ int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* 
     return finish_plan(h, G, 1, bits, HS_PATH_TILED_INTRA, plan, 2 * state_bytes(h));
 }
 
+// CX layer (SURVEY 8f fusion): CX gates on disjoint qubit pairs in ONE in-place pass
+// (cx_layer_kernel); equal to applying them one by one (native.cpp:433-549 per gate), bit for bit.
+// Single-GPU states.
+int hs_apply_cx_layer(hs_state* h, int npairs, const uint32_t* controls, const uint32_t* targets, hs_plan* plan) {
+    if (!h || npairs < 1 || npairs > 32 || !controls || !targets)
+        return set_err(HS_ERR_INVALID, "bad CX layer (1 .. 32 pairs)");
+    if (h->Plog)
+        return set_err(HS_ERR_UNSUPPORTED, "CX layers run on single-GPU states");
+    uint64_t used = 0;
+    CxLayer L{};
+    L.n = (uint32_t)npairs;
+    for (int k = 0; k < npairs; ++k) {
+        if (controls[k] >= (uint32_t)h->n || targets[k] >= (uint32_t)h->n)
+            return set_err(HS_ERR_RANGE, "CX layer: qubit out of range");
+        const uint64_t b = (1ull << controls[k]) | (1ull << targets[k]);
+        if (controls[k] == targets[k] || (used & b))
+            return set_err(HS_ERR_INVALID, "CX layer: the pairs must be disjoint");
+        used |= b;
+        L.c[k] = controls[k];
+        L.t[k] = targets[k];
+    }
+    DeviceGuard dg(h->device);
+    const uint64_t ntiles = h->count >> (2 * h->m);
+    const uint64_t grid = std::min<uint64_t>(ntiles, (uint64_t)sm_count(h->device) * 8);
+    cx_layer_kernel<<<(unsigned)grid, 256, 0, h->stream>>>(h->d, ntiles, (uint32_t)h->m, (uint32_t)h->n, L);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, std::string("cx_layer_kernel launch: ") + cudaGetErrorString(e));
+    if (plan) {
+        std::memset(plan, 0, sizeof(*plan));
+        plan->path = HS_PATH_NATIVE_PERMUTATION;
+        plan->k = 2;
+        plan->targets[0] = std::min(controls[0], targets[0]);
+        plan->targets[1] = std::max(controls[0], targets[0]);
+        plan->touched_bytes = 2 * state_bytes(h);
+    }
+    return HS_OK;
+}
+
 // Fused grid program: one k = 1 step on each of nsteps (<= 3) distinct grid qubits
 // (>= m), applied in ONE pass: the units of the g = nsteps grid bits are gathered (warp-specialised
 // gather) and the steps run one after another on the staged logical tiles.  kinds / s as for

@@ -228,4 +228,76 @@ __global__ void fill_pauli_kernel(double2* st, uint64_t count, uint32_t logM, ui
         st[e] = acc;
     }
 }
+
+// ---------------------------------------------------------------- CX layer (fusion)
+// A product of CX gates on disjoint (control, target) pairs is an involutive, GF(2)-linear basis
+// permutation pi (x -> x ^ sum_k x_ck e_tk), and rho'(i, j) = rho(pi(i), pi(j)).  In place, one pass:
+// every canonical slot (off-diagonal tiles, the lower half of diagonal tiles) pairs with the
+// canonical slot of (pi(i), pi(j)) -- conjugated when that logical element lies above the diagonal
+// -- and the lower slot of each pair swaps both (pi is an involution, so the pairing is symmetric).
+// The upper half of a diagonal tile is written with its canonical mirror.  pi splits over the
+// tile and in-tile bits (linearity), so an element costs two XORs with a per-tile and an in-tile
+// (shared-memory) image.
+struct CxLayer {
+    uint32_t n;
+    uint32_t c[32], t[32];
+};
+__device__ __forceinline__ uint64_t cx_pi(const CxLayer& L, uint64_t x) {
+    uint64_t y = x;
+    for (uint32_t k = 0; k < L.n; ++k)
+        y ^= ((x >> L.c[k]) & 1ull) << L.t[k];
+    return y;
+}
+__global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st, uint64_t ntiles, uint32_t logM,
+                                                       uint32_t nq, const CxLayer L) {
+    __shared__ uint64_t tab[32];  // pi of the in-tile offsets
+    const uint32_t M = 1u << logM, lMM = 2 * logM, nel = 1u << lMM;
+    if (threadIdx.x < M)
+        tab[threadIdx.x] = cx_pi(L, threadIdx.x);
+    __syncthreads();
+    auto put = [&](uint64_t slot, bool diag, uint32_t x, uint32_t y, double2 v) {
+        st[slot] = v;
+        if (diag && x > y)  // mirror in the upper half of a diagonal tile
+            st[slot - ((uint64_t)x << logM) - y + ((uint64_t)y << logM) + x] = make_double2(v.x, -v.y);
+    };
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        uint64_t ti, tj;
+        tri_loose(tile, ti, tj);
+        const uint64_t pi_i = cx_pi(L, ti << logM), pi_j = cx_pi(L, tj << logM);
+        const bool diag = ti == tj;
+        for (uint32_t pos = threadIdx.x; pos < nel; pos += blockDim.x) {
+            const uint32_t x = pos >> logM, y = pos & (M - 1);
+            if ((diag && x < y) || (((ti << logM) | x) >> nq) || (((tj << logM) | y) >> nq))
+                continue;  // mirror half, or zero padding (n < m): left as it is
+            const uint64_t p = pi_i ^ tab[x], q = pi_j ^ tab[y];
+            uint64_t tp = p >> logM, tq = q >> logM;
+            uint32_t px = (uint32_t)(p & (M - 1)), qy = (uint32_t)(q & (M - 1));
+            const bool cj = tp < tq || (tp == tq && px < qy);
+            if (cj) {
+                const uint64_t tt = tp;
+                tp = tq;
+                tq = tt;
+                const uint32_t xx = px;
+                px = qy;
+                qy = xx;
+            }
+            const uint64_t e = (tile << lMM) + pos;
+            const uint64_t s2 = ((tp * (tp + 1) / 2 + tq) << lMM) + ((uint64_t)px << logM) + qy;
+            if (s2 < e || (s2 == e && !cj))
+                continue;  // the lower slot of the pair owns it; or a fixed point
+            double2 a = st[e];
+            if (s2 == e) {  // rho'(i, j) = rho(j, i)
+                put(e, diag, x, y, make_double2(a.x, -a.y));
+                continue;
+            }
+            double2 b = st[s2];
+            if (cj) {
+                a.y = -a.y;
+                b.y = -b.y;
+            }
+            put(e, diag, x, y, b);
+            put(s2, tp == tq, px, qy, a);
+        }
+    }
+}
 }  // namespace

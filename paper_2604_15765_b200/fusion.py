@@ -17,7 +17,9 @@ kernels.cpp:510-549). ``apply_sequence`` gives the same result for a whole seque
 * any other operation (k >= 2) ends the run; consecutive multi-qubit unitaries on the same qubit
   set (C1's CX then Haar U on each ordered pair) are composed into one unitary U2 U1 (the second
   re-indexed to the first's target order, first-listed target = most significant bit,
-  channel.cpp:209-216) and applied in one pass.
+  channel.cpp:209-216) and applied in one pass;
+* consecutive CX gates on disjoint qubit pairs (C4's matchings) run as one in-place permutation
+  pass (`hs_apply_cx_layer`, bit-identical to one CX after the other).
 
 The result equals applying the sequence one operation at a time up to floating-point rounding
 (the composition reorders products); ``tests/test_gpu_fusion.py`` checks it at 1e-12 * ||rho||_F.
@@ -90,10 +92,23 @@ def _unitary_k(spec: H.ChannelSpec) -> np.ndarray | None:
     return u if np.allclose(u @ u.conj().T, np.eye(u.shape[0]), atol=1e-13) else None
 
 
+def _is_cx(spec: H.ChannelSpec) -> bool:
+    return spec.kind == "permutation" and spec.k == 2 and spec.name == "cnot"
+
+
 def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_groups: int = 3,
-                  compose_multi: bool = True) -> Plan:
+                  compose_multi: bool = True, cx_layers: bool = True) -> Plan:
     """ops: iterable of (ChannelSpec, targets)."""
     plan = Plan()
+    cx_pend: list = []  # consecutive CX on disjoint pairs: [(spec, [control, target])]
+
+    def emit_cx():
+        if len(cx_pend) >= 2:
+            plan.items.append(("cxlayer", [tuple(tg) for _, tg in cx_pend]))
+        else:
+            for spec, tg in cx_pend:
+                plan.items.append(("op", spec, tg))
+        cx_pend.clear()
     edge = min(m, n)  # in-tile qubits
     run: dict[int, Step] = {}   # grid qubits: composed per qubit
     order: list[int] = []
@@ -143,6 +158,13 @@ def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_gro
     for spec, targets in ops:
         targets = list(targets)
         plan.ops += 1
+        if cx_layers and _is_cx(spec) and len(targets) == 2:
+            flush()
+            if any(q in (c, t) for _, (c, t) in cx_pend for q in targets):
+                emit_cx()
+            cx_pend.append((spec, targets))
+            continue
+        emit_cx()
         if spec.k != 1 or len(targets) != 1:
             flush()
             last = plan.items[-1] if plan.items else None
@@ -176,6 +198,7 @@ def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_gro
         else:
             run[q] = Step(q, s, is_h, 1, u)
             order.append(q)
+    emit_cx()
     flush()
     return plan
 
@@ -227,6 +250,8 @@ def execute(st: H.TiledHermitian, plan: Plan, opts: H.ApplyOptions | None = None
             nat.check(L.hs_apply_grid_program(st.handle, len(steps), kinds.ctypes.data_as(nat.c_i32_p),
                                               bits.ctypes.data_as(nat.c_u32_p), s.ctypes.data_as(nat.c_double_p),
                                               None), "apply_grid_program")
+        elif item[0] == "cxlayer":
+            H.apply_cx_layer(st, item[1])
         elif item[0] == "step":
             x = item[1]
             if x.lone_h:

@@ -460,6 +460,15 @@ def apply_permutation(h: TiledHermitian, table, targets, plan=None) -> None:
               "apply_permutation")
 
 
+def apply_cx_layer(h: TiledHermitian, pairs, plan=None) -> None:
+    """CX gates on disjoint (control, target) pairs in one pass (fusion; bit-identical to applying
+    native_gate("cnot") on each pair in turn).  Single-GPU states."""
+    pairs = [(int(c), int(t)) for c, t in pairs]
+    c, cp = _u32([p[0] for p in pairs])
+    t, tp = _u32([p[1] for p in pairs])
+    nat.check(nat.engine().hs_apply_cx_layer(h.handle, len(pairs), cp, tp, _plan_or_none(plan)), "apply_cx_layer")
+
+
 def launch_count() -> int:
     return int(nat.engine().hs_launch_count())
 

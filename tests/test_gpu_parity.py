@@ -144,6 +144,27 @@ def test_gather_staging_modes(H, HS, oracle, orc, dual):
     st.free()
 
 
+@pytest.mark.parametrize("n,m", [(10, 5), (9, 3), (7, 5), (3, 5), (8, 0)])
+def test_cx_layer_bit_identical(H, HS, n, m):
+    """hs_apply_cx_layer (fusion) equals one native CX after the other, bit for bit: in-tile,
+    grid, and mixed pairs in both directions, elements crossing the diagonal, diagonal tiles."""
+    rng = np.random.default_rng(100 * n + m)
+    psi = HS.rank_psi(n, 19, 4)
+    a, b = H.TiledHermitian(n, m), H.TiledHermitian(n, m)
+    cx = H.native_gate("cnot")
+    for rep in range(4):
+        a.fill_mixture(psi)
+        b.fill_mixture(psi)
+        perm = [int(q) for q in rng.permutation(n)]
+        pairs = [(perm[2 * i], perm[2 * i + 1]) for i in range(n // 2)][: 1 + rep * 2]
+        for c, t in pairs:
+            H.apply(a, cx, [c, t])
+        H.apply_cx_layer(b, pairs)
+        assert np.array_equal(a.download().view(np.uint64), b.download().view(np.uint64)), (n, m, pairs)
+    a.free()
+    b.free()
+
+
 def test_generic_path_without_native(H, HS, oracle, orc):
     """allow_native = false routes native gates through the generic engines (kernels.cpp:515)."""
     n, m = 8, 5

@@ -218,6 +218,24 @@ def test_fusion_plan_counts():
     assert np.allclose(p2.items[0][1].kraus[0], fusion.reorder_targets(u, [2, 6], [6, 2]) @ cx.kraus[0])
     assert np.allclose(fusion.reorder_targets(cx.kraus[0], [0, 1], [1, 0]),
                        np.array([[1, 0, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0], [0, 1, 0, 0]]))
+    # C4: the CX of each layer's matching run as one CX layer (disjoint pairs)
+    c4 = []
+    for op in HS.config_ops("c4", 17):
+        if op.kind == "rz":
+            c4.append((H.native_gate("rz", op.param), list(op.targets)))
+        elif op.kind == "h":
+            c4.append((h, list(op.targets)))
+        elif op.kind == "cnot":
+            c4.append((cx, list(op.targets)))
+        else:
+            c4.append((H.depolarising(op.param), list(op.targets)))
+    p4 = fusion.plan_sequence(c4, 17, 5)
+    layers = [it for it in p4.items if it[0] == "cxlayer"]
+    assert p4.ops == 590 and len(layers) == 10 and all(len(it[1]) == 8 for it in layers)
+    assert p4.launches == 65
+    # CX sharing a qubit end a layer; a lone CX stays a plain operation
+    p5 = fusion.plan_sequence([(cx, [0, 1]), (cx, [2, 3]), (cx, [1, 4]), (h, [0])], 8, 5)
+    assert [it[0] for it in p5.items] == ["cxlayer", "op", "program"]
     # composition order: S(second) @ S(first)
     s_rz = fusion.transfer_rowstacked(H.native_gate("rz", 0.3).kraus)
     s_h = fusion.transfer_rowstacked(h.kraus)

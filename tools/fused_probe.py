@@ -34,6 +34,8 @@ for i, item in enumerate(plan.items):
     nat.check(L.hs_event_elapsed_ms(ev[2 * i], ev[2 * i + 1], ctypes.byref(x)))
     if item[0] == "op":
         what = f"op {item[1].name} k={item[1].k} targets {item[2]} g={sum(1 for t in item[2] if t >= m)}"
+    elif item[0] == "cxlayer":
+        what = f"cxlayer pairs {item[1]}"
     else:
         what = f"{item[0]} qubits {[s.qubit for s in item[1]] if isinstance(item[1], list) else item[1].qubit}"
     print(f"{i:4d} {x.value:8.3f} ms  {what}")
