@@ -385,11 +385,13 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
 template <uint32_t NCW, int NS, bool TMAB = false>
 __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, const Coef<NS>& cf, uint32_t p,
                                                uint64_t am, double2* sb, uint32_t tid) {
-    // TMA boxes: tiles in stored orientation (adjoint ones transposed), 8 x 8 boxes, phase T.tsk[slot]
+    // TMA boxes: tiles in stored orientation (adjoint ones transposed), 8 x 8 boxes; for grid
+    // programs every box has phase 0 and box `slot` sits at slot * 64 (plan_gather), so the
+    // address is pure arithmetic (no table lookups)
     const uint32_t nbx = G.S0 >> 3, lbpt = 2 * (G.logS0 - 3);
     auto tma_at = [&](uint32_t t, uint32_t i, uint32_t j, uint32_t f) -> uint32_t {
         const uint32_t x = f ? j : i, y = f ? i : j, sl = (t << lbpt) + (x >> 3) * nbx + (y >> 3);
-        return T.cdir[sl] + (x & 7u) * 8u + ((y & 7u) ^ ((x + T.tsk[sl]) & 7u));
+        return sl * 64u + (x & 7u) * 8u + ((y ^ x) & 7u);
     };
     const uint32_t g = G.g, NG = 1u << g, e = 1u << cf.pbit[p], lo = e - 1;
     const uint32_t S0 = G.S0, P = S0 + 1, npos = S0 * S0, lp = 2 * G.logS0;
