@@ -26,6 +26,10 @@ def _ops(H, HS, n):
         (H.make_generic("u2", u2), [top, 5]), (H.make_generic("u2", u2), [2, top - 1]),
         (H.make_generic("u3", u3), [top, 4, 0]), (H.make_generic("u3", u3), [6, 5, 8]),
         (H.native_gate("y"), [top]), (H.native_gate("swap"), [top - 2, 1]), (H.depolarising(0.02), [5]),
+        # shard-local tensor-core paths: in-tile k = 3 (4-tile items), k = 3 on two grid bits (TMA boxes,
+        # quadrant mode), k = 2 promoted to k = 3 (in-tile pair, grid pair)
+        (H.make_generic("u3", u3), [1, 4, 3]), (H.make_generic("u3", u3), [1, 6, 7]),
+        (H.make_generic("u2", u2), [0, 3]), (H.make_generic("u2", u2), [5, 7]),
         # several top targets: the group of 4 (8) shards exchanges all-to-all
         (H.native_gate("cnot"), [top, top - 1]), (H.native_gate("cnot"), [top - 2, top]),
         (H.make_generic("u2", u2), [top - 1, top - 2]), (H.native_gate("swap"), [top, top - 2]),
