@@ -389,10 +389,6 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
     // programs every box has phase 0 and box `slot` sits at slot * 64 (plan_gather), so the
     // address is pure arithmetic (no table lookups)
     const uint32_t nbx = G.S0 >> 3, lbpt = 2 * (G.logS0 - 3);
-    auto tma_at = [&](uint32_t t, uint32_t i, uint32_t j, uint32_t f) -> uint32_t {
-        const uint32_t x = f ? j : i, y = f ? i : j, sl = (t << lbpt) + (x >> 3) * nbx + (y >> 3);
-        return sl * 64u + (x & 7u) * 8u + ((y ^ x) & 7u);
-    };
     const uint32_t g = G.g, NG = 1u << g, e = 1u << cf.pbit[p], lo = e - 1;
     const uint32_t S0 = G.S0, P = S0 + 1, npos = S0 * S0, lp = 2 * G.logS0;
     const uint32_t nq = (NG / 2) * (NG / 2) * npos;
@@ -407,10 +403,15 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
         const uint32_t f2 = (uint32_t)((am >> t2) & 1ull) << 31, f3 = (uint32_t)((am >> t3) & 1ull) << 31;
         uint32_t a0, a1, a2, a3;
         if constexpr (TMAB) {
-            a0 = tma_at(t0, i, j, f0);
-            a1 = tma_at(t1, i, j, f1);
-            a2 = tma_at(t2, i, j, f2);
-            a3 = tma_at(t3, i, j, f3);
+            // one position, four tiles: the direct and the transposed in-tile offsets once (the
+            // swizzle term (x ^ y) & 7 is symmetric), the tile's slot base and orientation per tile
+            const uint32_t sw = (i ^ j) & 7u;
+            const uint32_t ad = (((i >> 3) * nbx + (j >> 3)) << 6) + (i & 7u) * 8u + sw;
+            const uint32_t aa = (((j >> 3) * nbx + (i >> 3)) << 6) + (j & 7u) * 8u + sw;
+            a0 = (t0 << (lbpt + 6)) + (f0 ? aa : ad);
+            a1 = (t1 << (lbpt + 6)) + (f1 ? aa : ad);
+            a2 = (t2 << (lbpt + 6)) + (f2 ? aa : ad);
+            a3 = (t3 << (lbpt + 6)) + (f3 ? aa : ad);
         } else {
             const uint32_t off = i * P + j;
             a0 = t0 * G.TS + T.tsk[t0] + off;
