@@ -635,8 +635,8 @@ def pipelined_e2e(args, H, L, nat, st, host0, S, n, m, nops, world, fplan, ops, 
     for s in states:
         s.synchronize()
     # enough steps that the pipeline fill (first upload alone) and drain (last download alone) are
-    # a small part of the timed region: B = 3 -> 12 steps
-    K = max(4 * B, args.e2e_steps)
+    # a small part of the timed region (steady-state serving throughput): B = 3 -> 24 steps
+    K = max(8 * B, args.e2e_steps)
     L.hs_event_record(ev[0], st.handle)  # all streams are idle: every later copy / kernel starts after it
     for k in range(K):
         one(k)
