@@ -242,6 +242,20 @@ def test_fusion_plan_counts():
     assert np.allclose(plan.items[1][1].s, s_h @ s_rz)
 
 
+def test_reorder_targets_properties():
+    """fusion.reorder_targets: the same operator listed in another target order (first listed =
+    most significant bit): kron factors swap places, and reordering back is the identity."""
+    from paper_2604_15765_b200 import fusion
+    rng = np.random.default_rng(5)
+    a, b, c = (rng.normal(size=(2, 2)) + 1j * rng.normal(size=(2, 2)) for _ in range(3))
+    u = np.kron(np.kron(a, b), c)  # targets [7, 2, 4]
+    assert np.allclose(fusion.reorder_targets(u, [7, 2, 4], [4, 7, 2]), np.kron(np.kron(c, a), b))
+    assert np.allclose(fusion.reorder_targets(u, [7, 2, 4], [2, 4, 7]), np.kron(np.kron(b, c), a))
+    v = rng.normal(size=(8, 8)) + 1j * rng.normal(size=(8, 8))
+    w = fusion.reorder_targets(fusion.reorder_targets(v, [0, 1, 2], [2, 0, 1]), [2, 0, 1], [0, 1, 2])
+    assert np.allclose(w, v)
+
+
 def test_ohrm_header_validation_without_device(tmp_path):
     """hs_state_load validates the OHRM header (storage_io.cpp:58-83) before touching a device:
     each malformed header fails with the reference's IoErrorKind."""
