@@ -722,6 +722,9 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
     G.nG_items = G.nU_strict << (2 * G.log_nsb_side);
 }
 
+// internal: a k = 2 Kraus sum the tensor-core gather cannot take (hs_apply_kraus falls back)
+constexpr int RC_NO_KRAUS_SUM = -1000;
+
 int sm_count(int device) {
     static int cache[64] = {0};
     if (device < 0 || device >= 64)
@@ -862,6 +865,9 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
                 Gg.qstride = d;
             }
             ws = !(Gg.dbg & 32u) && quad_ok;
+            if constexpr (K == 2 && MODE == M_DIRECT)
+                if (cf.nk > 1 && !ws)
+                    return RC_NO_KRAUS_SUM;  // the caller falls back to the transfer matrix
             if (ws && !(Gg.dbg & 64u)) {  // contiguous sub-block rows: bulk row copies (bit 6: off)
                 const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;
                 // k = 3 sub-blocks with 128-B rows: tensor-map boxes (bit 8: off); not for ops reading
@@ -934,6 +940,9 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
         return HS_OK;
     }
 pipe_path:
+    if constexpr (K == 2 && MODE == M_DIRECT)
+        if (cf.nk > 1)
+            return RC_NO_KRAUS_SUM;  // the pipeline's direct transform applies one operator
     const bool pipe = MODE != M_KRAUS && G.stages >= 3 && (G.nU_items > 0 || G.nD_items > 0);
     if (pipe && G.g >= 1 && G.slabs == 1) {
         // whole-unit items: the pipeline handles the diagonal base pairs as well
@@ -1723,6 +1732,25 @@ int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32
     if (nops == 1 && k >= 2)
         return hs_apply_unitary(h, k, ops, t, plan);
     const double2* L = reinterpret_cast<const double2*>(ops);
+    if (k == 2 && nops <= 4 && h->m == 5) {
+        // sum_a L_a B L_a^dagger on the tensor-core gather (I2 (x) L pairing) when it applies: at
+        // least one grid target and the paired geometry; otherwise the transfer matrix below
+        DeviceGuard dg(h->device);
+        Geo G;
+        plan_geo(h, 2, t, G, 1);
+        if (G.g >= 1) {
+            Coef<64> cf{};
+            std::memcpy(cf.s, ops, (size_t)nops * 16 * sizeof(double2));
+            cf.nk = (uint32_t)nops;
+            KrausArgs ka{nullptr, 0};
+            rc = launch<2, M_DIRECT, 64>(h, G, cf, ka, 1);
+            if (rc != RC_NO_KRAUS_SUM) {
+                if (rc)
+                    return rc;
+                return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+            }
+        }
+    }
     if (k <= 2) {
         // S = sum_a conj(L_a) (x) L_a, row-stacked
         const int dd = d * d;

@@ -223,6 +223,67 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         pass(b, b + NC / 32, b + NC / 32 < nblk);
 }
 
+// k = 2 Kraus sum sum_a L_a B L_a^dagger (2 <= nk <= 4 operators) on the I2 (x) L pairing: the same
+// 8 x 8 tensor-core transform per operator, accumulated in registers; the operators' per-lane
+// fragment values (Lr, Li, Lr + Li, Lr - Li for chunks 0, 1) come from shared memory (kf[a][8][32]).
+// One block per pass (register budget).  Offsets and tiles: the fragment of operator 0.
+template <int NC, bool BULK>
+__device__ __forceinline__ void dmma_sum2(const Geo& G, const Tabs& T, const DmmaFrag& f, const double* kf,
+                                          uint32_t nk, uint64_t am, double2* sb, uint32_t warp) {
+    constexpr uint32_t sh = 1u;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
+    const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
+    const uint32_t logNy = G.logNyb - sh, ymask = (G.nyb >> sh) - 1, nblk = (G.nxb >> sh) << logNy;
+    for (uint32_t b = warp; b < nblk; b += NC / 32) {
+        const uint32_t xbv = T.xb[(b >> logNy) << sh], ybv = T.yb[(b & ymask) << sh];
+        const uint32_t base = xbv * G.PD + ybv, baseA = ybv * G.PD + xbv;
+        double2 v0, v1;
+        if constexpr (BULK) {
+            v0 = sb[cld0 ? baseA + f.oldA[0] : base + f.old[0]];
+            v1 = sb[cld1 ? baseA + f.oldA[1] : base + f.old[1]];
+        } else {
+            v0 = sb[base + f.old[0]];
+            v1 = sb[base + f.old[1]];
+        }
+        v0.y = flip_sign(v0.y, cld0);
+        v1.y = flip_sign(v1.y, cld1);
+        const double s0 = v0.x + v0.y, s1 = v1.x + v1.y;
+        double zr0 = 0.0, zr1 = 0.0, zi0 = 0.0, zi1 = 0.0;
+        for (uint32_t a = 0; a < nk; ++a) {
+            const double* q = kf + a * 256 + lane;
+            const double lr0 = q[0], lr1 = q[32], li0 = q[64], li1 = q[96];
+            const double ls0 = q[128], ls1 = q[160], ld0 = q[192], ld1 = q[224];
+            double t1a = 0.0, t1b = 0.0, t2a = 0.0, t2b = 0.0, t3a = 0.0, t3b = 0.0;
+            dmma_acc(t1a, t1b, lr0, v0.x);
+            dmma_acc(t2a, t2b, li0, v0.y);
+            dmma_acc(t3a, t3b, ls0, s0);
+            dmma_acc(t1a, t1b, lr1, v1.x);
+            dmma_acc(t2a, t2b, li1, v1.y);
+            dmma_acc(t3a, t3b, ls1, s1);
+            const double yr0 = t1a - t2a, yr1 = t1b - t2b, yi0 = t3a - t1a - t2a, yi1 = t3b - t1b - t2b;
+            double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
+            dmma_acc(u1a, u1b, yr0, lr0);
+            dmma_acc(u2a, u2b, yi0, li0);
+            dmma_acc(u3a, u3b, yr0 + yi0, ld0);
+            dmma_acc(u1a, u1b, yr1, lr1);
+            dmma_acc(u2a, u2b, yi1, li1);
+            dmma_acc(u3a, u3b, yr1 + yi1, ld1);
+            zr0 += u1a + u2a;
+            zr1 += u1b + u2b;
+            zi0 += u3a - u1a + u2a;
+            zi1 += u3b - u1b + u2b;
+        }
+        if constexpr (BULK) {
+            sb[cst0 ? baseA + f.ostA[0] : base + f.ost[0]] = make_double2(zr0, flip_sign(zi0, cst0));
+            sb[cst1 ? baseA + f.ostA[1] : base + f.ost[1]] = make_double2(zr1, flip_sign(zi1, cst1));
+        } else {
+            sb[base + f.ost[0]] = make_double2(zr0, flip_sign(zi0, cst0));
+            sb[base + f.ost[1]] = make_double2(zr1, flip_sign(zi1, cst1));
+        }
+    }
+}
+
 __device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group
 template <int K, int MODE, int NS, int NC>
 __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
@@ -492,13 +553,41 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         DmmaFrag fr;
         if constexpr (MODE == M_DIRECT)
             fr = dmma_frag<K, NS, BULK, TMAB>(G, T, cf);
+        double* kf = nullptr;
+        if constexpr (K == 2 && MODE == M_DIRECT && NS >= 64) {
+            // Kraus sum: every operator's per-lane fragment values, [a][8][lane] (8 KiB)
+            __shared__ double kfrag[4 * 8 * 32];
+            kf = kfrag;
+            if (cf.nk > 1 && tid < 32) {
+                const uint32_t gq = tid >> 2, cq = tid & 3;
+                for (uint32_t a = 0; a < cf.nk; ++a)
+                    for (int j = 0; j < 2; ++j) {
+                        const uint32_t c8 = 2 * cq + j;
+                        const double2 l = (gq >> 2) == (c8 >> 2) ? cf.s[16 * a + (gq & 3) * 4 + (c8 & 3)]
+                                                                 : make_double2(0.0, 0.0);
+                        kfrag[a * 256 + (0 + j) * 32 + tid] = l.x;
+                        kfrag[a * 256 + (2 + j) * 32 + tid] = l.y;
+                        kfrag[a * 256 + (4 + j) * 32 + tid] = l.x + l.y;
+                        kfrag[a * 256 + (6 + j) * 32 + tid] = l.x - l.y;
+                    }
+            }
+            asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+        }
         for (uint64_t i = 0; i < nlocal; ++i) {
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
             double2* sb = ring + (size_t)s * G.stage_elems;
             if constexpr (MODE == M_DIRECT) {
-                if (!(G.dbg & 1u))
+                if constexpr (K == 2 && NS >= 64) {
+                    if (cf.nk > 1) {
+                        if (!(G.dbg & 1u))
+                            dmma_sum2<NCW, BULK>(G, T, fr, kf, cf.nk, am[i % TSL][0], sb, tid >> 5);
+                    } else if (!(G.dbg & 1u)) {
+                        dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
+                    }
+                } else if (!(G.dbg & 1u)) {
                     dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
+                }
             } else {
                 for (uint32_t p = 0; p < cf.nsteps; ++p) {
                     grid_prog_step<NCW, NS, TMAB>(G, T, cf, p, am[i % TSL][0], sb, tid);

@@ -133,6 +133,8 @@ struct Coef {
     // k = 1 transfer matrix that couples only (00, 11) and (01, 10) (depolarising, amplitude
     // damping, dephasing, ...): w = S v reads only class-consistent components
     uint32_t xpat;
+    // k = 2 Kraus sum on the tensor-core gather: nk (2..4) operators L_a in s[16a .. 16a + 15]
+    uint32_t nk;
     // monomial that is diagonal (phases only): element-wise scaling fast path; ibit = in-tile
     // target bits (ascending), nib of them
     uint32_t diag, nib;

@@ -313,7 +313,15 @@ ApplyPlan apply_on_handle(hs_state* hs, const ChannelSpec& spec, std::span<const
     }
     // apply_generic (kernels.cpp:457-506)
     const std::size_t d = std::size_t{1} << k;
-    if (k <= 2 && !(k == 2 && bc.kraus.ops.size() == 1)) {
+    if (k == 2 && bc.kraus.ops.size() >= 2 && bc.kraus.ops.size() <= 4) {
+        // small k = 2 Kraus sets: the engine sums L_a B L_a^dagger on the tensor cores where the
+        // geometry allows, else it applies the transfer matrix itself
+        std::vector<cplx> ops;
+        ops.reserve(bc.kraus.ops.size() * d * d);
+        for (const Mat& l : bc.kraus.ops)
+            ops.insert(ops.end(), l.data(), l.data() + d * d);
+        check(hs_apply_kraus(hs, k, static_cast<int>(bc.kraus.ops.size()), dptr(ops.data()), tq, pp), "apply");
+    } else if (k <= 2 && !(k == 2 && bc.kraus.ops.size() == 1)) {
         const auto sr = row_stacked(bc.transfer);  // TransferQuad / matvec<16> engines
         check(hs_apply_transfer(hs, k, dptr(sr.data()), tq, pp), "apply");
     } else if (bc.kraus.ops.size() == 1) {
