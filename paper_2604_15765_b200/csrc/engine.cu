@@ -887,6 +887,12 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             if constexpr ((K == 3 && MODE == M_DIRECT) || (K == 2 && MODE == M_DIRECT))
                 if (Gg.bulk)
                     kw = gather_ws_kernel<K, NS, M_DIRECT, true>;
+            if constexpr (K == 2 && MODE == M_DIRECT && NS == 64)
+                if (cf.nk > 1) {
+                    if (!Gg.bulk)
+                        return RC_NO_KRAUS_SUM;
+                    kw = gather_ws_kernel<K, NS, M_DIRECT, true, false, true>;
+                }
             if constexpr (K == 3 && MODE == M_PROG)
                 if (Gg.tma)
                     kw = gather_ws_kernel<K, NS, M_PROG, true, true>;

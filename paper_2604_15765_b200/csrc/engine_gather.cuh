@@ -506,7 +506,8 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
 // at bit 4: 128-B rows, too short for row copies) move as 2-D tensor-map copies (one 1 KiB box per
 // tile and box position), SWIZZLE_128B, each box at a 128-B phase of its own (host search) so the
 // DMMA lane patterns spread over the bank groups; same two-copy-group schedule as BULK.
-template <int K, int NS, int MODE = M_DIRECT, bool BULK = false, bool TMAB = false>
+// KSUM: the k = 2 Kraus-sum variant (own instantiation, so the unitary kernels keep their registers)
+template <int K, int NS, int MODE = M_DIRECT, bool BULK = false, bool TMAB = false, bool KSUM = false>
 __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st,
                                                            const __grid_constant__ CUtensorMap tin,
                                                            const __grid_constant__ CUtensorMap tout) {
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         if constexpr (MODE == M_DIRECT)
             fr = dmma_frag<K, NS, BULK, TMAB>(G, T, cf);
         double* kf = nullptr;
-        if constexpr (K == 2 && MODE == M_DIRECT && NS >= 64) {
+        if constexpr (KSUM) {
             // Kraus sum: every operator's per-lane fragment values, [a][8][lane] (8 KiB)
             __shared__ double kfrag[4 * 8 * 32];
             kf = kfrag;
@@ -578,13 +579,9 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
             double2* sb = ring + (size_t)s * G.stage_elems;
             if constexpr (MODE == M_DIRECT) {
-                if constexpr (K == 2 && NS >= 64) {
-                    if (cf.nk > 1) {
-                        if (!(G.dbg & 1u))
-                            dmma_sum2<NCW, BULK>(G, T, fr, kf, cf.nk, am[i % TSL][0], sb, tid >> 5);
-                    } else if (!(G.dbg & 1u)) {
-                        dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
-                    }
+                if constexpr (KSUM) {
+                    if (!(G.dbg & 1u))
+                        dmma_sum2<NCW, BULK>(G, T, fr, kf, cf.nk, am[i % TSL][0], sb, tid >> 5);
                 } else if (!(G.dbg & 1u)) {
                     dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
                 }
