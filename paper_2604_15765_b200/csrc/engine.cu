@@ -899,6 +899,11 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             if constexpr (K == 3 && MODE == M_DIRECT)
                 if (Gg.tma)
                     kw = gather_ws_kernel<K, NS, M_DIRECT, true, true>;
+            if constexpr (K == 3 && MODE == M_DIRECT && NS == 256)
+                if (cf.nk > 1)  // last: overrides the unitary choices above; k = 3 Kraus sums in every staging mode (the same arithmetic sharded or not)
+                    kw = Gg.tma ? gather_ws_kernel<K, NS, M_DIRECT, true, true, true>
+                                : Gg.bulk ? gather_ws_kernel<K, NS, M_DIRECT, true, false, true>
+                                          : gather_ws_kernel<K, NS, M_DIRECT, false, false, true>;
             e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess)
                 return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
@@ -1738,6 +1743,23 @@ int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32
     if (nops == 1 && k >= 2)
         return hs_apply_unitary(h, k, ops, t, plan);
     const double2* L = reinterpret_cast<const double2*>(ops);
+    if (k == 3 && nops <= 4 && h->m == 5) {
+        // sum_a L_a B L_a^dagger on the k = 3 tensor-core gather (every regime), per-operator fragments
+        DeviceGuard dg(h->device);
+        Geo G;
+        plan_geo(h, 3, t, G, 1);
+        auto* cf = new Coef<256>();
+        std::memcpy(cf->s, ops, (size_t)nops * 64 * sizeof(double2));
+        cf->nk = (uint32_t)nops;
+        KrausArgs ka{nullptr, 0};
+        rc = launch<3, M_DIRECT, 256>(h, G, *cf, ka, 1);
+        delete cf;
+        if (rc != RC_NO_KRAUS_SUM) {
+            if (rc)
+                return rc;
+            return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+        }
+    }
     if (k == 2 && nops <= 4 && h->m == 5) {
         // sum_a L_a B L_a^dagger on the tensor-core gather (I2 (x) L pairing) when it applies: at
         // least one grid target and the paired geometry; otherwise the transfer matrix below

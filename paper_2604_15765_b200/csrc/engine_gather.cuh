@@ -115,9 +115,13 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
     }
     return f;
 }
-template <int NC, int K = 3, bool BULK = false, bool TMAB = false>
+// KS: Kraus sum sum_a L_a B L_a^dagger over nk operators whose per-lane fragment values come from
+// shared memory (kf[a][8][lane]: Lr, Li, Lr + Li, Lr - Li for chunks 0, 1), accumulated in registers.
+template <int NC, int K = 3, bool BULK = false, bool TMAB = false, bool KS = false>
 __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
-                                             double2* sb, uint32_t warp) {
+                                             double2* sb, uint32_t warp, const double* kf = nullptr,
+                                             uint32_t nk = 1) {
+    const uint32_t lane = threadIdx.x & 31u;
     constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
     const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
     const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
@@ -152,42 +156,72 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
             v0[q].y = flip_sign(v0[q].y, cld0);
             v1[q].y = flip_sign(v1[q].y, cld1);
         }
-        // 3M form (Gauss): three real products per complex product.  Stage 1: Y = L B with
-        // T1 = Lr Br, T2 = Li Bi, T3 = (Lr + Li)(Br + Bi); Yr = T1 - T2, Yi = T3 - T1 - T2
-        double yr0[2], yr1[2], yi0[2], yi1[2];
+        double zr0[2] = {0.0, 0.0}, zr1[2] = {0.0, 0.0}, zi0[2] = {0.0, 0.0}, zi1[2] = {0.0, 0.0};
+        for (uint32_t op = 0; op < (KS ? nk : 1u); ++op) {
+            double lr0, lr1, li0, li1, ls0, ls1, ld0, ld1;
+            if constexpr (KS) {
+                const double* kq = kf + op * 256 + lane;
+                lr0 = kq[0];
+                lr1 = kq[32];
+                li0 = kq[64];
+                li1 = kq[96];
+                ls0 = kq[128];
+                ls1 = kq[160];
+                ld0 = kq[192];
+                ld1 = kq[224];
+            } else {
+                lr0 = f.lr[0];
+                lr1 = f.lr[1];
+                li0 = f.li[0];
+                li1 = f.li[1];
+                ls0 = f.ls[0];
+                ls1 = f.ls[1];
+                ld0 = f.ld[0];
+                ld1 = f.ld[1];
+            }
+            // 3M form (Gauss): three real products per complex product.  Stage 1: Y = L B with
+            // T1 = Lr Br, T2 = Li Bi, T3 = (Lr + Li)(Br + Bi); Yr = T1 - T2, Yi = T3 - T1 - T2
+            double yr0[2], yr1[2], yi0[2], yi1[2];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            double t1a = 0.0, t1b = 0.0, t2a = 0.0, t2b = 0.0, t3a = 0.0, t3b = 0.0;
-            const double s0 = v0[q].x + v0[q].y, s1 = v1[q].x + v1[q].y;
-            dmma_acc(t1a, t1b, f.lr[0], v0[q].x);
-            dmma_acc(t2a, t2b, f.li[0], v0[q].y);
-            dmma_acc(t3a, t3b, f.ls[0], s0);
-            dmma_acc(t1a, t1b, f.lr[1], v1[q].x);
-            dmma_acc(t2a, t2b, f.li[1], v1[q].y);
-            dmma_acc(t3a, t3b, f.ls[1], s1);
-            yr0[q] = t1a - t2a;
-            yr1[q] = t1b - t2b;
-            yi0[q] = t3a - t1a - t2a;
-            yi1[q] = t3b - t1b - t2b;
-        }
-        // stage 2: Z = Y P, P = L^dagger (B fragment of chunk j: P[2c + j][g] = conj(L[g][2c + j]));
-        // U1 = Yr Pr, U2 = Yi Pi, U3 = (Yr + Yi)(Pr + Pi); Zr = U1 - U2, Zi = U3 - U1 - U2.  With
-        // Pi = -Li^T the code accumulates V2 = Yi Li^T = -U2: Zr = U1 + V2, Zi = U3 - U1 + V2
-        double zr0[2], zr1[2], zi0[2], zi1[2];
+            for (int q = 0; q < 2; ++q) {
+                double t1a = 0.0, t1b = 0.0, t2a = 0.0, t2b = 0.0, t3a = 0.0, t3b = 0.0;
+                const double s0 = v0[q].x + v0[q].y, s1 = v1[q].x + v1[q].y;
+                dmma_acc(t1a, t1b, lr0, v0[q].x);
+                dmma_acc(t2a, t2b, li0, v0[q].y);
+                dmma_acc(t3a, t3b, ls0, s0);
+                dmma_acc(t1a, t1b, lr1, v1[q].x);
+                dmma_acc(t2a, t2b, li1, v1[q].y);
+                dmma_acc(t3a, t3b, ls1, s1);
+                yr0[q] = t1a - t2a;
+                yr1[q] = t1b - t2b;
+                yi0[q] = t3a - t1a - t2a;
+                yi1[q] = t3b - t1b - t2b;
+            }
+            // stage 2: Z = Y P, P = L^dagger (B fragment of chunk j: P[2c + j][g] = conj(L[g][2c + j]));
+            // U1 = Yr Pr, U2 = Yi Pi, U3 = (Yr + Yi)(Pr + Pi); Zr = U1 - U2, Zi = U3 - U1 - U2.  With
+            // Pi = -Li^T the code accumulates V2 = Yi Li^T = -U2: Zr = U1 + V2, Zi = U3 - U1 + V2
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
-            const double s0 = yr0[q] + yi0[q], s1 = yr1[q] + yi1[q];
-            dmma_acc(u1a, u1b, yr0[q], f.lr[0]);
-            dmma_acc(u2a, u2b, yi0[q], f.li[0]);
-            dmma_acc(u3a, u3b, s0, f.ld[0]);
-            dmma_acc(u1a, u1b, yr1[q], f.lr[1]);
-            dmma_acc(u2a, u2b, yi1[q], f.li[1]);
-            dmma_acc(u3a, u3b, s1, f.ld[1]);
-            zr0[q] = u1a + u2a;
-            zr1[q] = u1b + u2b;
-            zi0[q] = u3a - u1a + u2a;
-            zi1[q] = u3b - u1b + u2b;
+            for (int q = 0; q < 2; ++q) {
+                double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
+                const double s0 = yr0[q] + yi0[q], s1 = yr1[q] + yi1[q];
+                dmma_acc(u1a, u1b, yr0[q], lr0);
+                dmma_acc(u2a, u2b, yi0[q], li0);
+                dmma_acc(u3a, u3b, s0, ld0);
+                dmma_acc(u1a, u1b, yr1[q], lr1);
+                dmma_acc(u2a, u2b, yi1[q], li1);
+                dmma_acc(u3a, u3b, s1, ld1);
+                if constexpr (KS) {
+                    zr0[q] += u1a + u2a;
+                    zr1[q] += u1b + u2b;
+                    zi0[q] += u3a - u1a + u2a;
+                    zi1[q] += u3b - u1b + u2b;
+                } else {
+                    zr0[q] = u1a + u2a;
+                    zr1[q] = u1b + u2b;
+                    zi0[q] = u3a - u1a + u2a;
+                    zi1[q] = u3b - u1b + u2b;
+                }
+            }
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -221,67 +255,6 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
     }
     for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32))
         pass(b, b + NC / 32, b + NC / 32 < nblk);
-}
-
-// k = 2 Kraus sum sum_a L_a B L_a^dagger (2 <= nk <= 4 operators) on the I2 (x) L pairing: the same
-// 8 x 8 tensor-core transform per operator, accumulated in registers; the operators' per-lane
-// fragment values (Lr, Li, Lr + Li, Lr - Li for chunks 0, 1) come from shared memory (kf[a][8][32]).
-// One block per pass (register budget).  Offsets and tiles: the fragment of operator 0.
-template <int NC, bool BULK>
-__device__ __forceinline__ void dmma_sum2(const Geo& G, const Tabs& T, const DmmaFrag& f, const double* kf,
-                                          uint32_t nk, uint64_t am, double2* sb, uint32_t warp) {
-    constexpr uint32_t sh = 1u;
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
-    const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
-    const uint32_t logNy = G.logNyb - sh, ymask = (G.nyb >> sh) - 1, nblk = (G.nxb >> sh) << logNy;
-    for (uint32_t b = warp; b < nblk; b += NC / 32) {
-        const uint32_t xbv = T.xb[(b >> logNy) << sh], ybv = T.yb[(b & ymask) << sh];
-        const uint32_t base = xbv * G.PD + ybv, baseA = ybv * G.PD + xbv;
-        double2 v0, v1;
-        if constexpr (BULK) {
-            v0 = sb[cld0 ? baseA + f.oldA[0] : base + f.old[0]];
-            v1 = sb[cld1 ? baseA + f.oldA[1] : base + f.old[1]];
-        } else {
-            v0 = sb[base + f.old[0]];
-            v1 = sb[base + f.old[1]];
-        }
-        v0.y = flip_sign(v0.y, cld0);
-        v1.y = flip_sign(v1.y, cld1);
-        const double s0 = v0.x + v0.y, s1 = v1.x + v1.y;
-        double zr0 = 0.0, zr1 = 0.0, zi0 = 0.0, zi1 = 0.0;
-        for (uint32_t a = 0; a < nk; ++a) {
-            const double* q = kf + a * 256 + lane;
-            const double lr0 = q[0], lr1 = q[32], li0 = q[64], li1 = q[96];
-            const double ls0 = q[128], ls1 = q[160], ld0 = q[192], ld1 = q[224];
-            double t1a = 0.0, t1b = 0.0, t2a = 0.0, t2b = 0.0, t3a = 0.0, t3b = 0.0;
-            dmma_acc(t1a, t1b, lr0, v0.x);
-            dmma_acc(t2a, t2b, li0, v0.y);
-            dmma_acc(t3a, t3b, ls0, s0);
-            dmma_acc(t1a, t1b, lr1, v1.x);
-            dmma_acc(t2a, t2b, li1, v1.y);
-            dmma_acc(t3a, t3b, ls1, s1);
-            const double yr0 = t1a - t2a, yr1 = t1b - t2b, yi0 = t3a - t1a - t2a, yi1 = t3b - t1b - t2b;
-            double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
-            dmma_acc(u1a, u1b, yr0, lr0);
-            dmma_acc(u2a, u2b, yi0, li0);
-            dmma_acc(u3a, u3b, yr0 + yi0, ld0);
-            dmma_acc(u1a, u1b, yr1, lr1);
-            dmma_acc(u2a, u2b, yi1, li1);
-            dmma_acc(u3a, u3b, yr1 + yi1, ld1);
-            zr0 += u1a + u2a;
-            zr1 += u1b + u2b;
-            zi0 += u3a - u1a + u2a;
-            zi1 += u3b - u1b + u2b;
-        }
-        if constexpr (BULK) {
-            sb[cst0 ? baseA + f.ostA[0] : base + f.ost[0]] = make_double2(zr0, flip_sign(zi0, cst0));
-            sb[cst1 ? baseA + f.ostA[1] : base + f.ost[1]] = make_double2(zr1, flip_sign(zi1, cst1));
-        } else {
-            sb[base + f.ost[0]] = make_double2(zr0, flip_sign(zi0, cst0));
-            sb[base + f.ost[1]] = make_double2(zr1, flip_sign(zi1, cst1));
-        }
-    }
 }
 
 __device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group
@@ -564,8 +537,11 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                 for (uint32_t a = 0; a < cf.nk; ++a)
                     for (int j = 0; j < 2; ++j) {
                         const uint32_t c8 = 2 * cq + j;
-                        const double2 l = (gq >> 2) == (c8 >> 2) ? cf.s[16 * a + (gq & 3) * 4 + (c8 & 3)]
-                                                                 : make_double2(0.0, 0.0);
+                        double2 l;
+                        if constexpr (K == 3)
+                            l = cf.s[64 * a + gq * 8 + c8];
+                        else
+                            l = (gq >> 2) == (c8 >> 2) ? cf.s[16 * a + (gq & 3) * 4 + (c8 & 3)] : make_double2(0.0, 0.0);
                         kfrag[a * 256 + (0 + j) * 32 + tid] = l.x;
                         kfrag[a * 256 + (2 + j) * 32 + tid] = l.y;
                         kfrag[a * 256 + (4 + j) * 32 + tid] = l.x + l.y;
@@ -581,7 +557,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             if constexpr (MODE == M_DIRECT) {
                 if constexpr (KSUM) {
                     if (!(G.dbg & 1u))
-                        dmma_sum2<NCW, BULK>(G, T, fr, kf, cf.nk, am[i % TSL][0], sb, tid >> 5);
+                        dmma_direct3<NCW, K, BULK, TMAB, true>(G, T, fr, am[i % TSL][0], sb, tid >> 5, kf, cf.nk);
                 } else if (!(G.dbg & 1u)) {
                     dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
                 }

@@ -38,10 +38,31 @@ def test_graph_refuses_uncapturable():
     from paper_2604_15765_b200 import harness as HS
     from paper_2604_15765_b200 import hermsim as H
     st = H.TiledHermitian(9)
-    k3 = H.make_generic("k3", np.stack([np.sqrt(0.5) * HS.haar(3, 3), np.sqrt(0.5) * HS.haar(3, 4)]))
+    # k = 3 Kraus sets of more than 4 operators go through the three-buffer sum, whose Kraus set is
+    # uploaded from host memory at apply time (up to 4 operators ride in the kernel parameters)
+    ops = np.stack([np.sqrt(0.2) * HS.haar(3, 3 + i) for i in range(5)])
+    k3 = H.make_generic("k3", ops)
     with pytest.raises(Exception):
         with H.capture(st):
             H.apply(st, k3, [8, 2, 0])
+
+
+def test_graph_of_small_kraus_sum():
+    """A k = 3 Kraus sum of 2 operators (tensor-core gather, coefficients in the kernel parameters)
+    is capturable and replays bit-identically."""
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    n = 9
+    psi = HS.rank_psi(n, 4, 4)
+    a, b = H.TiledHermitian(n), H.TiledHermitian(n)
+    a.fill_mixture(psi)
+    b.fill_mixture(psi)
+    k3 = H.make_generic("k3", np.stack([np.sqrt(0.5) * HS.haar(3, 3), np.sqrt(0.5) * HS.haar(3, 4)]))
+    with H.capture(a) as g:
+        H.apply(a, k3, [8, 2, 0])
+    g.launch()
+    H.apply(b, k3, [8, 2, 0])
+    assert np.array_equal(a.download().view(np.uint64), b.download().view(np.uint64))
 
 
 def test_graph_of_fused_sequence():
