@@ -122,6 +122,9 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
                                              double2* sb, uint32_t warp, const double* kf = nullptr,
                                              uint32_t nk = 1) {
     const uint32_t lane = threadIdx.x & 31u;
+    // blocks per pass: two independent chains for the unitary; one for the Kraus sum (its
+    // accumulators would otherwise spill)
+    constexpr int NQ = KS ? 1 : 2;
     constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
     const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
     const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
@@ -135,7 +138,7 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         uint32_t base[2], baseA[2];
         double2 v0[2], v1[2];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < NQ; ++q) {
             const uint32_t bq0 = (q && two) ? b1 : b0, bq = bq0 & ((1u << lbt) - 1);
             uint32_t xbv = T.xb[(bq >> logNy) << sh], ybv = T.yb[(bq & ymask) << sh];
             base[q] = (bq0 >> lbt) * G.TS + xbv * G.PD + ybv;
@@ -183,7 +186,7 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
             // T1 = Lr Br, T2 = Li Bi, T3 = (Lr + Li)(Br + Bi); Yr = T1 - T2, Yi = T3 - T1 - T2
             double yr0[2], yr1[2], yi0[2], yi1[2];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < NQ; ++q) {
                 double t1a = 0.0, t1b = 0.0, t2a = 0.0, t2b = 0.0, t3a = 0.0, t3b = 0.0;
                 const double s0 = v0[q].x + v0[q].y, s1 = v1[q].x + v1[q].y;
                 dmma_acc(t1a, t1b, lr0, v0[q].x);
@@ -201,7 +204,7 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
             // U1 = Yr Pr, U2 = Yi Pi, U3 = (Yr + Yi)(Pr + Pi); Zr = U1 - U2, Zi = U3 - U1 - U2.  With
             // Pi = -Li^T the code accumulates V2 = Yi Li^T = -U2: Zr = U1 + V2, Zi = U3 - U1 + V2
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < NQ; ++q) {
                 double u1a = 0.0, u1b = 0.0, u2a = 0.0, u2b = 0.0, u3a = 0.0, u3b = 0.0;
                 const double s0 = yr0[q] + yi0[q], s1 = yr1[q] + yi1[q];
                 dmma_acc(u1a, u1b, yr0[q], lr0);
@@ -224,7 +227,7 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
             }
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < NQ; ++q) {
             if (q && !two)
                 break;
             if constexpr (TMAB) {
@@ -245,16 +248,16 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         // block row and column: block index bits 2 and 5 of 8 x 8 blocks), 16 blocks, NW / 4 warps
         constexpr uint32_t NWQ = NC / 32 / 4;
         const uint32_t qd = warp & 3u, wi = warp >> 2;
-        for (uint32_t jb = wi; jb < 16; jb += 2 * NWQ) {
+        for (uint32_t jb = wi; jb < 16; jb += NQ * NWQ) {
             const uint32_t j1 = jb + NWQ;
             const uint32_t b0 = ((((qd >> 1) << 2) | (jb >> 2)) << 3) | ((qd & 1u) << 2) | (jb & 3u);
             const uint32_t b1 = ((((qd >> 1) << 2) | (j1 >> 2)) << 3) | ((qd & 1u) << 2) | (j1 & 3u);
-            pass(b0, b1, j1 < 16);
+            pass(b0, b1, NQ == 2 && j1 < 16);
         }
         return;
     }
-    for (uint32_t b = warp; b < nblk; b += 2 * (NC / 32))
-        pass(b, b + NC / 32, b + NC / 32 < nblk);
+    for (uint32_t b = warp; b < nblk; b += NQ * (NC / 32))
+        pass(b, b + NC / 32, NQ == 2 && b + NC / 32 < nblk);
 }
 
 __device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group
