@@ -1766,6 +1766,28 @@ int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32
         DeviceGuard dg(h->device);
         Geo G;
         plan_geo(h, 2, t, G, 1);
+        if (G.g == 0 && h->n >= h->m + 4) {
+            // both targets in-tile: the k = 3 sum of I2 (x) L_a on (t0, t1, m), as for unitaries
+            // (the extra qubit m is never one of the top three: the same path sharded or not)
+            uint32_t t3[3] = {t[0], t[1], (uint32_t)h->m};
+            Geo G3;
+            plan_geo(h, 3, t3, G3, 1);
+            auto* cf = new Coef<256>();
+            for (int a = 0; a < nops; ++a)
+                for (int r = 0; r < 8; ++r)
+                    for (int c = 0; c < 8; ++c)
+                        cf->s[64 * a + r * 8 + c] =
+                            (r >> 2) == (c >> 2) ? L[16 * a + (r & 3) * 4 + (c & 3)] : make_double2(0.0, 0.0);
+            cf->nk = (uint32_t)nops;
+            KrausArgs ka{nullptr, 0};
+            rc = launch<3, M_DIRECT, 256>(h, G3, *cf, ka, 1);
+            delete cf;
+            if (rc != RC_NO_KRAUS_SUM) {
+                if (rc)
+                    return rc;
+                return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+            }
+        }
         if (G.g >= 1) {
             Coef<64> cf{};
             std::memcpy(cf.s, ops, (size_t)nops * 16 * sizeof(double2));
