@@ -127,7 +127,7 @@ int hs_host_free(void* p);
  * 4^k x 4^k complex, k in {1, 2}.  plan may be NULL. */
 int hs_apply_transfer(hs_state* h, int k, const double* s_rowstacked, const uint32_t* targets, hs_plan* plan);
 /* Fused program (no reference counterpart: the reference applies one op per pass):
- * nsteps <= 8 single-qubit steps on in-tile qubits (< m) in ONE pass over the triangle, equal to
+ * nsteps <= 16 single-qubit steps on in-tile qubits (< m) in ONE pass over the triangle, equal to
  * applying them in order.  kinds[p]: 0 = row-stacked 4x4 transfer matrix s[16p..16p+15]
  * (interleaved complex), 1 = Hadamard (s ignored), 2 = diagonal transfer (diagonal of s used). */
 int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s, hs_plan* plan);
@@ -168,12 +168,12 @@ int hs_frobenius(const hs_state* h, double* out);
  * stored element is formed with explicitly rounded products and sums in a fixed order, so
  * the payload is bit-identical to the host construction hsg_rho_payload (harness.c). */
 int hs_state_fill_mixture(hs_state* h, int rank, const double* psi);
-/* O = sum_s coef_s P_s for Pauli strings with X-mask x[s], Z-mask z[s] (Y sets both) and
- * ny[s] = #Y; bit-identical to hsg_pauli_payload (harness.c). */
 /* hermsim::random_hermitian(n, seed) and basis_projector(n, basis) (storage.cpp:195-239), generated
  * on the device (counter-based RNG: elements equal the reference's to ~1e-16 relative). */
 int hs_state_fill_random_hermitian(hs_state* h, uint64_t seed);
 int hs_state_fill_basis_projector(hs_state* h, uint64_t basis);
+/* O = sum_s coef_s P_s for Pauli strings with X-mask x[s], Z-mask z[s] (Y sets both) and
+ * ny[s] = #Y; bit-identical to hsg_pauli_payload (harness.c). */
 int hs_state_fill_pauli_sum(hs_state* h, int count, const uint64_t* x, const uint64_t* z, const int32_t* ny,
                             const double* coef);
 

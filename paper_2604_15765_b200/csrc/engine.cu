@@ -865,9 +865,9 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
                 Gg.qstride = d;
             }
             ws = !(Gg.dbg & 32u) && quad_ok;
-            if constexpr (K == 2 && MODE == M_DIRECT)
+            if constexpr (MODE == M_DIRECT && (K == 2 || NS == 256))
                 if (cf.nk > 1 && !ws)
-                    return RC_NO_KRAUS_SUM;  // the caller falls back to the transfer matrix
+                    return RC_NO_KRAUS_SUM;  // the caller falls back (transfer matrix / three-buffer sum)
             if (ws && !(Gg.dbg & 64u)) {  // contiguous sub-block rows: bulk row copies (bit 6: off)
                 const uint32_t qs = Gg.qstride, dbgf = Gg.dbg;
                 // k = 3 sub-blocks with 128-B rows: tensor-map boxes (bit 8: off); not for ops reading
@@ -951,7 +951,7 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
         return HS_OK;
     }
 pipe_path:
-    if constexpr (K == 2 && MODE == M_DIRECT)
+    if constexpr (MODE == M_DIRECT && (K == 2 || NS == 256))
         if (cf.nk > 1)
             return RC_NO_KRAUS_SUM;  // the pipeline's direct transform applies one operator
     const bool pipe = MODE != M_KRAUS && G.stages >= 3 && (G.nU_items > 0 || G.nD_items > 0);
@@ -1010,6 +1010,10 @@ int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, 
         h->flip ^= 1u;
         h->d = h->buf[h->flip];
     }
+    // an exchange licenses exactly one cross-shard operation: after it, this shard's and the
+    // members' payloads have moved on and the exchange slots are stale
+    if (rc == HS_OK && G0.cmask && !h->peer_mode)
+        h->recv_mask = 0;
     return rc;
 }
 
@@ -1692,10 +1696,10 @@ int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* t, hs_
                             make_double2(x.x * y.x + x.y * y.y, x.x * y.y - x.y * y.x);
                     }
         rc = launch<1, M_S1, 16>(h, G, cf, ka, 1);
-    } else if (k == 2 && G.g == 0 && h->m == 5 && h->n >= h->m + 4) {
+    } else if (k == 2 && G.g == 0 && h->m == 5 && h->n >= h->m + 4 && (uint32_t)(h->n - h->m) > h->Plog) {
         // both targets in-tile: run I2 (x) L on (t0, t1, m) -- the lowest grid qubit m as the most
-        // significant local bit; never one of the top three qubits, so never a shard bit for up to
-        // 8 shards and the same choice sharded or not -- through the k = 3 tensor-core gather (bulk
+        // significant local bit; only when m is not a shard bit (n - m > log2 P), so the promoted op
+        // stays shard-local; the same choice sharded or not -- through the k = 3 tensor-core gather (bulk
         // rows): identical result up to rounding, 0.96 -> ~0.70 ms at n = 14 instead of the
         // scalar two-stage transform of the whole-tile pipeline
         uint32_t t3[3] = {t[0], t[1], (uint32_t)h->m};
@@ -1766,7 +1770,7 @@ int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32
         DeviceGuard dg(h->device);
         Geo G;
         plan_geo(h, 2, t, G, 1);
-        if (G.g == 0 && h->n >= h->m + 4) {
+        if (G.g == 0 && h->n >= h->m + 4 && (uint32_t)(h->n - h->m) > h->Plog) {
             // both targets in-tile: the k = 3 sum of I2 (x) L_a on (t0, t1, m), as for unitaries
             // (the extra qubit m is never one of the top three: the same path sharded or not)
             uint32_t t3[3] = {t[0], t[1], (uint32_t)h->m};

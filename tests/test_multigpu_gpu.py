@@ -43,7 +43,9 @@ def _ops(H, HS, n):
 
 
 @pytest.mark.parametrize("n,P,peer", [(9, 2, False), (10, 4, False), (11, 8, False), (10, 2, False), (13, 8, False),
-                                      (13, 4, False), (9, 2, True), (10, 4, True), (11, 8, True), (13, 8, True)])
+                                      (13, 4, False), (9, 2, True), (10, 4, True), (11, 8, True), (13, 8, True),
+                                      # P = G: every grid bit is a shard bit (no in-tile k = 2 promotion)
+                                      (9, 16, False), (9, 16, True)])
 def test_sharded_bit_identical(n, P, peer):
     from paper_2604_15765_b200 import harness as HS
     from paper_2604_15765_b200 import hermsim as H
@@ -82,6 +84,10 @@ def test_group_exchange_required():
     # but not one that moves both (SWAP)
     nat.check(nat.engine().hs_state_exchange_group_from(st.handle, grp.shards[0].handle, 1))
     H.apply(st, H.native_gate("cnot"), [9, 8])
+    # the exchange licensed that one operation only: its slots are stale now
+    with pytest.raises((ValueError, nat.NativeError)):
+        H.apply(st, H.native_gate("cnot"), [9, 8])
+    nat.check(nat.engine().hs_state_exchange_group_from(st.handle, grp.shards[0].handle, 1))
     with pytest.raises((ValueError, nat.NativeError)):
         H.apply(st, H.native_gate("swap"), [9, 8])
 

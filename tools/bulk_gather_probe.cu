@@ -2,7 +2,7 @@
 // gather items made of small 1-D bulk copies (cp.async.bulk, rows of `row_bytes` from scattered 16 KiB
 // tiles, C3-like unit order) issued by many threads, vs 16-byte cp.async (LDGSTS) + st.global from
 // the same threads.  Three stages, every copy thread works on every stage in turn.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/bulk_gather_probe tools/bulk_gather_probe.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -cudart shared -o tools/bulk_gather_probe tools/bulk_gather_probe.cu
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>

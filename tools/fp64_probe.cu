@@ -1,6 +1,6 @@
 // FP64 throughput probe on B200 (design evidence for the k = 3 direct transform):
 // DFMA (vector pipe) vs DMMA (mma.sync m8n8k4 f64 tensor path) vs both interleaved.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/fp64_probe tools/fp64_probe.cu
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o tools/fp64_probe tools/fp64_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 

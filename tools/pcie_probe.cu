@@ -1,7 +1,7 @@
 // Probe (design evidence for the end-to-end measurement): host <-> device copy rates
 // from pinned memory on this box -- one direction alone, both directions at once, and each
 // direction split over several streams (copy engines).
-// nvcc -O2 -o tools/pcie_probe tools/pcie_probe.cu
+// nvcc -O2 -cudart shared -o tools/pcie_probe tools/pcie_probe.cu
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <vector>

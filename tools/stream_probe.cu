@@ -3,7 +3,7 @@
 // every complex128 of a buffer once (x <- 0.5 x), like a transform that touches the whole state.
 //   v1: plain LDG.128 / STG.128, grid-stride, UNR elements per thread in flight
 //   v2: TMA bulk ring (1 CTA/SM, producer warp + consumer warps), chunk bytes / stages variable
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o stream_probe stream_probe.cu
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -cudart shared -o stream_probe stream_probe.cu
 #include <cuda_runtime.h>
 
 #include <cstdint>

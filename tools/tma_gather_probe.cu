@@ -2,7 +2,7 @@
 // "gather items" made of many small 2-D TMA boxes (rows of 128 B, 8 or 16 rows per box) from
 // scattered 16 KiB tiles, three-stage ring, one producer warp per stage (all lanes issue), no transform.
 // Reports GB/s (read + write) per box shape.
-// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/tma_gather_probe tools/tma_gather_probe.cu -lcuda
+// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -cudart shared -o tools/tma_gather_probe tools/tma_gather_probe.cu -lcuda
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>

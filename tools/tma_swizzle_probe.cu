@@ -2,7 +2,7 @@
 // land when its shared-memory base is 128-byte but not 1024-byte aligned?  Hypothesis A: the XOR uses
 // absolute smem address bits (chunk' = chunk ^ ((addr >> 7) & 7)), so a base offset of phi * 128 B
 // rotates the pattern; hypothesis B: the pattern is relative to the box (chunk' = chunk ^ row).
-// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/tma_swizzle_probe tools/tma_swizzle_probe.cu -lcuda
+// nvcc -gencode arch=compute_100a,code=sm_100a -O2 -cudart shared -o tools/tma_swizzle_probe tools/tma_swizzle_probe.cu -lcuda
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdio>
