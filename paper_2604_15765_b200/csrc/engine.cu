@@ -484,7 +484,7 @@ void search_put(uint64_t key, const std::array<uint8_t, 65>& v) {
 // bulk: stage sub-block rows with cp.async.bulk, one copy per run of >= 8 contiguous elements
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
 void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false,
-                 bool prog = false) {
+                 bool prog = false, bool sform = false) {
     const uint32_t M = G.M, g = G.g, NT = G.grp4 ? 4u : 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -521,8 +521,12 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
     // bulk rows: runs of the low contiguous sub-block bits, at least 16 elements (256 B; 128-B runs
     // are bound by the bulk-copy engine's operation rate: C3 g = 3 15.4 -> 20.7 ms measured)
     G.logRun = std::min<uint32_t>(__builtin_ctz(~cmask), G.logS0);
-    G.bulk = bulk && dmma && G.logRun >= 4;
+    G.bulk = bulk && (dmma || sform) && G.logRun >= 4;
     G.TS = S0 * (S0 + 1);
+    G.s8 = 0;
+    G.sf_xfast = 0;
+    for (uint32_t i = 0; i < 16; ++i)
+        G.sf_pi[i] = G.sf_sigma[i] = (uint8_t)i;
     const uint32_t D = G.D, kinm = (1u << kin) - 1;
     for (uint32_t t = 0; t < 64; ++t)
         G.tsk[t] = 0;
@@ -531,15 +535,150 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
             for (uint32_t gam = 0; gam < D; ++gam) {
                 const uint32_t R = rho >> kin, C = gam >> kin, i = rho * D + gam, t = R * NG + C;
                 G.ttr[i] = (uint8_t)t;
-                G.cdir[i] = G.cadj[i] =
-                    (uint16_t)(t * G.TS + G.tsk[t] + G.xs_in[rho & kinm] * G.PD + G.y_in[gam & kinm]);
+                const uint32_t xr = G.xs_in[rho & kinm], yc = G.y_in[gam & kinm];
+                G.cdir[i] = G.cadj[i] = (uint16_t)(t * G.TS + G.tsk[t] + xr * G.PD + (xr >> 3) * G.s8 + yc);
                 if (G.bulk)  // adjoint tiles in stored orientation: logical (x, y) at row y, column x
-                    G.cadj[i] = (uint16_t)(t * G.TS + G.tsk[t] + G.y_in[gam & kinm] * G.PD + G.xs_in[rho & kinm]);
+                    G.cadj[i] = (uint16_t)(t * G.TS + G.tsk[t] + yc * G.PD + (yc >> 3) * G.s8 + xr);
             }
     };
     tables();
     uint32_t extra = 0;
-    if (dmma && (D == 8 || (D == 4 && qstride))) {
+    if (sform && G.bulk && D == 4) {
+        // S-form transform (sform2): a quarter-warp touches blocks 2ph, 2ph + 1 of a pass x the four
+        // components of a k-step (loads) or of an output pair (stores).  Spread each over the eight
+        // 16-byte bank groups: search the block order, the row skew s8, the tile pitch, the
+        // contraction / output orders and per-tile skews (cached per shape).
+        const uint32_t lbt = G.logNxb + G.logNyb, npass = ((G.grp4 ? 4u : 1u) << lbt) >> 3;
+        const uint32_t TS0 = G.TS, NTs = NT;
+        const uint32_t smp[4] = {0, npass > 1 ? 1u : 0u, npass / 2, npass - 1};
+        const bool any_adj = !G.grp4 && g > 0;
+        auto cost_of = [&]() {
+            const uint32_t lf = G.sf_xfast ? G.logNxb : G.logNyb;
+            uint32_t cost = 0;
+            for (uint32_t si = 0; si < 4; ++si)
+                for (uint32_t adj = 0; adj < (any_adj ? 2u : 1u); ++adj)
+                    for (uint32_t pat = 0; pat < 8; ++pat)
+                        for (uint32_t ph = 0; ph < 4; ++ph) {
+                            uint32_t cnt[8] = {0}, mx = 0;
+                            for (uint32_t l = 8 * ph; l < 8 * ph + 8; ++l) {
+                                const uint32_t gq = l >> 2, cq = l & 3u, b = 8 * smp[si] + gq;
+                                const uint32_t bq = b & ((1u << lbt) - 1), i0 = bq & ((1u << lf) - 1), i1 = bq >> lf;
+                                const uint32_t xbv = G.xb_tab[G.sf_xfast ? i0 : i1], ybv = G.yb_tab[G.sf_xfast ? i1 : i0];
+                                const uint32_t slot = (b >> lbt) * G.TS;
+                                const uint32_t comp = pat < 4 ? G.sf_pi[4 * pat + cq]
+                                                              : G.sf_sigma[8 * ((pat - 4) >> 1) + 2 * cq + ((pat - 4) & 1u)];
+                                const uint32_t a = adj ? slot + ybv * G.PD + (ybv >> 3) * G.s8 + xbv + G.cadj[comp]
+                                                       : slot + xbv * G.PD + (xbv >> 3) * G.s8 + ybv + G.cdir[comp];
+                                mx = std::max(mx, ++cnt[a & 7u]);
+                            }
+                            cost += mx;
+                        }
+            return cost;
+        };
+        // one descent pass over pairwise swaps of the contraction and output orders
+        auto swap_pass = [&](uint32_t& cur) {
+            for (int which = 0; which < 2; ++which) {
+                uint8_t* perm = which ? G.sf_sigma : G.sf_pi;
+                for (uint32_t a = 0; a < 16; ++a)
+                    for (uint32_t b = a + 1; b < 16; ++b) {
+                        std::swap(perm[a], perm[b]);
+                        const uint32_t c = cost_of();
+                        if (c < cur)
+                            cur = c;
+                        else
+                            std::swap(perm[a], perm[b]);
+                    }
+            }
+        };
+        const uint32_t ideal = 4u * (any_adj ? 2u : 1u) * 8u * 4u;
+        const size_t stage_cap = 213u * 1024u / 16u;  // elements per stage (3 stages + static tables)
+        const uint64_t key = search_key(G, 3, 0);
+        std::array<uint8_t, 65> cached;
+        if (search_get(key, cached)) {
+            for (uint32_t t = 0; t < NTs; ++t)
+                G.tsk[t] = cached[t];
+            for (uint32_t i = 0; i < 16; ++i) {
+                G.sf_pi[i] = cached[16 + i];
+                G.sf_sigma[i] = cached[32 + i];
+            }
+            G.s8 = cached[48];
+            G.sf_xfast = cached[49];
+            G.TS = TS0 + (S0 >> 3) * G.s8 + cached[50];
+            tables();
+        } else {
+            uint32_t best = ~0u, bx = 0, bs = 0, be = 0;
+            uint8_t bpi[16], bsig[16];
+            for (uint32_t xf = 0; xf < 2 && best > ideal; ++xf)
+                for (uint32_t s8 = 0; s8 < 8 && best > ideal; ++s8)
+                    for (uint32_t e = 0; e < 8 && best > ideal; ++e) {
+                        const uint32_t TS = TS0 + (S0 >> 3) * s8 + e;
+                        if (NTs * TS + 7 > stage_cap)
+                            continue;
+                        G.sf_xfast = xf;
+                        G.s8 = s8;
+                        G.TS = TS;
+                        for (uint32_t i = 0; i < 16; ++i)
+                            G.sf_pi[i] = G.sf_sigma[i] = (uint8_t)i;
+                        for (uint32_t t = 0; t < 64; ++t)
+                            G.tsk[t] = 0;
+                        tables();
+                        uint32_t cur = cost_of();
+                        if (cur > ideal)
+                            swap_pass(cur);
+                        if (cur < best) {
+                            best = cur;
+                            bx = xf;
+                            bs = s8;
+                            be = e;
+                            std::memcpy(bpi, G.sf_pi, 16);
+                            std::memcpy(bsig, G.sf_sigma, 16);
+                        }
+                    }
+            G.sf_xfast = bx;
+            G.s8 = bs;
+            G.TS = TS0 + (S0 >> 3) * bs + be;
+            std::memcpy(G.sf_pi, bpi, 16);
+            std::memcpy(G.sf_sigma, bsig, 16);
+            tables();
+            uint32_t cur = best;
+            for (uint32_t pass = 0; pass < 2 && cur > ideal; ++pass) {
+                for (uint32_t t = 0; t < NTs && NTs > 1; ++t) {  // per-tile skews
+                    uint8_t bv = G.tsk[t];
+                    for (uint32_t v = 0; v < 8; ++v) {
+                        G.tsk[t] = (uint8_t)v;
+                        tables();
+                        const uint32_t c = cost_of();
+                        if (c < cur) {
+                            cur = c;
+                            bv = (uint8_t)v;
+                        }
+                    }
+                    G.tsk[t] = bv;
+                    tables();
+                }
+                swap_pass(cur);
+            }
+            std::array<uint8_t, 65> v{};
+            for (uint32_t t = 0; t < NTs; ++t)
+                v[t] = G.tsk[t];
+            for (uint32_t i = 0; i < 16; ++i) {
+                v[16 + i] = G.sf_pi[i];
+                v[32 + i] = G.sf_sigma[i];
+            }
+            v[48] = (uint8_t)G.s8;
+            v[49] = (uint8_t)G.sf_xfast;
+            v[50] = (uint8_t)(G.TS - TS0 - (S0 >> 3) * G.s8);
+            search_put(key, v);
+        }
+        if (G.grp4) {  // independent tiles at slot t * TS: one skew
+            for (uint32_t t = 1; t < NTs; ++t)
+                G.tsk[t] = G.tsk[0];
+            tables();
+        }
+        G.sf_cost = cost_of();
+        G.sf_ideal = ideal;
+        extra = 7;
+    } else if (dmma && (D == 8 || (D == 4 && qstride))) {
         // the DMMA transform's lane patterns (load B[2c+j][g], store Z[g][2c+j]; k = 2: the 8 x 8
         // matrix of four quadrant blocks at offset qstride) hit 16-byte bank groups (addr mod 8) by
         // component offset: pick a tile pitch and per-tile skews that spread every quarter-warp
@@ -724,6 +863,13 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
 
 // internal: a k = 2 Kraus sum the tensor-core gather cannot take (hs_apply_kraus falls back)
 constexpr int RC_NO_KRAUS_SUM = -1000;
+// k = 2 Kraus sums of rank 2..4: the per-operator direct form on the k = 3 gather (96 FMA per element
+// per operator pair through I2 (x) L) instead of the S form (48 per element, any rank); off by
+// default, kept for comparison (HS_KRAUS2_DIRECT=1)
+const bool g_kraus2_direct = [] {
+    const char* e = getenv("HS_KRAUS2_DIRECT");
+    return e && atoi(e) != 0;
+}();
 
 int sm_count(int device) {
     static int cache[64] = {0};
@@ -738,8 +884,11 @@ int sm_count(int device) {
     return cache[device];
 }
 
-template <int K, int MODE, int NS>
-int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+// Shard prelude of every launch: a cross-shard operation reads the group members' tiles -- in
+// place (peer mode: their current buffers; the result goes to this shard's other buffer) or from
+// the exchange slots of the last exchange.  carry_over: tiles the operation leaves untouched must be
+// copied into the output buffer first (monomials, three-buffer Kraus sums in peer mode).
+int shard_prelude(hs_state* h, const Geo& G0, bool carry_over, Geo& G) {
     const bool peer = G0.cmask && h->peer_mode;
     if (peer) {
         for (uint32_t d = 1; d < 32; ++d)
@@ -748,7 +897,7 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
     } else if (G0.cmask && (!h->recv || (G0.cmask & ~h->recv_mask) ||
                             h->recv_slots < (1u << __builtin_popcount(h->recv_mask)) - 1))
         return set_err(HS_ERR_INVALID, "cross-shard operation: exchange with the group's shards first");
-    Geo G = G0;
+    G = G0;
     if (peer) {
         // read the group members' current payloads where they lie, write ours into the other
         // buffer (the members read our current one concurrently); slots follow the op's own mask
@@ -769,7 +918,7 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
             G.rbase[slot - 1] = h->peer_buf[h->shard ^ d][h->flip];
         }
         G.out = h->buf[h->flip ^ 1];
-        if (MODE == M_MONO || MODE == M_KRAUS)  // tiles a monomial leaves untouched must carry over
+        if (carry_over)  // tiles a monomial leaves untouched must carry over
             CUDA_TRY(cudaMemcpyAsync(G.out, h->d, h->count * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
     } else if (G.cmask) {  // exchange-slot layout of the last exchange (it may cover more bits than needed)
         G.xmask = h->recv_mask;
@@ -782,6 +931,17 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
     }
     G.rev = (uint32_t)(h->sweeps++ & 1u);
     G.dbg = 0;
+    return HS_OK;
+}
+
+template <int K, int MODE, int NS>
+int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+    Geo G;
+    {
+        const int rc = shard_prelude(h, G0, MODE == M_MONO || MODE == M_KRAUS, G);
+        if (rc)
+            return rc;
+    }
     if (MODE == M_MONO && G.groups) {
         // tile permutation on >= 2 grid bits: whole-tile pipeline, items = (unit, cycle group);
         // diagonal units through the slab kernel's wedge path
@@ -1002,19 +1162,71 @@ pipe_path:
     return HS_OK;
 }
 
-// One operation's kernels.  Peer mode: the result went to the other buffer, which becomes current.
-template <int K, int MODE, int NS>
-int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
-    const int rc = launch_impl<K, MODE, NS>(h, G0, cf, ka, buffers);
+// k = 2 Kraus sum in S form (16 x 16 transfer matrix) on the tensor-core gather, every regime:
+// whole tiles (no grid target: items of 4 local tiles; one grid target: 2 x 2-tile units) or 16 x 16
+// sub-blocks of 4 x 4-tile units (two grid targets), bulk-row staging, sform2 transform.
+int launch_sform2_impl(hs_state* h, const Geo& G0, const Coef<256>& cf) {
+    if (h->m != 5)
+        return RC_NO_KRAUS_SUM;
+    Geo G;
+    {
+        const int rc = shard_prelude(h, G0, false, G);
+        if (rc)
+            return rc;
+    }
+    if (G.g == 0) {
+        G.grp4 = 1;
+        G.logNT = 2;
+        G.nloc_tiles = h->count >> 10;
+    }
+    plan_gather(G, false, true, 0, false, false, true);
+    {
+        static const char* dbg = getenv("HS_DEBUG_FLAGS");
+        G.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
+    }
+    if (!G.bulk)
+        return RC_NO_KRAUS_SUM;
+    if (G.dbg & 512u)
+        fprintf(stderr, "sform2: g=%u in_mask=%x S0=%u TS=%u s8=%u xfast=%u bank cost %u (ideal %u) stage %u elems\n", G.g,
+                G.in_mask, G.S0, G.TS, G.s8, G.sf_xfast, G.sf_cost, G.sf_ideal, G.stage_elems);
+    G.ws_diag = 1;
+    G.nG_items = G.grp4 ? (G.nloc_tiles + 3) / 4 : G.nU_loose << (2 * G.log_nsb_side);
+    const size_t smem = (size_t)G.stages * G.stage_elems * sizeof(double2);
+    auto kw = gather_ws_kernel<2, 256, M_SF2, true>;
+    cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(sform2): ") + cudaGetErrorString(e));
+    const uint64_t grid = std::min<uint64_t>(G.nG_items, (uint64_t)sm_count(h->device));
+    if (grid) {
+        CUtensorMap tin{}, tout{};
+        kw<<<(unsigned)grid, 512, smem, h->stream>>>(G, cf, h->d, tin, tout);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return set_err(HS_ERR_CUDA, std::string("gather_ws_kernel(sform2) launch: ") + cudaGetErrorString(e));
+    }
+    return HS_OK;
+}
+
+// After a launch: peer mode makes the output buffer current; an exchange licenses one operation.
+int after_launch(hs_state* h, const Geo& G0, int rc) {
     if (rc == HS_OK && G0.cmask && h->peer_mode) {
         h->flip ^= 1u;
         h->d = h->buf[h->flip];
     }
-    // an exchange licenses exactly one cross-shard operation: after it, this shard's and the
-    // members' payloads have moved on and the exchange slots are stale
     if (rc == HS_OK && G0.cmask && !h->peer_mode)
         h->recv_mask = 0;
     return rc;
+}
+
+int launch_sform2(hs_state* h, const Geo& G0, const Coef<256>& cf) {
+    return after_launch(h, G0, launch_sform2_impl(h, G0, cf));
+}
+
+// One operation's kernels.  Peer mode: the result went to the other buffer, which becomes current.
+template <int K, int MODE, int NS>
+int launch(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs& ka, int buffers) {
+    return after_launch(h, G0, launch_impl<K, MODE, NS>(h, G0, cf, ka, buffers));
 }
 
 // Subcase counters (SubcaseCounters, kernels.hpp:29-41) for the cross/mixed engines: A = unit
@@ -1545,9 +1757,12 @@ int hs_apply_transfer(hs_state* h, int k, const double* s, const uint32_t* t, hs
             G.cmask = 0;
         rc = launch<1, M_S1, 16>(h, G, cf, ka, 1);
     } else {
+        // the 16 x 16 transfer matrix on the FP64 tensor path (sform2), else the scalar pipeline
         auto* cf = new Coef<256>();
         std::memcpy(cf->s, s, sizeof(cf->s));
-        rc = launch<2, M_S2, 256>(h, G, *cf, ka, 1);
+        rc = launch_sform2(h, G, *cf);
+        if (rc == RC_NO_KRAUS_SUM)
+            rc = launch<2, M_S2, 256>(h, G, *cf, ka, 1);
         delete cf;
     }
     if (rc)
@@ -1764,7 +1979,7 @@ int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32
             return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
         }
     }
-    if (k == 2 && nops <= 4 && h->m == 5) {
+    if (k == 2 && nops <= 4 && h->m == 5 && g_kraus2_direct) {
         // sum_a L_a B L_a^dagger on the tensor-core gather (I2 (x) L pairing) when it applies: at
         // least one grid target and the paired geometry; otherwise the transfer matrix below
         DeviceGuard dg(h->device);

@@ -260,6 +260,113 @@ __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const 
         pass(b, b + NC / 32, NQ == 2 && b + NC / 32 < nblk);
 }
 
+// k = 2 Kraus sum through its row-stacked transfer matrix S (16 x 16 complex; kernels.cpp:27-48,
+// the reference's matvec<16> per block) on the FP64 tensor path: W^T = V^T S^T for 8 blocks per warp
+// pass, one mma.sync m8n8k4 per (k-step ks, n-tile nt, real product).  A fragment = the blocks'
+// components (lane (g, c): block g, component sf_pi[4 ks + c]), B fragment = S^T, constant per lane
+// (S[sf_sigma[8 nt + g]][sf_pi[4 ks + c]]), accumulator = outputs (lane (g, c): block g, components
+// sf_sigma[8 nt + 2 c + j]).  3M form: P1 = Vr Sr^T, P2 = Vi Si^T, P3 = (Vr + Vi)(Sr + Si)^T;
+// Wr = P1 - P2, Wi = P3 - P1 - P2: 24 DMMA per 8 blocks (48 FMA per element, whatever the rank;
+// the direct form costs 24 per element per Kraus operator).  Staged tiles keep their stored
+// orientation (bulk rows); adjoint components are addressed through cadj and conjugated.
+struct SfFrag {
+    double sr[2][4], si[2][4];
+    uint32_t ld[4], st[4];  // component offsets: direct (low 16 bits) | adjoint (high 16 bits)
+    uint32_t tl, ts;        // their logical tiles, 4 bits each (adjoint flags per item)
+};
+template <int NS>
+__device__ __forceinline__ SfFrag sform2_frag(const Geo& G, const Tabs& T, const Coef<NS>& cf) {
+    SfFrag f;
+    const uint32_t lane = threadIdx.x & 31u, gq = lane >> 2, cq = lane & 3u;
+    f.tl = f.ts = 0;
+#pragma unroll
+    for (uint32_t ks = 0; ks < 4; ++ks) {
+        const uint32_t ci = G.sf_pi[4 * ks + cq];
+#pragma unroll
+        for (uint32_t nt = 0; nt < 2; ++nt) {
+            const double2 v = cf.s[G.sf_sigma[8 * nt + gq] * 16 + ci];
+            f.sr[nt][ks] = v.x;
+            f.si[nt][ks] = v.y;
+        }
+        f.ld[ks] = (uint32_t)T.cdir[ci] | ((uint32_t)T.cadj[ci] << 16);
+        f.tl |= (uint32_t)T.ttr[ci] << (4 * ks);
+    }
+#pragma unroll
+    for (uint32_t q = 0; q < 4; ++q) {
+        const uint32_t co = G.sf_sigma[8 * (q >> 1) + 2 * cq + (q & 1u)];
+        f.st[q] = (uint32_t)T.cdir[co] | ((uint32_t)T.cadj[co] << 16);
+        f.ts |= (uint32_t)T.ttr[co] << (4 * q);
+    }
+    return f;
+}
+template <int NC>
+__device__ __forceinline__ void sform2(const Geo& G, const Tabs& T, const SfFrag& f, uint64_t am, double2* sb,
+                                       uint32_t warp) {
+    // passes in flight per warp: one (two independent chains spill at the 128 registers of a 512-thread
+    // CTA; the eight transform warps keep the FP64 pipe fed with three chains each)
+    constexpr uint32_t NQ = 1;
+    const uint32_t lane = threadIdx.x & 31u, gq = lane >> 2;
+    uint32_t fl = 0;  // bit ks: loaded component adjoint; bit 4 + q: stored component adjoint
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) {
+        fl |= (uint32_t)((am >> ((f.tl >> (4 * i)) & 15u)) & 1ull) << i;
+        fl |= (uint32_t)((am >> ((f.ts >> (4 * i)) & 15u)) & 1ull) << (4 + i);
+    }
+    const uint32_t lbt = G.logNxb + G.logNyb, npass = ((G.grp4 ? 4u : 1u) << lbt) >> 3;
+    const uint32_t lfast = G.sf_xfast ? G.logNxb : G.logNyb, fmask = (1u << lfast) - 1;
+    for (uint32_t p0 = warp; p0 < npass; p0 += NQ * (NC / 32)) {
+        uint32_t base[NQ], baseA[NQ];
+        double vr[NQ][4], vi[NQ][4];
+#pragma unroll
+        for (uint32_t q = 0; q < NQ; ++q) {
+            const uint32_t p = min(p0 + q * (NC / 32), npass - 1);  // a missing pass recomputes the last one
+            const uint32_t b = 8 * p + gq, bq = b & ((1u << lbt) - 1);
+            const uint32_t i0 = bq & fmask, i1 = bq >> lfast;
+            const uint32_t xbv = T.xb[G.sf_xfast ? i0 : i1], ybv = T.yb[G.sf_xfast ? i1 : i0];
+            const uint32_t slot = (b >> lbt) * G.TS;
+            base[q] = slot + xbv * G.PD + (xbv >> 3) * G.s8 + ybv;
+            baseA[q] = slot + ybv * G.PD + (ybv >> 3) * G.s8 + xbv;
+#pragma unroll
+            for (uint32_t ks = 0; ks < 4; ++ks) {
+                const uint32_t adj = (fl >> ks) & 1u;
+                const double2 v = sb[adj ? baseA[q] + (f.ld[ks] >> 16) : base[q] + (f.ld[ks] & 0xffffu)];
+                vr[q][ks] = v.x;
+                vi[q][ks] = flip_sign(v.y, adj << 31);
+            }
+        }
+        const bool two = p0 + (NC / 32) < npass;
+#pragma unroll
+        for (uint32_t nt = 0; nt < 2; ++nt) {
+            double p1[NQ][2], p2[NQ][2], p3[NQ][2];
+#pragma unroll
+            for (uint32_t q = 0; q < NQ; ++q)
+                p1[q][0] = p1[q][1] = p2[q][0] = p2[q][1] = p3[q][0] = p3[q][1] = 0.0;
+#pragma unroll
+            for (uint32_t ks = 0; ks < 4; ++ks) {
+                const double ss = f.sr[nt][ks] + f.si[nt][ks];
+#pragma unroll
+                for (uint32_t q = 0; q < NQ; ++q) {
+                    dmma_acc(p1[q][0], p1[q][1], vr[q][ks], f.sr[nt][ks]);
+                    dmma_acc(p2[q][0], p2[q][1], vi[q][ks], f.si[nt][ks]);
+                    dmma_acc(p3[q][0], p3[q][1], vr[q][ks] + vi[q][ks], ss);
+                }
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < NQ; ++q) {
+                if (q && !two)
+                    break;
+#pragma unroll
+                for (uint32_t j = 0; j < 2; ++j) {
+                    const uint32_t o = 2 * nt + j, adj = (fl >> (4 + o)) & 1u;
+                    const double wr = p1[q][j] - p2[q][j], wi = p3[q][j] - p1[q][j] - p2[q][j];
+                    sb[adj ? baseA[q] + (f.st[o] >> 16) : base[q] + (f.st[o] & 0xffffu)] =
+                        make_double2(wr, flip_sign(wi, adj << 31));
+                }
+            }
+        }
+    }
+}
+
 __device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group
 template <int K, int MODE, int NS, int NC>
 __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
@@ -483,12 +590,18 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
 // tile and box position), SWIZZLE_128B, each box at a 128-B phase of its own (host search) so the
 // DMMA lane patterns spread over the bank groups; same two-copy-group schedule as BULK.
 // KSUM: the k = 2 Kraus-sum variant (own instantiation, so the unitary kernels keep their registers)
+// SF (MODE == M_SF2): the S-form transform; 8 transform warps and 8 copy warps (512 threads, 128
+// registers: the per-lane S fragments stay in registers).  With 16-row sub-blocks (two grid targets)
+// the copy side issues 512 bulk row copies per item: 2 copy warps streamed 4.2 TB/s, 8 copy warps
+// 6.2 TB/s (n = 16, copies alone); transform alone 8.8 ms (profiles/r02_kraus_sform.txt).
 template <int K, int NS, int MODE = M_DIRECT, bool BULK = false, bool TMAB = false, bool KSUM = false>
-__global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st,
-                                                           const __grid_constant__ CUtensorMap tin,
-                                                           const __grid_constant__ CUtensorMap tout) {
+__global__ void __launch_bounds__(MODE == M_SF2 ? 512 : 768, 1)
+    gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st, const __grid_constant__ CUtensorMap tin,
+                     const __grid_constant__ CUtensorMap tout) {
     // bulk rows need few copy instructions: 16 transform warps and 8 copy warps (else 8 and 16)
-    constexpr uint32_t NCW = BULK ? 512 : 256, NMW = BULK ? 256 : 512, S = 3;
+    constexpr bool SF = MODE == M_SF2;
+    static_assert(!SF || BULK, "the S-form transform runs on bulk-row staging");
+    constexpr uint32_t NCW = SF ? 256 : BULK ? 512 : 256, NMW = SF ? 256 : BULK ? 256 : 512, S = 3;
     // tile tables by item % TSL, built S items ahead (BULK: by two copy groups that may be one item
     // apart, hence two more slots)
     constexpr uint32_t TSL = BULK ? S + 3 : S + 1;
@@ -530,6 +643,9 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         DmmaFrag fr;
         if constexpr (MODE == M_DIRECT)
             fr = dmma_frag<K, NS, BULK, TMAB>(G, T, cf);
+        SfFrag sf;
+        if constexpr (SF)
+            sf = sform2_frag(G, T, cf);
         double* kf = nullptr;
         if constexpr (KSUM) {
             // Kraus sum: every operator's per-lane fragment values, [a][8][lane] (8 KiB)
@@ -557,7 +673,10 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
             double2* sb = ring + (size_t)s * G.stage_elems;
-            if constexpr (MODE == M_DIRECT) {
+            if constexpr (SF) {
+                if (!(G.dbg & 1u))
+                    sform2<NCW>(G, T, sf, am[i % TSL][0], sb, tid >> 5);
+            } else if constexpr (MODE == M_DIRECT) {
                 if constexpr (KSUM) {
                     if (!(G.dbg & 1u))
                         dmma_direct3<NCW, K, BULK, TMAB, true>(G, T, fr, am[i % TSL][0], sb, tid >> 5, kf, cf.nk);
@@ -640,6 +759,8 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
         const unsigned bal = __ballot_sync(0xffffffffu, adj);
         if ((t & 31) == 0)
             reinterpret_cast<uint32_t*>(&am[ts][0])[t >> 5] = bal;  // little endian: tiles 0-31, 32-63
+        if (NMW / 2 == 32 && t == 0)  // one-warp copy groups (NT <= 32): tiles 32-63 absent
+            reinterpret_cast<uint32_t*>(&am[ts][0])[1] = 0u;
     };
     // cp.async of item j into stage j % S (its table is visible: a copy-warp barrier separates them)
     auto issue = [&](uint64_t j) {
@@ -730,7 +851,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                         const bool adj = (ent & F_ADJ) != 0;
                         const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
                         mbar_expect(&full[s], rbytes);
-                        bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD + c) * 16u, tile_base(G, ent, st) + g, rbytes,
+                        bulk_g2s(base + (t * G.TS + T.tsk[t] + r * G.PD + (r >> 3) * G.s8 + c) * 16u, tile_base(G, ent, st) + g, rbytes,
                                  &full[s]);
                     }
                 }
@@ -773,7 +894,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                         if (!(ent & F_NOSTORE)) {
                             const bool adj = (ent & F_ADJ) != 0;
                             const uint64_t g = ((ent & F_MASK) << (2 * G.logM)) + run_off(adj, x0, y0, r, c);
-                            bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD + c), rbytes);
+                            bulk_s2g(G.out + g, smem_u32(sb + t * G.TS + T.tsk[t] + r * G.PD + (r >> 3) * G.s8 + c), rbytes);
                             bulk_commit();
                         }
                     }
@@ -788,7 +909,7 @@ __global__ void __launch_bounds__(768, 1) gather_ws_kernel(const Geo G, const Co
                                 const uint32_t sl = (tt << lbpt) + (j0 >> 3) * nbx + (i0 >> 3);
                                 a = T.cdir[sl] + (j0 & 7u) * 8u + ((i0 & 7u) ^ (((j0 & 7u) + T.tsk[sl]) & 7u));
                             } else {
-                                a = tt * G.TS + T.tsk[tt] + j0 * P + i0;
+                                a = tt * G.TS + T.tsk[tt] + j0 * P + (j0 >> 3) * G.s8 + i0;
                             }
                             const double2 w = sb[a];
                             G.out[((ent & F_MASK) << (2 * G.logM)) + ((uint64_t)(y0 | T.xdep[i0]) << G.logM) +

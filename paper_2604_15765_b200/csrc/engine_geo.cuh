@@ -13,7 +13,7 @@ constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in 
 constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_NOSTORE = 1ull << 60,
                    F_REMOTE = 1ull << 59, F_MIRROR = 1ull << 55, F_MASK = (1ull << 55) - 1;
 
-enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5, M_PROG = 6 };
+enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5, M_PROG = 6, M_SF2 = 7 };
 
 thread_local std::string g_err;
 thread_local bool g_plan_subcases = true;  // hs_set_plan_subcases
@@ -103,6 +103,16 @@ struct Geo {
     uint32_t tq;                  // tma: 4 when bit 3 of the sub-block is a block-position bit (quadrant per warp)
     uint32_t grp4;                // gather_ws, in-tile k = 3: an item is 4 consecutive local stored tiles
     uint64_t nloc_tiles;          // grp4: local stored tiles
+    // bulk staging: row x of a staged tile sits at x * PD + (x >> 3) * s8 (rows 8 apart share banks
+    // otherwise; the offset is additive over disjoint row bits, so block bases and component offsets
+    // still add)
+    uint32_t s8;
+    // S-form transform (M_SF2, k = 2 transfer matrix on the FP64 tensor path): contraction order
+    // (k-step ks, lane column c) -> component sf_pi[4 ks + c], output order (n-tile, column) ->
+    // component sf_sigma[8 nt + n]; blocks of a pass run along rows (sf_xfast) or columns
+    uint8_t sf_pi[16], sf_sigma[16];
+    uint32_t sf_xfast;
+    uint32_t sf_cost, sf_ideal;   // planner diagnostics: bank-group cost of the chosen S-form layout / its ideal
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).

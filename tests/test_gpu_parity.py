@@ -144,6 +144,38 @@ def test_gather_staging_modes(H, HS, oracle, orc, dual):
     st.free()
 
 
+def _depolarising2(p):
+    """Two-qubit depolarising channel: rank 16 (sqrt(1 - p) I, sqrt(p / 15) P for the 15 Paulis)."""
+    P = [np.eye(2), np.array([[0, 1], [1, 0]]), np.array([[0, -1j], [1j, 0]]), np.diag([1.0, -1.0])]
+    ops = [np.kron(a, b).astype(np.complex128) for a in P for b in P]
+    w = [np.sqrt(1 - p)] + [np.sqrt(p / 15)] * 15
+    return np.stack([wi * o for wi, o in zip(w, ops)])
+
+
+@pytest.mark.parametrize("rank", [2, 4, 16])
+def test_kraus2_sform_every_pair(H, HS, oracle, orc, rank):
+    """k = 2 Kraus sums of rank 2, 4 and 16 (the S-form transform on the FP64 tensor path) on every
+    ordered target pair at n = 10, m = 5: in-tile, mixed and cross regimes, diagonal units."""
+    n, m = 10, 5
+    ops = _depolarising2(0.2) if rank == 16 else _random_kraus(2, rank, 400 + rank)
+    spec, och = H.make_generic("k", ops), oracle.generic(ops)
+    psi = HS.rank_psi(n, 93, 4)
+    base = HS.rho_payload(n, psi, m)
+    fro = orc.frobenius(base, n, m)
+    st = H.TiledHermitian(n, m)
+    worst = 0.0
+    for tg in itertools.permutations(range(n), 2):
+        want = base.copy()
+        orc.apply(want, n, m, och, list(tg))
+        st.upload(base)
+        H.apply(st, spec, list(tg))
+        err = oracle.rel_max_err(st.download(), want, fro)
+        worst = max(worst, err)
+        assert err <= TOL, f"rank {rank} {tg}: err {err}"
+    print(f"kraus2 rank {rank}: worst rel err {worst:.3e} over {n * (n - 1)} pairs")
+    st.free()
+
+
 @pytest.mark.parametrize("n,m", [(10, 5), (9, 3), (7, 5), (3, 5), (8, 0)])
 def test_cx_layer_bit_identical(H, HS, n, m):
     """hs_apply_cx_layer (fusion) equals one native CX after the other, bit for bit: in-tile,

@@ -27,21 +27,26 @@ def kraus(k, r, seed):
     return q.reshape(r, d, d)
 
 
-cases = [(1, [3]), (1, [9]), (2, [1, 3]), (2, [2, 9]), (2, [8, 12]), (3, [0, 2, 4]), (3, [1, 3, 9]),
-         (3, [2, 8, 12]), (3, [6, 9, 13])]
+cases = [(1, [3]), (1, [9]), (2, [1, 3]), (2, [3, 4]), (2, [2, 9]), (2, [9, 2]), (2, [8, 12]), (2, [14, 15]),
+         (3, [0, 2, 4]), (3, [1, 3, 9]), (3, [2, 8, 12]), (3, [6, 9, 13])]
+ranks = {1: (2, 4), 2: tuple(int(x) for x in os.environ.get("RANKS2", "2,4,16").split(",")),
+         3: tuple(int(x) for x in os.environ.get("RANKS3", "2,4").split(","))}
+reps = int(os.environ.get("REPS", "3"))
 ev = [ctypes.c_void_p() for _ in range(2)]
 for e in ev:
     nat.check(L.hs_event_create(ctypes.byref(e)))
 for k, tg in cases:
-    for r in (2, 4):
+    for r in ranks[k]:
         spec = H.make_generic(f"kraus{k}_{r}", kraus(k, r, 10 * k + r))
         H.apply(st, spec, tg, opts)
         st.synchronize()
         L.hs_event_record(ev[0], st.handle)
-        plan = H.apply(st, spec, tg, opts)
+        for _ in range(reps):
+            plan = H.apply(st, spec, tg, opts)
         L.hs_event_record(ev[1], st.handle)
         st.synchronize()
         x = ctypes.c_float()
         nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(x)))
-        print(f"k={k} rank={r} targets {str(tg):12s} path={plan.path:14s} {x.value:8.3f} ms  "
-              f"{2 * S / x.value / 1e6:7.0f} GB/s at 2S")
+        t = x.value / reps
+        print(f"k={k} rank={r:2d} targets {str(tg):12s} path={plan.path:14s} {t:8.3f} ms  "
+              f"{2 * S / t / 1e6:7.0f} GB/s at 2S", flush=True)
