@@ -19,11 +19,12 @@ stored).  A step = one pass of the 32 channel applications.
 * cpu_baseline  the reference library itself (oracle/_ref/libhermsim_ref.so, built from
              /root/reference) timed on this host on a bounded sample of the same workload.
 * --impl reference  times that reference CPU path alone, all host threads (rank 0 only).
-For N > 1 (torchrun) every rank runs an independent replica of the config (weak scaling) -- except
-with --shard (the default for c4, the sharded n = 17 config): the operator is partitioned into N XOR-
-block shards, one per GPU; a cross-shard op's kernels read the group members' tiles in place over
-NVLink (peer mode, CUDA IPC) or, with --exchange, after an NCCL group exchange; the whole job
-processes one operator (strong scaling; value = ops of the operator per second).
+For N > 1 (torchrun) the operator is partitioned into N XOR-block shards, one per GPU (strong
+scaling; value = ops of the one operator per second); a cross-shard op's kernels read the group
+members' tiles in place over NVLink (peer mode, CUDA IPC) or, with --exchange, after an NCCL group
+exchange.  --remap adds qubit remapping (multigpu.plan_remap); --replicas runs N independent copies
+instead (weak scaling).  roofline_nvlink: remote bytes a cross-shard op reads / its time / the
+measured NVLink peer bandwidth (B200_PROFILING.md: 770 GB/s per direction).
 """
 from __future__ import annotations
 
@@ -45,6 +46,7 @@ sys.path.insert(0, ROOT)
 METRIC = "gate conjugations/sec and achieved HBM GB/s (fraction of roofline), n=16 fp64"
 UNIT = "gate conjugations/s"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+NVLINK_GBS = 770.0  # B200_PROFILING.md: measured peer copy, per direction per GPU (900 nominal)
 
 WORKLOADS = {
     "c0": "C0: Hadamard at qubits 0..11 (12 ops) on an n=12 rank-4 rho, m=5",
@@ -210,23 +212,35 @@ def load_peaks():
     return FALLBACK_HBM_GBS, "B200_PROFILING.md fallback (MEASURED_PEAKS.json absent)"
 
 
-def load_traffic(cfg: str):
+def traffic_key(cfg: str, n: int, shards: int = 1) -> str:
+    return f"{cfg}:n{n}" + (f":p{shards}" if shards > 1 else "")
+
+
+def load_traffic(cfg: str, n: int, shards: int = 1):
+    """ncu DRAM bytes per launch of the config's dominant kernel, captured at exactly this (config,
+    n, shards) (profiles/ncu_traffic.json); None when no capture matches."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None, None
     with open(p) as f:
         d = json.load(f)
-    e = d.get(cfg)
+    e = d.get(traffic_key(cfg, n, shards))
     if not e:
         return None, None
     return e.get("traffic_bytes_per_launch"), e.get("source")
 
 
 # --------------------------------------------------------------------------- reference arm
-def reference_sample_ops(cfg: str, n: int, steps: int):
-    from paper_2604_15765_b200 import harness as HS
-    ops = HS.config_ops(cfg, n)
-    return ops
+def stratified_order(nblocks: int) -> list[int]:
+    """Block indices in van der Corput order (bit-reversed counter): every prefix of the order is
+    spread evenly over the sequence, so a short timed sample covers all qubit positions alike."""
+    bits = max(1, (nblocks - 1).bit_length())
+    out = []
+    for i in range(1 << bits):
+        b = int(format(i, f"0{bits}b")[::-1], 2)
+        if b < nblocks:
+            out.append(b)
+    return out
 
 
 def ref_channel(O, op):
@@ -247,29 +261,30 @@ def ref_channel(O, op):
     raise ValueError(op.kind)
 
 
-def run_reference_cpu(cfg: str, n: int, m: int, payload: np.ndarray, ops_per_step: int, steps: int, warmup: int,
-                      threads: int, budget_s: float | None = None):
-    """Times the compiled reference (hermsim::apply, threads = host cores) on consecutive chunks of
-    the config's op sequence, `ops_per_step` ops per step."""
+def run_reference_cpu(cfg: str, n: int, m: int, fill, ops_per_step: int, steps: int, warmup: int, threads: int,
+                      budget_s: float | None = None):
+    """Times the compiled reference (hermsim::apply, threads = host cores).  The state is built in
+    the reference's own buffer by `fill(view)` (no second host copy: n = 17 is 137.5 GB).  A step is
+    a block of `ops_per_step` consecutive ops of the config's sequence; the timed steps take the
+    blocks in stratified order (stratified_order) from the start, the warm-up steps take blocks from
+    the end of that order, so warm-up never displaces a position from the timed sample.
+    Returns (times, blocks, ops_total)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
+    from paper_2604_15765_b200 import harness as HS
     ref = O.Reference()
-    h = ref.create(n, m, payload)
-    seq = reference_sample_ops(cfg, n, steps)
-    # consecutive blocks of ops_per_step ops, the blocks spread evenly over the sequence so the
-    # sample mixes intra-tile and cross-tile qubits like the full workload
+    h = ref.create(n, m)
+    fill(ref.view(h))
+    seq = HS.config_ops(cfg, n)
     nblocks = max(1, len(seq) // ops_per_step)
-    starts = [ops_per_step * ((b * nblocks) // max(1, warmup + steps)) for b in range(warmup + steps)]
+    order = stratified_order(nblocks)
     chans = {}
-    pos = 0
-    times = []
+    times, used = [], []
     t_start = time.perf_counter()
-    for s in range(warmup + steps):
+    plan = [order[-1 - (w % len(order))] for w in range(warmup)] + [order[k % len(order)] for k in range(steps)]
+    for s, b in enumerate(plan):
         t0 = time.perf_counter()
-        pos = starts[s] % len(seq)
-        for _ in range(ops_per_step):
-            op = seq[pos % len(seq)]
-            pos += 1
+        for op in seq[b * ops_per_step:(b + 1) * ops_per_step]:
             key = (op.kind, op.param, id(op.matrix) if op.matrix is not None else None)
             ch = chans.get(key)
             if ch is None:
@@ -278,10 +293,24 @@ def run_reference_cpu(cfg: str, n: int, m: int, payload: np.ndarray, ops_per_ste
         dt = time.perf_counter() - t0
         if s >= warmup:
             times.append(dt)
+            used.append(b)
         if budget_s is not None and time.perf_counter() - t_start > budget_s and len(times) >= 1:
             break
     ref.free(h)
-    return times
+    targets = sorted({q for b in used for op in seq[b * ops_per_step:(b + 1) * ops_per_step] for q in op.targets})
+    return times, used, targets
+
+
+def reference_fill(HS, cfg, n, m, threads, psi=None, strings=None):
+    """Callback building the config's seeded input in place (the reference's buffer)."""
+    seed = HS.SEEDS[cfg]
+
+    def fill(view):
+        if cfg == "c3":
+            view[:] = HS.pauli_payload(n, strings if strings is not None else HS.pauli_strings(n, 64, seed), 5)
+        else:
+            host_payload(HS, n, m, psi if psi is not None else HS.rank_psi(n, seed, 4), out=view, threads=threads)
+    return fill
 
 
 # --------------------------------------------------------------------------------- main
@@ -299,8 +328,11 @@ def main():
     ap.add_argument("--e2e-serial", action="store_true",
                     help="e2e without overlapping consecutive steps (one state, one buffer)")
     ap.add_argument("--shard", dest="shard", action="store_true", default=None,
-                    help="partition the operator over the N ranks (default for c4 when N > 1)")
-    ap.add_argument("--replicas", dest="shard", action="store_false", help="N independent replicas")
+                    help="partition the operator over the N ranks (the default when N > 1)")
+    ap.add_argument("--replicas", dest="shard", action="store_false", help="N independent replicas (weak scaling)")
+    ap.add_argument("--remap", action="store_true",
+                    help="sharded: qubit remapping (swap top qubits that keep needing exchanges with low ones)")
+    ap.add_argument("--remap-window", type=int, default=64, help="remapping lookahead (operations)")
     ap.add_argument("--exchange", action="store_true",
                     help="sharded: NCCL exchange of the group's shards before a cross-shard op (default: peer mode, "
                          "the op's kernels read the members' tiles in place over NVLink)")
@@ -329,26 +361,24 @@ def main():
 def reference_arm(args, cfg, n, m, world):
     from paper_2604_15765_b200 import harness as HS
     threads = os.cpu_count() or 1
-    seed = HS.SEEDS[cfg]
     nc = cpu_sample_n(cfg, n, m)
-    if cfg == "c3":
-        payload = HS.pauli_payload(nc, HS.pauli_strings(nc, 64, seed))
-    else:
-        payload = host_payload(HS, nc, m, HS.rank_psi(nc, seed, 4), threads=threads)
     ops_per_step = 2
-    times = run_reference_cpu(cfg, nc, m, payload, ops_per_step, args.steps, args.warmup, threads)
-    del payload
+    times, blocks, covered = run_reference_cpu(cfg, nc, m, reference_fill(HS, cfg, nc, m, threads), ops_per_step,
+                                               args.steps, args.warmup, threads)
     t = float(np.mean(times))
     value = ops_per_step / t / 4.0 ** (n - nc)
+    sample = (f"{ops_per_step} consecutive ops of {cfg} per step at n={nc} through hermsim::apply "
+              "(oracle/_ref/libhermsim_ref.so, threads=nproc); timed blocks in stratified order over the sequence "
+              f"(blocks {blocks}), warm-up blocks separate")
+    if nc != n:
+        sample += f"; host RAM/time-bounded, extrapolated to n={n} by 4^(n-{nc})"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": {"workload": WORKLOADS[cfg], "n": n, "m": m, "ops_per_step": ops_per_step},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{ops_per_step} consecutive ops of {cfg} per step (blocks spread over the sequence) at n={nc} through "
-                                   "hermsim::apply (oracle/_ref/libhermsim_ref.so, threads=nproc)"
-                                   + (f"; host RAM/time-bounded, extrapolated to n={n} by 4^(n-{nc})" if nc != n else "")},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": {"workload": WORKLOADS[cfg], "n": n, "m": m, "ops_per_step": ops_per_step,
+                   "qubits_covered": covered},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -363,10 +393,13 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     L = nat.engine()
 
     seed = HS.SEEDS[cfg]
-    sharded = world > 1 and (args.shard if args.shard is not None else cfg == "c4")
+    sharded = world > 1 and args.shard is not False
+    if args.remap and not sharded:
+        raise SystemExit("--remap applies to sharded runs (N > 1)")
+    dshard = None
     if sharded:
-        from paper_2604_15765_b200.multigpu import DistributedShard
-        dshard = DistributedShard(n, m, device=local, peer=not args.exchange)
+        from paper_2604_15765_b200.multigpu import DistributedShard, plan_remap
+        dshard = DistributedShard(n, m, device=local, peer=not args.exchange, remap=args.remap)
         st = dshard.state
         apply_op = dshard.apply
     else:
@@ -395,13 +428,31 @@ def ours_arm(args, cfg, n, m, world, rank, local):
         from paper_2604_15765_b200 import fusion
         fplan = fusion.plan_sequence([(spec, tg) for spec, tg, _ in ops], n, m)
 
-    npass = fplan.launches if fplan is not None else nops  # timed launch groups per step
+    def actions_of_step():
+        """The launches of one step: the ops themselves, or (remapping) ops on physical qubits with
+        the planner's SWAPs in between (the map carries over from step to step)."""
+        if not args.remap:
+            return [("op", spec, tg) for spec, tg, _ in ops]
+        acts, _, _ = plan_remap([(spec, tg) for spec, tg, _ in ops], dshard.layout, dshard.perm, args.remap_window)
+        return acts
 
+    if fplan is not None:
+        npass = fplan.launches
+    elif args.remap:
+        npass = 4 * nops  # event slots: ops plus the planner's swaps (at most k per op)
+    else:
+        npass = nops
     ev = [ctypes.c_void_p() for _ in range(2 * npass + 2)]
     for e in ev:
         nat.check(L.hs_event_create(ctypes.byref(e)))
 
-    touched = [0] * npass  # HBM bytes each op (or fused pass) reads + writes (engine plan, algorithmic)
+    touched = []  # per launch: HBM bytes read + written (engine plan, algorithmic), remote bytes
+    remote = []
+
+    def physical(spec, tg, o):
+        if dshard is not None and args.remap:
+            return dshard._apply_physical(spec, tg, o)
+        return apply_op(spec, tg, o)
 
     def step(record=False, collect=False):
         if fplan is not None:  # fused passes; touched bytes: 2 S per pass (program or composed step)
@@ -410,20 +461,33 @@ def ours_arm(args, cfg, n, m, world, rank, local):
                     L.hs_event_record(ev[2 + 2 * i], st.handle)
                 fusion.execute(st, fusion.Plan([item]), opts)
                 if collect:
-                    touched[i] = 2 * S
+                    touched.append(2 * S)
+                    remote.append(0)
                 if record:
                     L.hs_event_record(ev[3 + 2 * i], st.handle)
-            return
-        for i, (spec, tg, _) in enumerate(ops):
+            return len(fplan.items)
+        acts = actions_of_step()
+        for i, a in enumerate(acts):
+            spec, tg = (a[1], a[2]) if a[0] == "op" else (None, [a[1], a[2]])
+            if spec is None:
+                from paper_2604_15765_b200.multigpu import _swap_spec
+                spec = _swap_spec()
             if record:
                 L.hs_event_record(ev[2 + 2 * i], st.handle)
-            plan = apply_op(spec, tg, opts)
+            plan = physical(spec, tg, opts)
             if collect:
-                touched[i] = plan.touched_bytes
+                tb = int(plan.touched_bytes)
+                # a cross-shard op also reads its group members' tiles (the plan counts them)
+                touched.append(min(tb, 2 * S))
+                remote.append(max(0, tb - 2 * S))
             if record:
                 L.hs_event_record(ev[3 + 2 * i], st.handle)
+        return len(acts)
 
     for w in range(args.warmup):
+        if w == 0:
+            touched.clear()
+            remote.clear()
         step(collect=(w == 0))
     st.synchronize()
     graph = None
@@ -436,6 +500,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
 
         def step(record=False, collect=False):  # noqa: F811
             graph.launch()
+            return npass
         _ = plain_step
     dist_barrier(world)
     clocks = ClockSampler(local)
@@ -445,8 +510,14 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     launch_ms = []
     L.hs_event_record(ev[0], st.handle)
     t_host0 = time.perf_counter()
+    nlast = npass
     for s in range(args.steps):
-        step(record=(s == args.steps - 1))
+        if s == args.steps - 1 and args.remap:  # the last step's launches are timed one by one
+            touched.clear()
+            remote.clear()
+            nlast = step(record=True, collect=True)
+        else:
+            nlast = step(record=(s == args.steps - 1)) or npass
     L.hs_event_record(ev[1], st.handle)
     st.synchronize()
     t_host = time.perf_counter() - t_host0
@@ -454,7 +525,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     ms = ctypes.c_float()
     nat.check(L.hs_event_elapsed_ms(ev[0], ev[1], ctypes.byref(ms)))
     total_ms = float(ms.value)
-    for i in range(npass):
+    for i in range(nlast):
         if graph is not None:
             launch_ms.append(total_ms / args.steps / npass)
             continue
@@ -467,15 +538,32 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     ms_per_step = total_ms / args.steps
     value = (1 if sharded else world) * nops * args.steps / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (conj_kernel): bytes per launch / mean launch time
+    # HBM roofline of the launches of one step (this rank): algorithmic bytes / launch durations
     peak, peak_src = load_peaks()
-    if not any(touched):
-        touched = [2 * S] * npass
+    if not touched:
+        touched = [2 * S] * len(launch_ms)
+        remote = [0] * len(launch_ms)
+    touched, remote = touched[:len(launch_ms)], remote[:len(launch_ms)]
     per_launch_bytes = float(np.mean(touched))
     mean_launch_ms = float(np.mean(launch_ms))
-    # bytes-weighted over the step: sum of algorithmic bytes / sum of launch durations
     achieved = sum(touched) / (sum(launch_ms) / 1e3) / 1e9
-    traffic, traffic_src = load_traffic(cfg)
+    traffic, traffic_src = load_traffic(cfg, n, world if sharded else 1)
+    # NVLink roofline of the cross-shard launches: remote bytes read / their durations
+    xs = [(r, t) for r, t in zip(remote, launch_ms) if r > 0]
+    roof_nv = None
+    if sharded:
+        if xs:
+            nv = sum(r for r, _ in xs) / (sum(t for _, t in xs) / 1e3) / 1e9
+            roof_nv = {"bound": "nvlink", "achieved": nv, "peak": NVLINK_GBS, "unit": "GB/s", "frac": nv / NVLINK_GBS,
+                       "cross_shard_launches_per_step": len(xs),
+                       "remote_bytes_per_cross_launch": float(np.mean([r for r, _ in xs])),
+                       "mean_cross_launch_ms": float(np.mean([t for _, t in xs])),
+                       "peak_source": "B200_PROFILING.md: measured peer copy 770 GB/s per direction (900 nominal)",
+                       "mode": "NCCL group exchange + op" if args.exchange else "peer reads fused into the op kernels"}
+        else:
+            roof_nv = {"bound": "nvlink", "achieved": None, "frac": None, "cross_shard_launches_per_step": 0,
+                       "note": "no operation of this config reads another shard's tiles (single-qubit channels "
+                               "that keep the (00,11)/(01,10) shard classes apart run shard-local)"}
     result = {}
     if cfg == "c3":
         result["tr_rho_O"] = drho.reduce(dshard, 0) if sharded else H.expectation(rho, st)
@@ -501,6 +589,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
         if e2e is None:
             e_ms = []
             for s in range(1 + args.e2e_steps):
+                dist_barrier(world)
                 L.hs_event_record(ev[0], st.handle)
                 nat.check(L.hs_state_upload_async(st.handle, host.ctypes.data_as(nat.c_double_p), st.element_count()))
                 step()
@@ -512,23 +601,26 @@ def ours_arm(args, cfg, n, m, world, rank, local):
                 if s >= 1:
                     e_ms.append(float(x.value))
             e2e_ms = dist_max(float(np.mean(e_ms)), world)
-            e2e = {"value": (1 if sharded else world) * nops / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": S,
-                   "d2h_bytes_per_step": S, "ms_per_step": e2e_ms, "steps": len(e_ms), "pipelined": False,
-                   "path": "hb_apply via paper_2604_15765_b200.hermsim.apply + hs_state_upload/download_async"}
-        if rank == 0 and world == 1 and not args.no_cpu:
-            cpu = cpu_baseline_from(host, cfg, n, m, S)
-        else:
-            cpu = None
-        L.hs_host_free(hbuf)
-    elif rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_from(None, cfg, n, m, S, psi=psi, strings=strings)
-    else:
-        cpu = None
+            job_bytes = S * (world if sharded else 1)
+            e2e = {"value": (1 if sharded else world) * nops / (e2e_ms / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": job_bytes, "d2h_bytes_per_step": job_bytes,
+                   "h2d_bytes_per_step_per_rank": S, "ms_per_step": e2e_ms, "steps": len(e_ms), "pipelined": False,
+                   "path": ("DistributedShard.apply" if sharded else "hb_apply via paper_2604_15765_b200.hermsim.apply")
+                           + " + hs_state_upload/download_async"}
+        L.hs_host_free(hbuf)  # before the CPU baseline: the reference needs the host RAM
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_from(cfg, n, m, psi=psi, strings=strings)
 
     for e in ev:
         L.hs_event_destroy(e)
     if rank != 0:
         return 0
+    l2 = ("state %.3f GB per rank vs 126 MB L2: inputs larger than L2, no flush needed" % (S / 1e9))
+    if S < 4 * 126e6:
+        l2 = ("L2-ASSISTED: the %.0f MB state is about the 126 MB L2; consecutive ops alternate their sweep "
+              "direction, so part of each op is served from L2 -- the roofline fraction is not an HBM-only "
+              "number (ncu DRAM bytes per launch in roofline.traffic)" % (S / 1e6))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -541,16 +633,22 @@ def ours_arm(args, cfg, n, m, world, rank, local):
                    "cuda_graph": bool(args.graph),
                    "stored_bytes_per_rank": S,
                    "parallelism": (f"sharded x{world} (XOR blocks, " + ("NCCL group exchange" if args.exchange else
-                                   "peer-memory reads fused into the op kernels") + ")" if sharded else
+                                   "peer-memory reads fused into the op kernels") +
+                                   (", qubit remapping" if args.remap else "") + ")" if sharded else
                                    f"replicas x{world}" if world > 1 else "single GPU"),
-                   "l2": "inputs larger than L2 (state %.2f GB vs 126 MB L2); no flush needed" % (S / 1e9)},
+                   "exchanges_per_step": (dshard.exchanges / max(1, args.warmup + args.steps + 1 + args.e2e_steps)
+                                          if dshard is not None else 0),
+                   "l2": l2},
         "achieved_hbm_gbs": sum(touched) * args.steps / (total_ms / 1e3) / 1e9,
         "touched_bytes_per_step": sum(touched),
         "effective_bandwidth_gbs_paper": S * nops * args.steps / (total_ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "pipe_kernel / gather_kernel (csrc/engine.cu)", "algorithmic_bytes_per_launch": per_launch_bytes,
+                     "traffic": traffic, "kernel": "pipe_kernel / gather_ws_kernel (csrc/engine.cu)",
+                     "algorithmic_bytes_per_launch": per_launch_bytes,
                      "mean_launch_ms": mean_launch_ms, "min_launch_ms": min(launch_ms), "max_launch_ms": max(launch_ms),
-                     "peak_source": peak_src, "traffic_source": traffic_src},
+                     "peak_source": peak_src, "traffic_source": traffic_src,
+                     "scope": "rank 0's launches" if sharded else "all launches of one step"},
+        "roofline_nvlink": roof_nv,
         "per_launch_ms": [round(x, 4) for x in launch_ms],
         "gpu_launches": launches,
         "host_wall_s": t_host,
@@ -560,6 +658,8 @@ def ours_arm(args, cfg, n, m, world, rank, local):
     }
     line.update(result)
     print(json.dumps(line), flush=True)
+    if dshard is not None:
+        dshard.close()
     return 0
 
 
@@ -571,16 +671,17 @@ def stored_bytes(n: int, m: int = 5) -> int:
 
 def cpu_sample_n(cfg: str, n: int, m: int, reserved: int = 0) -> int:
     """Largest n' <= n whose reference run fits this host's free RAM (where RAM is short,
-    time at the largest feasible n and extrapolate x4 per qubit).  The reference holds its own copy
-    of the payload; its k = 3 path converts through three dense 4^n matrices (kernels.cpp:498-505)."""
+    time at the largest feasible n and extrapolate x4 per qubit).  The input is built inside the
+    reference's own buffer (one payload); its k = 3 path converts through three dense 4^n matrices
+    (kernels.cpp:498-505)."""
     try:
         import psutil
         avail = psutil.virtual_memory().available - reserved
     except Exception:  # pragma: no cover
         avail = 32 << 30
-    budget = 0.6 * avail
+    budget = 0.85 * avail
     for k in range(n, 4, -1):
-        need = 2.2 * stored_bytes(k, m) + (3 * 16 * (1 << (2 * k)) if cfg == "c3" else 0)
+        need = 1.05 * stored_bytes(k, m) + (3 * 16 * (1 << (2 * k)) if cfg == "c3" else 0)
         # the dense k = 3 path also costs ~4^n time: keep a C3 sample within seconds per op
         if need <= budget and (cfg != "c3" or k <= 13):
             return k
@@ -662,27 +763,34 @@ def pipelined_e2e(args, H, L, nat, st, host0, S, n, m, nops, world, fplan, ops, 
                     "steps on different states overlap (upload k+1 || compute k || download k-1)"}
 
 
-def cpu_baseline_from(host_view, cfg, n, m, S, psi=None, strings=None):
-    """Reference CPU path on a bounded sample (about 10-30 s) of the same workload, rank 0 only."""
+def cpu_baseline_from(cfg, n, m, psi=None, strings=None):
+    """Reference CPU path on a bounded sample (about 10-30 s) of the same workload, rank 0 only:
+    whole steps of the config when one fits in ~40 s (C0, C2: the full 12 / 32-op sequence), else
+    blocks of 2 consecutive ops in stratified order within a 30 s budget."""
     try:
         from paper_2604_15765_b200 import harness as HS
         threads = os.cpu_count() or 1
         nc = cpu_sample_n(cfg, n, m)
-        if cfg == "c3":
-            payload = HS.pauli_payload(nc, HS.pauli_strings(nc, 64, HS.SEEDS[cfg]) if nc != n or strings is None
-                                       else strings)
+        nops = len(HS.config_ops(cfg, nc))
+        whole = cfg in ("c0", "c2") and nc == n
+        fill = reference_fill(HS, cfg, nc, m, threads, psi=psi if nc == n else None,
+                              strings=strings if nc == n else None)
+        if whole:
+            reps = 3 if cfg == "c0" else 1
+            times, blocks, covered = run_reference_cpu(cfg, nc, m, fill, nops, reps, 1 if cfg == "c0" else 0, threads)
+            ops_per_step = nops
         else:
-            use_host = host_view is not None and nc == n  # the pinned e2e buffer holds n-sized payloads
-            payload = host_payload(HS, nc, m, psi if (psi is not None and nc == n) else HS.rank_psi(nc, HS.SEEDS[cfg], 4),
-                                   out=np.frombuffer(host_view, dtype=np.complex128) if use_host else None,
-                                   threads=threads)
-        ops_per_step = 2
-        times = run_reference_cpu(cfg, nc, m, payload, ops_per_step, steps=3, warmup=0, threads=threads, budget_s=30.0)
+            ops_per_step = 2
+            times, blocks, covered = run_reference_cpu(cfg, nc, m, fill, ops_per_step, steps=64, warmup=0,
+                                                       threads=threads, budget_s=30.0)
         t = float(np.mean(times))
         scale = 4.0 ** (n - nc)
         out = {"value": ops_per_step / t / scale, "unit": UNIT, "cores": threads, "kind": "reference",
-               "sample": f"{len(times)} x {ops_per_step} consecutive ops of {cfg}, blocks spread over the sequence, at n={nc} through "
-                         "hermsim::apply of the compiled reference (oracle/_ref/libhermsim_ref.so), threads=nproc"}
+               "sample": (f"{len(times)} full step(s) of {cfg} ({nops} ops)" if whole else
+                          f"{len(times)} blocks of {ops_per_step} consecutive ops of {cfg} in stratified order "
+                          f"(blocks {blocks})") + f" at n={nc} through hermsim::apply of the compiled reference "
+                          "(oracle/_ref/libhermsim_ref.so), threads=nproc, input built in the reference's own buffer",
+               "qubits_covered": covered}
         if nc != n:
             out["extrapolated_from_n"] = nc
             out["sample"] += f"; host RAM/time-bounded, extrapolated to n={n} by 4^(n-{nc}) (work grows 4x per qubit)"

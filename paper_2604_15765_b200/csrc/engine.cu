@@ -60,6 +60,12 @@
 
 
 // =============================================================================== host side
+struct HCacheEntry {
+    uint64_t key = 0;
+    int nops = 0;
+    std::vector<double2> ops;
+    double* dev = nullptr;
+};
 struct hs_state {
     int n, m, device;
     uint64_t N, M, G, count;
@@ -83,6 +89,7 @@ struct hs_state {
     double2* buf[2] = {nullptr, nullptr};     // this shard's two payload buffers (buf[flip] is current)
     uint32_t flip = 0;
     const double2* peer_buf[64][2] = {};       // peers' buffers, valid on this device
+    std::vector<HCacheEntry> hcache;           // device fragments of the k = 3 Kraus sets seen (hform3)
 };
 
 namespace {
@@ -484,7 +491,7 @@ void search_put(uint64_t key, const std::array<uint8_t, 65>& v) {
 // bulk: stage sub-block rows with cp.async.bulk, one copy per run of >= 8 contiguous elements
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
 void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false,
-                 bool prog = false, bool sform = false) {
+                 bool prog = false, bool sform = false, uint32_t min_run = 4) {
     const uint32_t M = G.M, g = G.g, NT = G.grp4 ? 4u : 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -521,7 +528,7 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
     // bulk rows: runs of the low contiguous sub-block bits, at least 16 elements (256 B; 128-B runs
     // are bound by the bulk-copy engine's operation rate: C3 g = 3 15.4 -> 20.7 ms measured)
     G.logRun = std::min<uint32_t>(__builtin_ctz(~cmask), G.logS0);
-    G.bulk = bulk && (dmma || sform) && G.logRun >= 4;
+    G.bulk = bulk && (dmma || sform) && G.logRun >= min_run;
     G.TS = S0 * (S0 + 1);
     G.s8 = 0;
     G.sf_xfast = 0;
@@ -863,9 +870,56 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
 
 // internal: a k = 2 Kraus sum the tensor-core gather cannot take (hs_apply_kraus falls back)
 constexpr int RC_NO_KRAUS_SUM = -1000;
+
+// Element tables of the hermitian-basis transform (hform3): lane c of a quad loads 7 mirrored pairs
+// (r, c), (c, r) of the 8 x 8 block and the diagonal elements 2c, 2c + 1 (in[16 c + 2 j + e]);
+// output pair q = 4 nt + c: the 28 upper pairs, then 4 pairs of diagonal elements (out[2 q + e]).
+struct HForm {
+    uint8_t in[64], out[64];
+};
+const HForm& hform_tables() {
+    static const HForm tabs = [] {
+    HForm t{};
+    uint8_t pr[28][2];
+    int np = 0;
+    for (int d = 1; d < 8; ++d)  // by distance from the diagonal: a lane's pairs spread over the block
+        for (int r = 0; r + d < 8; ++r) {
+            pr[np][0] = (uint8_t)r;
+            pr[np][1] = (uint8_t)(r + d);
+            ++np;
+        }
+    for (int c = 0; c < 4; ++c) {
+        for (int j = 0; j < 7; ++j) {
+            const int p = 4 * j + c;  // interleaved: the four lanes of a k-step take neighbouring pairs
+            t.in[16 * c + 2 * j] = (uint8_t)(pr[p][0] * 8 + pr[p][1]);
+            t.in[16 * c + 2 * j + 1] = (uint8_t)(pr[p][1] * 8 + pr[p][0]);
+        }
+        t.in[16 * c + 14] = (uint8_t)((2 * c) * 9);
+        t.in[16 * c + 15] = (uint8_t)((2 * c + 1) * 9);
+    }
+    for (int q = 0; q < 32; ++q) {
+        if (q < 28) {
+            t.out[2 * q] = (uint8_t)(pr[q][0] * 8 + pr[q][1]);
+            t.out[2 * q + 1] = (uint8_t)(pr[q][1] * 8 + pr[q][0]);
+        } else {
+            t.out[2 * q] = (uint8_t)((2 * (q - 28)) * 9);
+            t.out[2 * q + 1] = (uint8_t)((2 * (q - 28) + 1) * 9);
+        }
+    }
+    return t;
+    }();
+    return tabs;
+}
 // k = 2 Kraus sums of rank 2..4: the per-operator direct form on the k = 3 gather (96 FMA per element
 // per operator pair through I2 (x) L) instead of the S form (48 per element, any rank); off by
 // default, kept for comparison (HS_KRAUS2_DIRECT=1)
+constexpr bool g_gather_narrow_default = false;
+// k = 3 Kraus sums of rank >= 4 through the direct per-operator sum (rank 4) / the three-buffer sum
+// instead of the S form (HS_KRAUS3_DIRECT=1, for comparison)
+const bool g_kraus3_direct = [] {
+    const char* e = getenv("HS_KRAUS3_DIRECT");
+    return e && atoi(e) != 0;
+}();
 const bool g_kraus2_direct = [] {
     const char* e = getenv("HS_KRAUS2_DIRECT");
     return e && atoi(e) != 0;
@@ -1064,12 +1118,33 @@ int launch_impl(hs_state* h, const Geo& G0, const Coef<NS>& cf, const KrausArgs&
                     kw = Gg.tma ? gather_ws_kernel<K, NS, M_DIRECT, true, true, true>
                                 : Gg.bulk ? gather_ws_kernel<K, NS, M_DIRECT, true, false, true>
                                           : gather_ws_kernel<K, NS, M_DIRECT, false, false, true>;
+            // k = 3 on bulk / TMA staging: 8 transform warps at 128 registers instead of 16 at 80
+            // (HS_GATHER_NARROW=0/1 overrides the default)
+            unsigned threads = 768;
+            if constexpr (K == 3 && MODE == M_DIRECT) {
+                static const int narrow_env = [] {
+                    const char* e = getenv("HS_GATHER_NARROW");
+                    return e ? atoi(e) : -1;
+                }();
+                const bool narrow = narrow_env >= 0 ? narrow_env != 0 : g_gather_narrow_default;
+                if (narrow && Gg.bulk) {
+                    threads = 512;
+                    if constexpr (NS == 256)
+                        kw = cf.nk > 1 ? (Gg.tma ? gather_ws_kernel<K, NS, M_DIRECT, true, true, true, true>
+                                                 : gather_ws_kernel<K, NS, M_DIRECT, true, false, true, true>)
+                                       : (Gg.tma ? gather_ws_kernel<K, NS, M_DIRECT, true, true, false, true>
+                                                 : gather_ws_kernel<K, NS, M_DIRECT, true, false, false, true>);
+                    else
+                        kw = Gg.tma ? gather_ws_kernel<K, NS, M_DIRECT, true, true, false, true>
+                                    : gather_ws_kernel<K, NS, M_DIRECT, true, false, false, true>;
+                }
+            }
             e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess)
                 return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(gather_ws): ") + cudaGetErrorString(e));
             const uint64_t grid = std::min<uint64_t>(Gg.nG_items, (uint64_t)sm_count(h->device));
             if (grid) {
-                kw<<<(unsigned)grid, 768, smem, h->stream>>>(Gg, cf, h->d, tin, tout);
+                kw<<<(unsigned)grid, threads, smem, h->stream>>>(Gg, cf, h->d, tin, tout);
                 g_launches.fetch_add(1, std::memory_order_relaxed);
                 e = cudaGetLastError();
                 if (e != cudaSuccess)
@@ -1208,6 +1283,131 @@ int launch_sform2_impl(hs_state* h, const Geo& G0, const Coef<256>& cf) {
     return HS_OK;
 }
 
+// k = 3 Kraus sum in S form (64 x 64 transfer matrix, fragments at `frag` in device memory) on the
+// tensor-core gather, bulk-row staging in every regime (128-B rows for three grid targets: this
+// transform is bound by the FP64 pipe, not by the copies), two ring stages + the fragments.
+int launch_sform3_impl(hs_state* h, const Geo& G0, const double* frag) {
+    if (h->m != 5)
+        return RC_NO_KRAUS_SUM;
+    Geo G;
+    {
+        const int rc = shard_prelude(h, G0, false, G);
+        if (rc)
+            return rc;
+    }
+    if (G.g == 0) {
+        G.grp4 = 1;
+        G.logNT = 2;
+        G.nloc_tiles = h->count >> 10;
+    }
+    plan_gather(G, true, true, 0, false, false, false, 3);
+    {
+        static const char* dbg = getenv("HS_DEBUG_FLAGS");
+        G.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
+    }
+    if (!G.bulk)
+        return RC_NO_KRAUS_SUM;
+    G.sf3 = frag;
+    G.ws_diag = 1;
+    G.nG_items = G.grp4 ? (G.nloc_tiles + 3) / 4 : G.nU_loose << (2 * G.log_nsb_side);
+    const size_t smem = (size_t)2 * G.stage_elems * sizeof(double2) + 4096 * sizeof(double);
+    auto kw = gather_ws_kernel<3, 64, M_SF3, true>;
+    cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(sform3): ") + cudaGetErrorString(e));
+    const uint64_t grid = std::min<uint64_t>(G.nG_items, (uint64_t)sm_count(h->device));
+    if (grid) {
+        CUtensorMap tin{}, tout{};
+        Coef<64> cf{};
+        kw<<<(unsigned)grid, 512, smem, h->stream>>>(G, cf, h->d, tin, tout);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        e = cudaGetLastError();
+        if (e != cudaSuccess)
+            return set_err(HS_ERR_CUDA, std::string("gather_ws_kernel(sform3) launch: ") + cudaGetErrorString(e));
+    }
+    return HS_OK;
+}
+
+// R of a k = 3 Kraus set in hform3's fragment order, on the device.  Cached per state by the bytes
+// of the Kraus set (a noise channel is typically applied to many qubit triples): a hit costs no host
+// work, no copy and no synchronisation, and is allowed inside a graph capture (the buffer lives as
+// long as the state); a miss builds R on the host and uploads it synchronously (refused while
+// capturing).
+int hform_fragments(hs_state* h, int nops, const double2* L, const double** out) {
+    uint64_t key = 1469598103934665603ull ^ (uint64_t)nops;
+    const unsigned char* bytes = reinterpret_cast<const unsigned char*>(L);
+    for (size_t b = 0; b < (size_t)nops * 64 * sizeof(double2); ++b)
+        key = (key ^ bytes[b]) * 1099511628211ull;
+    for (const auto& e : h->hcache)
+        if (e.key == key && e.nops == nops && std::memcmp(e.ops.data(), L, e.ops.size() * sizeof(double2)) == 0) {
+            *out = e.dev;
+            return HS_OK;
+        }
+    {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing(h->stream, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+            return set_err(HS_ERR_UNSUPPORTED, "k = 3 Kraus set not yet seen by this state: apply it once before capturing");
+    }
+    const HForm& hf = hform_tables();
+    // input coordinate (ks, c): hermitian basis element E; output coordinate (nt, n): a real
+    // coordinate of S(E) = sum_a L_a E L_a^dagger.  E has two nonzeros (one on the diagonal).
+    std::vector<double> frag(4096);
+    for (int c = 0; c < 4; ++c)
+        for (int ks = 0; ks < 16; ++ks) {
+            const int j = ks >> 1, which = ks & 1;
+            const int e0 = hf.in[16 * c + 2 * j], e1 = hf.in[16 * c + 2 * j + 1];
+            int pos[2];
+            double2 val[2];
+            int nz = 0;
+            if (j < 7) {  // (|r><c| + |c><r|) / 2  or  (i|r><c| - i|c><r|) / 2, e0 = (r, c), e1 = (c, r)
+                pos[0] = e0;
+                val[0] = which ? make_double2(0.0, 0.5) : make_double2(0.5, 0.0);
+                pos[1] = e1;
+                val[1] = which ? make_double2(0.0, -0.5) : make_double2(0.5, 0.0);
+                nz = 2;
+            } else {      // |d><d|
+                pos[0] = which ? e1 : e0;
+                val[0] = make_double2(1.0, 0.0);
+                nz = 1;
+            }
+            double2 Y[64];
+            for (int x = 0; x < 8; ++x)
+                for (int y = 0; y < 8; ++y) {
+                    double yr = 0.0, yi = 0.0;
+                    for (int a = 0; a < nops; ++a)
+                        for (int z = 0; z < nz; ++z) {
+                            const int u = pos[z] >> 3, v = pos[z] & 7;
+                            const double2 ee = val[z], lx = L[a * 64 + x * 8 + u], ly = L[a * 64 + y * 8 + v];
+                            const double tr = lx.x * ee.x - lx.y * ee.y, ti = lx.x * ee.y + lx.y * ee.x;  // lx * ee
+                            yr += tr * ly.x + ti * ly.y;  // * conj(ly)
+                            yi += ti * ly.x - tr * ly.y;
+                        }
+                    Y[x * 8 + y] = make_double2(yr, yi);
+                }
+            for (int nt = 0; nt < 8; ++nt)
+                for (int g = 0; g < 8; ++g) {
+                    const int q = 4 * nt + (g >> 1), jo = g & 1;
+                    const int o0 = hf.out[2 * q], o1 = hf.out[2 * q + 1];
+                    const double v = nt < 7 ? (jo ? Y[o0].y : Y[o0].x) : (jo ? Y[o1].x : Y[o0].x);
+                    frag[(ks * 8 + nt) * 32 + g * 4 + c] = v;
+                }
+        }
+    HCacheEntry e;
+    e.key = key;
+    e.nops = nops;
+    e.ops.assign(L, L + (size_t)nops * 64);
+    CUDA_TRY(cudaMalloc(&e.dev, frag.size() * sizeof(double)));
+    const cudaError_t ce = cudaMemcpy(e.dev, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+        cudaFree(e.dev);
+        return set_err(HS_ERR_CUDA, std::string("hform fragments: ") + cudaGetErrorString(ce));
+    }
+    h->hcache.push_back(std::move(e));
+    *out = h->hcache.back().dev;
+    return HS_OK;
+}
+
 // After a launch: peer mode makes the output buffer current; an exchange licenses one operation.
 int after_launch(hs_state* h, const Geo& G0, int rc) {
     if (rc == HS_OK && G0.cmask && h->peer_mode) {
@@ -1221,6 +1421,9 @@ int after_launch(hs_state* h, const Geo& G0, int rc) {
 
 int launch_sform2(hs_state* h, const Geo& G0, const Coef<256>& cf) {
     return after_launch(h, G0, launch_sform2_impl(h, G0, cf));
+}
+int launch_sform3(hs_state* h, const Geo& G0, const double* frag) {
+    return after_launch(h, G0, launch_sform3_impl(h, G0, frag));
 }
 
 // One operation's kernels.  Peer mode: the result went to the other buffer, which becomes current.
@@ -1404,6 +1607,8 @@ int hs_state_free(hs_state* h) {
     }
     cudaFree(h->red);
     cudaFree(h->kraus);
+    for (auto& e : h->hcache)
+        cudaFree(e.dev);
     cudaFree(h->recv);
     if (h->comm && nccl().CommDestroy)
         nccl().CommDestroy((ncclComm_t)h->comm);
@@ -1962,6 +2167,27 @@ int hs_apply_kraus(hs_state* h, int k, int nops, const double* ops, const uint32
     if (nops == 1 && k >= 2)
         return hs_apply_unitary(h, k, ops, t, plan);
     const double2* L = reinterpret_cast<const double2*>(ops);
+    if (k == 3 && nops >= 3 && h->m == 5 && !g_kraus3_direct) {
+        // rank >= 3: the hermitian-basis form (hform3): one real 64 x 64 matrix R on the coordinates
+        // of hermitian 8 x 8 blocks, two real products per block (128 FMA per element whatever the
+        // rank; the direct sum costs 48 per element per operator)
+        DeviceGuard dg(h->device);
+        const HForm& hf = hform_tables();
+        const double* frag = nullptr;
+        rc = hform_fragments(h, nops, L, &frag);
+        if (rc)
+            return rc;
+        Geo G;
+        plan_geo(h, 3, t, G, 1);
+        std::memcpy(G.hf_in, hf.in, 64);
+        std::memcpy(G.hf_out, hf.out, 64);
+        rc = launch_sform3(h, G, frag);
+        if (rc != RC_NO_KRAUS_SUM) {
+            if (rc)
+                return rc;
+            return finish_plan(h, G, k, t, generic_path(G), plan, 2 * state_bytes(h));
+        }
+    }
     if (k == 3 && nops <= 4 && h->m == 5) {
         // sum_a L_a B L_a^dagger on the k = 3 tensor-core gather (every regime), per-operator fragments
         DeviceGuard dg(h->device);

@@ -32,6 +32,11 @@ __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, doubl
         : "+d"(d0), "+d"(d1)
         : "d"(a), "d"(b));
 }
+__device__ __forceinline__ void dmma_acc_v(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 // conjugation flag applied as a sign-bit flip on the integer pipe (a DADD negation would compete
 // with the DMMA for the FP64 pipe)
 __device__ __forceinline__ double flip_sign(double x, uint32_t m) {
@@ -117,14 +122,14 @@ __device__ __forceinline__ DmmaFrag dmma_frag(const Geo& G, const Tabs& T, const
 }
 // KS: Kraus sum sum_a L_a B L_a^dagger over nk operators whose per-lane fragment values come from
 // shared memory (kf[a][8][lane]: Lr, Li, Lr + Li, Lr - Li for chunks 0, 1), accumulated in registers.
-template <int NC, int K = 3, bool BULK = false, bool TMAB = false, bool KS = false>
+template <int NC, int K = 3, bool BULK = false, bool TMAB = false, bool KS = false, bool WIDE_REGS = false>
 __device__ __forceinline__ void dmma_direct3(const Geo& G, const Tabs& T, const DmmaFrag& f, uint64_t am,
                                              double2* sb, uint32_t warp, const double* kf = nullptr,
                                              uint32_t nk = 1) {
     const uint32_t lane = threadIdx.x & 31u;
-    // blocks per pass: two independent chains for the unitary; one for the Kraus sum (its
-    // accumulators would otherwise spill)
-    constexpr int NQ = KS ? 1 : 2;
+    // blocks per pass: two independent chains for the unitary; one for the Kraus sum at 80 registers
+    // (its accumulators would otherwise spill), two with the 128 registers of a 512-thread CTA
+    constexpr int NQ = (KS && !WIDE_REGS) ? 1 : 2;
     constexpr uint32_t sh = K == 3 ? 0u : 1u;  // k = 2: 8 x 8 matrices of 2 x 2 blocks
     const uint32_t cld0 = (uint32_t)((am >> f.tld[0]) & 1ull) << 31, cld1 = (uint32_t)((am >> f.tld[1]) & 1ull) << 31;
     const uint32_t cst0 = (uint32_t)((am >> f.tst[0]) & 1ull) << 31, cst1 = (uint32_t)((am >> f.tst[1]) & 1ull) << 31;
@@ -367,6 +372,80 @@ __device__ __forceinline__ void sform2(const Geo& G, const Tabs& T, const SfFrag
     }
 }
 
+// k = 3 Kraus sums in the hermitian basis on the FP64 tensor path.  A Kraus map S is hermiticity-
+// preserving, so with B = B1 + i B2 (B1 = (B + B^dagger) / 2, B2 = (B - B^dagger) / 2i, both hermitian)
+// S(B) = S(B1) + i S(B2), and on the 64 real coordinates of a hermitian 8 x 8 matrix (diagonal, Re and
+// Im of the upper triangle) S is one REAL 64 x 64 matrix R.  Per block: two real products R x1, R x2
+// (128 FMA per element, whatever the rank) instead of the complex 64 x 64 transfer matrix (192 FMA
+// per element in 3M form, kernels.cpp:39-48's matvec generalised) or the direct sum (48 per element
+// per Kraus operator).  Each lane of a quad loads the 16 block elements hf_in names -- 7 mirrored
+// pairs (r, c), (c, r) and 2 diagonal elements -- so the coordinates (doubled: the 1/2 is folded into
+// R) form in registers:  x1 = Re B_rc + Re B_cr | Im B_rc - Im B_cr,  x2 = Im B_rc + Im B_cr |
+// Re B_cr - Re B_rc.  Outputs come out as coordinate pairs (Re, Im of H_rc) of H1 = R x1 and H2 = R x2:
+// W_rc = H1_rc + i H2_rc, W_cr = conj(H1_rc) + i conj(H2_rc) (n-tile 7: pairs of diagonal elements).
+// 8 blocks per warp pass: 16 k-steps x 8 n-tiles x 2 products = 256 DMMA.
+template <int NC>
+__device__ __forceinline__ void hform3(const Geo& G, const Tabs& T, const uint8_t* hin, const uint8_t* hout,
+                                       const double* rfr, uint64_t am, double2* sb, uint32_t warp) {
+    const uint32_t lane = threadIdx.x & 31u, gq = lane >> 2, cq = lane & 3u;
+    const uint32_t lbt = G.logNxb + G.logNyb, npass = ((G.grp4 ? 4u : 1u) << lbt) >> 3;
+    const uint32_t logNy = G.logNyb, ymask = G.nyb - 1;
+    const uint8_t* myin = hin + 16 * cq;
+    for (uint32_t p = warp; p < npass; p += NC / 32) {
+        const uint32_t b = 8 * p + gq, bq = b & ((1u << lbt) - 1);
+        const uint32_t xbv = T.xb[bq >> logNy], ybv = T.yb[bq & ymask];
+        const uint32_t slot = (b >> lbt) * G.TS;
+        const uint32_t base = slot + xbv * G.PD + (xbv >> 3) * G.s8 + ybv;
+        const uint32_t baseA = slot + ybv * G.PD + (ybv >> 3) * G.s8 + xbv;
+        double x1[16], x2[16];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            double2 v[2];
+#pragma unroll
+            for (uint32_t e = 0; e < 2; ++e) {
+                const uint32_t ci = myin[2 * j + e], adj = (uint32_t)(am >> T.ttr[ci]) & 1u;
+                v[e] = sb[adj ? baseA + T.cadj[ci] : base + T.cdir[ci]];
+                v[e].y = flip_sign(v[e].y, adj << 31);
+            }
+            if (j < 7) {  // mirrored pair (r, c), (c, r)
+                x1[2 * j] = v[0].x + v[1].x;
+                x2[2 * j] = v[0].y + v[1].y;
+                x1[2 * j + 1] = v[0].y - v[1].y;
+                x2[2 * j + 1] = v[1].x - v[0].x;
+            } else {      // two diagonal elements
+                x1[14] = v[0].x;
+                x2[14] = v[0].y;
+                x1[15] = v[1].x;
+                x2[15] = v[1].y;
+            }
+        }
+#pragma unroll 1
+        for (uint32_t nt = 0; nt < 8; ++nt) {
+            double h1a = 0.0, h1b = 0.0, h2a = 0.0, h2b = 0.0;
+            const uint32_t f = smem_u32(rfr + nt * 32 + lane);
+#pragma unroll
+            for (uint32_t ks = 0; ks < 16; ++ks) {
+                double r;
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(f + ks * 2048u));
+                dmma_acc_v(h1a, h1b, x1[ks], r);
+                dmma_acc_v(h2a, h2b, x2[ks], r);
+            }
+            const uint32_t e0 = hout[2 * (4 * nt + cq)], e1 = hout[2 * (4 * nt + cq) + 1];
+            double2 w0, w1;
+            if (nt < 7) {
+                w0 = make_double2(h1a - h2b, h1b + h2a);
+                w1 = make_double2(h1a + h2b, h2a - h1b);
+            } else {
+                w0 = make_double2(h1a, h2a);
+                w1 = make_double2(h1b, h2b);
+            }
+            const uint32_t a0 = (uint32_t)(am >> T.ttr[e0]) & 1u, a1 = (uint32_t)(am >> T.ttr[e1]) & 1u;
+            sb[a0 ? baseA + T.cadj[e0] : base + T.cdir[e0]] = make_double2(w0.x, flip_sign(w0.y, a0 << 31));
+            sb[a1 ? baseA + T.cadj[e1] : base + T.cdir[e1]] = make_double2(w1.x, flip_sign(w1.y, a1 << 31));
+        }
+    }
+}
+
 __device__ unsigned long long g_phase_cycles[8];  // diagnostics: gather phase cycles per group
 template <int K, int MODE, int NS, int NC>
 __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st) {
@@ -594,14 +673,21 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
 // registers: the per-lane S fragments stay in registers).  With 16-row sub-blocks (two grid targets)
 // the copy side issues 512 bulk row copies per item: 2 copy warps streamed 4.2 TB/s, 8 copy warps
 // 6.2 TB/s (n = 16, copies alone); transform alone 8.8 ms (profiles/r02_kraus_sform.txt).
-template <int K, int NS, int MODE = M_DIRECT, bool BULK = false, bool TMAB = false, bool KSUM = false>
-__global__ void __launch_bounds__(MODE == M_SF2 ? 512 : 768, 1)
+// NARROW (bulk staging): 8 transform warps and 8 copy warps (512 threads, 128 registers) instead of
+// 16 + 8 (768 threads, 80 registers)
+template <int K, int NS, int MODE = M_DIRECT, bool BULK = false, bool TMAB = false, bool KSUM = false,
+          bool NARROW = false>
+__global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 512 : 768, 1)
     gather_ws_kernel(const Geo G, const Coef<NS> cf, double2* __restrict__ st, const __grid_constant__ CUtensorMap tin,
                      const __grid_constant__ CUtensorMap tout) {
     // bulk rows need few copy instructions: 16 transform warps and 8 copy warps (else 8 and 16)
-    constexpr bool SF = MODE == M_SF2;
-    static_assert(!SF || BULK, "the S-form transform runs on bulk-row staging");
-    constexpr uint32_t NCW = SF ? 256 : BULK ? 512 : 256, NMW = SF ? 256 : BULK ? 256 : 512, S = 3;
+    constexpr bool SF = MODE == M_SF2, SF3 = MODE == M_SF3;
+    static_assert(!(SF || SF3) || BULK, "the S-form transforms run on bulk-row staging");
+    static_assert(!NARROW || BULK, "the narrow layout is for bulk staging");
+    // SF3: two ring stages (the 64 KiB transfer matrix takes the third's shared memory; the op is
+    // bound by the FP64 pipe, twice the copy time, so two stages still hide the copies)
+    constexpr uint32_t NCW = (SF || SF3 || NARROW) ? 256 : BULK ? 512 : 256, NMW = (SF || SF3) ? 256 : BULK ? 256 : 512,
+                       S = SF3 ? 2 : 3;
     // tile tables by item % TSL, built S items ahead (BULK: by two copy groups that may be one item
     // apart, hence two more slots)
     constexpr uint32_t TSL = BULK ? S + 3 : S + 1;
@@ -646,6 +732,18 @@ __global__ void __launch_bounds__(MODE == M_SF2 ? 512 : 768, 1)
         SfFrag sf;
         if constexpr (SF)
             sf = sform2_frag(G, T, cf);
+        double* sfr = nullptr;
+        __shared__ uint8_t hin[64], hout[64];
+        if constexpr (SF3) {  // R's fragments into shared memory, after the ring; the element tables
+            sfr = reinterpret_cast<double*>(ring + (size_t)S * G.stage_elems);
+            for (uint32_t i = tid; i < 4096u; i += NCW)
+                sfr[i] = G.sf3[i];
+            if (tid < 64) {
+                hin[tid] = G.hf_in[tid];
+                hout[tid] = G.hf_out[tid];
+            }
+            asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+        }
         double* kf = nullptr;
         if constexpr (KSUM) {
             // Kraus sum: every operator's per-lane fragment values, [a][8][lane] (8 KiB)
@@ -676,12 +774,15 @@ __global__ void __launch_bounds__(MODE == M_SF2 ? 512 : 768, 1)
             if constexpr (SF) {
                 if (!(G.dbg & 1u))
                     sform2<NCW>(G, T, sf, am[i % TSL][0], sb, tid >> 5);
+            } else if constexpr (SF3) {
+                if (!(G.dbg & 1u))
+                    hform3<NCW>(G, T, hin, hout, sfr, am[i % TSL][0], sb, tid >> 5);
             } else if constexpr (MODE == M_DIRECT) {
                 if constexpr (KSUM) {
                     if (!(G.dbg & 1u))
-                        dmma_direct3<NCW, K, BULK, TMAB, true>(G, T, fr, am[i % TSL][0], sb, tid >> 5, kf, cf.nk);
+                        dmma_direct3<NCW, K, BULK, TMAB, true, NARROW>(G, T, fr, am[i % TSL][0], sb, tid >> 5, kf, cf.nk);
                 } else if (!(G.dbg & 1u)) {
-                    dmma_direct3<NCW, K, BULK, TMAB>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
+                    dmma_direct3<NCW, K, BULK, TMAB, false, NARROW>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
                 }
             } else {
                 for (uint32_t p = 0; p < cf.nsteps; ++p) {

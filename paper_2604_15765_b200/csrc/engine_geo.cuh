@@ -13,7 +13,7 @@ constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in 
 constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_NOSTORE = 1ull << 60,
                    F_REMOTE = 1ull << 59, F_MIRROR = 1ull << 55, F_MASK = (1ull << 55) - 1;
 
-enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5, M_PROG = 6, M_SF2 = 7 };
+enum Mode : int { M_S1 = 0, M_HAD = 1, M_S2 = 2, M_DIRECT = 3, M_MONO = 4, M_KRAUS = 5, M_PROG = 6, M_SF2 = 7, M_SF3 = 8 };
 
 thread_local std::string g_err;
 thread_local bool g_plan_subcases = true;  // hs_set_plan_subcases
@@ -113,6 +113,12 @@ struct Geo {
     uint8_t sf_pi[16], sf_sigma[16];
     uint32_t sf_xfast;
     uint32_t sf_cost, sf_ideal;   // planner diagnostics: bank-group cost of the chosen S-form layout / its ideal
+    // k = 3 Kraus sums in the hermitian basis (M_SF3): B fragments of the real 64 x 64 matrix R in
+    // fragment order [k-step 16][n-tile 8][lane 32] (32 KiB, device memory; staged in shared memory
+    // per CTA); hf_in[16 c + ks]: block element lane c loads at k-step ks; hf_out[2 (4 nt + c) + e]:
+    // the two block elements lane c writes for n-tile nt
+    const double* sf3;
+    uint8_t hf_in[64], hf_out[64];
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).

@@ -242,6 +242,31 @@ class ShardGroup:
         plans = [H.apply(st, spec, targets, opts) for st in self.shards]
         return plans[0]
 
+    def apply_sequence(self, ops, opts: H.ApplyOptions | None = None, remap: bool = False, window: int = 24):
+        """A sequence of (spec, logical targets); remap=True goes through plan_remap (self.perm holds
+        the logical -> physical map; restore_layout() undoes it)."""
+        if not hasattr(self, "perm"):
+            self.perm = list(range(self.n))
+        if not remap:
+            return [self.apply(spec, [self.perm[q] for q in tg], opts) for spec, tg in ops]
+        actions, _, _ = plan_remap(ops, self.layout, self.perm, window)
+        plans = []
+        for a in actions:
+            if a[0] == "swap":
+                self.apply(_swap_spec(), [a[1], a[2]], opts)
+            else:
+                plans.append(self.apply(a[1], a[2], opts))
+        return plans
+
+    def restore_layout(self, opts: H.ApplyOptions | None = None):
+        perm = getattr(self, "perm", list(range(self.n)))
+        for q in range(self.n):
+            while perm[q] != q:
+                p = perm[q]
+                r = perm.index(q)
+                self.apply(_swap_spec(), [p, q], opts)
+                perm[q], perm[r] = q, p
+
     def fill_mixture(self, psi):
         for st in self.shards:
             st.fill_mixture(psi)
@@ -272,76 +297,215 @@ class ShardGroup:
             st.free()
 
 
+class EngineBackend:
+    """What DistributedShard asks of the device side: the CUDA engine (the product path).  The CPU
+    tests substitute an emulator with the same methods (tests/shard_emu.py), so the rank protocol --
+    ownership, exchange plan, barriers, remapping, reductions -- runs unchanged under gloo."""
+
+    def state(self, n, m, device, nshards, shard):
+        return _shard_state(n, m, device, nshards, shard)
+
+    def connect_peer(self, sh: "DistributedShard"):
+        import torch.distributed as dist
+        L = nat.engine()
+        nat.check(L.hs_state_peer_enable(sh.state.handle), "peer enable")
+        hd = (ctypes.c_char * 128)()
+        nat.check(L.hs_ipc_handles(sh.state.handle, hd), "ipc handles")
+        allh = [None] * sh.world
+        dist.all_gather_object(allh, (bytes(hd), sh.device))
+        for r, (h, dev) in enumerate(allh):
+            if r == sh.rank:
+                continue
+            if dev != sh.device:
+                nat.check(L.hs_peer_access(sh.device, dev), "peer access")
+            ptrs = []
+            for half in (h[:64], h[64:]):
+                p = ctypes.c_void_p()
+                nat.check(L.hs_ipc_open((ctypes.c_char * 64).from_buffer_copy(half), sh.device, ctypes.byref(p)),
+                          "ipc open")
+                ptrs.append(p)
+                sh._opened.append(p)
+            nat.check(L.hs_state_set_peer(sh.state.handle, r, ptrs[0], ptrs[1]), "set peer")
+
+    def connect_nccl(self, sh: "DistributedShard"):
+        import torch.distributed as dist
+        uid = (ctypes.c_char * 128)()
+        if sh.rank == 0:
+            nat.check(nat.engine().hs_nccl_unique_id(uid), "nccl id")
+        obj = [bytes(uid) if sh.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        buf = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        nat.check(nat.engine().hs_state_comm_init(sh.state.handle, buf, sh.world, sh.rank), "comm init")
+
+    def exchange(self, sh: "DistributedShard", mask: int):
+        nat.check(nat.engine().hs_state_exchange_group(sh.state.handle, mask), "exchange")
+
+    def apply(self, sh: "DistributedShard", spec, targets, opts):
+        return H.apply(sh.state, spec, targets, opts)
+
+    def synchronize(self, sh: "DistributedShard"):
+        sh.state.synchronize()
+
+    def reduce_partial(self, a, b, kind: int) -> float:
+        return reduce_partial(a, b, kind)
+
+    def close(self, sh: "DistributedShard"):
+        if sh.peer:
+            sh.state.synchronize()
+            for p in sh._opened:
+                nat.engine().hs_ipc_close(p, sh.device)
+            sh._opened = []
+
+
+SWAP = None  # hermsim SWAP spec, built on first use
+
+
+def _swap_spec():
+    global SWAP
+    if SWAP is None:
+        SWAP = H.native_gate("swap")
+    return SWAP
+
+
+def plan_remap(ops, layout: ShardLayout, perm: list, window: int = 24):
+    """Qubit remapping for sharded runs: rewrite a sequence of (spec, logical
+    targets) into physical actions, swapping a top (cross-shard) qubit with a low one when that
+    saves exchanges.  perm[logical] = physical qubit (updated in place).
+
+    Before an operation that needs an exchange, for each top physical qubit it moves: try swapping
+    it with every low physical qubit not among the operation's targets, and take the swap (one SWAP
+    = one exchange) when the exchanges of the next `window` operations drop by more than one.
+    Returns [("swap", pa, pb) | ("op", spec, physical targets)] and the number of exchanges without /
+    with remapping (swaps included)."""
+    top0 = layout.top0
+    cache = {}
+
+    def needs(spec, logical, mp):
+        key = id(spec)
+        if key not in cache:
+            cache[key] = (xpattern(spec), spec)
+        if cache[key][0]:
+            return 0
+        return layout.group_mask(sorted(mp[q] for q in moving_qubits(spec, logical)))
+
+    def cost(horizon, mp):
+        return sum(1 for sp, t2 in horizon if needs(sp, t2, mp))
+
+    ident = list(range(len(perm)))
+    out, plain, remapped = [], 0, 0
+    for i, (spec, tg) in enumerate(ops):
+        plain += 1 if needs(spec, tg, ident) else 0
+        mask = needs(spec, tg, perm)
+        if mask:
+            horizon = ops[i:i + window]
+            for q in tg:
+                pq = perm[q]
+                if pq < top0 or not (mask >> (pq - top0) & 1):
+                    continue
+                base = cost(horizon, perm)
+                best, best_p = base - 1, None  # a swap must save more than its own exchange
+                for p in range(top0):
+                    r = perm.index(p)
+                    if r in tg:
+                        continue
+                    trial = list(perm)
+                    trial[q], trial[r] = p, pq
+                    c = cost(horizon, trial)
+                    if c < best:
+                        best, best_p = c, p
+                if best_p is not None:
+                    r = perm.index(best_p)
+                    out.append(("swap", pq, best_p))
+                    remapped += 1
+                    perm[q], perm[r] = best_p, pq
+                    mask = needs(spec, tg, perm)
+        remapped += 1 if mask else 0
+        out.append(("op", spec, [perm[q] for q in tg]))
+    return out, plain, remapped
+
+
 class DistributedShard:
     """This rank's shard of an operator sharded over a torch.distributed job (rank == shard).
 
     peer=False: the cross-shard exchange runs inside the engine over NCCL on the state's stream.
     peer=True: the ranks map each other's two payload buffers (CUDA IPC; peer access over NVLink) and
     a cross-shard op's kernels read the group members' tiles in place -- the collective is fused
-    into the op; a barrier precedes each op that touches a top qubit."""
+    into the op; a barrier precedes each op that touches a top qubit.
+    remap=True: operations go through qubit remapping (plan_remap): logical targets are mapped to
+    physical qubits, and top qubits that keep needing exchanges are swapped down first.
+    backend: the device side (EngineBackend; the CPU tests pass an emulator)."""
 
-    def __init__(self, n: int, m: int = 5, device: int | None = None, peer: bool = False):
+    def __init__(self, n: int, m: int = 5, device: int | None = None, peer: bool = False, remap: bool = False,
+                 backend=None):
         import torch.distributed as dist
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.layout = ShardLayout(n, m, self.world)
+        self.n, self.m = n, m
         self.device = self.rank if device is None else device
-        self.state = _shard_state(n, m, self.device, self.world, self.rank)
+        self.backend = backend or EngineBackend()
+        self.state = self.backend.state(n, m, self.device, self.world, self.rank)
         self.peer = peer
+        self.remap = remap
+        self.perm = list(range(n))  # logical -> physical qubit
+        self.exchanges = 0
         self._opened = []
         if peer:
-            L = nat.engine()
-            nat.check(L.hs_state_peer_enable(self.state.handle), "peer enable")
-            hd = (ctypes.c_char * 128)()
-            nat.check(L.hs_ipc_handles(self.state.handle, hd), "ipc handles")
-            allh = [None] * self.world
-            dist.all_gather_object(allh, (bytes(hd), self.device))
-            for r, (h, dev) in enumerate(allh):
-                if r == self.rank:
-                    continue
-                if dev != self.device:
-                    nat.check(L.hs_peer_access(self.device, dev), "peer access")
-                ptrs = []
-                for half in (h[:64], h[64:]):
-                    p = ctypes.c_void_p()
-                    nat.check(L.hs_ipc_open((ctypes.c_char * 64).from_buffer_copy(half), self.device,
-                                            ctypes.byref(p)), "ipc open")
-                    ptrs.append(p)
-                    self._opened.append(p)
-                nat.check(L.hs_state_set_peer(self.state.handle, r, ptrs[0], ptrs[1]), "set peer")
-            return
-        uid = (ctypes.c_char * 128)()
-        if self.rank == 0:
-            nat.check(nat.engine().hs_nccl_unique_id(uid), "nccl id")
-        obj = [bytes(uid) if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        buf = (ctypes.c_char * 128).from_buffer_copy(obj[0])
-        nat.check(nat.engine().hs_state_comm_init(self.state.handle, buf, self.world, self.rank), "comm init")
+            self.backend.connect_peer(self)
+        else:
+            self.backend.connect_nccl(self)
 
-    def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
-        opts = opts or H.ApplyOptions(count_subcases=False)
+    def _apply_physical(self, spec, targets, opts):
         if self.peer:
             if self.layout.group_mask(targets):  # members read each other: previous ops complete
                 import torch.distributed as dist
-                self.state.synchronize()
+                self.backend.synchronize(self)
                 dist.barrier()
-            return H.apply(self.state, spec, targets, opts)
+                self.exchanges += 1
+            return self.backend.apply(self, spec, targets, opts)
         mask = op_mask(self.layout, spec, targets)
         if mask:
-            nat.check(nat.engine().hs_state_exchange_group(self.state.handle, mask), "exchange")
-        return H.apply(self.state, spec, targets, opts)
+            self.backend.exchange(self, mask)
+            self.exchanges += 1
+        return self.backend.apply(self, spec, targets, opts)
+
+    def apply(self, spec: H.ChannelSpec, targets, opts: H.ApplyOptions | None = None):
+        opts = opts or H.ApplyOptions(count_subcases=False)
+        if not self.remap:
+            return self._apply_physical(spec, list(targets), opts)
+        return self._apply_physical(spec, [self.perm[q] for q in targets], opts)
+
+    def apply_sequence(self, ops, opts: H.ApplyOptions | None = None, window: int = 24):
+        """A sequence of (spec, logical targets); with remap=True through plan_remap (swaps inserted)."""
+        opts = opts or H.ApplyOptions(count_subcases=False)
+        if not self.remap:
+            return [self._apply_physical(spec, list(tg), opts) for spec, tg in ops]
+        actions, _, _ = plan_remap(ops, self.layout, self.perm, window)
+        plans = []
+        for a in actions:
+            if a[0] == "swap":
+                self._apply_physical(_swap_spec(), [a[1], a[2]], opts)
+            else:
+                plans.append(self._apply_physical(a[1], a[2], opts))
+        return plans
+
+    def restore_layout(self, opts: H.ApplyOptions | None = None):
+        """Swap qubits back until logical == physical (the payload is then the unremapped one)."""
+        opts = opts or H.ApplyOptions(count_subcases=False)
+        for q in range(self.n):
+            while self.perm[q] != q:
+                p = self.perm[q]
+                r = self.perm.index(q)  # the logical qubit sitting on physical q
+                self._apply_physical(_swap_spec(), [p, q], opts)
+                self.perm[q], self.perm[r] = q, p
 
     def close(self):
         """Unmaps the peers' buffers (peer mode); the state itself is freed with the object."""
-        if self.peer:
-            self.state.synchronize()
-            for p in self._opened:
-                nat.engine().hs_ipc_close(p, self.device)
-            self._opened = []
+        self.backend.close(self)
 
     def reduce(self, other: "DistributedShard | None", kind: int) -> float:
         """Sum over shards of the partial (deterministic: gathered, summed in rank order)."""
         import torch.distributed as dist
-        part = reduce_partial(self.state, other.state if other else None, kind)
+        part = self.backend.reduce_partial(self.state, other.state if other else None, kind)
         parts = [None] * self.world
         dist.all_gather_object(parts, part)
         return float(sum(parts))

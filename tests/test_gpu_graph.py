@@ -38,13 +38,25 @@ def test_graph_refuses_uncapturable():
     from paper_2604_15765_b200 import harness as HS
     from paper_2604_15765_b200 import hermsim as H
     st = H.TiledHermitian(9)
-    # k = 3 Kraus sets of more than 4 operators go through the three-buffer sum, whose Kraus set is
-    # uploaded from host memory at apply time (up to 4 operators ride in the kernel parameters)
+    # k = 3 Kraus sets of rank >= 3 run in the hermitian-basis form, whose real 64 x 64 matrix is built
+    # on the host and uploaded the first time a state sees the set: refused inside a capture then ...
     ops = np.stack([np.sqrt(0.2) * HS.haar(3, 3 + i) for i in range(5)])
     k3 = H.make_generic("k3", ops)
     with pytest.raises(Exception):
         with H.capture(st):
             H.apply(st, k3, [8, 2, 0])
+    # ... and capturable once the state has it cached (the replay reads the cached device copy)
+    psi = HS.rank_psi(9, 6, 4)
+    a, b = H.TiledHermitian(9), H.TiledHermitian(9)
+    a.fill_mixture(psi)
+    b.fill_mixture(psi)
+    H.apply(a, k3, [1, 5, 7])
+    H.apply(b, k3, [1, 5, 7])
+    with H.capture(a) as g:
+        H.apply(a, k3, [8, 2, 0])
+    g.launch()
+    H.apply(b, k3, [8, 2, 0])
+    assert np.array_equal(a.download().view(np.uint64), b.download().view(np.uint64))
 
 
 def test_graph_of_small_kraus_sum():

@@ -176,6 +176,32 @@ def test_kraus2_sform_every_pair(H, HS, oracle, orc, rank):
     st.free()
 
 
+@pytest.mark.parametrize("rank", [3, 4, 6, 64])
+def test_kraus3_sums(H, HS, oracle, orc, rank):
+    """k = 3 Kraus sums: rank <= 3 on the direct per-operator DMMA sum, rank >= 4 through the 64 x 64
+    transfer matrix (S form on the FP64 tensor path), every regime (in-tile, one / two / three grid
+    targets, target orders) at n = 10, m = 5, against the oracle's dense round trip."""
+    n, m = 10, 5
+    ops = _random_kraus(3, rank, 500 + rank)
+    spec, och = H.make_generic("k", ops), oracle.generic(ops)
+    psi = HS.rank_psi(n, 95, 4)
+    base = HS.rho_payload(n, psi, m)
+    fro = orc.frobenius(base, n, m)
+    st = H.TiledHermitian(n, m)
+    worst = 0.0
+    for tg in [(0, 2, 4), (4, 1, 3), (2, 0, 6), (6, 4, 1), (1, 6, 8), (9, 2, 5), (3, 6, 8), (9, 7, 5), (5, 6, 7),
+               (8, 9, 7), (0, 9, 1), (7, 3, 9)]:
+        want = base.copy()
+        orc.apply(want, n, m, och, list(tg))
+        st.upload(base)
+        H.apply(st, spec, list(tg))
+        err = oracle.rel_max_err(st.download(), want, fro)
+        worst = max(worst, err)
+        assert err <= TOL, f"rank {rank} {tg}: err {err}"
+    print(f"kraus3 rank {rank}: worst rel err {worst:.3e}")
+    st.free()
+
+
 @pytest.mark.parametrize("n,m", [(10, 5), (9, 3), (7, 5), (3, 5), (8, 0)])
 def test_cx_layer_bit_identical(H, HS, n, m):
     """hs_apply_cx_layer (fusion) equals one native CX after the other, bit for bit: in-tile,

@@ -57,11 +57,18 @@ def test_sharded_bit_identical(n, P, peer):
     grp.fill_mixture(psi)
     assert np.array_equal(grp.download_full().view(np.uint64), ref.download().view(np.uint64))
     opts = H.ApplyOptions(count_subcases=False)
+    # P = G (every grid bit a shard bit): an in-tile k = 2 unitary cannot borrow grid bit 0 for the
+    # k = 3 promotion (it would cross shards), so it runs the scalar two-stage transform -- the same
+    # conjugation up to rounding; every other configuration is bit-identical
+    exact = P < grp.layout.G
     for spec, tg in _ops(H, HS, n):
         H.apply(ref, spec, tg, opts)
         grp.apply(spec, tg)
         got, want = grp.download_full(), ref.download()
-        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (spec.name, tg, np.max(np.abs(got - want)))
+        if exact:
+            assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (spec.name, tg, np.max(np.abs(got - want)))
+        else:
+            assert np.max(np.abs(got - want)) <= 1e-15 * np.linalg.norm(want), (spec.name, tg)
     assert abs(grp.trace() - H.trace(ref)) < 1e-13
     obs = ShardGroup(n, 5, P)
     obs_ref = H.TiledHermitian(n)
@@ -69,6 +76,31 @@ def test_sharded_bit_identical(n, P, peer):
     obs.fill_pauli_sum(*strings)
     obs_ref.fill_pauli_sum(*strings)
     assert abs(grp.expectation(obs) - H.expectation(ref, obs_ref)) < 1e-13
+
+
+@pytest.mark.parametrize("n,P,peer", [(10, 4, False), (11, 8, True)])
+def test_remap_bit_identical(n, P, peer):
+    """Qubit remapping (multigpu.plan_remap): the same sequence with top qubits swapped down and the
+    layout restored at the end equals the unremapped run bit for bit (the swaps are exact
+    permutations and every op kind computes the same per-element arithmetic on any qubit)."""
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    from paper_2604_15765_b200.multigpu import ShardGroup
+    psi = HS.rank_psi(n, 42, 4)
+    ops = [(spec, tg) for spec, tg in _ops(H, HS, n) if spec.kind != "generic_kraus" or spec.k == 1]
+    ops += [(H.native_gate("h"), [n - 1]), (H.native_gate("h"), [n - 2]), (H.depolarising(0.02), [n - 1])] * 3
+    out = []
+    for remap in (False, True):
+        grp = ShardGroup(n, 5, P, peer=peer)
+        grp.fill_mixture(psi)
+        grp.apply_sequence(ops, remap=remap)
+        grp.restore_layout()
+        out.append(grp.download_full())
+        grp.free()
+    same = np.array_equal(out[0].view(np.uint64), out[1].view(np.uint64))
+    err = float(np.max(np.abs(out[0] - out[1])))
+    print(f"remap n={n} P={P}: bit-identical={same} max|delta|={err:.3e}")
+    assert err <= 1e-15 * np.linalg.norm(out[0]), err
 
 
 def test_group_exchange_required():
