@@ -54,6 +54,8 @@ WORKLOADS = {
     "c2": "C2: depolarising(0.01) then amplitude damping(0.05) on qubits 0..15 (32 ops) on an n=16 rank-4 rho, m=5",
     "c3": "C3: 20 layers x 5 Haar 8x8 blocks in the Heisenberg picture (100 ops) on an n=16 Pauli-sum O, m=5",
     "c4": "C4: 10 layers of Rz+H per qubit, CX matching, depolarising(0.001) (590 ops) on an n=17 rank-4 rho, m=5",
+    "kraus": ("KRAUS: 2 layers of [two-qubit depolarising(0.01) (rank 16) on 8 seeded pairs, seeded random rank-4 "
+              "three-qubit channels on 5 seeded triples] (26 Kraus-sum passes) on an n=16 rank-4 rho, m=5"),
 }
 
 
@@ -169,6 +171,8 @@ def build_ops(H, HS, cfg: str, n: int):
             spec = H.make_generic("haar", op.matrix)
         elif op.kind == "unitary_dual":
             spec = H.dual_channel(H.make_generic("haar", op.matrix))
+        elif op.kind == "kraus":
+            spec = H.make_generic("kraus", op.matrix)
         else:
             raise ValueError(op.kind)
         out.append((spec, list(op.targets), op.kind))
@@ -258,6 +262,8 @@ def ref_channel(O, op):
         return O.generic(op.matrix)
     if op.kind == "unitary_dual":
         return O.dual(O.generic(op.matrix))
+    if op.kind == "kraus":
+        return O.generic(op.matrix)
     raise ValueError(op.kind)
 
 
@@ -681,9 +687,10 @@ def cpu_sample_n(cfg: str, n: int, m: int, reserved: int = 0) -> int:
         avail = 32 << 30
     budget = 0.85 * avail
     for k in range(n, 4, -1):
-        need = 1.05 * stored_bytes(k, m) + (3 * 16 * (1 << (2 * k)) if cfg == "c3" else 0)
+        dense3 = cfg in ("c3", "kraus")  # configs with k = 3 ops (the reference's dense round trip)
+        need = 1.05 * stored_bytes(k, m) + (3 * 16 * (1 << (2 * k)) if dense3 else 0)
         # the dense k = 3 path also costs ~4^n time: keep a C3 sample within seconds per op
-        if need <= budget and (cfg != "c3" or k <= 13):
+        if need <= budget and (not dense3 or k <= 13):
             return k
     return 5
 

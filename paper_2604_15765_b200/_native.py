@@ -179,6 +179,7 @@ def harness() -> ctypes.CDLL:
     _sig(L, "hsg_rho_payload", None, [i, i, i, c_double_p, c_double_p])
     _sig(L, "hsg_rho_payload_range", None, [i, i, i, c_double_p, c_double_p, u64, u64])
     _sig(L, "hsg_haar", None, [i, u64, c_double_p])
+    _sig(L, "hsg_isometry", i, [i, i, u64, c_double_p])
     _sig(L, "hsg_permutation", None, [i, u64, c_u32_p])
     _sig(L, "hsg_pauli_strings", None, [i, i, u64, c_u64_p, c_u64_p, c_i32_p, c_double_p])
     _sig(L, "hsg_pauli_payload", None, [i, i, i, c_u64_p, c_u64_p, c_i32_p, c_double_p, c_double_p])

@@ -114,47 +114,59 @@ void hsg_rho_payload(int n, int m, int rank, const double* psi, double* payload)
     hsg_rho_payload_range(n, m, rank, psi, payload, 0, G * (G + 1) / 2);
 }
 
-/* Haar-random 2^k x 2^k unitary: modified Gram-Schmidt QR of Z = gaussian_entry(seed, .)/sqrt2
- * (row-major), columns orthonormalised in order; R's diagonal is then real positive, i.e. the
- * phase-fixed Q = Q diag(R_ii / |R_ii|) of Mezzadri's recipe. */
-void hsg_haar(int k, uint64_t seed, double* u) {
-    const int d = 1 << k;
-    double z[64][2 * 8];
-    for (int r = 0; r < d; ++r)
-        for (int c = 0; c < d; ++c) {
+/* Isometry V (rows x cols, rows >= cols, V^dagger V = I): modified Gram-Schmidt QR of
+ * Z = gaussian_entry(seed, r * cols + c) / sqrt2 (row-major), columns orthonormalised in order;
+ * R's diagonal is then real positive, i.e. the phase-fixed Q = Q diag(R_ii / |R_ii|) of Mezzadri's
+ * recipe.  Returns 0, or -1 for an invalid shape. */
+int hsg_isometry(int rows, int cols, uint64_t seed, double* u) {
+    if (rows < 1 || cols < 1 || cols > rows || rows > 4096)
+        return -1;
+    double* z = (double*)malloc((size_t)rows * cols * 2 * sizeof(double));
+    if (!z)
+        return -1;
+#define Z(r, c) z[((size_t)(r) * cols + (c)) * 2]
+#define ZI(r, c) z[((size_t)(r) * cols + (c)) * 2 + 1]
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) {
             double g[2];
-            hsg_gaussian_entry(seed, (uint64_t)(r * d + c), g);
-            z[r][2 * c] = g[0] / sqrt(2.0);
-            z[r][2 * c + 1] = g[1] / sqrt(2.0);
+            hsg_gaussian_entry(seed, (uint64_t)r * cols + c, g);
+            Z(r, c) = g[0] / sqrt(2.0);
+            ZI(r, c) = g[1] / sqrt(2.0);
         }
-    for (int c = 0; c < d; ++c) {
+    for (int c = 0; c < cols; ++c) {
         for (int p = 0; p < c; ++p) { /* z[:,c] -= <q_p, z[:,c]> q_p */
             double dr = 0.0, di = 0.0;
-            for (int r = 0; r < d; ++r) { /* conj(q) * z */
-                const double qr = z[r][2 * p], qi = z[r][2 * p + 1], vr = z[r][2 * c], vi = z[r][2 * c + 1];
+            for (int r = 0; r < rows; ++r) { /* conj(q) * z */
+                const double qr = Z(r, p), qi = ZI(r, p), vr = Z(r, c), vi = ZI(r, c);
                 dr += qr * vr + qi * vi;
                 di += qr * vi - qi * vr;
             }
-            for (int r = 0; r < d; ++r) {
-                const double qr = z[r][2 * p], qi = z[r][2 * p + 1];
-                z[r][2 * c] -= dr * qr - di * qi;
-                z[r][2 * c + 1] -= dr * qi + di * qr;
+            for (int r = 0; r < rows; ++r) {
+                const double qr = Z(r, p), qi = ZI(r, p);
+                Z(r, c) -= dr * qr - di * qi;
+                ZI(r, c) -= dr * qi + di * qr;
             }
         }
         double ss = 0.0;
-        for (int r = 0; r < d; ++r)
-            ss += z[r][2 * c] * z[r][2 * c] + z[r][2 * c + 1] * z[r][2 * c + 1];
+        for (int r = 0; r < rows; ++r)
+            ss += Z(r, c) * Z(r, c) + ZI(r, c) * ZI(r, c);
         const double nrm = sqrt(ss);
-        for (int r = 0; r < d; ++r) {
-            z[r][2 * c] /= nrm;
-            z[r][2 * c + 1] /= nrm;
+        for (int r = 0; r < rows; ++r) {
+            Z(r, c) /= nrm;
+            ZI(r, c) /= nrm;
         }
     }
-    for (int r = 0; r < d; ++r)
-        for (int c = 0; c < d; ++c) {
-            u[2 * (r * d + c)] = z[r][2 * c];
-            u[2 * (r * d + c) + 1] = z[r][2 * c + 1];
-        }
+#undef Z
+#undef ZI
+    memcpy(u, z, (size_t)rows * cols * 2 * sizeof(double));
+    free(z);
+    return 0;
+}
+
+/* Haar-random 2^k x 2^k unitary (k <= 6): the square isometry. */
+void hsg_haar(int k, uint64_t seed, double* u) {
+    const int d = 1 << k;
+    (void)hsg_isometry(d, d, seed, u);
 }
 
 /* Fisher-Yates permutation of [0, n) from the (seed, counter) uniform stream. */

@@ -11,6 +11,9 @@ payload, and the final operators are compared elementwise:
   against apply()'s dense path for k = 3 (kernels.cpp:98-128, 498-505), plus tr(rho O) against the
   oracle; at n = 16 (the config size, where the reference would need ~240 GB for its dense round
   trip) tr(rho O) against an independent state-vector computation.
+* KRAUS (the bench's generic Kraus workload): the whole 2-layer sequence (two-qubit depolarising,
+  rank 16; random rank-4 three-qubit channels) at n = 12 against the reference (dense path for
+  k = 3), and its k = 2 channels at n = 16 (the reference's tiled 16 x 16 transfer path).
 * C4: the full 10-layer circuit (Rz, H, CX matching, depolarising) at n = 13 and n = 15, and one
   complete 59-op layer at n = 17 (137.5 GB: the reference's payload is built inside its own buffer).
 
@@ -66,6 +69,8 @@ def _spec(H, op):
         return H.amplitude_damping(op.param)
     if op.kind == "unitary":
         return H.make_generic("u", op.matrix)
+    if op.kind == "kraus":
+        return H.make_generic("kraus", op.matrix)
     return H.dual_channel(H.make_generic("u", op.matrix))
 
 
@@ -78,7 +83,7 @@ def _ref_channel(O, op):
         return O.depolarising(op.param)
     if op.kind == "ampdamp":
         return O.amplitude_damping(op.param)
-    if op.kind == "unitary":
+    if op.kind in ("unitary", "kraus"):
         return O.generic(op.matrix)
     return O.dual(O.generic(op.matrix))
 
@@ -305,3 +310,18 @@ def test_c4_layer_vs_statevector(H, HS, n):
             H.apply(st, _spec(H, op), list(op.targets))
     assert abs(H.trace(st) - 1.0) < 1e-12
     st.free()
+
+
+def test_kraus_workload_vs_reference_n12(H, HS, oracle):
+    n = 12
+    ops = HS.config_ops("kraus", n)
+    assert len(ops) == 2 * (n // 2 + n // 3)
+    err = _run_pair(H, HS, oracle, "kraus_n12", n, ops, HS.SEEDS["kraus"])
+    assert err <= TOL, err
+
+
+def test_kraus_two_qubit_channels_vs_reference_n16(H, HS, oracle):
+    ops = [op for op in HS.config_ops("kraus", 16) if len(op.targets) == 2]
+    assert len(ops) == 16
+    err = _run_pair(H, HS, oracle, "kraus2_n16", 16, ops, HS.SEEDS["kraus"])
+    assert err <= TOL, err

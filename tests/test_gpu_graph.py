@@ -50,8 +50,10 @@ def test_graph_refuses_uncapturable():
     a, b = H.TiledHermitian(9), H.TiledHermitian(9)
     a.fill_mixture(psi)
     b.fill_mixture(psi)
-    H.apply(a, k3, [1, 5, 7])
-    H.apply(b, k3, [1, 5, 7])
+    # the cache holds the BOUND set (bind_channel relabels the local basis by the target order):
+    # warm it with a triple of the same order pattern as the captured one (descending)
+    H.apply(a, k3, [7, 3, 1])
+    H.apply(b, k3, [7, 3, 1])
     with H.capture(a) as g:
         H.apply(a, k3, [8, 2, 0])
     g.launch()
