@@ -119,6 +119,24 @@ int hs_state_set_stream(hs_state* h, void* stream);
 void* hs_state_stream(const hs_state* h);
 void* hs_state_device_ptr(hs_state* h);
 
+/* Format conversions on the device (hermsim::to_dense / convert, storage.cpp:241-292; bit-identical
+ * to the reference's results).  dense = N x N row-major complex128 (DenseHermitian, storage.hpp:12-35),
+ * packed = column-major lower triangle, N(N+1)/2 complex128 (PackedHermitian, storage.hpp:37-58).
+ * `on_device` != 0: the buffer is device memory on the state's device (the call is stream-ordered on
+ * the state's stream); 0: host memory, streamed through device staging bands (synchronous).
+ * from_* follow convert()'s fill_from_lower: stored (i >= j) = d(i, j), a diagonal tile's upper half
+ * = conj(d(j, i)).  Unsharded states only (HS_ERR_UNSUPPORTED otherwise). */
+int hs_state_to_dense(const hs_state* h, double* out, int on_device);
+int hs_state_to_packed(const hs_state* h, double* out, int on_device);
+int hs_state_from_dense(hs_state* h, const double* in, int on_device);
+int hs_state_from_packed(hs_state* h, const double* in, int on_device);
+/* convert(src, tiled, dst's tile exponent): same n, any m on both sides, same device. */
+int hs_state_convert(const hs_state* src, hs_state* dst);
+/* Device memory helpers for the conversion buffers (cudaMalloc / cudaFree on `device`). */
+int hs_device_alloc(int device, uint64_t bytes, void** out);
+int hs_device_free(int device, void* p);
+int hs_copy_d2h(int device, void* host, const void* dev, uint64_t bytes);
+
 int hs_host_alloc(uint64_t bytes, void** out);   /* pinned host memory */
 int hs_host_free(void* p);
 

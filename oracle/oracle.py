@@ -263,6 +263,12 @@ class Reference:
         L.ref_random_hermitian.restype = ctypes.c_void_p
         L.ref_random_hermitian.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
         L.ref_save.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+        L.ref_convert.restype = ctypes.c_void_p
+        L.ref_convert.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        L.ref_dense_create.restype = ctypes.c_void_p
+        L.ref_dense_create.argtypes = [ctypes.c_int]
+        L.ref_format.restype = ctypes.c_int
+        L.ref_format.argtypes = [ctypes.c_void_p]
         L.ref_load.restype = ctypes.c_void_p
         L.ref_load.argtypes = [ctypes.c_char_p]
 
@@ -292,6 +298,21 @@ class Reference:
         if not h:
             raise IOError(self.lib.ref_last_error().decode())
         return h
+
+    def create_dense(self, n: int, dense: np.ndarray | None = None):
+        h = self.lib.ref_dense_create(n)
+        if not h:
+            raise ValueError(self.lib.ref_last_error().decode())
+        if dense is not None:
+            self.view(h)[:] = np.ascontiguousarray(dense, np.complex128).reshape(-1)
+        return h
+
+    def convert(self, h, fmt: str, m: int = 5):
+        """hermsim::convert(h, format, m) into a new handle (free it with free())."""
+        out = self.lib.ref_convert(h, {"dense": 0, "packed": 1, "tiled": 2}[fmt], m)
+        if not out:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return out
 
     def random_hermitian(self, n, seed, m=5):
         h = self.lib.ref_random_hermitian(n, seed, 2, m)

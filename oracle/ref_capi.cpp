@@ -104,6 +104,16 @@ void* ref_to_dense(void* h) {
     }
 }
 
+// hermsim::convert (storage.cpp:285-292) into a fresh handle of `format` (dense 0, packed 1, tiled 2).
+void* ref_convert(void* h, int format, int m) {
+    try {
+        return new MatrixHandle(convert(*static_cast<MatrixHandle*>(h), static_cast<Format>(format), m));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
 void* ref_random_hermitian(int n, uint64_t seed, int format, int m) {
     try {
         return new MatrixHandle(random_hermitian(n, seed, static_cast<Format>(format), m));

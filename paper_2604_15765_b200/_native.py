@@ -136,6 +136,12 @@ def engine() -> ctypes.CDLL:
     _sig(L, "hs_graph_nodes", i, [vp, c_u64_p])
     _sig(L, "hs_graph_free", i, [vp])
     _sig(L, "hs_state_save", i, [vp, ctypes.c_char_p])
+    for fn in ("hs_state_to_dense", "hs_state_to_packed", "hs_state_from_dense", "hs_state_from_packed"):
+        _sig(L, fn, i, [vp, vp, i])
+    _sig(L, "hs_state_convert", i, [vp, vp])
+    _sig(L, "hs_device_alloc", i, [i, u64, pp])
+    _sig(L, "hs_device_free", i, [i, vp])
+    _sig(L, "hs_copy_d2h", i, [i, vp, vp, u64])
     _sig(L, "hs_state_load", i, [ctypes.c_char_p, i, pp])
     _sig(L, "hs_state_recv_reserve", i, [vp, i])
     _sig(L, "hs_state_exchange_group_from", i, [vp, vp, ctypes.c_uint32])

@@ -57,6 +57,7 @@
 #include "engine_kernels.cuh"
 #include "engine_gather.cuh"
 #include "engine_aux.cuh"
+#include "engine_convert.cuh"
 
 
 // =============================================================================== host side
@@ -2686,6 +2687,175 @@ extern "C" int hs_debug_phase_cycles(unsigned long long* out8) {
     CUDA_TRY(cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z)));
     return HS_OK;
 }
+
+// ------------------------------------------------------------------- format conversions
+// hermsim::to_dense / convert (storage.cpp:241-292) on the device: engine_convert.cuh.  Host buffers
+// stream through two device staging bands of <= CV_BAND bytes (band b + 1's kernel overlaps band b's
+// copy on a second stream).
+namespace {
+constexpr uint64_t CV_BAND = 256ull << 20;
+int conv_grid(uint64_t items) { return (int)std::min<uint64_t>(std::max<uint64_t>(items, 1), 148ull * 8); }
+uint64_t packed_off_h(uint64_t N, uint64_t j) { return j * N - j * (j - 1) / 2; }
+uint64_t tri_h(uint64_t t) { return t * (t + 1) / 2; }
+
+// Tile-row (dense) or tile-column (packed) bands of <= CV_BAND bytes: [b[i], b[i + 1])
+std::vector<uint64_t> conv_bands(const hs_state* h, bool packed) {
+    const uint64_t M = h->M, G = h->G, N = h->N, E = std::min(M, N);
+    std::vector<uint64_t> b{0};
+    uint64_t acc = 0;
+    for (uint64_t t = 0; t < G; ++t) {
+        const uint64_t j0 = t * E, j1 = std::min(N, (t + 1) * E);
+        const uint64_t bytes = 16 * (packed ? packed_off_h(N, j1) - packed_off_h(N, j0) : (j1 - j0) * N);
+        if (acc && acc + bytes > CV_BAND) {
+            b.push_back(t);
+            acc = 0;
+        }
+        acc += bytes;
+    }
+    b.push_back(G);
+    return b;
+}
+
+int conv_check(const hs_state* h, const void* buf) {
+    if (!h || !buf)
+        return set_err(HS_ERR_INVALID, "null argument");
+    if (h->Plog)
+        return set_err(HS_ERR_UNSUPPORTED, "format conversion of a sharded state: gather the shards first");
+    return HS_OK;
+}
+
+// out: to_dense / to_packed of the whole state (dir = 0), or in: from_dense / from_packed (dir = 1)
+int convert_linear(hs_state* h, double2* buf, bool packed, bool from, bool on_device) {
+    DeviceGuard dg(h->device);
+    const uint32_t m = (uint32_t)h->m;
+    const uint64_t N = h->N, G = h->G, M = h->M, E = std::min(M, N);
+    auto launch_band = [&](uint64_t t0, uint64_t t1, double2* p, cudaStream_t s) {
+        if (!from && !packed)
+            to_dense_kernel<<<conv_grid(tri_h(t1) - tri_h(t0) + (t1 - t0) * G), CV_T, 0, s>>>(h->d, m, N, G, t0, t1, p);
+        else if (!from)
+            to_packed_kernel<<<conv_grid((t1 - t0) * G), CV_T, 0, s>>>(h->d, m, N, G, t0, t1, p);
+        else if (!packed)
+            from_dense_kernel<<<conv_grid(tri_h(t1) - tri_h(t0)), CV_T, 0, s>>>(h->d, m, N, t0, t1, p);
+        else
+            from_packed_kernel<<<conv_grid((t1 - t0) * G), CV_T, 0, s>>>(h->d, m, N, G, t0, t1, p);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError();
+    };
+    auto band_bytes = [&](uint64_t t0, uint64_t t1) {
+        const uint64_t j0 = t0 * E, j1 = std::min(N, t1 * E);
+        return 16 * (packed ? packed_off_h(N, j1) - packed_off_h(N, j0) : (j1 - j0) * N);
+    };
+    auto band_elem = [&](uint64_t t0) { return packed ? packed_off_h(N, t0 * E) : t0 * E * N; };
+    if (on_device) {
+        CUDA_TRY(launch_band(0, G, buf, h->stream));
+        return HS_OK;
+    }
+    const std::vector<uint64_t> b = conv_bands(h, packed);
+    uint64_t cap = 0;
+    for (size_t i = 0; i + 1 < b.size(); ++i)
+        cap = std::max(cap, band_bytes(b[i], b[i + 1]));
+    double2* stage[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    cudaError_t e = cudaSuccess;
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+        e = cudaMalloc(&stage[k], cap);
+        if (e == cudaSuccess)
+            e = cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming);
+    }
+    // band i: (from) host -> stage -> kernel, or kernel -> stage -> host; stage i & 1 is reused
+    // once band i - 2 finished with it (events on the state's stream)
+    for (size_t i = 0; e == cudaSuccess && i + 1 < b.size(); ++i) {
+        const int k = (int)(i & 1);
+        double2* hp = buf + band_elem(b[i]);
+        const uint64_t bytes = band_bytes(b[i], b[i + 1]);
+        if (i >= 2)
+            e = cudaEventSynchronize(done[k]);  // the host copy of band i - 2 has left stage k
+        if (e == cudaSuccess && from)
+            e = cudaMemcpyAsync(stage[k], hp, bytes, cudaMemcpyHostToDevice, h->stream);
+        if (e == cudaSuccess)
+            e = launch_band(b[i], b[i + 1], stage[k], h->stream);
+        if (e == cudaSuccess && !from)
+            e = cudaMemcpyAsync(hp, stage[k], bytes, cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess)
+            e = cudaEventRecord(done[k], h->stream);
+    }
+    if (e == cudaSuccess)
+        e = cudaStreamSynchronize(h->stream);
+    for (int k = 0; k < 2; ++k) {
+        cudaFree(stage[k]);
+        if (done[k])
+            cudaEventDestroy(done[k]);
+    }
+    if (e != cudaSuccess)
+        return set_err(HS_ERR_CUDA, std::string("format conversion: ") + cudaGetErrorString(e));
+    return HS_OK;
+}
+}  // namespace
+
+extern "C" {
+int hs_state_to_dense(const hs_state* h, double* out, int on_device) {
+    int rc = conv_check(h, out);
+    return rc ? rc : convert_linear(const_cast<hs_state*>(h), reinterpret_cast<double2*>(out), false, false, on_device);
+}
+int hs_state_to_packed(const hs_state* h, double* out, int on_device) {
+    int rc = conv_check(h, out);
+    return rc ? rc : convert_linear(const_cast<hs_state*>(h), reinterpret_cast<double2*>(out), true, false, on_device);
+}
+int hs_state_from_dense(hs_state* h, const double* in, int on_device) {
+    int rc = conv_check(h, in);
+    return rc ? rc : convert_linear(h, reinterpret_cast<double2*>(const_cast<double*>(in)), false, true, on_device);
+}
+int hs_state_from_packed(hs_state* h, const double* in, int on_device) {
+    int rc = conv_check(h, in);
+    return rc ? rc : convert_linear(h, reinterpret_cast<double2*>(const_cast<double*>(in)), true, true, on_device);
+}
+int hs_state_convert(const hs_state* src, hs_state* dst) {
+    int rc = conv_check(src, dst);
+    if (rc)
+        return rc;
+    if (dst->Plog)
+        return set_err(HS_ERR_UNSUPPORTED, "format conversion of a sharded state: gather the shards first");
+    if (src->n != dst->n)
+        return set_err(HS_ERR_INVALID, "convert: qubit counts differ");
+    if (src->device != dst->device)
+        return set_err(HS_ERR_INVALID, "convert: states on different devices");
+    if (src == dst)
+        return HS_OK;
+    DeviceGuard dg(dst->device);
+    // dst's stream waits for src's pending work
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev, src->stream));
+    CUDA_TRY(cudaStreamWaitEvent(dst->stream, ev, 0));
+    CUDA_TRY(cudaEventDestroy(ev));
+    retile_kernel<<<conv_grid((dst->count + CV_T - 1) / CV_T), CV_T, 0, dst->stream>>>(dst->d, (uint32_t)dst->m, dst->count,
+                                                                                      dst->N, src->d, (uint32_t)src->m);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CUDA_TRY(cudaGetLastError());
+    return HS_OK;
+}
+int hs_device_alloc(int device, uint64_t bytes, void** out) {
+    if (!out)
+        return set_err(HS_ERR_INVALID, "null out");
+    DeviceGuard dg(device);
+    if (cudaMalloc(out, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return set_err(HS_ERR_NOMEM, "cudaMalloc failed");
+    }
+    return HS_OK;
+}
+int hs_device_free(int device, void* p) {
+    DeviceGuard dg(device);
+    CUDA_TRY(cudaFree(p));
+    return HS_OK;
+}
+int hs_copy_d2h(int device, void* host, const void* dev, uint64_t bytes) {
+    DeviceGuard dg(device);
+    CUDA_TRY(cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost));
+    return HS_OK;
+}
+}  // extern "C"
 
 // ---------------------------------------------------------------------- OHRM save / load
 // The reference's container (storage_io.cpp:34-118, storage_io.hpp:22-29): magic "OHRM", version

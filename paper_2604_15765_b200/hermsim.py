@@ -165,6 +165,45 @@ class TiledHermitian:
         """hermsim::basis_projector(n, basis, tiled, m) (storage.cpp:230-239)."""
         nat.check(nat.engine().hs_state_fill_basis_projector(self.handle, basis), "basis_projector")
 
+    # -- format conversions on the device (hermsim::to_dense / convert, storage.cpp:241-292) ------
+    def to_dense(self, out: np.ndarray | None = None) -> np.ndarray:
+        """hermsim::to_dense: the N x N row-major matrix (bit-identical to the reference's)."""
+        N = self.dim()
+        if out is None:
+            out = np.empty((N, N), np.complex128)
+        if out.shape != (N, N) or out.dtype != np.complex128 or not out.flags.c_contiguous:
+            raise ValueError("to_dense: out must be a C-contiguous (N, N) complex128 array")
+        nat.check(nat.engine().hs_state_to_dense(self.handle, out.ctypes.data, 0), "to_dense")
+        return out
+
+    def to_packed(self, out: np.ndarray | None = None) -> np.ndarray:
+        """convert(h, packed): the column-major packed lower triangle, N(N+1)/2 elements."""
+        N = self.dim()
+        cnt = N * (N + 1) // 2
+        if out is None:
+            out = np.empty(cnt, np.complex128)
+        if out.shape != (cnt,) or out.dtype != np.complex128 or not out.flags.c_contiguous:
+            raise ValueError("to_packed: out must be a contiguous complex128 array of N(N+1)/2 elements")
+        nat.check(nat.engine().hs_state_to_packed(self.handle, out.ctypes.data, 0), "to_packed")
+        return out
+
+    def from_dense(self, dense: np.ndarray) -> None:
+        """convert(MatrixHandle(dense), tiled, m): stored (i >= j) = d(i, j), diagonal-tile upper halves
+        = conj(d(j, i))."""
+        N = self.dim()
+        d = np.ascontiguousarray(dense, np.complex128)
+        if d.shape != (N, N):
+            raise ValueError("from_dense: shape must be (N, N)")
+        nat.check(nat.engine().hs_state_from_dense(self.handle, d.ctypes.data, 0), "from_dense")
+
+    def from_packed(self, packed: np.ndarray) -> None:
+        """convert(MatrixHandle(packed), tiled, m)."""
+        N = self.dim()
+        p = np.ascontiguousarray(packed, np.complex128)
+        if p.shape != (N * (N + 1) // 2,):
+            raise ValueError("from_packed: need N(N+1)/2 elements")
+        nat.check(nat.engine().hs_state_from_packed(self.handle, p.ctypes.data, 0), "from_packed")
+
     def save(self, path: str) -> None:
         """hermsim::save (storage_io.cpp:34-56): OHRM container, tiled format."""
         nat.check(nat.engine().hs_state_save(self.handle, os.fsencode(path)), "save")
@@ -395,6 +434,27 @@ class Graph:
 
 def capture(state: TiledHermitian) -> Graph:
     return Graph(state)
+
+
+def convert(h: TiledHermitian, target: str = "tiled", tile_exp: int = 5):
+    """hermsim::convert (storage.cpp:285-292) on the device.  target "tiled" returns a new
+    TiledHermitian with tile exponent `tile_exp` on the same device; "dense" / "packed" return the
+    host array of that format (the reference's DenseHermitian / PackedHermitian payloads)."""
+    if target == "dense":
+        return h.to_dense()
+    if target == "packed":
+        return h.to_packed()
+    if target != "tiled":
+        raise ValueError(f"convert: unknown format '{target}'")
+    out = TiledHermitian(h.qubits(), tile_exp, device=h.device)
+    h.synchronize()
+    nat.check(nat.engine().hs_state_convert(h.handle, out.handle), "convert")
+    return out
+
+
+def to_dense(h: TiledHermitian) -> np.ndarray:
+    """hermsim::to_dense (storage.cpp:241-283)."""
+    return h.to_dense()
 
 
 def expectation(rho: TiledHermitian, obs: TiledHermitian) -> float:

@@ -9,7 +9,7 @@ every staging mode: bulk rows, TMA boxes with and without quadrants, 4-tile item
 k = 2 unitaries through the pairing and the promotions; k = 2 Kraus sums in S form on whole tiles,
 mixed and cross units; k = 3 Kraus sums of rank 2..4; grid programs), gather_kernel and conj_kernel
 (k = 3 Kraus sums of rank > 4, k = 2 transfer matrices for m < 5, diagonal units), cx_layer_kernel,
-reductions, device generators, and peer-mode sharded ops (ShardGroup, one process).
+reductions, device generators, format conversions, and peer-mode sharded ops (ShardGroup, one process).
 Each case also checks its result against the CPU oracle, so a sanitizer run doubles as a parity run.
 """
 import itertools
@@ -98,6 +98,11 @@ def main():
         H.frobenius(st)
         obs.fill_random_hermitian(7)
         obs.fill_basis_projector(3)
+        # format conversions (to_dense / convert, storage.cpp:241-292)
+        dense = obs.to_dense()
+        obs.from_dense(dense)
+        obs.from_packed(obs.to_packed())
+        H.convert(obs, "tiled", max(0, m - 2)).free()
         obs.free()
         st.free()
     # sharded, peer mode and exchange mode (one process, one GPU)
