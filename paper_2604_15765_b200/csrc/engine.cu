@@ -491,8 +491,13 @@ void search_put(uint64_t key, const std::array<uint8_t, 65>& v) {
 
 // bulk: stage sub-block rows with cp.async.bulk, one copy per run of >= 8 contiguous elements
 // (tiles keep their stored orientation, adjoint components addressed through cadj).
+// element tables of the hermitian-basis transform (hform3; built by hform_tables below)
+struct HForm {
+    uint8_t in[64], out[64];
+};
+const HForm& hform_tables();
 void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride = 0, bool tma = false,
-                 bool prog = false, bool sform = false, uint32_t min_run = 4) {
+                 bool prog = false, bool sform = false, uint32_t min_run = 4, bool hform = false) {
     const uint32_t M = G.M, g = G.g, NT = G.grp4 ? 4u : 1u << (2 * g), NG = 1u << g, kin = G.kin;
     const uint32_t in_mask = G.in_mask;
     uint32_t S0 = 1;
@@ -777,7 +782,86 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
     // (preferred to bulk rows where both apply: 64 box copies per item instead of 256 row copies,
     // C3 g = 2 ops 13.5-14.5 ms with rows vs 12.0-12.8 ms with boxes)
     G.tq = 1;
-    if (tma && prog && M == 32 && G.logRun >= 3 && S0 >= 8 && NT * bpt <= 64) {
+    if (tma && hform && D == 8 && M == 32 && (S0 == 8 || S0 == 16) && NT * bpt == 64 && G.logRun >= 3 &&
+        G.nxb == 8 && G.nyb == 8) {
+        // hform3 (k = 3 Kraus sums) with 8 x 8 boxes on two or three grid targets: 64 box copies per
+        // item instead of 512 bulk rows of 128 / 256 B.  Component ci of block (xb, yb) sits at
+        // sub-block position (xb | xr, yb | yc) of logical tile t; the box is (x >> 3, y >> 3) of the
+        // tile (stored orientation: transposed for adjoint tiles).  A quarter-warp of a hform3 load /
+        // store touches 2 blocks (yb, yb' at one xb) x the 4 components of its lanes (hin / hout);
+        // pick each slot's swizzle phase by coordinate descent so those 8 accesses fall into
+        // distinct 16-byte bank groups, for all-direct and all-adjoint units.
+        G.tma = 1;
+        G.bulk = 0;
+        const HForm& hf = hform_tables();
+        for (uint32_t ci = 0; ci < 64; ++ci) {
+            const uint32_t rho = ci >> 3, gam = ci & 7u, t = (rho >> kin) * NG + (gam >> kin);
+            G.hsd[ci] = (uint8_t)(t * bpt);
+            G.hsa[ci] = (uint8_t)((G.xs_in[rho & kinm] << 4) | G.y_in[gam & kinm]);
+        }
+        uint8_t phi[64];
+        for (uint32_t t = 0; t < 64; ++t)
+            phi[t] = (uint8_t)((2 * t) & 7u);
+        const uint32_t nbx_ = nbx;
+        auto chunk = [&](uint32_t ci, uint32_t xb, uint32_t yb, uint32_t ori) {
+            uint32_t x = xb | (G.hsa[ci] >> 4), y = yb | (G.hsa[ci] & 15u);
+            if (ori)
+                std::swap(x, y);
+            const uint32_t sl = G.hsd[ci] + (x >> 3) * nbx_ + (y >> 3);
+            return (y & 7u) ^ (((x & 7u) + phi[sl]) & 7u);
+        };
+        auto hcost = [&]() {
+            uint32_t cost = 0;
+            for (uint32_t xi = 0; xi < 8; xi += 3)  // sample passes (block row xi of the sub-block)
+                for (uint32_t ori = 0; ori < 2; ++ori)
+                    for (uint32_t ins = 0; ins < 32; ++ins)  // 16 loads (j, e), 16 stores (nt, e)
+                        for (uint32_t ph = 0; ph < 4; ++ph) {
+                            uint32_t cnt[8] = {0}, mx = 0;
+                            for (uint32_t l = 8 * ph; l < 8 * ph + 8; ++l) {
+                                const uint32_t gq = l >> 2, cq = l & 3u;
+                                const uint32_t ci = ins < 16 ? hf.in[16 * cq + ins]
+                                                             : hf.out[2 * (4 * ((ins - 16) >> 1) + cq) + (ins & 1u)];
+                                mx = std::max(mx, ++cnt[chunk(ci, G.xb_tab[xi], G.yb_tab[gq], ori)]);
+                            }
+                            cost += mx;
+                        }
+            return cost;
+        };
+        const uint64_t key = search_key(G, 4, 0);
+        std::array<uint8_t, 65> cached;
+        const bool hit = search_get(key, cached);
+        if (hit)
+            for (uint32_t q = 0; q < 64; ++q)
+                phi[q] = cached[q];
+        const uint32_t ideal = 3u * 2u * 32u * 4u;
+        uint32_t cur = hit ? 0u : hcost();
+        for (uint32_t pass = 0; pass < 4 && cur > ideal; ++pass)
+            for (uint32_t q = 0; q < 64; ++q) {
+                uint8_t bv = phi[q];
+                for (uint32_t v = 0; v < 8; ++v) {
+                    phi[q] = (uint8_t)v;
+                    const uint32_t c = hcost();
+                    if (c < cur) {
+                        cur = c;
+                        bv = (uint8_t)v;
+                    }
+                }
+                phi[q] = bv;
+            }
+        if (!hit) {
+            std::array<uint8_t, 65> v{};
+            for (uint32_t q = 0; q < 64; ++q)
+                v[q] = phi[q];
+            search_put(key, v);
+        }
+        uint32_t k = 0;  // slots in order of phase (see below)
+        for (uint32_t v = 0; v < 8; ++v)
+            for (uint32_t q = 0; q < 64; ++q)
+                if (phi[q] == v) {
+                    G.cdir[q] = (uint16_t)(k++ * 64 + v * 8);
+                    G.tsk[q] = (uint8_t)v;
+                }
+    } else if (tma && prog && M == 32 && G.logRun >= 3 && S0 >= 8 && NT * bpt <= 64) {
         // grid programs: consecutive threads take consecutive positions of one logical tile, so
         // any phase is conflict-free in both placements (the in-box chunk y ^ x, resp. x ^ y, is a
         // bijection along the row): phase 0, boxes packed
@@ -787,7 +871,7 @@ void plan_gather(Geo& G, bool dmma = false, bool bulk = false, uint32_t qstride 
             G.cdir[q] = (uint16_t)(q * 64);
             G.tsk[q] = 0;
         }
-    } else if (tma && dmma && D == 8 && M == 32 && G.logRun >= 3 && (S0 == 8 || S0 == 16) && NT * bpt <= 64 &&
+    } else if (tma && dmma && !hform && D == 8 && M == 32 && G.logRun >= 3 && (S0 == 8 || S0 == 16) && NT * bpt <= 64 &&
         (!(((S0 - 1) & ~xs_tmask) & 8u) || (G.nxb == 8 && G.nyb == 8))) {
         G.bulk = 0;
         G.tq = (((S0 - 1) & ~xs_tmask) & 8u) ? 4 : 1;  // bit 3 free: it selects the box per block
@@ -875,9 +959,6 @@ constexpr int RC_NO_KRAUS_SUM = -1000;
 // Element tables of the hermitian-basis transform (hform3): lane c of a quad loads 7 mirrored pairs
 // (r, c), (c, r) of the 8 x 8 block and the diagonal elements 2c, 2c + 1 (in[16 c + 2 j + e]);
 // output pair q = 4 nt + c: the 28 upper pairs, then 4 pairs of diagonal elements (out[2 q + e]).
-struct HForm {
-    uint8_t in[64], out[64];
-};
 const HForm& hform_tables() {
     static const HForm tabs = [] {
     HForm t{};
@@ -926,7 +1007,28 @@ const bool g_kraus2_direct = [] {
     return e && atoi(e) != 0;
 }();
 
+// HS_DEBUG_FLAGS (diagnostics; read once).  DBG_POISON: the copy side fills every ring stage with
+// NaN after its write-back has left the stage and before the next load is issued, so a transform
+// that reads a stage before its load landed, or a write-back that reads after the refill started,
+// puts NaN into the result (the race / synchronisation check that replaces compute-sanitizer, which
+// this pool does not run: tests/test_gpu_races.py).
+uint32_t debug_flags() {
+    static const uint32_t v = [] {
+        const char* e = getenv("HS_DEBUG_FLAGS");
+        return e ? (uint32_t)atoi(e) : 0u;
+    }();
+    return v;
+}
+
+// Persistent-grid size: the SM count, or HS_DEBUG_GRID (tests: a different number of CTAs takes a
+// different share of the items, so inter-CTA ordering bugs change the result)
 int sm_count(int device) {
+    static const int grid_override = [] {
+        const char* e = getenv("HS_DEBUG_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    if (grid_override > 0)
+        return grid_override;
     static int cache[64] = {0};
     if (device < 0 || device >= 64)
         return 148;
@@ -985,7 +1087,7 @@ int shard_prelude(hs_state* h, const Geo& G0, bool carry_over, Geo& G) {
             G.rbase[j] = j < h->recv_slots ? h->recv + (uint64_t)j * h->recv_count : nullptr;
     }
     G.rev = (uint32_t)(h->sweeps++ & 1u);
-    G.dbg = 0;
+    G.dbg = debug_flags() & DBG_POISON;  // the pipeline takes only the stage-poisoning bit
     return HS_OK;
 }
 
@@ -1301,24 +1403,27 @@ int launch_sform3_impl(hs_state* h, const Geo& G0, const double* frag) {
         G.logNT = 2;
         G.nloc_tiles = h->count >> 10;
     }
-    plan_gather(G, true, true, 0, false, false, false, 3);
-    {
-        static const char* dbg = getenv("HS_DEBUG_FLAGS");
-        G.dbg = dbg ? (uint32_t)atoi(dbg) : 0u;
-    }
-    if (!G.bulk)
+    // two / three grid targets: 8 x 8 TMA boxes instead of 128-B bulk rows where plan_gather can
+    // place them (local tiles only: the tensor maps cover this shard's payload; HS_DEBUG_FLAGS bit 8:
+    // off)
+    const uint32_t dbgf = debug_flags();
+    CUtensorMap tin{}, tout{};
+    const bool maps = G.g >= 2 && !G.cmask && !(dbgf & 256u) && G.M == 32 && encode_tile_map(&tin, h->d, h->count) &&
+                      encode_tile_map(&tout, G.out, h->count);
+    plan_gather(G, true, true, 0, maps, false, false, 3, true);
+    G.dbg = dbgf;
+    if (!G.bulk && !G.tma)
         return RC_NO_KRAUS_SUM;
     G.sf3 = frag;
     G.ws_diag = 1;
     G.nG_items = G.grp4 ? (G.nloc_tiles + 3) / 4 : G.nU_loose << (2 * G.log_nsb_side);
-    const size_t smem = (size_t)2 * G.stage_elems * sizeof(double2) + 4096 * sizeof(double);
-    auto kw = gather_ws_kernel<3, 64, M_SF3, true>;
+    const size_t smem = (size_t)2 * G.stage_elems * sizeof(double2) + 4096 * sizeof(double) + (G.tma ? 1024 : 0);
+    auto kw = G.tma ? gather_ws_kernel<3, 64, M_SF3, true, true> : gather_ws_kernel<3, 64, M_SF3, true>;
     cudaError_t e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess)
         return set_err(HS_ERR_CUDA, std::string("cudaFuncSetAttribute(sform3): ") + cudaGetErrorString(e));
     const uint64_t grid = std::min<uint64_t>(G.nG_items, (uint64_t)sm_count(h->device));
     if (grid) {
-        CUtensorMap tin{}, tout{};
         Coef<64> cf{};
         kw<<<(unsigned)grid, 512, smem, h->stream>>>(G, cf, h->d, tin, tout);
         g_launches.fetch_add(1, std::memory_order_relaxed);

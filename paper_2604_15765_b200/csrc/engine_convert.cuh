@@ -9,7 +9,8 @@
 //                     the conjugate of its mirror;
 //   convert(.., packed / tiled):  fill_from_lower(gen = to_dense(src).at) (storage.cpp:149-189,
 //                     285-292): stored (i >= j) = d(i, j); a tiled target's diagonal-tile upper half
-//                     = conj(d(j, i)); padding (N < M) = 0.
+//                     = conj(d(j, i)); padding (N < M) = 0;
+//   to_dense(packed): d(i, j) = P(i, j), d(j, i) = conj(P(i, j)), so d(i, i) = conj(P(i, i)).
 // HBM layout: every kernel moves whole 32 x 32 (or M x M) blocks through shared memory so both the
 // read and the write side are coalesced rows of >= 128 B (the transposed half of a dense matrix is
 // written from the staged stored tile, the packed columns are read / written along rows i).  Pure
@@ -130,7 +131,9 @@ __global__ void __launch_bounds__(CV_T) from_dense_kernel(double2* dst, uint32_t
 
 // Packed columns [tj0 * M, tj1 * M) (in points at column tj0 * M) -> the stored tiles (ti, tj),
 // tj in [tj0, tj1): lower elements read along i (contiguous in the packed column), a diagonal tile's
-// upper half = conj(lower mirror).
+// upper half = conj(lower mirror).  The matrix diagonal is conj(P(i, i)): the reference's
+// to_dense(packed) sets d(i, j) = v, then d(j, i) = conj(v), which for i == j leaves conj(v)
+// (storage.cpp:249-256; only visible for a payload whose diagonal is not real).
 __global__ void __launch_bounds__(CV_T) from_packed_kernel(double2* dst, uint32_t m, uint64_t N, uint64_t G,
                                                            uint64_t tj0, uint64_t tj1, const double2* __restrict__ in) {
     __shared__ double2 s[32][33];
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(CV_T) from_packed_kernel(double2* dst, uint32_
             const uint32_t r = e >> m, c = e & (M - 1);
             double2 v = make_double2(0.0, 0.0);
             if (r < E && c < E)
-                v = (ti != tj || r >= c) ? s[r][c] : cconj(s[c][r]);
+                v = (ti != tj || r > c) ? s[r][c] : cconj(s[c][r]);
             tp[e] = v;
         }
     }

@@ -384,13 +384,27 @@ __device__ __forceinline__ void sform2(const Geo& G, const Tabs& T, const SfFrag
 // Re B_cr - Re B_rc.  Outputs come out as coordinate pairs (Re, Im of H_rc) of H1 = R x1 and H2 = R x2:
 // W_rc = H1_rc + i H2_rc, W_cr = conj(H1_rc) + i conj(H2_rc) (n-tile 7: pairs of diagonal elements).
 // 8 blocks per warp pass: 16 k-steps x 8 n-tiles x 2 products = 256 DMMA.
-template <int NC>
+// TMAB: component ci of block (xb, yb) is sub-block position (x, y) = (xb | xr, yb | yc) of logical
+// tile t (T.hsd[ci] = t * boxes per tile, T.hsa[ci] = xr << 4 | yc), transposed for adjoint tiles
+// (stored orientation); it sits in the 8 x 8 box (x >> 3, y >> 3) of the tile (base T.cdir[slot],
+// swizzle phase T.tsk[slot]) at (x & 7) * 8 + ((y & 7) ^ (((x & 7) + phi) & 7)).
+template <int NC, bool TMAB = false>
 __device__ __forceinline__ void hform3(const Geo& G, const Tabs& T, const uint8_t* hin, const uint8_t* hout,
                                        const double* rfr, uint64_t am, double2* sb, uint32_t warp) {
     const uint32_t lane = threadIdx.x & 31u, gq = lane >> 2, cq = lane & 3u;
     const uint32_t lbt = G.logNxb + G.logNyb, npass = ((G.grp4 ? 4u : 1u) << lbt) >> 3;
     const uint32_t logNy = G.logNyb, ymask = G.nyb - 1;
     const uint8_t* myin = hin + 16 * cq;
+    auto addr = [&](uint32_t ci, uint32_t adj, uint32_t base, uint32_t baseA, uint32_t xbv, uint32_t ybv) -> uint32_t {
+        if constexpr (TMAB) {
+            const uint32_t xy = T.hsa[ci], xd = xbv | (xy >> 4), yd = ybv | (xy & 15u);
+            const uint32_t x = adj ? yd : xd, y = adj ? xd : yd;
+            const uint32_t sl = T.hsd[ci] + ((x >> 3) << (G.logS0 - 3)) + (y >> 3);
+            return T.cdir[sl] + (x & 7u) * 8u + ((y & 7u) ^ (((x & 7u) + T.tsk[sl]) & 7u));
+        } else {
+            return adj ? baseA + T.cadj[ci] : base + T.cdir[ci];
+        }
+    };
     for (uint32_t p = warp; p < npass; p += NC / 32) {
         const uint32_t b = 8 * p + gq, bq = b & ((1u << lbt) - 1);
         const uint32_t xbv = T.xb[bq >> logNy], ybv = T.yb[bq & ymask];
@@ -404,7 +418,7 @@ __device__ __forceinline__ void hform3(const Geo& G, const Tabs& T, const uint8_
 #pragma unroll
             for (uint32_t e = 0; e < 2; ++e) {
                 const uint32_t ci = myin[2 * j + e], adj = (uint32_t)(am >> T.ttr[ci]) & 1u;
-                v[e] = sb[adj ? baseA + T.cadj[ci] : base + T.cdir[ci]];
+                v[e] = sb[addr(ci, adj, base, baseA, xbv, ybv)];
                 v[e].y = flip_sign(v[e].y, adj << 31);
             }
             if (j < 7) {  // mirrored pair (r, c), (c, r)
@@ -419,17 +433,7 @@ __device__ __forceinline__ void hform3(const Geo& G, const Tabs& T, const uint8_
                 x2[15] = v[1].y;
             }
         }
-#pragma unroll 1
-        for (uint32_t nt = 0; nt < 8; ++nt) {
-            double h1a = 0.0, h1b = 0.0, h2a = 0.0, h2b = 0.0;
-            const uint32_t f = smem_u32(rfr + nt * 32 + lane);
-#pragma unroll
-            for (uint32_t ks = 0; ks < 16; ++ks) {
-                double r;
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(f + ks * 2048u));
-                dmma_acc_v(h1a, h1b, x1[ks], r);
-                dmma_acc_v(h2a, h2b, x2[ks], r);
-            }
+        auto store = [&](uint32_t nt, double h1a, double h1b, double h2a, double h2b) {
             const uint32_t e0 = hout[2 * (4 * nt + cq)], e1 = hout[2 * (4 * nt + cq) + 1];
             double2 w0, w1;
             if (nt < 7) {
@@ -440,8 +444,29 @@ __device__ __forceinline__ void hform3(const Geo& G, const Tabs& T, const uint8_
                 w1 = make_double2(h1b, h2b);
             }
             const uint32_t a0 = (uint32_t)(am >> T.ttr[e0]) & 1u, a1 = (uint32_t)(am >> T.ttr[e1]) & 1u;
-            sb[a0 ? baseA + T.cadj[e0] : base + T.cdir[e0]] = make_double2(w0.x, flip_sign(w0.y, a0 << 31));
-            sb[a1 ? baseA + T.cadj[e1] : base + T.cdir[e1]] = make_double2(w1.x, flip_sign(w1.y, a1 << 31));
+            sb[addr(e0, a0, base, baseA, xbv, ybv)] = make_double2(w0.x, flip_sign(w0.y, a0 << 31));
+            sb[addr(e1, a1, base, baseA, xbv, ybv)] = make_double2(w1.x, flip_sign(w1.y, a1 << 31));
+        };
+        // two n-tiles at a time: four independent accumulator chains per warp keep the FP64 tensor
+        // pipe fed (two chains left it waiting on the DMMA latency); R's fragments come from shared
+        // memory (ks stride 256 doubles)
+#pragma unroll 1
+        for (uint32_t nt = 0; nt < 8; nt += 2) {
+            double h1a = 0.0, h1b = 0.0, h2a = 0.0, h2b = 0.0, g1a = 0.0, g1b = 0.0, g2a = 0.0, g2b = 0.0;
+            const uint32_t f = smem_u32(rfr + nt * 32 + lane);
+            // (volatile: program order bounds the live fragment registers to two)
+#pragma unroll
+            for (uint32_t ks = 0; ks < 16; ++ks) {
+                double r0, r1;
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r0) : "r"(f + ks * 2048u));
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r1) : "r"(f + ks * 2048u + 256u));
+                dmma_acc_v(h1a, h1b, x1[ks], r0);
+                dmma_acc_v(h2a, h2b, x2[ks], r0);
+                dmma_acc_v(g1a, g1b, x1[ks], r1);
+                dmma_acc_v(g2a, g2b, x2[ks], r1);
+            }
+            store(nt, h1a, h1b, h2a, h2b);
+            store(nt + 1, g1a, g1b, g2a, g2b);
         }
     }
 }
@@ -580,6 +605,10 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
         }
         gbar();
         long long t3 = prof ? clock64() : 0;
+        if (i + S < nlocal && (G.dbg & DBG_POISON)) {  // diagnostics: NaN until the copies of item i + S land
+            poison_stage(sb, G.stage_elems, gtid, NH);
+            gbar();
+        }
         if (i + S < nlocal)
             load(i + S);
         if (prof) {
@@ -714,6 +743,10 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
         T.cadj[tid] = G.cadj[tid];
         T.ttr[tid] = G.ttr[tid];
         T.tsk[tid] = G.tsk[tid];
+        if constexpr (MODE == M_SF3 && TMAB) {
+            T.hsd[tid] = G.hsd[tid];
+            T.hsa[tid] = G.hsa[tid];
+        }
     }
     if (tid == 0)
         for (uint32_t q = 0; q < S; ++q) {
@@ -776,7 +809,7 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                     sform2<NCW>(G, T, sf, am[i % TSL][0], sb, tid >> 5);
             } else if constexpr (SF3) {
                 if (!(G.dbg & 1u))
-                    hform3<NCW>(G, T, hin, hout, sfr, am[i % TSL][0], sb, tid >> 5);
+                    hform3<NCW, TMAB>(G, T, hin, hout, sfr, am[i % TSL][0], sb, tid >> 5);
             } else if constexpr (MODE == M_DIRECT) {
                 if constexpr (KSUM) {
                     if (!(G.dbg & 1u))
@@ -1021,6 +1054,10 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                 bulk_wait_read0();  // this thread's rows have left shared memory
             }
             gsync();  // the group's stores have read stage s; the table of item i + S is visible
+            if (more && (G.dbg & DBG_POISON)) {  // diagnostics: NaN until the loads of item i + S land
+                poison_stage(ring + (size_t)s * G.stage_elems, G.stage_elems, gtid, NGT);
+                gsync();
+            }
             if (more)
                 bissue(i + S);
         }
@@ -1081,6 +1118,10 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
         }
         mbar_sync();  // every write-back read of stage s is done; the next table is visible
         const long long t2 = prof ? clock64() : 0;
+        if (more && (G.dbg & DBG_POISON)) {  // diagnostics: NaN until the copies of item i + S land
+            poison_stage(ring + (size_t)s * G.stage_elems, G.stage_elems, mtid, NMW);
+            mbar_sync();
+        }
         if (more)
             issue(i + S);
         if (prof) {

@@ -10,6 +10,15 @@ constexpr uint32_t CAP = 2048;     // target complex elements staged per CTA ite
 constexpr uint32_t CAPD = 2048;    // same for diagonal-unit items
 constexpr uint32_t CAP_WHOLE = 4096;  // units up to 64 KiB are staged as whole stored tiles
 constexpr uint32_t MAX_TT = 256;   // max logical tiles per item (tile table in smem)
+constexpr uint32_t DBG_POISON = 1024u;  // HS_DEBUG_FLAGS bit: NaN-fill ring stages between uses
+// NaN-fill n elements of a ring stage (threads t of nt), then order those generic-proxy writes before
+// the async-proxy (TMA / bulk) loads the caller issues next
+__device__ __forceinline__ void poison_stage(double2* sb, uint32_t n, uint32_t t, uint32_t nt) {
+    const double nan = __longlong_as_double(0x7ff8dead0000beefll);
+    for (uint32_t e = t; e < n; e += nt)
+        sb[e] = make_double2(nan, nan);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 constexpr uint64_t F_ADJ = 1ull << 63, F_SKIP = 1ull << 62, F_BAD = 1ull << 61, F_NOSTORE = 1ull << 60,
                    F_REMOTE = 1ull << 59, F_MIRROR = 1ull << 55, F_MASK = (1ull << 55) - 1;
 
@@ -119,6 +128,8 @@ struct Geo {
     // the two block elements lane c writes for n-tile nt
     const double* sf3;
     uint8_t hf_in[64], hf_out[64];
+    // hform3 on TMA boxes: staging slot (tile, box) of each block component, direct / adjoint tile
+    uint8_t hsd[64], hsa[64];
 };
 
 // Per-CTA copies of the small index tables of Geo (shared memory).
@@ -128,6 +139,7 @@ struct Tabs {
     uint8_t ttr[64];
     uint8_t tsk[64];
     uint8_t slt[64];  // pipe kernel, monomials: staging slot -> logical tile (compacted active tiles)
+    uint8_t hsd[64], hsa[64];  // hform3 on TMA boxes: slot of each component (direct / adjoint tile)
 };
 
 template <int NS>

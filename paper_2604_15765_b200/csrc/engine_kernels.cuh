@@ -1045,6 +1045,10 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
                 if (j >= S)
                     bulk_wait_read0();  // the store of item j - S has left the stage
                 __syncwarp();
+                if (G.dbg & DBG_POISON) {  // diagnostics: the stage holds NaN until the loads land
+                    poison_stage(sb, G.stage_elems, lane, 32);
+                    __syncwarp();
+                }
                 if (lane == 0)
                     mbar_arrive_expect(&full[p], bytes);
                 __syncwarp();

@@ -1,5 +1,14 @@
-"""Every kernel instantiation of the engine at small n, for compute-sanitizer (racecheck, synccheck,
-memcheck, initcheck).  Run on a GPU box, e.g.
+"""Every kernel instantiation of the engine at small n: the race / synchronisation stress driver.
+
+compute-sanitizer is closed on this GPU pool ("runs under it have left GPUs needing a reset"), so
+races and barrier bugs are hunted by perturbation instead (tests/test_gpu_races.py runs this script
+under each setting and requires the same SHA-256 digest of every result, plus oracle parity):
+  HS_DEBUG_FLAGS=1024   every ring stage is NaN-filled between its write-back and its next load, so
+                        a transform that reads before the copies landed, or a write-back that reads
+                        after the refill started, leaves NaN in the result;
+  HS_DEBUG_GRID=g       g persistent CTAs instead of one per SM: items move between CTAs and the
+                        per-CTA item order changes.
+Where compute-sanitizer is available the same script is its workload:
 
   compute-sanitizer --tool racecheck --racecheck-report hazard python tools/sanitize_cases.py
 
@@ -12,6 +21,7 @@ mixed and cross units; k = 3 Kraus sums of rank 2..4; grid programs), gather_ker
 reductions, device generators, format conversions, and peer-mode sharded ops (ShardGroup, one process).
 Each case also checks its result against the CPU oracle, so a sanitizer run doubles as a parity run.
 """
+import hashlib
 import itertools
 import os
 import sys
@@ -30,6 +40,11 @@ from paper_2604_15765_b200.multigpu import ShardGroup  # noqa: E402
 orc = O.Oracle()
 worst = 0.0
 count = 0
+DIGEST = hashlib.sha256()
+
+
+def digest(arr):
+    DIGEST.update(np.ascontiguousarray(arr).view(np.uint8).tobytes())
 
 
 def kraus(k, r, seed):
@@ -46,7 +61,9 @@ def check(st, spec, och, n, m, tg, base):
     orc.apply(want, n, m, och, list(tg))
     st.upload(base)
     H.apply(st, spec, list(tg))
-    err = O.rel_max_err(st.download(), want, orc.frobenius(base, n, m))
+    got = st.download()
+    digest(got)
+    err = O.rel_max_err(got, want, orc.frobenius(base, n, m))
     worst = max(worst, err)
     count += 1
     if err > 1e-12:
@@ -89,20 +106,22 @@ def main():
         st.upload(base)
         fusion.execute(st, plan)
         H.apply_cx_layer(st, [(0, n - 1), (2, 3), (n - 2, 1)])
+        digest(st.download())
         # reductions and generators
         st.fill_mixture(psi)
         obs = H.TiledHermitian(n, m)
         obs.fill_pauli_sum(*HS.pauli_strings(n, 16, 3))
-        H.expectation(st, obs)
-        H.trace(st)
-        H.frobenius(st)
+        digest(np.array([H.expectation(st, obs), H.trace(st), H.frobenius(st)]))
         obs.fill_random_hermitian(7)
         obs.fill_basis_projector(3)
         # format conversions (to_dense / convert, storage.cpp:241-292)
         dense = obs.to_dense()
         obs.from_dense(dense)
         obs.from_packed(obs.to_packed())
-        H.convert(obs, "tiled", max(0, m - 2)).free()
+        rt = H.convert(obs, "tiled", max(0, m - 2))
+        digest(dense)
+        digest(rt.download())
+        rt.free()
         obs.free()
         st.free()
     # sharded, peer mode and exchange mode (one process, one GPU)
@@ -115,8 +134,11 @@ def main():
                          (H.depolarising(0.1), [8])):
             grp.apply(spec, tg)
         grp.synchronize()
+        for sh in grp.shards:
+            digest(sh.download())
         grp.free()
     print(f"sanitize_cases: {count} checked cases, worst rel err {worst:.3e}")
+    print(f"DIGEST {DIGEST.hexdigest()}")
 
 
 if __name__ == "__main__":
