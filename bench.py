@@ -47,6 +47,27 @@ METRIC = "gate conjugations/sec and achieved HBM GB/s (fraction of roofline), n=
 UNIT = "gate conjugations/s"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 NVLINK_GBS = 770.0  # B200_PROFILING.md: measured peer copy, per direction per GPU (900 nominal)
+# FP64 tensor (DMMA) peak: measured on B200 by tools/fp64_probe.cu (profiles/r01_fp64_probe.txt:
+# m8n8k4, 8-32 warps/SM, 37.0-37.1 TFLOP/s; DFMA shares the pipe at 36.8)
+FP64_TFLOPS = 37.1
+
+
+def fp64_fma_per_element(op) -> int:
+    """Algorithmic FP64 FMAs per stored element of one op's transform (DESIGN.md 4.2 / 4.5): the
+    k = 3 direct form L B L^dagger in 3M form 48; a k = 2 unitary through I2 (x) L on the k = 3
+    path 48; the k = 2 Kraus S form (16 x 16, 3M) 48; a k = 3 Kraus sum of rank 2 as two direct
+    conjugations 96; rank >= 3 in the hermitian basis (two real 64 x 64 products per block) 128;
+    single-qubit ops and permutations are HBM streams (<= 16, counted 0)."""
+    k = len(op.targets)
+    if op.kind in ("unitary", "unitary_dual"):
+        return 48 if k >= 2 else 0
+    if op.kind == "kraus":
+        r = op.matrix.shape[0]
+        if k == 3:
+            return 48 if r == 1 else 96 if r == 2 else 128
+        if k == 2:
+            return 48
+    return 0
 
 WORKLOADS = {
     "c0": "C0: Hadamard at qubits 0..11 (12 ops) on an n=12 rank-4 rho, m=5",
@@ -570,6 +591,24 @@ def ours_arm(args, cfg, n, m, world, rank, local):
             roof_nv = {"bound": "nvlink", "achieved": None, "frac": None, "cross_shard_launches_per_step": 0,
                        "note": "no operation of this config reads another shard's tiles (single-qubit channels "
                                "that keep the (00,11)/(01,10) shard classes apart run shard-local)"}
+    # min(HBM, FP64) roofline for configs with FP64-heavy transforms (k = 3 Kraus sums): each launch
+    # is bound by max(bytes / HBM peak, flops / DMMA peak); frac = sum of bounds / sum of launch times
+    roof_mixed = None
+    seq = HS.config_ops(cfg, n)
+    if fplan is None and not args.remap and len(seq) == len(launch_ms):
+        elems = S / 16.0
+        fl = [2.0 * fp64_fma_per_element(op) * elems for op in seq]
+        if any(fl):
+            bounds = [max(tb / (peak * 1e9), f / (FP64_TFLOPS * 1e12)) for tb, f in zip(touched, fl)]
+            nfp = sum(1 for tb, f in zip(touched, fl) if f / (FP64_TFLOPS * 1e12) > tb / (peak * 1e9))
+            fp_t = sum(t for t, tb, f in zip(launch_ms, touched, fl) if f / (FP64_TFLOPS * 1e12) > tb / (peak * 1e9))
+            fp_f = sum(f for tb, f in zip(touched, fl) if f / (FP64_TFLOPS * 1e12) > tb / (peak * 1e9))
+            roof_mixed = {"bound": "max(hbm, fp64) per launch", "frac": sum(bounds) / (sum(launch_ms) / 1e3),
+                          "hbm_peak_gbs": peak, "fp64_peak_tflops": FP64_TFLOPS,
+                          "fp64_bound_launches_per_step": nfp,
+                          "fp64_achieved_tflops": (fp_f / (fp_t / 1e3) / 1e12) if fp_t else None,
+                          "fp64_peak_source": "tools/fp64_probe.cu on B200 (profiles/r01_fp64_probe.txt), DMMA m8n8k4",
+                          "flops_model": "bench.fp64_fma_per_element x 2 x stored elements"}
     result = {}
     if cfg == "c3":
         result["tr_rho_O"] = drho.reduce(dshard, 0) if sharded else H.expectation(rho, st)
@@ -655,6 +694,7 @@ def ours_arm(args, cfg, n, m, world, rank, local):
                      "peak_source": peak_src, "traffic_source": traffic_src,
                      "scope": "rank 0's launches" if sharded else "all launches of one step"},
         "roofline_nvlink": roof_nv,
+        "roofline_hbm_fp64": roof_mixed,
         "per_launch_ms": [round(x, 4) for x in launch_ms],
         "gpu_launches": launches,
         "host_wall_s": t_host,
