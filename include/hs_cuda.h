@@ -93,8 +93,11 @@ int hs_device_count(int* out);
 
 /* ---- state (TiledHermitian) ------------------------------------------------------------ */
 /* Allocates the tiled payload in HBM (zero-filled, like AlignedArray, types.hpp:37-42).
- * Limits as the reference: 1 <= n <= 30, 0 <= m <= n + 2 (storage.cpp:12-20); this build
- * additionally requires m <= 5 (tiles of at most 32 x 32). */
+ * Limits as the reference: 1 <= n <= 30, 0 <= m <= n + 2 (storage.cpp:12-20).  For m > 5 the
+ * operator is held in HBM in the m = 5 layout (every kernel unchanged) and every payload-facing call
+ * (info, upload / download and their ranges, save / load) speaks the m layout, converted on the fly
+ * on the device; hs_state_device_ptr then exposes the internal m = 5 layout, and sharding needs
+ * m <= 5. */
 int hs_state_create(int n, int m, int device, hs_state** out);
 int hs_state_free(hs_state* h);
 int hs_state_info(const hs_state* h, int* n, int* m, uint64_t* count, uint64_t* grid);

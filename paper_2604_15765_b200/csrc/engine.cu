@@ -91,6 +91,11 @@ struct hs_state {
     uint32_t flip = 0;
     const double2* peer_buf[64][2] = {};       // peers' buffers, valid on this device
     std::vector<HCacheEntry> hcache;           // device fragments of the k = 3 Kraus sets seen (hform3)
+    // tile exponents m > 5: the operator lives in HBM in the m = 5 layout (every kernel unchanged);
+    // the user-facing payload (info, upload / download, save / load) is the mu layout, converted on
+    // the fly by the retile kernel.  mu == m and ucount == count otherwise.
+    int mu = 0;
+    uint64_t ucount = 0, uG = 0;
 };
 
 namespace {
@@ -1585,6 +1590,7 @@ void count_subcases(const hs_state* h, const Geo& G, uint64_t* sub) {
     sub[1] = b;
 }
 
+void user_plan(const hs_state* h, hs_plan* plan);
 int finish_plan(hs_state* h, const Geo& G, int k, const uint32_t* t, int path, hs_plan* plan, uint64_t touched) {
     if (!plan)
         return HS_OK;
@@ -1599,10 +1605,61 @@ int finish_plan(hs_state* h, const Geo& G, int k, const uint32_t* t, int path, h
     plan->touched_bytes = G.cmask ? touched / 2 * ((1ull << __builtin_popcount(G.cmask)) + 1) : touched;
     if (g_plan_subcases)
         count_subcases(h, G, plan->subcases);
+    user_plan(h, plan);
     return HS_OK;
 }
 
 uint64_t state_bytes(const hs_state* h) { return h->count * sizeof(double2); }
+
+// m > 5: the user-layout payload (mu) in a stream-ordered temporary, from / into the internal m = 5
+// layout (retile_kernel, engine_convert.cuh).  The temporary is freed stream-ordered as well.
+bool big_tiles(const hs_state* h) { return h->mu > h->m; }
+struct UserTemp {
+    double2* p = nullptr;
+    cudaStream_t s = nullptr;
+    void release() {
+        if (p)
+            cudaFreeAsync(p, s);
+        p = nullptr;
+    }
+    ~UserTemp() { release(); }
+};
+int user_alloc(const hs_state* h, UserTemp& t) {
+    t.s = h->stream;
+    if (cudaMallocAsync(&t.p, h->ucount * sizeof(double2), h->stream) != cudaSuccess) {
+        cudaGetLastError();
+        t.p = nullptr;
+        return set_err(HS_ERR_NOMEM, "user-layout staging buffer (tile exponent > 5)");
+    }
+    return HS_OK;
+}
+int retile_launch(double2* dst, uint32_t m2, uint64_t cnt2, uint64_t N, const double2* src, uint32_t m1,
+                  cudaStream_t s);
+int to_user(const hs_state* h, UserTemp& t) {  // t.p <- the operator in the mu layout
+    int rc = user_alloc(h, t);
+    return rc ? rc : retile_launch(t.p, (uint32_t)h->mu, h->ucount, h->N, h->d, (uint32_t)h->m, h->stream);
+}
+int from_user(hs_state* h, const double2* u) {  // the operator <- u in the mu layout
+    return retile_launch(h->d, (uint32_t)h->m, h->count, h->N, u, (uint32_t)h->mu, h->stream);
+}
+// the path tag, grid-target count and subcase counters as the reference reports them for the
+// user's tile exponent (kernels.cpp:448-549 classify by a < m)
+void user_plan(const hs_state* h, hs_plan* plan) {
+    if (!plan || !big_tiles(h))
+        return;
+    Geo U{};
+    U.k = (uint32_t)plan->k;
+    U.g = 0;
+    for (int i = 0; i < plan->k; ++i)
+        if (plan->targets[i] >= (uint32_t)h->mu)
+            U.gr_pos[U.g++] = plan->targets[i] - (uint32_t)h->mu;
+    U.nb = h->uG >> U.g;
+    plan->grid_bits = (int)U.g;
+    if (plan->path == HS_PATH_TILED_INTRA || plan->path == HS_PATH_TILED_CROSS || plan->path == HS_PATH_TILED_MIXED)
+        plan->path = U.g == 0 ? HS_PATH_TILED_INTRA : U.g == U.k ? HS_PATH_TILED_CROSS : HS_PATH_TILED_MIXED;
+    if (g_plan_subcases)
+        count_subcases(h, U, plan->subcases);
+}
 
 int generic_path(const Geo& G) {
     if (G.g == 0)
@@ -1640,8 +1697,11 @@ int hs_state_create_sharded(int n, int m, int device, int nshards, int shard, hs
         return set_err(HS_ERR_INVALID, "qubit count must be in [1, 30]");
     if (m < 0 || m > n + 2)
         return set_err(HS_ERR_INVALID, "tile exponent must be in [0, n + 2]");
+    if (m > 5 && nshards != 1)
+        return set_err(HS_ERR_UNSUPPORTED, "tile exponents m > 5 are supported for unsharded operators");
+    const int mu = m;
     if (m > 5)
-        return set_err(HS_ERR_UNSUPPORTED, "this build supports tile exponents m <= 5");
+        m = 5;  // internal layout (see hs_state::mu)
     const uint64_t Gt = (1ull << n) >= (1ull << m) ? (1ull << n) >> m : 1;
     if (nshards < 1 || (nshards & (nshards - 1)) || (uint64_t)nshards > Gt)
         return set_err(HS_ERR_INVALID, "shard count must be a power of two <= tiles per grid row");
@@ -1666,6 +1726,14 @@ int hs_state_create_sharded(int n, int m, int device, int nshards, int shard, hs
         const uint64_t B = 1ull << h->logB, P = (uint64_t)nshards;
         const uint64_t tiles = shard == 0 ? P * (B * (B + 1) / 2) : (P / 2) * B * B;
         h->count = tiles * h->M * h->M;
+    }
+    h->mu = mu;
+    h->ucount = h->count;
+    h->uG = h->G;
+    if (mu > m) {
+        const uint64_t Mu = 1ull << mu;
+        h->uG = h->N >= Mu ? h->N / Mu : 1;
+        h->ucount = h->uG * (h->uG + 1) / 2 * Mu * Mu;
     }
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -1730,11 +1798,11 @@ int hs_state_info(const hs_state* h, int* n, int* m, uint64_t* count, uint64_t* 
     if (n)
         *n = h->n;
     if (m)
-        *m = h->m;
+        *m = h->mu;
     if (count)
-        *count = h->count;
+        *count = h->ucount;
     if (grid)
-        *grid = h->G;
+        *grid = h->uG;
     return HS_OK;
 }
 
@@ -1933,10 +2001,21 @@ int hs_state_exchange(hs_state* h, int partner) {
 int hs_state_upload_range(hs_state* h, const double* host, uint64_t offset, uint64_t count) {
     if (!h || (!host && count))
         return set_err(HS_ERR_INVALID, "null argument");
-    if (offset > h->count || count > h->count - offset)
+    if (offset > h->ucount || count > h->ucount - offset)
         return set_err(HS_ERR_RANGE, "upload range exceeds the payload");
     DeviceGuard dg(h->device);
-    CUDA_TRY(cudaMemcpyAsync(h->d + offset, host, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+    if (big_tiles(h)) {  // into the user-layout image of the operator, then back to the m = 5 layout
+        UserTemp t;
+        int rc = count == h->ucount ? user_alloc(h, t) : to_user(h, t);
+        if (rc)
+            return rc;
+        CUDA_TRY(cudaMemcpyAsync(t.p + offset, host, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+        rc = from_user(h, t.p);
+        if (rc)
+            return rc;
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(h->d + offset, host, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+    }
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     return HS_OK;
 }
@@ -1944,38 +2023,62 @@ int hs_state_upload_range(hs_state* h, const double* host, uint64_t offset, uint
 int hs_state_download_range(const hs_state* h, double* host, uint64_t offset, uint64_t count) {
     if (!h || (!host && count))
         return set_err(HS_ERR_INVALID, "null argument");
-    if (offset > h->count || count > h->count - offset)
+    if (offset > h->ucount || count > h->ucount - offset)
         return set_err(HS_ERR_RANGE, "download range exceeds the payload");
     DeviceGuard dg(h->device);
-    CUDA_TRY(cudaMemcpyAsync(host, h->d + offset, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    if (big_tiles(h)) {
+        UserTemp t;
+        const int rc = to_user(h, t);
+        if (rc)
+            return rc;
+        CUDA_TRY(cudaMemcpyAsync(host, t.p + offset, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(host, h->d + offset, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    }
     CUDA_TRY(cudaStreamSynchronize(h->stream));
     return HS_OK;
 }
 
 int hs_state_upload(hs_state* h, const double* host, uint64_t count) {
-    if (h && count != h->count)
+    if (h && count != h->ucount)
         return set_err(HS_ERR_INVALID, "payload length mismatch");
     return hs_state_upload_range(h, host, 0, count);
 }
 
 int hs_state_download(const hs_state* h, double* host, uint64_t count) {
-    if (h && count != h->count)
+    if (h && count != h->ucount)
         return set_err(HS_ERR_INVALID, "payload length mismatch");
     return hs_state_download_range(h, host, 0, count);
 }
 
 int hs_state_upload_async(hs_state* h, const double* host, uint64_t count) {
-    if (!h || !host || count != h->count)
+    if (!h || !host || count != h->ucount)
         return set_err(HS_ERR_INVALID, "bad upload arguments");
     DeviceGuard dg(h->device);
+    if (big_tiles(h)) {
+        UserTemp t;
+        const int rc = user_alloc(h, t);
+        if (rc)
+            return rc;
+        CUDA_TRY(cudaMemcpyAsync(t.p, host, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+        return from_user(h, t.p);
+    }
     CUDA_TRY(cudaMemcpyAsync(h->d, host, count * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
     return HS_OK;
 }
 
 int hs_state_download_async(const hs_state* h, double* host, uint64_t count) {
-    if (!h || !host || count != h->count)
+    if (!h || !host || count != h->ucount)
         return set_err(HS_ERR_INVALID, "bad download arguments");
     DeviceGuard dg(h->device);
+    if (big_tiles(h)) {
+        UserTemp t;
+        const int rc = to_user(h, t);
+        if (rc)
+            return rc;
+        CUDA_TRY(cudaMemcpyAsync(host, t.p, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+        return HS_OK;
+    }
     CUDA_TRY(cudaMemcpyAsync(host, h->d, count * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
     return HS_OK;
 }
@@ -1983,7 +2086,7 @@ int hs_state_download_async(const hs_state* h, double* host, uint64_t count) {
 int hs_state_copy(hs_state* dst, const hs_state* src) {
     if (!dst || !src)
         return set_err(HS_ERR_INVALID, "null state");
-    if (dst->count != src->count || dst->m != src->m || dst->n != src->n)
+    if (dst->count != src->count || dst->m != src->m || dst->n != src->n || dst->mu != src->mu)
         return set_err(HS_ERR_INVALID, "state shapes differ");
     DeviceGuard dg(dst->device);
     CUDA_TRY(cudaStreamSynchronize(src->stream));
@@ -2897,6 +3000,16 @@ int convert_linear(hs_state* h, double2* buf, bool packed, bool from, bool on_de
 }
 }  // namespace
 
+namespace {
+int retile_launch(double2* dst, uint32_t m2, uint64_t cnt2, uint64_t N, const double2* src, uint32_t m1,
+                  cudaStream_t s) {
+    retile_kernel<<<conv_grid((cnt2 + CV_T - 1) / CV_T), CV_T, 0, s>>>(dst, m2, cnt2, N, src, m1);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    CUDA_TRY(cudaGetLastError());
+    return HS_OK;
+}
+}  // namespace
+
 extern "C" {
 int hs_state_to_dense(const hs_state* h, double* out, int on_device) {
     int rc = conv_check(h, out);
@@ -2933,11 +3046,7 @@ int hs_state_convert(const hs_state* src, hs_state* dst) {
     CUDA_TRY(cudaEventRecord(ev, src->stream));
     CUDA_TRY(cudaStreamWaitEvent(dst->stream, ev, 0));
     CUDA_TRY(cudaEventDestroy(ev));
-    retile_kernel<<<conv_grid((dst->count + CV_T - 1) / CV_T), CV_T, 0, dst->stream>>>(dst->d, (uint32_t)dst->m, dst->count,
-                                                                                      dst->N, src->d, (uint32_t)src->m);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    CUDA_TRY(cudaGetLastError());
-    return HS_OK;
+    return retile_launch(dst->d, (uint32_t)dst->m, dst->count, dst->N, src->d, (uint32_t)src->m, dst->stream);
 }
 int hs_device_alloc(int device, uint64_t bytes, void** out) {
     if (!out)
@@ -2989,11 +3098,16 @@ int hs_state_save(const hs_state* h, const char* path) {
     FILE* f = std::fopen(path, "wb");
     if (!f)
         return set_err(HS_ERR_IO, std::string("io_failure: save: cannot open ") + path);
-    unsigned char hdr[16] = {'O', 'H', 'R', 'M', 1, 0, 0, 0, 2, (unsigned char)h->n, (unsigned char)h->m, 0, 0, 0, 0, 0};
+    unsigned char hdr[16] = {'O', 'H', 'R', 'M', 1, 0, 0, 0, 2, (unsigned char)h->n, (unsigned char)h->mu, 0, 0, 0, 0, 0};
     bool ok = std::fwrite(hdr, 1, 16, f) == 16;
     DeviceGuard dg(h->device);
+    UserTemp ut;  // m > 5: stream the user-layout image
+    if (big_tiles(h) && to_user(h, ut)) {
+        std::fclose(f);
+        return HS_ERR_NOMEM;
+    }
     PinnedPair pp;
-    const uint64_t total = h->count * sizeof(double2);
+    const uint64_t total = h->ucount * sizeof(double2);
     for (int i = 0; i < 2 && ok; ++i)
         if (cudaHostAlloc(&pp.b[i], IO_CHUNK, cudaHostAllocDefault) != cudaSuccess) {
             cudaGetLastError();
@@ -3003,7 +3117,7 @@ int hs_state_save(const hs_state* h, const char* path) {
     cudaEvent_t ev[2];
     cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
-    const char* src = reinterpret_cast<const char*>(h->d);
+    const char* src = reinterpret_cast<const char*>(ut.p ? ut.p : h->d);
     uint64_t off = 0;
     int cur = 0;
     bool pending = false;
@@ -3080,8 +3194,14 @@ int hs_state_load(const char* path, int device, hs_state** out) {
             hs_state_free(h);
             return fail(HS_ERR_NOMEM, "load: pinned staging buffer");
         }
-    const uint64_t total = h->count * sizeof(double2);
-    char* dst = reinterpret_cast<char*>(h->d);
+    UserTemp ut;  // m > 5: read the user-layout image, then convert
+    if (big_tiles(h) && user_alloc(h, ut)) {
+        hs_state_free(h);
+        std::fclose(f);
+        return HS_ERR_NOMEM;
+    }
+    const uint64_t total = h->ucount * sizeof(double2);
+    char* dst = reinterpret_cast<char*>(ut.p ? ut.p : h->d);
     uint64_t off = 0;
     int cur = 0;
     cudaEvent_t ev[2];
@@ -3103,6 +3223,9 @@ int hs_state_load(const char* path, int device, hs_state** out) {
         off += len;
         cur ^= 1;
     }
+    if (ok && ut.p)
+        ok = from_user(h, ut.p) == HS_OK;
+    ut.release();
     cudaStreamSynchronize(h->stream);
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
