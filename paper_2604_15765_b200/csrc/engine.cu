@@ -61,6 +61,7 @@
 
 
 // =============================================================================== host side
+constexpr size_t HCACHE_MAX = 1024;  // cached k = 3 Kraus sets per state (32 KiB of fragments each)
 struct HCacheEntry {
     uint64_t key = 0;
     int nops = 0;
@@ -91,6 +92,7 @@ struct hs_state {
     uint32_t flip = 0;
     const double2* peer_buf[64][2] = {};       // peers' buffers, valid on this device
     std::vector<HCacheEntry> hcache;           // device fragments of the k = 3 Kraus sets seen (hform3)
+    double* hscratch = nullptr;                // fragments of an uncached set once the cache is full
     // tile exponents m > 5: the operator lives in HBM in the m = 5 layout (every kernel unchanged);
     // the user-facing payload (info, upload / download, save / load) is the mu layout, converted on
     // the fly by the retile kernel.  mu == m and ucount == count otherwise.
@@ -1504,6 +1506,17 @@ int hform_fragments(hs_state* h, int nops, const double2* L, const double** out)
                     frag[(ks * 8 + nt) * 32 + g * 4 + c] = v;
                 }
         }
+    if (h->hcache.size() >= HCACHE_MAX) {
+        // cache full (32 MiB of fragments): a scratch buffer, uploaded in stream order and not cached
+        // (cached entries are never freed before the state, so captured graphs stay valid)
+        if (!h->hscratch)
+            CUDA_TRY(cudaMalloc(&h->hscratch, frag.size() * sizeof(double)));
+        CUDA_TRY(cudaMemcpyAsync(h->hscratch, frag.data(), frag.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                 h->stream));
+        CUDA_TRY(cudaStreamSynchronize(h->stream));  // `frag` is freed on return
+        *out = h->hscratch;
+        return HS_OK;
+    }
     HCacheEntry e;
     e.key = key;
     e.nops = nops;
@@ -1783,6 +1796,7 @@ int hs_state_free(hs_state* h) {
     cudaFree(h->kraus);
     for (auto& e : h->hcache)
         cudaFree(e.dev);
+    cudaFree(h->hscratch);
     cudaFree(h->recv);
     if (h->comm && nccl().CommDestroy)
         nccl().CommDestroy((ncclComm_t)h->comm);

@@ -460,6 +460,8 @@ __device__ __forceinline__ void hform3(const Geo& G, const Tabs& T, const uint8_
                 double r0, r1;
                 asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r0) : "r"(f + ks * 2048u));
                 asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r1) : "r"(f + ks * 2048u + 256u));
+                // (m16n8k4 with x1 / x2 as rows g / g + 8 against the shared fragment is the same
+                // math in half the instructions, and measured 4-5% slower: profiles/r02/k3_m16n8k4_ab.txt)
                 dmma_acc_v(h1a, h1b, x1[ks], r0);
                 dmma_acc_v(h2a, h2b, x2[ks], r0);
                 dmma_acc_v(g1a, g1b, x1[ks], r1);
