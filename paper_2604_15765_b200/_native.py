@@ -15,7 +15,8 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "lib")
-ENGINE_PATH = os.path.join(LIB_DIR, "libhermsim_b200.so")
+# HS_ENGINE_LIB: another build of the engine (diagnostics: A/B of kernel variants on one box)
+ENGINE_PATH = os.environ.get("HS_ENGINE_LIB") or os.path.join(LIB_DIR, "libhermsim_b200.so")
 HARNESS_PATH = os.path.join(LIB_DIR, "libhs_harness.so")
 
 c_double_p = ctypes.POINTER(ctypes.c_double)

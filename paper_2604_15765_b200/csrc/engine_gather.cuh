@@ -450,25 +450,35 @@ __device__ __forceinline__ void hform3(const Geo& G, const Tabs& T, const uint8_
         // two n-tiles at a time: four independent accumulator chains per warp keep the FP64 tensor
         // pipe fed (two chains left it waiting on the DMMA latency); R's fragments come from shared
         // memory (ks stride 256 doubles)
+#ifndef HFORM_NTB
+#define HFORM_NTB 2  // 4 (eight chains) measured 5-9% slower: profiles/r02/k3_ntb_ab.txt
+#endif
+        constexpr uint32_t NTB = HFORM_NTB;  // n-tiles per batch: 2 x NTB accumulator chains per warp
 #pragma unroll 1
-        for (uint32_t nt = 0; nt < 8; nt += 2) {
-            double h1a = 0.0, h1b = 0.0, h2a = 0.0, h2b = 0.0, g1a = 0.0, g1b = 0.0, g2a = 0.0, g2b = 0.0;
+        for (uint32_t nt = 0; nt < 8; nt += NTB) {
+            double acc[NTB][4];
+#pragma unroll
+            for (uint32_t u = 0; u < NTB; ++u)
+                acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
             const uint32_t f = smem_u32(rfr + nt * 32 + lane);
-            // (volatile: program order bounds the live fragment registers to two)
+            // (volatile: program order bounds the live fragment registers to NTB)
 #pragma unroll
             for (uint32_t ks = 0; ks < 16; ++ks) {
-                double r0, r1;
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r0) : "r"(f + ks * 2048u));
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r1) : "r"(f + ks * 2048u + 256u));
+                double r[NTB];
+#pragma unroll
+                for (uint32_t u = 0; u < NTB; ++u)
+                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r[u]) : "r"(f + ks * 2048u + u * 256u));
                 // (m16n8k4 with x1 / x2 as rows g / g + 8 against the shared fragment is the same
                 // math in half the instructions, and measured 4-5% slower: profiles/r02/k3_m16n8k4_ab.txt)
-                dmma_acc_v(h1a, h1b, x1[ks], r0);
-                dmma_acc_v(h2a, h2b, x2[ks], r0);
-                dmma_acc_v(g1a, g1b, x1[ks], r1);
-                dmma_acc_v(g2a, g2b, x2[ks], r1);
+#pragma unroll
+                for (uint32_t u = 0; u < NTB; ++u) {
+                    dmma_acc_v(acc[u][0], acc[u][1], x1[ks], r[u]);
+                    dmma_acc_v(acc[u][2], acc[u][3], x2[ks], r[u]);
+                }
             }
-            store(nt, h1a, h1b, h2a, h2b);
-            store(nt + 1, g1a, g1b, g2a, g2b);
+#pragma unroll
+            for (uint32_t u = 0; u < NTB; ++u)
+                store(nt + u, acc[u][0], acc[u][1], acc[u][2], acc[u][3]);
         }
     }
 }
