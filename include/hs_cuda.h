@@ -152,9 +152,11 @@ int hs_apply_transfer(hs_state* h, int k, const double* s_rowstacked, const uint
  * applying them in order.  kinds[p]: 0 = row-stacked 4x4 transfer matrix s[16p..16p+15]
  * (interleaved complex), 1 = Hadamard (s ignored), 2 = diagonal transfer (diagonal of s used). */
 int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s, hs_plan* plan);
-/* Fused grid program: one step on each of 2 or 3 distinct grid qubits (>= m) in ONE pass over the
- * triangle (the units of those grid bits are gathered and the steps applied one after another).
- * Single-GPU states, m = 5. */
+/* Fused grid program: 2 .. 16 steps on 2 or 3 distinct grid qubits (>= m), each qubit's steps
+ * consecutive, in ONE pass over the triangle (the units of those grid bits are gathered; each qubit's
+ * chain of steps runs on every quad in registers, one shared-memory round trip per qubit).
+ * Single-GPU states, m = 5.  (hs_apply_program likewise runs consecutive steps on one qubit in one
+ * round trip.) */
 int hs_apply_grid_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s,
                           hs_plan* plan);
 /* CX layer (fusion; no reference counterpart): CX gates on npairs (<= 32) disjoint (control,

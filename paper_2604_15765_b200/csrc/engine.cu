@@ -2276,28 +2276,35 @@ int hs_apply_cx_layer(hs_state* h, int npairs, const uint32_t* controls, const u
 // hs_apply_program.  Single-GPU states only (a cross-shard step would need its own exchange).
 int hs_apply_grid_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s,
                           hs_plan* plan) {
-    if (!h || nsteps < 2 || nsteps > 3 || !kinds || !bits || !s)
-        return set_err(HS_ERR_INVALID, "bad grid program (2 or 3 steps; one step: hs_apply_transfer)");
+    if (!h || nsteps < 2 || nsteps > 16 || !kinds || !bits || !s)
+        return set_err(HS_ERR_INVALID, "bad grid program (2 .. 16 steps on 2 or 3 qubits)");
     if (h->Plog)
         return set_err(HS_ERR_UNSUPPORTED, "grid programs run on single-GPU states");
     uint32_t t[3];
+    int nq = 0;
     for (int p = 0; p < nsteps; ++p) {
         if (bits[p] < (uint32_t)h->m || bits[p] >= (uint32_t)h->n)
             return set_err(HS_ERR_RANGE, "grid program steps act on grid qubits (>= m) only");
         if (kinds[p] < 0 || kinds[p] > 3)
             return set_err(HS_ERR_INVALID, "bad program step kind");
-        for (int q = 0; q < p; ++q)
-            if (bits[q] == bits[p])
-                return set_err(HS_ERR_INVALID, "grid program: one step per qubit");
-        t[p] = bits[p];
+        if (p > 0 && bits[p] == bits[p - 1])
+            continue;  // the qubit's chain continues
+        for (int q = 0; q < nq; ++q)
+            if (t[q] == bits[p])
+                return set_err(HS_ERR_INVALID, "grid program: a qubit's steps must be consecutive");
+        if (nq == 3)
+            return set_err(HS_ERR_INVALID, "grid program: at most 3 qubits");
+        t[nq++] = bits[p];
     }
-    std::sort(t, t + nsteps);
-    if (h->m != 5 || ((uint64_t)1 << (2 * nsteps)) * 1024 < 4096)
+    if (nq < 2)
+        return set_err(HS_ERR_INVALID, "grid program: 2 or 3 qubits (one qubit: hs_apply_transfer)");
+    std::sort(t, t + nq);
+    if (h->m != 5 || ((uint64_t)1 << (2 * nq)) * 1024 < 4096)
         return set_err(HS_ERR_UNSUPPORTED, "grid programs need 32 x 32 tiles");
     DeviceGuard dg(h->device);
     Geo G;
-    plan_geo(h, nsteps, t, G, 1);
-    auto* cf = new Coef<64>();
+    plan_geo(h, nq, t, G, 1);
+    auto* cf = new Coef<256>();
     for (int p = 0; p < nsteps; ++p) {
         std::memcpy(cf->s + 16 * p, s + 32 * p, 16 * sizeof(double2));
         uint32_t l = 0;
@@ -2307,11 +2314,11 @@ int hs_apply_grid_program(hs_state* h, int nsteps, const int* kinds, const uint3
         cf->pkind[p] = (uint8_t)kinds[p];
     }
     cf->nsteps = (uint32_t)nsteps;
-    int rc = launch<3, M_PROG, 64>(h, G, *cf, KrausArgs{nullptr, 0}, 1);
+    int rc = launch<3, M_PROG, 256>(h, G, *cf, KrausArgs{nullptr, 0}, 1);
     delete cf;
     if (rc)
         return rc;
-    return finish_plan(h, G, nsteps, t, HS_PATH_TILED_CROSS, plan, 2 * state_bytes(h));
+    return finish_plan(h, G, nq, t, HS_PATH_TILED_CROSS, plan, 2 * state_bytes(h));
 }
 
 int hs_apply_unitary(hs_state* h, int k, const double* u, const uint32_t* t, hs_plan* plan) {

@@ -648,7 +648,8 @@ __global__ void __launch_bounds__(NC, 1) gather_kernel(const Geo G, const Coef<N
 // e = 2^l for the step's grid bit l; adjoint tiles are staged transposed and conjugated on the fly.
 template <uint32_t NCW, int NS, bool TMAB = false>
 __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, const Coef<NS>& cf, uint32_t p,
-                                               uint64_t am, double2* sb, uint32_t tid) {
+                                               uint32_t p1, uint64_t am, double2* sb, uint32_t tid) {
+    // steps [p, p1) act on one grid qubit: its chain runs on each quad in registers
     // TMA boxes: tiles in stored orientation (adjoint ones transposed), 8 x 8 boxes; for grid
     // programs every box has phase 0 and box `slot` sits at slot * 64 (plan_gather), so the
     // address is pure arithmetic (no table lookups)
@@ -656,8 +657,6 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
     const uint32_t g = G.g, NG = 1u << g, e = 1u << cf.pbit[p], lo = e - 1;
     const uint32_t S0 = G.S0, P = S0 + 1, npos = S0 * S0, lp = 2 * G.logS0;
     const uint32_t nq = (NG / 2) * (NG / 2) * npos;
-    const double2* S = cf.s + 16 * p;
-    const uint32_t kind = cf.pkind[p];
     for (uint32_t q = tid; q < nq; q += NCW) {
         const uint32_t tq = q >> lp, pos = q & (npos - 1), i = pos >> G.logS0, j = pos & (S0 - 1);
         const uint32_t rr = tq >> (g - 1), cc = tq & ((NG >> 1) - 1);
@@ -688,7 +687,8 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
         v1.y = flip_sign(v1.y, f1);
         v2.y = flip_sign(v2.y, f2);
         v3.y = flip_sign(v3.y, f3);
-        prog_quad(kind, S, v0, v1, v2, v3);
+        for (uint32_t pp = p; pp < p1; ++pp)
+            prog_quad(cf.pkind[pp], cf.s + 16 * pp, v0, v1, v2, v3);
         v0.y = flip_sign(v0.y, f0);
         v1.y = flip_sign(v1.y, f1);
         v2.y = flip_sign(v2.y, f2);
@@ -830,9 +830,13 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                     dmma_direct3<NCW, K, BULK, TMAB, false, NARROW>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
                 }
             } else {
-                for (uint32_t p = 0; p < cf.nsteps; ++p) {
-                    grid_prog_step<NCW, NS, TMAB>(G, T, cf, p, am[i % TSL][0], sb, tid);
+                for (uint32_t p = 0; p < cf.nsteps;) {  // one pass per qubit (its steps are consecutive)
+                    uint32_t p1 = p + 1;
+                    while (p1 < cf.nsteps && cf.pbit[p1] == cf.pbit[p])
+                        ++p1;
+                    grid_prog_step<NCW, NS, TMAB>(G, T, cf, p, p1, am[i % TSL][0], sb, tid);
                     asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+                    p = p1;
                 }
             }
             if constexpr (BULK)

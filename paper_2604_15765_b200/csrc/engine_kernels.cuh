@@ -869,10 +869,14 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
         // operations per qubit).  Quads of step p: rows (x, x + 2^a) x columns (y, y + 2^a),
         // row-stacked (h00, h01, h10, h11) as TransferQuad (kernels.cpp:66-77); consecutive threads
         // take consecutive quads along a row.
+        // Consecutive steps on the same qubit share one round trip through shared memory: the quad
+        // stays in registers while the chain (e.g. depolarising, Rz, H in their cheap forms) runs.
         const uint32_t lq = G.logM - 1, nq = nvalid_units << (2 * lq), M = G.M;
-        for (uint32_t p = 0; p < cf.nsteps; ++p) {
-            const uint32_t a = cf.pbit[p], sa = 1u << a, lo = sa - 1, kind = cf.pkind[p];
-            const double2* S = cf.s + 16 * p;
+        for (uint32_t p = 0; p < cf.nsteps;) {
+            const uint32_t a = cf.pbit[p], sa = 1u << a, lo = sa - 1;
+            uint32_t p1 = p + 1;
+            while (p1 < cf.nsteps && cf.pbit[p1] == a)
+                ++p1;
             for (uint32_t q = tid; q < nq; q += NC) {
                 const uint32_t u = q >> (2 * lq), r = q & ((1u << (2 * lq)) - 1);
                 const uint32_t qx = r >> lq, qy = r & ((1u << lq) - 1);
@@ -880,14 +884,16 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                 const uint32_t b0 = u * G.A * G.TS + x * M + y;
                 const uint32_t b1 = b0 + sa, b2 = b0 + sa * M, b3 = b2 + sa;
                 double2 v0 = sb[b0], v1 = sb[b1], v2 = sb[b2], v3 = sb[b3];
-                prog_quad(kind, S, v0, v1, v2, v3);
+                for (uint32_t pp = p; pp < p1; ++pp)
+                    prog_quad(cf.pkind[pp], cf.s + 16 * pp, v0, v1, v2, v3);
                 sb[b0] = v0;
                 sb[b1] = v1;
                 sb[b2] = v2;
                 sb[b3] = v3;
             }
-            if (p + 1 < cf.nsteps)
+            if (p1 < cf.nsteps)
                 asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NC) : "memory");  // consumer warps only
+            p = p1;
         }
     } else if constexpr (MODE == M_MONO) {
         if (cf.diag && cf.nib == 0 && !G.groups && G.SR == G.M && !G.logical) {

@@ -5,15 +5,17 @@ kernels.cpp:510-549). ``apply_sequence`` gives the same result for a whole seque
 
 * a run of consecutive single-qubit operations is regrouped per qubit (single-qubit channels on
   different qubits commute);
-* the operations of each qubit are composed into one transfer matrix S = S_last ... S_first
-  (row-stacked, the engine's `TransferQuad` order, kernels.cpp:66-77);
-* the composed steps of all in-tile qubits (< m) of the run go into ONE pass (`hs_apply_program`):
-  the staged tiles are transformed step after step in shared memory, each step in its cheapest form
-  (Hadamard butterfly, diagonal phase, real (00,11)/(01,10) transfer as for depolarising / amplitude
-  damping and their compositions, or a general transfer matrix);
-* the composed operations of up to three grid qubits share one pass (`hs_apply_grid_program`: the
-  units of those grid bits are gathered and the steps applied one after another; m = 5); without
-  grid programs, two unitary grid steps share a pass as U_a (x) U_b (tensor-core gather);
+* the operations of each qubit form a chain of steps, each in its cheapest form (Hadamard butterfly,
+  diagonal phase, real (00,11)/(01,10) transfer as for depolarising / amplitude damping, or a general
+  transfer matrix); neighbours are composed into one transfer matrix S = S_last ... S_first
+  (row-stacked, the engine's `TransferQuad` order, kernels.cpp:66-77) only where that is cheaper;
+* the chains of all in-tile qubits (< m) of the run go into ONE pass (`hs_apply_program`): the
+  staged tiles are transformed qubit after qubit in shared memory, each qubit's chain running on a
+  quad in registers (one shared-memory round trip per qubit);
+* the chains of up to three grid qubits share one pass (`hs_apply_grid_program`: the units of those
+  grid bits are gathered and each qubit's chain applied per quad; m = 5); a lone grid qubit's chain
+  is composed into one transfer matrix; without grid programs, two unitary grid steps share a pass
+  as U_a (x) U_b (tensor-core gather);
 * any other operation (k >= 2) ends the run; consecutive multi-qubit unitaries on the same qubit
   set (C1's CX then Haar U on each ordered pair) are composed into one unitary U2 U1 (the second
   re-indexed to the first's target order, first-listed target = most significant bit,
@@ -96,6 +98,15 @@ def _is_cx(spec: H.ChannelSpec) -> bool:
     return spec.kind == "permutation" and spec.k == 2 and spec.name == "cnot"
 
 
+def _compose(chain: list) -> Step:
+    """One step equal to a qubit's chain applied in order (S = S_last ... S_first)."""
+    st = chain[0]
+    for x in chain[1:]:
+        uu = x.u @ st.u if (x.u is not None and st.u is not None) else None
+        st = Step(st.qubit, x.s @ st.s, False, st.count + x.count, uu)
+    return st
+
+
 def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_groups: int = 3,
                   compose_multi: bool = True, cx_layers: bool = True) -> Plan:
     """ops: iterable of (ChannelSpec, targets)."""
@@ -110,36 +121,38 @@ def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_gro
                 plan.items.append(("op", spec, tg))
         cx_pend.clear()
     edge = min(m, n)  # in-tile qubits
-    run: dict[int, Step] = {}   # grid qubits: composed per qubit
     order: list[int] = []
-    chains: dict[int, list[Step]] = {}  # in-tile qubits: steps, composed only where it is cheaper
+    # per qubit: a chain of steps applied in order.  A program runs a qubit's chain on each quad in
+    # registers (one shared-memory round trip per qubit), so steps are composed only where the
+    # composition's arithmetic is cheaper than the chain's (_KIND_COST)
+    chains: dict[int, list[Step]] = {}
 
     def flush():
         intile = [x for q in order if q < edge for x in chains[q]]
         for i in range(0, len(intile), 16):
             plan.items.append(("program", intile[i:i + 16]))
-        grid = [run[q] for q in order if q >= edge]
+        grid = [q for q in order if q >= edge]
         if grid_groups > 1 and m == 5:
-            # grid qubits three (two) at a time in one gathered pass (hs_apply_grid_program)
+            # grid qubits three (two) at a time in one gathered pass (hs_apply_grid_program), each
+            # with its chain; at most 16 steps per pass
             i = 0
             while i < len(grid):
                 grp = grid[i:i + grid_groups]
+                while len(grp) > 1 and sum(len(chains[q]) for q in grp) > 16:
+                    grp = grp[:-1]
                 if len(grp) == 1:
-                    plan.items.append(("step", grp[0]))
+                    plan.items.append(("step", _compose(chains[grp[0]])))
                 else:
-                    plan.items.append(("gprogram", grp))
-                i += grid_groups
-            run.clear()
+                    plan.items.append(("gprogram", [x for q in grp for x in chains[q]]))
+                i += len(grp)
             chains.clear()
             order.clear()
             return
         # grid qubits: two unitary steps share one pass as the 2-qubit unitary U_a (x) U_b (the
         # tensor-core gather, k = 2 on two grid bits); others are one pass each
         pend = None
-        for q in order:
-            if q < edge:
-                continue
-            st = run[q]
+        for q in grid:
+            st = _compose(chains[q])
             if pair_unitaries and st.u is not None:
                 if pend is None:
                     pend = st
@@ -151,7 +164,6 @@ def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_gro
             plan.items.append(("step", st))
         if pend is not None:
             plan.items.append(("step", pend))
-        run.clear()
         chains.clear()
         order.clear()
 
@@ -178,26 +190,16 @@ def plan_sequence(ops, n: int, m: int = 5, pair_unitaries: bool = True, grid_gro
             plan.items.append(("op", spec, targets))
             continue
         q = int(targets[0])
-        s = _single_qubit_s(spec)
-        is_h = spec.kind == "hadamard"
-        if q < edge:
-            step = Step(q, s, is_h, 1)
-            ch = chains.setdefault(q, [])
-            if not ch:
-                order.append(q)
-            elif _cost(Step(q, s @ ch[-1].s, False, 2)) <= _cost(ch[-1]) + _cost(step):
-                prev = ch.pop()
-                step = Step(q, s @ prev.s, False, prev.count + 1)
-            ch.append(step)
-            continue
-        u = _unitary_of(spec)
-        if q in run:
-            prev = run[q]
-            uu = u @ prev.u if (u is not None and prev.u is not None) else None
-            run[q] = Step(q, s @ prev.s, False, prev.count + 1, uu)
-        else:
-            run[q] = Step(q, s, is_h, 1, u)
+        step = Step(q, _single_qubit_s(spec), spec.kind == "hadamard", 1, _unitary_of(spec))
+        ch = chains.setdefault(q, [])
+        if not ch:
             order.append(q)
+        else:
+            comp = _compose([ch[-1], step])
+            if _KIND_COST[_kind(comp)] <= _KIND_COST[_kind(ch[-1])] + _KIND_COST[_kind(step)]:
+                ch.pop()
+                step = comp
+        ch.append(step)
     emit_cx()
     flush()
     return plan
@@ -220,13 +222,10 @@ def _kind(step: Step) -> int:
     return 0
 
 
-# relative cost of a program step: one shared-memory round trip of the staged tiles (dominant:
-# measured ~1.4k cycles per 64 KiB item on B200) plus its arithmetic per quad
-_STEP_COST = {1: 0.5, 2: 1.0, 3: 1.0, 0: 4.0}
-
-
-def _cost(step: Step) -> float:
-    return 3.0 + _STEP_COST[_kind(step)]
+# relative arithmetic of a step per quad (FP64): Hadamard butterfly (adds), diagonal (4 complex
+# products), real (00,11)/(01,10) transfer (6 real x complex products), general 4 x 4 transfer
+# (16 complex FMA); a qubit's chain shares one shared-memory round trip, so only this counts
+_KIND_COST = {1: 0.5, 2: 1.0, 3: 1.0, 0: 4.0}
 
 
 def execute(st: H.TiledHermitian, plan: Plan, opts: H.ApplyOptions | None = None) -> int:

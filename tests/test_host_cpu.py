@@ -203,8 +203,10 @@ def test_fusion_plan_counts():
     assert paired.items[1][2] == [5, 6] and paired.items[1][1].k == 2
     assert paired.items[2][1].qubit == 7 and paired.items[-1][1].lone_h
     assert plan.items[-1][1].lone_h
-    # H o Rz: one general transfer step per qubit (a step's shared-memory round trip dominates)
-    assert [fusion._kind(s) for s in plan.items[0][1]] == [0] * 5
+    # Rz then H: a chain of two cheap steps per qubit (diagonal, Hadamard) rather than one general
+    # transfer -- a qubit's chain shares one shared-memory round trip, so only arithmetic counts
+    assert [fusion._kind(s) for s in plan.items[0][1]] == [2, 1] * 5
+    assert [s.qubit for s in plan.items[0][1]] == [0, 0, 1, 1, 2, 2, 3, 3, 4, 4]
     # C1: CX then Haar U on each ordered pair -> one composed unitary per pair, U @ CX in the pair's order
     c1 = [(cx if op.kind == "cnot" else H.make_generic("haar", op.matrix), list(op.targets))
           for op in HS.config_ops("c1", 14)]
