@@ -51,3 +51,4 @@ def test_reference_arm_two_ranks():
     line = _torchrun(2, ["--impl", "reference", "--config", "c2", "--qubits", "10", "--steps", "1",
                          "--warmup", "1"])
     assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "reference"
+
