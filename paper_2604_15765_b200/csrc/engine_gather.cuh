@@ -769,7 +769,18 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
     const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     auto item_of = [&](uint64_t j) { return sweep_item(G, nItems, j); };
     __syncthreads();
+    // register rebalancing between the warp groups (768-thread layouts compile at 80 registers):
+    // the copy warps (2 warp groups) release 16 per thread to 64, the DMMA transform warps (4 warp
+    // groups) take 8 more to 88 -- setmaxnreg.inc waits until the CTA's own released registers
+    // cover it, so the exchange must balance within the CTA (an unbalanced 96 / 64 never returns)
+#ifdef HS_NO_REBAL
+    constexpr bool REBAL = false;
+#else
+    constexpr bool REBAL = !(SF || SF3 || NARROW) && BULK && MODE == M_DIRECT;
+#endif
     if (tid < NCW) {
+        if constexpr (REBAL)
+            asm volatile("setmaxnreg.inc.sync.aligned.u32 88;" ::: "memory");
         // ---- transform warps
         DmmaFrag fr;
         if constexpr (MODE == M_DIRECT)
@@ -846,6 +857,8 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
         return;
     }
     // ---- copy warps
+    if constexpr (REBAL)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 64;" ::: "memory");
     const uint32_t mtid = tid - NCW;
     const uint32_t NT = 1u << G.logNT, NGm = (1u << G.logNG) - 1;
     const uint32_t logT = 2 * G.logS0, P = G.S0 + 1;
