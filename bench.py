@@ -352,6 +352,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-states", type=int, default=4,
+                    help="device states / pinned host buffers in flight in the pipelined e2e loop (as memory allows)")
     ap.add_argument("--e2e-serial", action="store_true",
                     help="e2e without overlapping consecutive steps (one state, one buffer)")
     ap.add_argument("--shard", dest="shard", action="store_true", default=None,
@@ -737,7 +739,7 @@ def cpu_sample_n(cfg: str, n: int, m: int, reserved: int = 0) -> int:
 
 def pipelined_e2e(args, H, L, nat, st, host0, S, n, m, nops, world, fplan, ops, opts):
     """End to end through the public API with consecutive steps overlapped, as a serving loop
-    would run: up to three device states and pinned host buffers; step k uploads its input into
+    would run: up to --e2e-states device states and pinned host buffers; step k uploads its input into
     state k % B, applies the sequence and downloads the result, all on that state's stream, so
     uploads, compute and downloads of neighbouring steps overlap (PCIe is full duplex: ~91 GB/s
     both ways together on the box, tools/pcie_probe.cu).  Every step still moves S bytes
@@ -745,7 +747,14 @@ def pipelined_e2e(args, H, L, nat, st, host0, S, n, m, nops, world, fplan, ops, 
     second state or pinned buffer fits (the serial loop is used then)."""
     cnt = st.element_count()
     states, bufs, pinned = [st], [host0], []
-    for _ in range(2):  # triple buffering when HBM and host memory allow
+    try:
+        import psutil
+        host_total = psutil.virtual_memory().total
+    except Exception:  # pragma: no cover
+        host_total = 0
+    for _ in range(max(0, args.e2e_states - 1)):  # up to e2e_states in flight when HBM and host memory allow
+        if host_total and (len(bufs) + 1) * S > 0.75 * host_total:
+            break  # keep a quarter of the host RAM free (pinned pages cannot be swapped)
         try:
             sx = H.TiledHermitian(n, m, device=st.device)
         except Exception:
