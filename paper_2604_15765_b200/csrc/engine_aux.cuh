@@ -260,43 +260,72 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
         if (diag && x > y)  // mirror in the upper half of a diagonal tile
             st[slot - ((uint64_t)x << logM) - y + ((uint64_t)y << logM) + x] = make_double2(v.x, -v.y);
     };
+    // Each thread takes CXB positions of a tile at once: every owner's two loads are issued before
+    // any store (memory-level parallelism; pairs are disjoint, so no other thread reads or writes
+    // them; the upper halves of diagonal tiles written as mirrors are never read).
+    constexpr uint32_t CXB = 4;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         uint64_t ti, tj;
         tri_loose(tile, ti, tj);
         const uint64_t pi_i = cx_pi(L, ti << logM), pi_j = cx_pi(L, tj << logM);
         const bool diag = ti == tj;
-        for (uint32_t pos = threadIdx.x; pos < nel; pos += blockDim.x) {
-            const uint32_t x = pos >> logM, y = pos & (M - 1);
-            if ((diag && x < y) || (((ti << logM) | x) >> nq) || (((tj << logM) | y) >> nq))
-                continue;  // mirror half, or zero padding (n < m): left as it is
-            const uint64_t p = pi_i ^ tab[x], q = pi_j ^ tab[y];
-            uint64_t tp = p >> logM, tq = q >> logM;
-            uint32_t px = (uint32_t)(p & (M - 1)), qy = (uint32_t)(q & (M - 1));
-            const bool cj = tp < tq || (tp == tq && px < qy);
-            if (cj) {
-                const uint64_t tt = tp;
-                tp = tq;
-                tq = tt;
-                const uint32_t xx = px;
-                px = qy;
-                qy = xx;
+        for (uint32_t pos0 = threadIdx.x; pos0 < nel; pos0 += CXB * blockDim.x) {
+            uint64_t eo[CXB], s2o[CXB];
+            uint32_t meta[CXB];  // bit 0: active pair, 1: self-pair, 2: conjugate, 3: partner in a diagonal tile
+            uint32_t pxo[CXB], qyo[CXB];
+            double2 av[CXB], bv[CXB];
+#pragma unroll
+            for (uint32_t k = 0; k < CXB; ++k) {
+                const uint32_t pos = pos0 + k * blockDim.x;
+                meta[k] = 0;
+                if (pos >= nel)
+                    continue;
+                const uint32_t x = pos >> logM, y = pos & (M - 1);
+                if ((diag && x < y) || (((ti << logM) | x) >> nq) || (((tj << logM) | y) >> nq))
+                    continue;  // mirror half, or zero padding (n < m): left as it is
+                const uint64_t p = pi_i ^ tab[x], q = pi_j ^ tab[y];
+                uint64_t tp = p >> logM, tq = q >> logM;
+                uint32_t px = (uint32_t)(p & (M - 1)), qy = (uint32_t)(q & (M - 1));
+                const bool cj = tp < tq || (tp == tq && px < qy);
+                if (cj) {
+                    const uint64_t tt = tp;
+                    tp = tq;
+                    tq = tt;
+                    const uint32_t xx = px;
+                    px = qy;
+                    qy = xx;
+                }
+                const uint64_t e = (tile << lMM) + pos;
+                const uint64_t s2 = ((tp * (tp + 1) / 2 + tq) << lMM) + ((uint64_t)px << logM) + qy;
+                if (s2 < e || (s2 == e && !cj))
+                    continue;  // the lower slot of the pair owns it; or a fixed point
+                eo[k] = e;
+                s2o[k] = s2;
+                pxo[k] = px;
+                qyo[k] = qy;
+                meta[k] = 1u | (s2 == e ? 2u : 0u) | (cj ? 4u : 0u) | (tp == tq ? 8u : 0u);
+                av[k] = st[e];
+                if (s2 != e)
+                    bv[k] = st[s2];
             }
-            const uint64_t e = (tile << lMM) + pos;
-            const uint64_t s2 = ((tp * (tp + 1) / 2 + tq) << lMM) + ((uint64_t)px << logM) + qy;
-            if (s2 < e || (s2 == e && !cj))
-                continue;  // the lower slot of the pair owns it; or a fixed point
-            double2 a = st[e];
-            if (s2 == e) {  // rho'(i, j) = rho(j, i)
-                put(e, diag, x, y, make_double2(a.x, -a.y));
-                continue;
+#pragma unroll
+            for (uint32_t k = 0; k < CXB; ++k) {
+                if (!(meta[k] & 1u))
+                    continue;
+                const uint32_t pos = pos0 + k * blockDim.x, x = pos >> logM, y = pos & (M - 1);
+                double2 a = av[k];
+                if (meta[k] & 2u) {  // rho'(i, j) = rho(j, i)
+                    put(eo[k], diag, x, y, make_double2(a.x, -a.y));
+                    continue;
+                }
+                double2 b = bv[k];
+                if (meta[k] & 4u) {
+                    a.y = -a.y;
+                    b.y = -b.y;
+                }
+                put(eo[k], diag, x, y, b);
+                put(s2o[k], (meta[k] & 8u) != 0, pxo[k], qyo[k], a);
             }
-            double2 b = st[s2];
-            if (cj) {
-                a.y = -a.y;
-                b.y = -b.y;
-            }
-            put(e, diag, x, y, b);
-            put(s2, tp == tq, px, qy, a);
         }
     }
 }
