@@ -251,10 +251,12 @@ __device__ __forceinline__ uint64_t cx_pi(const CxLayer& L, uint64_t x) {
 __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st, uint64_t ntiles, uint32_t logM,
                                                        uint32_t nq, const CxLayer L) {
     __shared__ uint64_t tab[32];  // pi of the in-tile offsets
+    // per tile: pi of its rows x (tile row rT, in-tile row rX, tri(rT)) and of its columns y
+    __shared__ uint64_t rT[32], rTri[32], cT[32], cTri[32];
+    __shared__ uint32_t rX[32], cY[32];
     const uint32_t M = 1u << logM, lMM = 2 * logM, nel = 1u << lMM;
     if (threadIdx.x < M)
         tab[threadIdx.x] = cx_pi(L, threadIdx.x);
-    __syncthreads();
     auto put = [&](uint64_t slot, bool diag, uint32_t x, uint32_t y, double2 v) {
         st[slot] = v;
         if (diag && x > y)  // mirror in the upper half of a diagonal tile
@@ -267,12 +269,27 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         uint64_t ti, tj;
         tri_loose(tile, ti, tj);
-        const uint64_t pi_i = cx_pi(L, ti << logM), pi_j = cx_pi(L, tj << logM);
+        __syncthreads();  // tab ready / the previous tile's tables are no longer read
+        if (threadIdx.x < 2 * M) {
+            const bool col = threadIdx.x >= M;
+            const uint32_t v = threadIdx.x & (M - 1);
+            const uint64_t pq = cx_pi(L, (col ? tj : ti) << logM) ^ tab[v], t = pq >> logM;
+            if (col) {
+                cT[v] = t;
+                cTri[v] = t * (t + 1) / 2;
+                cY[v] = (uint32_t)(pq & (M - 1));
+            } else {
+                rT[v] = t;
+                rTri[v] = t * (t + 1) / 2;
+                rX[v] = (uint32_t)(pq & (M - 1));
+            }
+        }
+        __syncthreads();
         const bool diag = ti == tj;
         for (uint32_t pos0 = threadIdx.x; pos0 < nel; pos0 += CXB * blockDim.x) {
-            uint64_t eo[CXB], s2o[CXB];
+            uint64_t s2o[CXB];
             uint32_t meta[CXB];  // bit 0: active pair, 1: self-pair, 2: conjugate, 3: partner in a diagonal tile
-            uint32_t pxo[CXB], qyo[CXB];
+            uint32_t pq[CXB];    // partner's in-tile row << 8 | column
             double2 av[CXB], bv[CXB];
 #pragma unroll
             for (uint32_t k = 0; k < CXB; ++k) {
@@ -283,26 +300,17 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
                 const uint32_t x = pos >> logM, y = pos & (M - 1);
                 if ((diag && x < y) || (((ti << logM) | x) >> nq) || (((tj << logM) | y) >> nq))
                     continue;  // mirror half, or zero padding (n < m): left as it is
-                const uint64_t p = pi_i ^ tab[x], q = pi_j ^ tab[y];
-                uint64_t tp = p >> logM, tq = q >> logM;
-                uint32_t px = (uint32_t)(p & (M - 1)), qy = (uint32_t)(q & (M - 1));
+                const uint64_t tp = rT[x], tq = cT[y];
+                const uint32_t px = rX[x], qy = cY[y];
                 const bool cj = tp < tq || (tp == tq && px < qy);
-                if (cj) {
-                    const uint64_t tt = tp;
-                    tp = tq;
-                    tq = tt;
-                    const uint32_t xx = px;
-                    px = qy;
-                    qy = xx;
-                }
+                // canonical slot of (pi(i), pi(j)): (tp, tq, px, qy), or its transpose when above the diagonal
+                const uint64_t s2 = ((cj ? cTri[y] + tp : rTri[x] + tq) << lMM) +
+                                    (cj ? ((uint64_t)qy << logM) + px : ((uint64_t)px << logM) + qy);
                 const uint64_t e = (tile << lMM) + pos;
-                const uint64_t s2 = ((tp * (tp + 1) / 2 + tq) << lMM) + ((uint64_t)px << logM) + qy;
                 if (s2 < e || (s2 == e && !cj))
                     continue;  // the lower slot of the pair owns it; or a fixed point
-                eo[k] = e;
                 s2o[k] = s2;
-                pxo[k] = px;
-                qyo[k] = qy;
+                pq[k] = cj ? (qy << 8) | px : (px << 8) | qy;
                 meta[k] = 1u | (s2 == e ? 2u : 0u) | (cj ? 4u : 0u) | (tp == tq ? 8u : 0u);
                 av[k] = st[e];
                 if (s2 != e)
@@ -313,9 +321,10 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
                 if (!(meta[k] & 1u))
                     continue;
                 const uint32_t pos = pos0 + k * blockDim.x, x = pos >> logM, y = pos & (M - 1);
+                const uint64_t e = (tile << lMM) + pos;
                 double2 a = av[k];
                 if (meta[k] & 2u) {  // rho'(i, j) = rho(j, i)
-                    put(eo[k], diag, x, y, make_double2(a.x, -a.y));
+                    put(e, diag, x, y, make_double2(a.x, -a.y));
                     continue;
                 }
                 double2 b = bv[k];
@@ -323,8 +332,8 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
                     a.y = -a.y;
                     b.y = -b.y;
                 }
-                put(eo[k], diag, x, y, b);
-                put(s2o[k], (meta[k] & 8u) != 0, pxo[k], qyo[k], a);
+                put(e, diag, x, y, b);
+                put(s2o[k], (meta[k] & 8u) != 0, pq[k] >> 8, pq[k] & 0xffu, a);
             }
         }
     }
