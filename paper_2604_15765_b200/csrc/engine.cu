@@ -1094,7 +1094,7 @@ int shard_prelude(hs_state* h, const Geo& G0, bool carry_over, Geo& G) {
             G.rbase[j] = j < h->recv_slots ? h->recv + (uint64_t)j * h->recv_count : nullptr;
     }
     G.rev = (uint32_t)(h->sweeps++ & 1u);
-    G.dbg = debug_flags() & DBG_POISON;  // the pipeline takes only the stage-poisoning bit
+    G.dbg = debug_flags() & (DBG_POISON | 2048u);  // the pipeline takes the stage-poisoning bit and bit 11 (one-quad program loop)
     return HS_OK;
 }
 

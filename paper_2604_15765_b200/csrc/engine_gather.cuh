@@ -700,6 +700,55 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
     }
 }
 
+// grid_prog_step for TMA boxes when an item holds exactly two quads per transform thread and qubit
+// (3 grid qubits: 16 tile quads x 64 positions; 2 grid qubits: 4 x 256; NCW = 512).  A thread's
+// position -- hence its direct / transposed in-box offsets `ad` / `aa` -- is the same for every
+// item, qubit and quad, and the two tile quads of each pass are the same for every item: both are
+// computed once per kernel (gather_ws_kernel), per item only the adjoint flags are looked up.  Both
+// quads are loaded before either chain runs (the compiler cannot hoist shared loads over shared
+// stores itself), and the adjoint flag rides in bit 31 of each address.
+template <int NS>
+__device__ __forceinline__ void grid_prog_step2(const Geo& G, const Coef<NS>& cf, uint32_t p, uint32_t p1, uint64_t am,
+                                                double2* sb, uint32_t t0ab, uint32_t ad, uint32_t dlt) {
+    // t0ab: the (0, 0) logical tile of this thread's two quads for this pass (bits 0-7, 8-15);
+    // ad: direct in-box offset of its position, dlt: transposed minus direct offset
+    const uint32_t g = G.g, sh = 2 * G.logS0, l = cf.pbit[p];  // box slots per tile << 6 == S0^2
+    const uint32_t o1 = 1u << l, o2 = o1 << g, o3 = o1 + o2;
+    uint32_t a[8];
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t t0 = (t0ab >> (8 * h)) & 0xffu;
+        const uint64_t amt = am >> t0;  // the quad's adjoint flags at bit offsets 0, o1, o2, o3 (<= 36)
+        const uint32_t base = (t0 << sh) + ad;
+        const uint32_t f0 = (uint32_t)amt & 1u, f1 = (uint32_t)(amt >> o1) & 1u, f2 = (uint32_t)(amt >> o2) & 1u,
+                       f3 = (uint32_t)(amt >> o3) & 1u;
+        a[4 * h + 0] = (base + f0 * dlt) | (f0 << 31);
+        a[4 * h + 1] = (base + (o1 << sh) + f1 * dlt) | (f1 << 31);
+        a[4 * h + 2] = (base + (o2 << sh) + f2 * dlt) | (f2 << 31);
+        a[4 * h + 3] = (base + (o3 << sh) + f3 * dlt) | (f3 << 31);
+    }
+    double2 va[4], vb[4];
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) {
+        va[c] = sb[a[c] & 0x7fffffffu];
+        vb[c] = sb[a[4 + c] & 0x7fffffffu];
+    }
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) {
+        va[c].y = flip_sign(va[c].y, a[c] & 0x80000000u);
+        vb[c].y = flip_sign(vb[c].y, a[4 + c] & 0x80000000u);
+    }
+    for (uint32_t pp = p; pp < p1; ++pp)
+        prog_quad2(cf.pkind[pp], cf.s + 16 * pp, va, vb);
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) {
+        va[c].y = flip_sign(va[c].y, a[c] & 0x80000000u);
+        vb[c].y = flip_sign(vb[c].y, a[4 + c] & 0x80000000u);
+        sb[a[c] & 0x7fffffffu] = va[c];
+        sb[a[4 + c] & 0x7fffffffu] = vb[c];
+    }
+}
+
 // BULK (G.bulk): sub-block rows are contiguous runs of S0 >= 16 elements; every tile is staged in its
 // stored orientation (pitch S0 + 1) by one cp.async.bulk per row (256 / 512 B, completing on the
 // stage's `full` mbarrier) and written back by one bulk store per row -- no per-element copy
@@ -776,7 +825,7 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
 #ifdef HS_NO_REBAL
     constexpr bool REBAL = false;
 #else
-    constexpr bool REBAL = !(SF || SF3 || NARROW) && BULK && MODE == M_DIRECT;
+    constexpr bool REBAL = !(SF || SF3 || NARROW) && BULK && (MODE == M_DIRECT || (MODE == M_PROG && TMAB));
 #endif
     if (tid < NCW) {
         if constexpr (REBAL)
@@ -823,6 +872,41 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
             }
             asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
         }
+        // grid programs on TMA boxes: this thread's position and its in-box offsets (direct / transposed;
+        // the swizzle term (x ^ y) & 7 is symmetric), fixed for the whole kernel (grid_prog_step2)
+        uint32_t pg_ad = 0, pg_dlt = 0, pg_t[3] = {0, 0, 0}, pg_end[3] = {0, 0, 0};
+        bool pg_two = false;
+        if constexpr (MODE == M_PROG && TMAB) {
+            const uint32_t nbx = G.S0 >> 3, lp = 2 * G.logS0, pos = tid & ((1u << lp) - 1), pi = pos >> G.logS0,
+                           pj = pos & (G.S0 - 1);
+            const uint32_t sw = (pi ^ pj) & 7u;
+            pg_ad = (((pi >> 3) * nbx + (pj >> 3)) << 6) + (pi & 7u) * 8u + sw;
+            pg_dlt = (((pj >> 3) * nbx + (pi >> 3)) << 6) + (pj & 7u) * 8u + sw - pg_ad;
+            // passes (one per qubit: its steps are consecutive), at most three; per pass the (0, 0)
+            // tiles of the thread's two quads
+            uint32_t p = 0;
+#pragma unroll
+            for (int np = 0; np < 3; ++np)
+                if (p < cf.nsteps) {
+                    uint32_t p1 = p + 1;
+                    while (p1 < cf.nsteps && cf.pbit[p1] == cf.pbit[p])
+                        ++p1;
+                    const uint32_t lo = (1u << cf.pbit[p]) - 1, hm = (1u << (G.g - 1)) - 1;
+                    uint32_t t0ab = 0;
+#pragma unroll
+                    for (uint32_t h = 0; h < 2; ++h) {
+                        const uint32_t tq = (tid >> lp) + h * (NCW >> lp);
+                        const uint32_t rr = tq >> (G.g - 1), cc = tq & hm;
+                        const uint32_t R0 = ((rr & ~lo) << 1) | (rr & lo), C0 = ((cc & ~lo) << 1) | (cc & lo);
+                        t0ab |= ((R0 << G.g) | C0) << (8 * h);
+                    }
+                    pg_t[np] = t0ab;
+                    pg_end[np] = p1;
+                    p = p1;
+                }
+            // bit 11: the one-quad loop
+            pg_two = p >= cf.nsteps && ((1u << (2 * G.g - 2)) << lp) == 2 * NCW && !(G.dbg & 2048u);
+        }
         for (uint64_t i = 0; i < nlocal; ++i) {
             const uint32_t s = (uint32_t)(i % S);
             mbar_wait(&full[s], (uint32_t)((i / S) & 1));
@@ -841,13 +925,25 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                     dmma_direct3<NCW, K, BULK, TMAB, false, NARROW>(G, T, fr, am[i % TSL][0], sb, tid >> 5);
                 }
             } else {
-                for (uint32_t p = 0; p < cf.nsteps;) {  // one pass per qubit (its steps are consecutive)
-                    uint32_t p1 = p + 1;
-                    while (p1 < cf.nsteps && cf.pbit[p1] == cf.pbit[p])
-                        ++p1;
-                    grid_prog_step<NCW, NS, TMAB>(G, T, cf, p, p1, am[i % TSL][0], sb, tid);
-                    asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
-                    p = p1;
+                if (TMAB && pg_two) {
+                    uint32_t p = 0;
+#pragma unroll
+                    for (int ps = 0; ps < 3; ++ps) {
+                        if (p < cf.nsteps) {
+                            grid_prog_step2<NS>(G, cf, p, pg_end[ps], am[i % TSL][0], sb, pg_t[ps], pg_ad, pg_dlt);
+                            asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+                            p = pg_end[ps];
+                        }
+                    }
+                } else {
+                    for (uint32_t p = 0; p < cf.nsteps;) {  // one pass per qubit (its steps are consecutive)
+                        uint32_t p1 = p + 1;
+                        while (p1 < cf.nsteps && cf.pbit[p1] == cf.pbit[p])
+                            ++p1;
+                        grid_prog_step<NCW, NS, TMAB>(G, T, cf, p, p1, am[i % TSL][0], sb, tid);
+                        asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+                        p = p1;
+                    }
                 }
             }
             if constexpr (BULK)

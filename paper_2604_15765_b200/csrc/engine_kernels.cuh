@@ -739,10 +739,52 @@ __device__ __forceinline__ void prog_quad(uint32_t kind, const double2* S, doubl
     v2 = w2;
     v3 = w3;
 }
+// One program step on two quads at once: the step's coefficients are fetched once and the two
+// independent dependency chains interleave on the FP64 pipe.
+__device__ __forceinline__ void prog_quad2(uint32_t kind, const double2* S, double2 (&a)[4], double2 (&b)[4]) {
+    if (kind == 1) {
+        prog_quad(1, S, a[0], a[1], a[2], a[3]);
+        prog_quad(1, S, b[0], b[1], b[2], b[3]);
+    } else if (kind == 2) {
+        const double2 s0 = S[0], s1 = S[5], s2 = S[10], s3 = S[15];
+        a[0] = cmul(s0, a[0]); b[0] = cmul(s0, b[0]);
+        a[1] = cmul(s1, a[1]); b[1] = cmul(s1, b[1]);
+        a[2] = cmul(s2, a[2]); b[2] = cmul(s2, b[2]);
+        a[3] = cmul(s3, a[3]); b[3] = cmul(s3, b[3]);
+    } else if (kind == 3) {
+        const double p00 = S[0].x, p03 = S[3].x, p30 = S[12].x, p33 = S[15].x;
+        const double p11 = S[5].x, p12 = S[6].x, p21 = S[9].x, p22 = S[10].x;
+        // in place: the cross terms first, then each result into its own operand's registers
+        auto pair = [&](double& x, double& y, double cxx, double cxy, double cyx, double cyy) {
+            const double tx = cxy * y, ty = cyx * x;
+            x = fma(cxx, x, tx);
+            y = fma(cyy, y, ty);
+        };
+        auto one = [&](double2 (&v)[4]) {
+            pair(v[0].x, v[3].x, p00, p03, p30, p33);
+            pair(v[0].y, v[3].y, p00, p03, p30, p33);
+            pair(v[1].x, v[2].x, p11, p12, p21, p22);
+            pair(v[1].y, v[2].y, p11, p12, p21, p22);
+        };
+        one(a);
+        one(b);
+    } else {
+        prog_quad(0, S, a[0], a[1], a[2], a[3]);
+        prog_quad(0, S, b[0], b[1], b[2], b[3]);
+    }
+}
+
+// In-tile programs: what a consumer thread needs per pass (one pass per qubit, at most MAXP), the
+// same for every item -- the bases of its two quads (bits 0-15, 16-31) and the pass's last step
+struct ProgPre {
+    static constexpr int MAXP = 5;
+    uint32_t base[MAXP], end[MAXP];
+    bool ok;
+};
 template <int K, int MODE, int NS, int NC = NCONS>
 __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const Coef<NS>& cf, const uint64_t* am,
                                              uint32_t nvalid_units, double2* sb, uint32_t grp = 0, int tidv = -1,
-                                             uint32_t barid = 1) {
+                                             uint32_t barid = 1, const ProgPre* pre = nullptr) {
     constexpr int D = 1 << K;
     const int tid = tidv >= 0 ? tidv : (int)threadIdx.x;
     const uint32_t nblk = G.U << (G.logNxb + G.logNyb);
@@ -872,16 +914,48 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
         // Consecutive steps on the same qubit share one round trip through shared memory: the quad
         // stays in registers while the chain (e.g. depolarising, Rz, H in their cheap forms) runs.
         const uint32_t lq = G.logM - 1, nq = nvalid_units << (2 * lq), M = G.M;
+        // two quads per thread and pass (4 whole tiles per item, 512 consumers): both are loaded
+        // before either chain runs (the compiler cannot hoist shared loads over shared stores
+        // itself), the step's coefficients are fetched once and the two chains interleave; the quad
+        // bases come precomputed (ProgPre)
+        if (pre && pre->ok && nq == 2 * NC) {
+            uint32_t p = 0;
+#pragma unroll
+            for (int ps = 0; ps < ProgPre::MAXP; ++ps)
+                if (p < cf.nsteps) {
+                    const uint32_t sa = 1u << cf.pbit[p], ba = pre->base[ps] & 0xffffu, bb = pre->base[ps] >> 16;
+                    const uint32_t o1 = sa, o2 = sa * M, o3 = o2 + sa;
+                    double2 va[4] = {sb[ba], sb[ba + o1], sb[ba + o2], sb[ba + o3]};
+                    double2 vb[4] = {sb[bb], sb[bb + o1], sb[bb + o2], sb[bb + o3]};
+                    for (uint32_t pp = p; pp < pre->end[ps]; ++pp)
+                        prog_quad2(cf.pkind[pp], cf.s + 16 * pp, va, vb);
+                    sb[ba] = va[0];
+                    sb[ba + o1] = va[1];
+                    sb[ba + o2] = va[2];
+                    sb[ba + o3] = va[3];
+                    sb[bb] = vb[0];
+                    sb[bb + o1] = vb[1];
+                    sb[bb + o2] = vb[2];
+                    sb[bb + o3] = vb[3];
+                    p = pre->end[ps];
+                    if (p < cf.nsteps)
+                        asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NC) : "memory");  // consumer warps only
+                }
+            return;
+        }
         for (uint32_t p = 0; p < cf.nsteps;) {
             const uint32_t a = cf.pbit[p], sa = 1u << a, lo = sa - 1;
             uint32_t p1 = p + 1;
             while (p1 < cf.nsteps && cf.pbit[p1] == a)
                 ++p1;
-            for (uint32_t q = tid; q < nq; q += NC) {
+            auto quad_base = [&](uint32_t q) {
                 const uint32_t u = q >> (2 * lq), r = q & ((1u << (2 * lq)) - 1);
                 const uint32_t qx = r >> lq, qy = r & ((1u << lq) - 1);
                 const uint32_t x = ((qx & ~lo) << 1) | (qx & lo), y = ((qy & ~lo) << 1) | (qy & lo);
-                const uint32_t b0 = u * G.A * G.TS + x * M + y;
+                return u * G.A * G.TS + x * M + y;
+            };
+            for (uint32_t q = tid; q < nq; q += NC) {
+                const uint32_t b0 = quad_base(q);
                 const uint32_t b1 = b0 + sa, b2 = b0 + sa * M, b3 = b2 + sa;
                 double2 v0 = sb[b0], v1 = sb[b1], v2 = sb[b2], v3 = sb[b3];
                 for (uint32_t pp = p; pp < p1; ++pp)
@@ -1065,6 +1139,33 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
         return;
     }
     // ---- consumer warps: transform each staged item in place
+    ProgPre pre;
+    pre.ok = false;
+    if constexpr (MODE == M_PROG) {
+        const uint32_t lq = G.logM - 1, tid = threadIdx.x;
+        uint32_t p = 0;
+#pragma unroll
+        for (int ps = 0; ps < ProgPre::MAXP; ++ps) {
+            pre.base[ps] = 0;
+            pre.end[ps] = 0;
+            if (p < cf.nsteps) {
+                uint32_t p1 = p + 1;
+                while (p1 < cf.nsteps && cf.pbit[p1] == cf.pbit[p])
+                    ++p1;
+                const uint32_t lo = (1u << cf.pbit[p]) - 1;
+#pragma unroll
+                for (uint32_t h = 0; h < 2; ++h) {
+                    const uint32_t q = tid + h * NCONS, u = q >> (2 * lq), r = q & ((1u << (2 * lq)) - 1);
+                    const uint32_t qx = r >> lq, qy = r & ((1u << lq) - 1);
+                    const uint32_t x = ((qx & ~lo) << 1) | (qx & lo), y = ((qy & ~lo) << 1) | (qy & lo);
+                    pre.base[ps] |= (u * G.A * G.TS + x * G.M + y) << (16 * h);
+                }
+                pre.end[ps] = p1;
+                p = p1;
+            }
+        }
+        pre.ok = p >= cf.nsteps && !(G.dbg & 2048u);  // bit 11: the one-quad loop
+    }
     for (uint64_t i = 0; i < nlocal; ++i) {
         const uint32_t s = (uint32_t)(i % S);
         double2* sb = ring + (size_t)s * G.stage_elems;
@@ -1073,7 +1174,7 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
         const uint64_t u0 = G.groups ? item / G.groups : (item >> G.logSlabs) << G.logU;
         const uint32_t nvalid = G.nU_units - u0 < G.U ? (uint32_t)(G.nU_units - u0) : G.U;
         mbar_wait(&full[s], (uint32_t)((i / S) & 1));
-        pipe_compute<K, MODE, NS>(G, T, cf, am[s], nvalid, sb, grp);
+        pipe_compute<K, MODE, NS>(G, T, cf, am[s], nvalid, sb, grp, -1, 1, &pre);
         fence_async_smem();
         __syncwarp();
         if (lane == 0)

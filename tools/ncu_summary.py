@@ -11,6 +11,7 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 
 
 def main(raw, sass=None, top=25):
+    top = int(top)
     r = list(csv.reader(open(raw)))
     hdr = r[0]
     st = [h for h in hdr if h.startswith('smsp__pcsamp_warps_issue_stalled') and not h.endswith('not_issued')]

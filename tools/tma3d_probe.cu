@@ -3,7 +3,9 @@
 //   (A) 2-D boxes of 8 rows x 128 B (1 KiB, SWIZZLE_128B): 64 boxes per item (the engine today);
 //   (B) 3-D boxes {128 B, 2 chunks, 8 rows} = 8 rows x 256 B contiguous (2 KiB, SWIZZLE_128B per
 //       128-B chunk): 32 boxes per item;
-//   (C) 3-D boxes of 16 rows x 256 B (4 KiB): 16 boxes per item.
+//   (C) 3-D boxes of 16 rows x 256 B (4 KiB): 16 boxes per item;
+//   (D) any of them behind a whole-tile L2 prefetch (cp.async.bulk.prefetch.L2, 16 KiB per tile) issued a few
+//       grid strides ahead by the CTA that holds a unit's sub-block 0.
 // Three-stage ring, one producer warp per stage, store back + reload (no transform).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O2 -cudart shared -o tools/tma3d_probe tools/tma3d_probe.cu -lcuda
 #include <cuda.h>
@@ -33,7 +35,8 @@ __device__ __forceinline__ void box_of(uint64_t j, int b, uint32_t tiles, int ro
 }
 
 __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensorMap tm, uint64_t n_items, uint32_t tiles,
-                                                int boxes, int rows, uint32_t box_bytes, int wide) {
+                                                int boxes, int rows, uint32_t box_bytes, int wide, int pf,
+                                                const unsigned char* base) {
     extern __shared__ __align__(1024) unsigned char ring[];
     __shared__ __align__(8) uint64_t full[STAGES];
     const uint32_t stage_bytes = boxes * box_bytes;
@@ -72,6 +75,15 @@ __global__ void __launch_bounds__(128, 1) probe(const __grid_constant__ CUtensor
         if (j >= n_items)
             break;
         __syncwarp();
+        // (D) whole-tile L2 prefetch: the CTA that holds sub-block 0 of a unit asks L2 for the unit's 16
+        // whole tiles pf grid strides ahead, so DRAM sees 16 KiB contiguous reads and the boxes hit L2
+        if (pf && (j & 3) == 0 && lane < 16) {
+            const uint64_t jp = j + (uint64_t)pf * gridDim.x;
+            if (jp < n_items) {
+                const uint64_t tile = ((jp / 4) * 16 + (uint64_t)lane * 977) % tiles;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + tile * 16384), "r"(16384) : "memory");
+            }
+        }
         if (lane == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])),
                          "r"(stage_bytes));
@@ -117,8 +129,8 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     struct Cfg {
-        int wide, rows;
-    } cfgs[] = {{0, 8}, {0, 16}, {1, 8}, {1, 16}};
+        int wide, rows, pf;
+    } cfgs[] = {{0, 8, 0}, {0, 16, 0}, {1, 8, 0}, {1, 16, 0}, {0, 8, 1}, {0, 8, 2}, {0, 8, 4}, {0, 8, 8}, {1, 16, 2}, {1, 16, 4}};
     for (int rep = 0; rep < 2; ++rep)
         for (const Cfg& c : cfgs) {
             CUtensorMap tm;
@@ -147,15 +159,16 @@ int main() {
             const uint32_t smem = STAGES * 65536;
             cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             const uint64_t items = (tiles * 16384ull) / 65536 * 2;
-            probe<<<sms, 128, smem>>>(tm, items / 4, tiles, boxes, c.rows, box_bytes, c.wide);
+            probe<<<sms, 128, smem>>>(tm, items / 4, tiles, boxes, c.rows, box_bytes, c.wide, c.pf, (const unsigned char*)d);
             cudaEventRecord(e0);
-            probe<<<sms, 128, smem>>>(tm, items, tiles, boxes, c.rows, box_bytes, c.wide);
+            probe<<<sms, 128, smem>>>(tm, items, tiles, boxes, c.rows, box_bytes, c.wide, c.pf, (const unsigned char*)d);
             cudaEventRecord(e1);
             cudaError_t e = cudaEventSynchronize(e1);
             float ms = 0;
             cudaEventElapsedTime(&ms, e0, e1);
-            printf("%s box %2d rows x %3d B (%5u B), %2d boxes/item: %s  %.1f GB/s\n", c.wide ? "3-D" : "2-D", c.rows,
-                   c.wide ? 256 : 128, box_bytes, boxes, cudaGetErrorString(e), 2.0 * items * 65536 / ms / 1e6);
+            printf("%s box %2d rows x %3d B (%5u B), %2d boxes/item, L2 tile prefetch %d ahead: %s  %.1f GB/s\n",
+                   c.wide ? "3-D" : "2-D", c.rows, c.wide ? 256 : 128, box_bytes, boxes, c.pf, cudaGetErrorString(e),
+                   2.0 * items * 65536 / ms / 1e6);
         }
     return 0;
 }
