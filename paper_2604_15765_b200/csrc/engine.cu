@@ -2223,6 +2223,13 @@ int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* 
         cf->pkind[p] = (uint8_t)kinds[p];
     }
     cf->nsteps = (uint32_t)nsteps;
+    // four whole 32 x 32 tiles per item: one spare element between them puts consecutive tiles one
+    // 16-B bank group apart (pipe_kernel's program passes on qubits 0 and 1 use it)
+    if (G.M == 32 && G.SR == G.M && G.TS == G.M * G.M && !G.g && !(debug_flags() & 4096u)) {  // bit 12: dense tiles
+        G.TS = G.M * G.M + 1;
+        G.stage_elems = ((G.U << G.logNT) * G.TS + 7) & ~7u;
+        G.stages = std::min<uint32_t>(MAX_STAGES, (200u * 1024u / 16u) / G.stage_elems);
+    }
     int rc = launch<1, M_PROG, 256>(h, G, *cf, ka, 1);
     delete cf;
     if (rc)

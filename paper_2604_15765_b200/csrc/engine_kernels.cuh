@@ -1155,7 +1155,17 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
                 const uint32_t lo = (1u << cf.pbit[p]) - 1;
 #pragma unroll
                 for (uint32_t h = 0; h < 2; ++h) {
-                    const uint32_t q = tid + h * NCONS, u = q >> (2 * lq), r = q & ((1u << (2 * lq)) - 1);
+                    uint32_t q = tid + h * NCONS;
+                    // skewed tiles (hs_apply_program: tile u at u * (M^2 + 1), one 16-B bank group
+                    // apart): for qubits 0 and 1 a quarter-warp's 8 lanes take 4 column pairs of
+                    // two tiles that are 1 / 2 bank groups apart (thread bit 2 <-> tile bit a), so
+                    // their 8 loads of one quad element hit 8 distinct bank groups; otherwise they
+                    // hit 4, each twice
+                    if (G.logM == 5 && (G.TS & 7u) == 1u && cf.pbit[p] < 2) {
+                        const uint32_t hb = 8 + cf.pbit[p], d = ((q >> 2) ^ (q >> hb)) & 1u;
+                        q ^= (d << 2) | (d << hb);
+                    }
+                    const uint32_t u = q >> (2 * lq), r = q & ((1u << (2 * lq)) - 1);
                     const uint32_t qx = r >> lq, qy = r & ((1u << lq) - 1);
                     const uint32_t x = ((qx & ~lo) << 1) | (qx & lo), y = ((qy & ~lo) << 1) | (qy & lo);
                     pre.base[ps] |= (u * G.A * G.TS + x * G.M + y) << (16 * h);
