@@ -150,7 +150,13 @@ int hs_apply_transfer(hs_state* h, int k, const double* s_rowstacked, const uint
 /* Fused program (no reference counterpart: the reference applies one op per pass):
  * nsteps <= 16 single-qubit steps on in-tile qubits (< m) in ONE pass over the triangle, equal to
  * applying them in order.  kinds[p]: 0 = row-stacked 4x4 transfer matrix s[16p..16p+15]
- * (interleaved complex), 1 = Hadamard (s ignored), 2 = diagonal transfer (diagonal of s used). */
+ * (interleaved complex), 1 = Hadamard (s ignored), 2 = diagonal transfer (diagonal of s used),
+ * 3 = real transfer coupling only (00,11) and (01,10) (real parts of s[0,3,12,15] and s[5,6,9,10]
+ * used: depolarising, amplitude damping, ...), 4 = real (00,11) block s[0,3,12,15] with a complex
+ * diagonal s[5], s[10] on (01,10) (the same channels composed with Rz / phase gates), 5 = Hadamard
+ * butterfly without its factor 1/2 (the caller has scaled the coefficients of the step before, on
+ * the same qubit, by 1/2 -- exact in binary floating point).  The caller
+ * vouches that s has the stated form; entries outside it are ignored. */
 int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s, hs_plan* plan);
 /* Fused grid program: 2 .. 16 steps on 2 or 3 distinct grid qubits (>= m), each qubit's steps
  * consecutive, in ONE pass over the triangle (the units of those grid bits are gathered; each qubit's

@@ -2201,7 +2201,8 @@ int hs_apply_transfer(hs_state* h, int k, const double* s, const uint32_t* t, hs
 // Fused program of nsteps (<= 8) single-qubit steps on in-tile qubits (< m), one HBM pass
 // (SURVEY 8f "op fusion": a run of consecutive in-tile single-qubit operations).  kinds[p]: 0 row-
 // stacked 4 x 4 transfer matrix s[16p..16p+15] (interleaved complex), 1 Hadamard, 2 diagonal
-// transfer (s diagonal used).  Equivalent to applying the steps one by one (hs_apply_transfer).
+// transfer (s diagonal used), 3 / 4 real (00,11)/(01,10) transfer / real (00,11) block with a complex
+// diagonal on (01,10).  Equivalent to applying the steps one by one (hs_apply_transfer).
 int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* bits, const double* s, hs_plan* plan) {
     if (!h || nsteps < 1 || nsteps > 16 || !kinds || !bits || !s)
         return set_err(HS_ERR_INVALID, "bad program");
@@ -2209,7 +2210,7 @@ int hs_apply_program(hs_state* h, int nsteps, const int* kinds, const uint32_t* 
     for (int p = 0; p < nsteps; ++p) {
         if (bits[p] >= edge)
             return set_err(HS_ERR_RANGE, "program steps act on in-tile qubits (< m) only");
-        if (kinds[p] < 0 || kinds[p] > 3)
+        if (kinds[p] < 0 || kinds[p] > 5)
             return set_err(HS_ERR_INVALID, "bad program step kind");
     }
     DeviceGuard dg(h->device);
@@ -2292,7 +2293,7 @@ int hs_apply_grid_program(hs_state* h, int nsteps, const int* kinds, const uint3
     for (int p = 0; p < nsteps; ++p) {
         if (bits[p] < (uint32_t)h->m || bits[p] >= (uint32_t)h->n)
             return set_err(HS_ERR_RANGE, "grid program steps act on grid qubits (>= m) only");
-        if (kinds[p] < 0 || kinds[p] > 3)
+        if (kinds[p] < 0 || kinds[p] > 5)
             return set_err(HS_ERR_INVALID, "bad program step kind");
         if (p > 0 && bits[p] == bits[p - 1])
             continue;  // the qubit's chain continues

@@ -707,7 +707,10 @@ __device__ __forceinline__ void stc(double2* sb, uint32_t a, bool cj, double2 v)
 
 // One program step on a quad, row-stacked (h00, h01, h10, h11).  kind: 0 transfer matrix,
 // 1 Hadamard (native.cpp:332-339), 2 diagonal transfer, 3 real transfer coupling only (00, 11) and
-// (01, 10) (depolarising, amplitude damping and their compositions).
+// (01, 10) (depolarising, amplitude damping and their compositions), 4 real (00, 11) block with a
+// complex diagonal on (01, 10) (the same channels composed with Rz / phase gates: 16 FP64
+// operations per quad, as kinds 2 and 3), 5 Hadamard butterfly without its factor 1/2 (the caller
+// has scaled the step before it by 1/2, which is exact).
 __device__ __forceinline__ void prog_quad(uint32_t kind, const double2* S, double2& v0, double2& v1, double2& v2,
                                           double2& v3) {
     double2 w0, w1, w2, w3;
@@ -718,11 +721,23 @@ __device__ __forceinline__ void prog_quad(uint32_t kind, const double2* S, doubl
         w1 = make_double2(0.5 * (b2.x + dd.x), 0.5 * (b2.y + dd.y));
         w2 = make_double2(0.5 * (aa.x - cc.x), 0.5 * (aa.y - cc.y));
         w3 = make_double2(0.5 * (b2.x - dd.x), 0.5 * (b2.y - dd.y));
+    } else if (kind == 5) {  // Hadamard butterfly without the 1/2 (folded into the step before, exactly)
+        const double2 aa = make_double2(v0.x + v1.x, v0.y + v1.y), b2 = make_double2(v0.x - v1.x, v0.y - v1.y);
+        const double2 cc = make_double2(v2.x + v3.x, v2.y + v3.y), dd = make_double2(v2.x - v3.x, v2.y - v3.y);
+        w0 = make_double2(aa.x + cc.x, aa.y + cc.y);
+        w1 = make_double2(b2.x + dd.x, b2.y + dd.y);
+        w2 = make_double2(aa.x - cc.x, aa.y - cc.y);
+        w3 = make_double2(b2.x - dd.x, b2.y - dd.y);
     } else if (kind == 2) {
         w0 = cmul(S[0], v0);
         w1 = cmul(S[5], v1);
         w2 = cmul(S[10], v2);
         w3 = cmul(S[15], v3);
+    } else if (kind == 4) {
+        w0 = make_double2(S[0].x * v0.x + S[3].x * v3.x, S[0].x * v0.y + S[3].x * v3.y);
+        w3 = make_double2(S[12].x * v0.x + S[15].x * v3.x, S[12].x * v0.y + S[15].x * v3.y);
+        w1 = cmul(S[5], v1);
+        w2 = cmul(S[10], v2);
     } else if (kind == 3) {
         w0 = make_double2(S[0].x * v0.x + S[3].x * v3.x, S[0].x * v0.y + S[3].x * v3.y);
         w3 = make_double2(S[12].x * v0.x + S[15].x * v3.x, S[12].x * v0.y + S[15].x * v3.y);
@@ -742,15 +757,27 @@ __device__ __forceinline__ void prog_quad(uint32_t kind, const double2* S, doubl
 // One program step on two quads at once: the step's coefficients are fetched once and the two
 // independent dependency chains interleave on the FP64 pipe.
 __device__ __forceinline__ void prog_quad2(uint32_t kind, const double2* S, double2 (&a)[4], double2 (&b)[4]) {
-    if (kind == 1) {
-        prog_quad(1, S, a[0], a[1], a[2], a[3]);
-        prog_quad(1, S, b[0], b[1], b[2], b[3]);
+    if (kind == 1 || kind == 5) {
+        prog_quad(kind, S, a[0], a[1], a[2], a[3]);
+        prog_quad(kind, S, b[0], b[1], b[2], b[3]);
     } else if (kind == 2) {
         const double2 s0 = S[0], s1 = S[5], s2 = S[10], s3 = S[15];
         a[0] = cmul(s0, a[0]); b[0] = cmul(s0, b[0]);
         a[1] = cmul(s1, a[1]); b[1] = cmul(s1, b[1]);
         a[2] = cmul(s2, a[2]); b[2] = cmul(s2, b[2]);
         a[3] = cmul(s3, a[3]); b[3] = cmul(s3, b[3]);
+    } else if (kind == 4) {
+        const double p00 = S[0].x, p03 = S[3].x, p30 = S[12].x, p33 = S[15].x;
+        const double2 s1 = S[5], s2 = S[10];
+        auto pair = [&](double& x, double& y) {
+            const double tx = p03 * y, ty = p30 * x;
+            x = fma(p00, x, tx);
+            y = fma(p33, y, ty);
+        };
+        pair(a[0].x, a[3].x); pair(b[0].x, b[3].x);
+        pair(a[0].y, a[3].y); pair(b[0].y, b[3].y);
+        a[1] = cmul(s1, a[1]); b[1] = cmul(s1, b[1]);
+        a[2] = cmul(s2, a[2]); b[2] = cmul(s2, b[2]);
     } else if (kind == 3) {
         const double p00 = S[0].x, p03 = S[3].x, p30 = S[12].x, p33 = S[15].x;
         const double p11 = S[5].x, p12 = S[6].x, p21 = S[9].x, p22 = S[10].x;

@@ -211,7 +211,9 @@ for _r, _c in ((0, 0), (0, 3), (3, 0), (3, 3), (1, 1), (1, 2), (2, 1), (2, 2)):
 
 
 def _kind(step: Step) -> int:
-    """Cheapest kernel form of a step: 1 Hadamard, 2 diagonal, 3 real (00,11)/(01,10), 0 general."""
+    """Cheapest kernel form of a step: 1 Hadamard, 2 diagonal, 3 real (00,11)/(01,10), 4 real (00,11)
+    block with a complex diagonal on (01,10) (kind 3 channels composed with Rz / phase gates),
+    0 general."""
     if step.lone_h:
         return 1
     s = step.s
@@ -219,13 +221,30 @@ def _kind(step: Step) -> int:
         return 2
     if not np.any(s.imag) and not np.any(s[~_XPAT]):
         return 3
+    if (not np.any(s[~_XPAT]) and s[1, 2] == 0 and s[2, 1] == 0
+            and not np.any(s[np.ix_([0, 3], [0, 3])].imag)):
+        return 4
     return 0
 
 
 # relative arithmetic of a step per quad (FP64): Hadamard butterfly (adds), diagonal (4 complex
-# products), real (00,11)/(01,10) transfer (6 real x complex products), general 4 x 4 transfer
-# (16 complex FMA); a qubit's chain shares one shared-memory round trip, so only this counts
-_KIND_COST = {1: 0.5, 2: 1.0, 3: 1.0, 0: 4.0}
+# products), real (00,11)/(01,10) transfer (6 real x complex products) or its composition with a
+# diagonal (kind 4, the same count), general 4 x 4 transfer (16 complex FMA); a qubit's chain shares
+# one shared-memory round trip, so only this counts
+_KIND_COST = {1: 0.5, 2: 1.0, 3: 1.0, 4: 1.0, 0: 4.0}
+
+
+def _program_args(steps):
+    """(kinds, bits, coefficients) of a program's steps.  A Hadamard that follows a coefficient
+    step on the same qubit runs as the bare butterfly (kind 5) with its factor 1/2 folded into that
+    step's coefficients -- a power of two, so the results are bit for bit the same."""
+    kinds = [_kind(x) for x in steps]
+    s = np.stack([x.s for x in steps]).astype(np.complex128)
+    for i in range(1, len(steps)):
+        if kinds[i] == 1 and steps[i - 1].qubit == steps[i].qubit and kinds[i - 1] in (0, 2, 3, 4):
+            s[i - 1] = s[i - 1] * 0.5
+            kinds[i] = 5
+    return (np.array(kinds, np.int32), np.array([x.qubit for x in steps], np.uint32), np.ascontiguousarray(s))
 
 
 def execute(st: H.TiledHermitian, plan: Plan, opts: H.ApplyOptions | None = None) -> int:
@@ -234,18 +253,14 @@ def execute(st: H.TiledHermitian, plan: Plan, opts: H.ApplyOptions | None = None
     L = nat.engine()
     for item in plan.items:
         if item[0] == "program":
+            kinds, bits, s = _program_args(item[1])
             steps = item[1]
-            kinds = np.array([_kind(x) for x in steps], np.int32)
-            bits = np.array([x.qubit for x in steps], np.uint32)
-            s = np.ascontiguousarray(np.stack([x.s for x in steps]).astype(np.complex128))
             nat.check(L.hs_apply_program(st.handle, len(steps), kinds.ctypes.data_as(nat.c_i32_p),
                                          bits.ctypes.data_as(nat.c_u32_p), s.ctypes.data_as(nat.c_double_p), None),
                       "apply_program")
         elif item[0] == "gprogram":
+            kinds, bits, s = _program_args(item[1])
             steps = item[1]
-            kinds = np.array([_kind(x) for x in steps], np.int32)
-            bits = np.array([x.qubit for x in steps], np.uint32)
-            s = np.ascontiguousarray(np.stack([x.s for x in steps]).astype(np.complex128))
             nat.check(L.hs_apply_grid_program(st.handle, len(steps), kinds.ctypes.data_as(nat.c_i32_p),
                                               bits.ctypes.data_as(nat.c_u32_p), s.ctypes.data_as(nat.c_double_p),
                                               None), "apply_grid_program")

@@ -17,7 +17,9 @@ def _seq(H, HS, name, n):
                for op in HS.config_ops("c1", n)][:60]
         return out + [(H.native_gate("cnot"), [6, 2]), (H.make_generic("haar", HS.haar(2, 9)), [2, 6])]
     out = []
-    for op in HS.config_ops("c4", n)[: 3 * n + 8]:  # one layer: Rz, H, CX matching, depolarising
+    # two layers (Rz, H, CX matching, depolarising): the second layer's chains start with the first's
+    # depolarising composed with Rz (step kind 4)
+    for op in HS.config_ops("c4", n)[: 7 * n]:
         if op.kind == "rz":
             out.append((H.native_gate("rz", op.param), list(op.targets)))
         elif op.kind == "h":
