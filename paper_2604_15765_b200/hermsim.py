@@ -117,8 +117,11 @@ class TiledHermitian:
         nat.check(nat.engine().hs_state_download(self.handle, _dp(out), self._count), "download")
         return out
 
-    def download_range(self, offset: int, count: int) -> np.ndarray:
-        out = np.empty(count, np.complex128)
+    def download_range(self, offset: int, count: int, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(count, np.complex128)
+        elif out.dtype != np.complex128 or out.size != count or not out.flags.c_contiguous:
+            raise ValueError("download_range: out must be a contiguous complex128 array of `count` elements")
         nat.check(nat.engine().hs_state_download_range(self.handle, _dp(out), offset, count), "download")
         return out
 
