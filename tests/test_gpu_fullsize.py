@@ -99,8 +99,9 @@ def _compare_with_ref(st, refview, n, m, chunk=1 << 24):
     tile = 1 << (2 * m)
     chunk = max(tile, chunk - chunk % tile)
 
-    def work(got, off):
-        want = refview[off:off + got.size]
+    def work(buf, c, off):
+        got = buf[:c]
+        want = refview[off:off + c]
         np.subtract(got, want, out=got)
         maxd = float(np.abs(got).max())
         w = want.view(np.float64).reshape(-1, 2 * tile)
@@ -111,17 +112,19 @@ def _compare_with_ref(st, refview, n, m, chunk=1 << 24):
         ti -= (ti * (ti + 1) // 2 > idx)
         ti += ((ti + 1) * (ti + 2) // 2 <= idx)
         diag = idx - ti * (ti + 1) // 2 == ti
-        return maxd, float(sq[diag].sum()), float(sq[~diag].sum()), sq.size
+        return maxd, float(sq[diag].sum()), float(sq[~diag].sum()), sq.size, buf
 
     workers = max(1, min(16, os.cpu_count() or 1))
     dsum = osum = maxd = 0.0
     t = 0
     pending = []
+    free = []  # host buffers are recycled (fresh pages for every chunk of 137 GB cost tens of seconds)
 
     def drain(keep):
         nonlocal dsum, osum, maxd, t
         while len(pending) > keep:
-            md, ds, os_, nt = pending.pop(0).result()
+            md, ds, os_, nt, buf = pending.pop(0).result()
+            free.append(buf)
             maxd = max(maxd, md)
             dsum += ds
             osum += os_
@@ -130,8 +133,9 @@ def _compare_with_ref(st, refview, n, m, chunk=1 << 24):
     with ThreadPoolExecutor(workers) as pool:
         for off in range(0, cnt, chunk):
             c = min(chunk, cnt - off)
-            got = st.download_range(off, c)
-            pending.append(pool.submit(work, got, off))
+            buf = free.pop() if free else np.empty(min(chunk, cnt), np.complex128)
+            st.download_range(off, c, out=buf[:c])
+            pending.append(pool.submit(work, buf, c, off))
             drain(2 * workers)
         drain(0)
     assert t == G * (G + 1) // 2
