@@ -286,6 +286,11 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
         }
         __syncthreads();
         const bool diag = ti == tj;
+        // Ownership of a pair {e, s2}: the slot whose canonical (row, column) comes first owns it.  Rows
+        // decide except on the 2^-npairs of rows pi fixes, so a warp (one tile row) owns all of its
+        // elements or none: owned rows are read and written as whole 512-B runs, the other warps leave
+        // before any per-element arithmetic.
+        const uint32_t I0 = (uint32_t)ti << logM, J0 = (uint32_t)tj << logM;
         for (uint32_t pos0 = threadIdx.x; pos0 < nel; pos0 += CXB * blockDim.x) {
             uint64_t s2o[CXB];
             uint32_t meta[CXB];  // bit 0: active pair, 1: self-pair, 2: conjugate, 3: partner in a diagonal tile
@@ -298,17 +303,20 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
                 if (pos >= nel)
                     continue;
                 const uint32_t x = pos >> logM, y = pos & (M - 1);
-                if ((diag && x < y) || (((ti << logM) | x) >> nq) || (((tj << logM) | y) >> nq))
+                const uint32_t I = I0 | x, J = J0 | y;
+                if ((diag && x < y) || (I >> nq) || (J >> nq))
                     continue;  // mirror half, or zero padding (n < m): left as it is
                 const uint64_t tp = rT[x], tq = cT[y];
                 const uint32_t px = rX[x], qy = cY[y];
-                const bool cj = tp < tq || (tp == tq && px < qy);
+                const uint32_t pI = ((uint32_t)tp << logM) | px, pJ = ((uint32_t)tq << logM) | qy;
+                const bool cj = pI < pJ;
+                const uint32_t I2 = cj ? pJ : pI, J2 = cj ? pI : pJ;  // canonical (row, column) of the partner
+                if (I2 != I ? I2 < I : (J2 < J || (J2 == J && !cj)))
+                    continue;  // the partner's thread owns the pair; or a fixed point
                 // canonical slot of (pi(i), pi(j)): (tp, tq, px, qy), or its transpose when above the diagonal
                 const uint64_t s2 = ((cj ? cTri[y] + tp : rTri[x] + tq) << lMM) +
                                     (cj ? ((uint64_t)qy << logM) + px : ((uint64_t)px << logM) + qy);
                 const uint64_t e = (tile << lMM) + pos;
-                if (s2 < e || (s2 == e && !cj))
-                    continue;  // the lower slot of the pair owns it; or a fixed point
                 s2o[k] = s2;
                 pq[k] = cj ? (qy << 8) | px : (px << 8) | qy;
                 meta[k] = 1u | (s2 == e ? 2u : 0u) | (cj ? 4u : 0u) | (tp == tq ? 8u : 0u);
