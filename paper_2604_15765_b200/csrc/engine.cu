@@ -2258,6 +2258,9 @@ int hs_apply_cx_layer(hs_state* h, int npairs, const uint32_t* controls, const u
         used |= b;
         L.c[k] = controls[k];
         L.t[k] = targets[k];
+        // sibling groups (cx_layer_kernel): in-tile controls 0 / 1 with a grid target; bit 14: off
+        if (h->m >= 2 && controls[k] < 2 && targets[k] >= (uint32_t)h->m && !(debug_flags() & 16384u))
+            L.gmask |= 1u << (targets[k] - (uint32_t)h->m);
     }
     DeviceGuard dg(h->device);
     const uint64_t ntiles = h->count >> (2 * h->m);

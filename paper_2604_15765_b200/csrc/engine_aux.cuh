@@ -241,6 +241,10 @@ __global__ void fill_pauli_kernel(double2* st, uint64_t count, uint32_t logM, ui
 struct CxLayer {
     uint32_t n;
     uint32_t c[32], t[32];
+    // Tile-column bits that are CX targets of the in-tile controls 0 / 1 (at most two bits): along a
+    // tile row the partners of such a control's two values alternate in runs of 16 / 32 B between
+    // tile columns tq and tq ^ bit, and the sibling tile (ti, tj ^ bit) holds the complementary runs.
+    uint32_t gmask;
 };
 __device__ __forceinline__ uint64_t cx_pi(const CxLayer& L, uint64_t x) {
     uint64_t y = x;
@@ -250,10 +254,12 @@ __device__ __forceinline__ uint64_t cx_pi(const CxLayer& L, uint64_t x) {
 }
 __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st, uint64_t ntiles, uint32_t logM,
                                                        uint32_t nq, const CxLayer L) {
+    constexpr uint32_t CXB = 4;   // positions a thread has in flight
+    constexpr uint32_t NMEM = 4;  // tiles of a sibling group, at most
     __shared__ uint64_t tab[32];  // pi of the in-tile offsets
-    // per tile: pi of its rows x (tile row rT, in-tile row rX, tri(rT)) and of its columns y
-    __shared__ uint64_t rT[32], rTri[32], cT[32], cTri[32];
-    __shared__ uint32_t rX[32], cY[32];
+    // per tile: pi of its rows x (tile row rT, in-tile row rX, tri(rT)) and, per group member, of its columns y
+    __shared__ uint64_t rT[32], rTri[32], cT[NMEM * 32], cTri[NMEM * 32];
+    __shared__ uint32_t rX[32], cY[NMEM * 32];
     const uint32_t M = 1u << logM, lMM = 2 * logM, nel = 1u << lMM;
     if (threadIdx.x < M)
         tab[threadIdx.x] = cx_pi(L, threadIdx.x);
@@ -262,22 +268,33 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
         if (diag && x > y)  // mirror in the upper half of a diagonal tile
             st[slot - ((uint64_t)x << logM) - y + ((uint64_t)y << logM) + x] = make_double2(v.x, -v.y);
     };
-    // Each thread takes CXB positions of a tile at once: every owner's two loads are issued before
-    // any store (memory-level parallelism; pairs are disjoint, so no other thread reads or writes
-    // them; the upper halves of diagonal tiles written as mirrors are never read).
-    constexpr uint32_t CXB = 4;
+    const uint32_t gmask = L.gmask, glo = gmask & (0u - gmask), ghi = gmask ^ glo;
+    const uint32_t lgn = gmask ? (ghi ? 2u : 1u) : 0u;  // log2 of a group's tile count
+    // Each thread takes CXB positions at once -- one column of CXB / nm adjacent rows in each of the
+    // nm tiles of a sibling group: every owner's two loads are issued before any store (memory-level
+    // parallelism; pairs are disjoint, so no other thread reads or writes them; the upper halves of
+    // diagonal tiles written as mirrors are never read).  Adjacent rows: where the partner tile is
+    // stored transposed they are adjacent elements of one partner row.  Sibling tiles: together their
+    // partners cover whole partner rows, requested back to back (DRAM moves 64-B granules, and L2 does
+    // not keep the half nobody asked for).
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         uint64_t ti, tj;
         tri_loose(tile, ti, tj);
+        // a group lies in one tile row; it is taken whole by its first tile when every member is stored
+        const bool grouped = gmask && ((tj | gmask) <= ti);
+        if (grouped && (tj & gmask))
+            continue;
+        const uint32_t lg = grouped ? lgn : 0u, nm = 1u << lg;
         __syncthreads();  // tab ready / the previous tile's tables are no longer read
-        if (threadIdx.x < 2 * M) {
+        if (threadIdx.x < (1 + nm) * M) {
             const bool col = threadIdx.x >= M;
-            const uint32_t v = threadIdx.x & (M - 1);
-            const uint64_t pq = cx_pi(L, (col ? tj : ti) << logM) ^ tab[v], t = pq >> logM;
+            const uint32_t v = threadIdx.x & (M - 1), mem = col ? (threadIdx.x >> logM) - 1 : 0;
+            const uint64_t tjm = tj | ((mem & 1u) ? glo : 0u) | ((mem & 2u) ? ghi : 0u);
+            const uint64_t pq = cx_pi(L, (col ? tjm : ti) << logM) ^ tab[v], t = pq >> logM;
             if (col) {
-                cT[v] = t;
-                cTri[v] = t * (t + 1) / 2;
-                cY[v] = (uint32_t)(pq & (M - 1));
+                cT[mem * 32 + v] = t;
+                cTri[mem * 32 + v] = t * (t + 1) / 2;
+                cY[mem * 32 + v] = (uint32_t)(pq & (M - 1));
             } else {
                 rT[v] = t;
                 rTri[v] = t * (t + 1) / 2;
@@ -285,38 +302,47 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
             }
         }
         __syncthreads();
-        const bool diag = ti == tj;
         // Ownership of a pair {e, s2}: the slot whose canonical (row, column) comes first owns it.  Rows
         // decide except on the 2^-npairs of rows pi fixes, so a warp (one tile row) owns all of its
         // elements or none: owned rows are read and written as whole 512-B runs, the other warps leave
         // before any per-element arithmetic.
-        const uint32_t I0 = (uint32_t)ti << logM, J0 = (uint32_t)tj << logM;
-        for (uint32_t pos0 = threadIdx.x; pos0 < nel; pos0 += CXB * blockDim.x) {
+        const uint32_t I0 = (uint32_t)ti << logM;
+        const uint32_t rpi = CXB >> lg;  // rows per thread and iteration
+        const uint32_t nbase = ((M + rpi - 1) / rpi) << logM;
+        for (uint32_t pos0 = threadIdx.x; pos0 < nbase; pos0 += blockDim.x) {
             uint64_t s2o[CXB];
             uint32_t meta[CXB];  // bit 0: active pair, 1: self-pair, 2: conjugate, 3: partner in a diagonal tile
             uint32_t pq[CXB];    // partner's in-tile row << 8 | column
             double2 av[CXB], bv[CXB];
+            auto where = [&](uint32_t k, uint32_t& x, uint32_t& y, uint32_t& mem, uint64_t& tjm) {
+                mem = k & (nm - 1);
+                x = (pos0 >> logM) * rpi + (k >> lg);
+                y = pos0 & (M - 1);
+                tjm = tj | ((mem & 1u) ? glo : 0u) | ((mem & 2u) ? ghi : 0u);
+            };
 #pragma unroll
             for (uint32_t k = 0; k < CXB; ++k) {
-                const uint32_t pos = pos0 + k * blockDim.x;
+                uint32_t x, y, mem;
+                uint64_t tjm;
+                where(k, x, y, mem, tjm);
                 meta[k] = 0;
-                if (pos >= nel)
+                if (x >= M)
                     continue;
-                const uint32_t x = pos >> logM, y = pos & (M - 1);
-                const uint32_t I = I0 | x, J = J0 | y;
-                if ((diag && x < y) || (I >> nq) || (J >> nq))
+                const uint32_t I = I0 | x, J = ((uint32_t)tjm << logM) | y;
+                if ((ti == tjm && x < y) || (I >> nq) || (J >> nq))
                     continue;  // mirror half, or zero padding (n < m): left as it is
-                const uint64_t tp = rT[x], tq = cT[y];
-                const uint32_t px = rX[x], qy = cY[y];
+                const uint32_t cy = mem * 32 + y;
+                const uint64_t tp = rT[x], tq = cT[cy];
+                const uint32_t px = rX[x], qy = cY[cy];
                 const uint32_t pI = ((uint32_t)tp << logM) | px, pJ = ((uint32_t)tq << logM) | qy;
                 const bool cj = pI < pJ;
                 const uint32_t I2 = cj ? pJ : pI, J2 = cj ? pI : pJ;  // canonical (row, column) of the partner
                 if (I2 != I ? I2 < I : (J2 < J || (J2 == J && !cj)))
                     continue;  // the partner's thread owns the pair; or a fixed point
                 // canonical slot of (pi(i), pi(j)): (tp, tq, px, qy), or its transpose when above the diagonal
-                const uint64_t s2 = ((cj ? cTri[y] + tp : rTri[x] + tq) << lMM) +
+                const uint64_t s2 = ((cj ? cTri[cy] + tp : rTri[x] + tq) << lMM) +
                                     (cj ? ((uint64_t)qy << logM) + px : ((uint64_t)px << logM) + qy);
-                const uint64_t e = (tile << lMM) + pos;
+                const uint64_t e = ((tile + (tjm - tj)) << lMM) + ((uint64_t)x << logM) + y;
                 s2o[k] = s2;
                 pq[k] = cj ? (qy << 8) | px : (px << 8) | qy;
                 meta[k] = 1u | (s2 == e ? 2u : 0u) | (cj ? 4u : 0u) | (tp == tq ? 8u : 0u);
@@ -328,8 +354,11 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
             for (uint32_t k = 0; k < CXB; ++k) {
                 if (!(meta[k] & 1u))
                     continue;
-                const uint32_t pos = pos0 + k * blockDim.x, x = pos >> logM, y = pos & (M - 1);
-                const uint64_t e = (tile << lMM) + pos;
+                uint32_t x, y, mem;
+                uint64_t tjm;
+                where(k, x, y, mem, tjm);
+                const bool diag = ti == tjm;
+                const uint64_t e = ((tile + (tjm - tj)) << lMM) + ((uint64_t)x << logM) + y;
                 double2 a = av[k];
                 if (meta[k] & 2u) {  // rho'(i, j) = rho(j, i)
                     put(e, diag, x, y, make_double2(a.x, -a.y));

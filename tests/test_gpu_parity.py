@@ -223,6 +223,32 @@ def test_cx_layer_bit_identical(H, HS, n, m):
     b.free()
 
 
+@pytest.mark.parametrize("n,m", [(10, 5), (11, 5), (9, 3), (8, 2)])
+def test_cx_layer_sibling_groups_bit_identical(H, HS, n, m):
+    """CX layers whose in-tile controls 0 / 1 have grid targets (cx_layer_kernel takes the sibling
+    tiles (ti, tj ^ target bit) together, one or two group bits; groups cut by the diagonal fall back
+    to single tiles), mixed with every other pair category, against sequential CX, bit for bit."""
+    rng = np.random.default_rng(300 * n + m)
+    psi = HS.rank_psi(n, 23, 4)
+    a, b = H.TiledHermitian(n, m), H.TiledHermitian(n, m)
+    cx = H.native_gate("cnot")
+    grid = list(range(m, n))
+    for rep in range(6):
+        a.fill_mixture(psi)
+        b.fill_mixture(psi)
+        g = [int(q) for q in rng.permutation(grid)]
+        pairs = [(0, g[0])] if rep % 3 == 0 else [(1, g[0])] if rep % 3 == 1 else [(0, g[0]), (1, g[1])]
+        rest = [int(q) for q in rng.permutation([q for q in range(n) if q not in {c for p in pairs for c in p}])]
+        pairs += [(rest[2 * i], rest[2 * i + 1]) for i in range(len(rest) // 2)][: rep]
+        pairs = [pairs[i] for i in rng.permutation(len(pairs))]
+        for c, t in pairs:
+            H.apply(a, cx, [c, t])
+        H.apply_cx_layer(b, pairs)
+        assert np.array_equal(a.download().view(np.uint64), b.download().view(np.uint64)), (n, m, pairs)
+    a.free()
+    b.free()
+
+
 def test_generic_path_without_native(H, HS, oracle, orc):
     """allow_native = false routes native gates through the generic engines (kernels.cpp:515)."""
     n, m = 8, 5
