@@ -2259,7 +2259,9 @@ int hs_apply_cx_layer(hs_state* h, int npairs, const uint32_t* controls, const u
         L.c[k] = controls[k];
         L.t[k] = targets[k];
         // sibling groups (cx_layer_kernel): in-tile controls 0 / 1 with a grid target; bit 14: off
-        if (h->m >= 2 && controls[k] < 2 && targets[k] >= (uint32_t)h->m && !(debug_flags() & 16384u))
+        // (controls 0 .. 2: partner runs of 16 / 32 / 64 B; the first two such pairs; measured at n = 17)
+        if (h->m >= 3 && controls[k] < 3 && targets[k] >= (uint32_t)h->m && !(debug_flags() & 16384u) &&
+            __builtin_popcount(L.gmask) < 2)
             L.gmask |= 1u << (targets[k] - (uint32_t)h->m);
     }
     DeviceGuard dg(h->device);

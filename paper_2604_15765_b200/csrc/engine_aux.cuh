@@ -241,8 +241,8 @@ __global__ void fill_pauli_kernel(double2* st, uint64_t count, uint32_t logM, ui
 struct CxLayer {
     uint32_t n;
     uint32_t c[32], t[32];
-    // Tile-column bits that are CX targets of the in-tile controls 0 / 1 (at most two bits): along a
-    // tile row the partners of such a control's two values alternate in runs of 16 / 32 B between
+    // Tile-column bits that are CX targets of low in-tile controls (at most two bits): along a tile
+    // row the partners of such a control's two values alternate in runs of 16 / 32 / 64 B between
     // tile columns tq and tq ^ bit, and the sibling tile (ti, tj ^ bit) holds the complementary runs.
     uint32_t gmask;
 };
@@ -252,7 +252,7 @@ __device__ __forceinline__ uint64_t cx_pi(const CxLayer& L, uint64_t x) {
         y ^= ((x >> L.c[k]) & 1ull) << L.t[k];
     return y;
 }
-__global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st, uint64_t ntiles, uint32_t logM,
+__global__ void __launch_bounds__(256, 3) cx_layer_kernel(double2* __restrict__ st, uint64_t ntiles, uint32_t logM,
                                                        uint32_t nq, const CxLayer L) {
     constexpr uint32_t CXB = 4;   // positions a thread has in flight
     constexpr uint32_t NMEM = 4;  // tiles of a sibling group, at most
@@ -306,30 +306,30 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
         // decide except on the 2^-npairs of rows pi fixes, so a warp (one tile row) owns all of its
         // elements or none: owned rows are read and written as whole 512-B runs, the other warps leave
         // before any per-element arithmetic.
-        const uint32_t I0 = (uint32_t)ti << logM;
+        const uint32_t ti32 = (uint32_t)ti, tj32 = (uint32_t)tj, I0 = ti32 << logM;
         const uint32_t rpi = CXB >> lg;  // rows per thread and iteration
         const uint32_t nbase = ((M + rpi - 1) / rpi) << logM;
         for (uint32_t pos0 = threadIdx.x; pos0 < nbase; pos0 += blockDim.x) {
             uint64_t s2o[CXB];
-            uint32_t meta[CXB];  // bit 0: active pair, 1: self-pair, 2: conjugate, 3: partner in a diagonal tile
-            uint32_t pq[CXB];    // partner's in-tile row << 8 | column
+            // bit 0: active pair, 1: self-pair, 2: conjugate, 3: partner in a diagonal tile; bits 8-15 / 16-23: the
+            // partner's in-tile column / row
+            uint32_t meta[CXB];
             double2 av[CXB], bv[CXB];
-            auto where = [&](uint32_t k, uint32_t& x, uint32_t& y, uint32_t& mem, uint64_t& tjm) {
+            auto where = [&](uint32_t k, uint32_t& x, uint32_t& y, uint32_t& mem, uint32_t& tjm) {
                 mem = k & (nm - 1);
                 x = (pos0 >> logM) * rpi + (k >> lg);
                 y = pos0 & (M - 1);
-                tjm = tj | ((mem & 1u) ? glo : 0u) | ((mem & 2u) ? ghi : 0u);
+                tjm = tj32 | ((mem & 1u) ? glo : 0u) | ((mem & 2u) ? ghi : 0u);
             };
 #pragma unroll
             for (uint32_t k = 0; k < CXB; ++k) {
-                uint32_t x, y, mem;
-                uint64_t tjm;
+                uint32_t x, y, mem, tjm;
                 where(k, x, y, mem, tjm);
                 meta[k] = 0;
                 if (x >= M)
                     continue;
-                const uint32_t I = I0 | x, J = ((uint32_t)tjm << logM) | y;
-                if ((ti == tjm && x < y) || (I >> nq) || (J >> nq))
+                const uint32_t I = I0 | x, J = (tjm << logM) | y;
+                if ((ti32 == tjm && x < y) || (I >> nq) || (J >> nq))
                     continue;  // mirror half, or zero padding (n < m): left as it is
                 const uint32_t cy = mem * 32 + y;
                 const uint64_t tp = rT[x], tq = cT[cy];
@@ -342,10 +342,10 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
                 // canonical slot of (pi(i), pi(j)): (tp, tq, px, qy), or its transpose when above the diagonal
                 const uint64_t s2 = ((cj ? cTri[cy] + tp : rTri[x] + tq) << lMM) +
                                     (cj ? ((uint64_t)qy << logM) + px : ((uint64_t)px << logM) + qy);
-                const uint64_t e = ((tile + (tjm - tj)) << lMM) + ((uint64_t)x << logM) + y;
+                const uint64_t e = ((tile + (tjm - tj32)) << lMM) + (x << logM) + y;
                 s2o[k] = s2;
-                pq[k] = cj ? (qy << 8) | px : (px << 8) | qy;
-                meta[k] = 1u | (s2 == e ? 2u : 0u) | (cj ? 4u : 0u) | (tp == tq ? 8u : 0u);
+                meta[k] = 1u | (s2 == e ? 2u : 0u) | (cj ? 4u : 0u) | (tp == tq ? 8u : 0u) |
+                          ((cj ? (qy << 8) | px : (px << 8) | qy) << 8);
                 av[k] = st[e];
                 if (s2 != e)
                     bv[k] = st[s2];
@@ -354,11 +354,10 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
             for (uint32_t k = 0; k < CXB; ++k) {
                 if (!(meta[k] & 1u))
                     continue;
-                uint32_t x, y, mem;
-                uint64_t tjm;
+                uint32_t x, y, mem, tjm;
                 where(k, x, y, mem, tjm);
-                const bool diag = ti == tjm;
-                const uint64_t e = ((tile + (tjm - tj)) << lMM) + ((uint64_t)x << logM) + y;
+                const bool diag = ti32 == tjm;
+                const uint64_t e = ((tile + (tjm - tj32)) << lMM) + (x << logM) + y;
                 double2 a = av[k];
                 if (meta[k] & 2u) {  // rho'(i, j) = rho(j, i)
                     put(e, diag, x, y, make_double2(a.x, -a.y));
@@ -370,7 +369,7 @@ __global__ void __launch_bounds__(256) cx_layer_kernel(double2* __restrict__ st,
                     b.y = -b.y;
                 }
                 put(e, diag, x, y, b);
-                put(s2o[k], (meta[k] & 8u) != 0, pq[k] >> 8, pq[k] & 0xffu, a);
+                put(s2o[k], (meta[k] & 8u) != 0, meta[k] >> 16, (meta[k] >> 8) & 0xffu, a);
             }
         }
     }

@@ -225,7 +225,7 @@ def test_cx_layer_bit_identical(H, HS, n, m):
 
 @pytest.mark.parametrize("n,m", [(10, 5), (11, 5), (9, 3), (8, 2)])
 def test_cx_layer_sibling_groups_bit_identical(H, HS, n, m):
-    """CX layers whose in-tile controls 0 / 1 have grid targets (cx_layer_kernel takes the sibling
+    """CX layers whose in-tile controls 0 / 1 / 2 have grid targets (cx_layer_kernel takes the sibling
     tiles (ti, tj ^ target bit) together, one or two group bits; groups cut by the diagonal fall back
     to single tiles), mixed with every other pair category, against sequential CX, bit for bit."""
     rng = np.random.default_rng(300 * n + m)
@@ -237,7 +237,8 @@ def test_cx_layer_sibling_groups_bit_identical(H, HS, n, m):
         a.fill_mixture(psi)
         b.fill_mixture(psi)
         g = [int(q) for q in rng.permutation(grid)]
-        pairs = [(0, g[0])] if rep % 3 == 0 else [(1, g[0])] if rep % 3 == 1 else [(0, g[0]), (1, g[1])]
+        ctl = [[0], [1], [0, 1], [2], [2, 0], [1, 2, 0]][rep]
+        pairs = [(c, g[i]) for i, c in enumerate(ctl) if c < m]
         rest = [int(q) for q in rng.permutation([q for q in range(n) if q not in {c for p in pairs for c in p}])]
         pairs += [(rest[2 * i], rest[2 * i + 1]) for i in range(len(rest) // 2)][: rep]
         pairs = [pairs[i] for i in rng.permutation(len(pairs))]
