@@ -926,13 +926,23 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                 }
             } else {
                 if (TMAB && pg_two) {
+                    // Steps never couple staged positions, and a thread keeps its position: the warps
+                    // holding the lower and the upper half of the positions synchronise separately
+                    // between passes (named barriers 5 / 6) and drift apart, one half's shared-memory
+                    // phase over the other's FP64 chains; after the last pass the stage's `done`
+                    // mbarrier is the only synchronisation.  Bit 13: one barrier over all transform
+                    // warps after every pass.
+                    const uint32_t half = (tid >> (2 * G.logS0 - 1)) & 1u;
                     uint32_t p = 0;
 #pragma unroll
                     for (int ps = 0; ps < 3; ++ps) {
                         if (p < cf.nsteps) {
                             grid_prog_step2<NS>(G, cf, p, pg_end[ps], am[i % TSL][0], sb, pg_t[ps], pg_ad, pg_dlt);
-                            asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
                             p = pg_end[ps];
+                            if (G.dbg & 8192u)
+                                asm volatile("bar.sync 2, %0;" ::"n"(NCW) : "memory");  // transform warps only
+                            else if (p < cf.nsteps)
+                                asm volatile("bar.sync %0, %1;" ::"r"(5 + half), "n"(NCW / 2) : "memory");
                         }
                     }
                 } else {
