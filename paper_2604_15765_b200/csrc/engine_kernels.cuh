@@ -529,6 +529,16 @@ __device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {  //
     asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef HS_MBAR_HINT  // A/B builds: suspend-time hint (ns) for waiting warps
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"((uint32_t)HS_MBAR_HINT)
+        : "memory");
+    return;
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
