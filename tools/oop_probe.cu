@@ -83,7 +83,10 @@ __global__ void __launch_bounds__(NCONS + 32, 1) ringk(double2* __restrict__ a, 
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_ef));
     asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol_x));
     const uint64_t nItems = n / chunk_elems;
-    const uint64_t nlocal = blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const uint64_t per = (nItems + gridDim.x - 1) / gridDim.x;
+    const uint64_t nlocal = (HINT & 16) ? (blockIdx.x * per < nItems ? (nItems - blockIdx.x * per < per ? nItems - blockIdx.x * per : per) : 0)
+                                        : (blockIdx.x < nItems ? (nItems - blockIdx.x + gridDim.x - 1) / gridDim.x : 0);
+    auto item_of = [&](uint64_t j) { return (HINT & 16) ? blockIdx.x * per + j : blockIdx.x + j * gridDim.x; };
     if (warp == NCONS / 32) {
         for (uint64_t j = 0; j < nlocal + S; ++j) {
             const uint32_t s = j % S;
@@ -91,7 +94,7 @@ __global__ void __launch_bounds__(NCONS + 32, 1) ringk(double2* __restrict__ a, 
             if (j >= S) {
                 const uint64_t jj = j - S;
                 mwait(&done[s], (jj / S) & 1);
-                double2* g = a + (blockIdx.x + jj * gridDim.x) * (uint64_t)chunk_elems;
+                double2* g = a + item_of(jj) * (uint64_t)chunk_elems;
                 for (uint32_t p = lane; p < pieces; p += 32) {
                     if (HINT & 2)
                         asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"((char*)g + p * pbytes),
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(NCONS + 32, 1) ringk(double2* __restrict__ a, 
                 if (lane == 0)
                     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(bytes) : "memory");
                 __syncwarp();
-                const double2* g = a + (blockIdx.x + j * gridDim.x) * (uint64_t)chunk_elems;
+                const double2* g = a + item_of(j) * (uint64_t)chunk_elems;
                 for (uint32_t p = lane; p < pieces; p += 32) {
                     if (HINT & 1)
                         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(su32(sb) + p * pbytes),
@@ -195,6 +198,7 @@ int main() {
         run_ring<2>(a, n, sms, e0, e1, "stores evict_first");
         run_ring<3>(a, n, sms, e0, e1, "loads + stores evict_first");
         run_ring<7>(a, n, sms, e0, e1, "loads evict_unchanged, stores evict_first");
+        run_ring<16>(a, n, sms, e0, e1, "no hints, contiguous slab per CTA");
     }
     CK(cudaGetLastError());
     return 0;
