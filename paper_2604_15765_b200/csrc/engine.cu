@@ -1094,7 +1094,7 @@ int shard_prelude(hs_state* h, const Geo& G0, bool carry_over, Geo& G) {
             G.rbase[j] = j < h->recv_slots ? h->recv + (uint64_t)j * h->recv_count : nullptr;
     }
     G.rev = (uint32_t)(h->sweeps++ & 1u);
-    G.dbg = debug_flags() & (DBG_POISON | 2048u);  // the pipeline takes the stage-poisoning bit and bit 11 (one-quad program loop)
+    G.dbg = debug_flags() & (DBG_POISON | 2048u | 32768u);  // the pipeline takes the stage-poisoning bit, bit 11 (one-quad program loop) and bit 15 (no paired passes)
     return HS_OK;
 }
 

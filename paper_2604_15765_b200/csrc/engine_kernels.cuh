@@ -816,6 +816,7 @@ __device__ __forceinline__ void prog_quad2(uint32_t kind, const double2* S, doub
 struct ProgPre {
     static constexpr int MAXP = 5;
     uint32_t base[MAXP], end[MAXP];
+    uint32_t pairm;  // bit ps: passes ps and ps + 1 share one shared-memory round trip (pipe_compute)
     bool ok;
 };
 template <int K, int MODE, int NS, int NC = NCONS>
@@ -958,7 +959,9 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
         if (pre && pre->ok && nq == 2 * NC) {
             uint32_t p = 0;
 #pragma unroll
-            for (int ps = 0; ps < ProgPre::MAXP; ++ps)
+            for (int ps = 0; ps < ProgPre::MAXP; ++ps) {
+                if (ps > 0 && ((pre->pairm >> (ps - 1)) & 1u))
+                    continue;  // the second pass of a pair ran with the first
                 if (p < cf.nsteps) {
                     const uint32_t sa = 1u << cf.pbit[p], ba = pre->base[ps] & 0xffffu, bb = pre->base[ps] >> 16;
                     const uint32_t o1 = sa, o2 = sa * M, o3 = o2 + sa;
@@ -966,6 +969,47 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                     double2 vb[4] = {sb[bb], sb[bb + o1], sb[bb + o2], sb[bb + o3]};
                     for (uint32_t pp = p; pp < pre->end[ps]; ++pp)
                         prog_quad2(cf.pkind[pp], cf.s + 16 * pp, va, vb);
+                    if (ps + 1 < ProgPre::MAXP && ((pre->pairm >> ps) & 1u)) {
+                        // Paired passes (qubits a, b): lanes l and l ^ 16 hold the four a-quads of one
+                        // 4 x 4 block (rows / columns x0 + {0, 2^a, 2^b, 2^a + 2^b}), this lane those of
+                        // block row bit b = its role.  After the a-chains role 0 keeps the a-row-0
+                        // halves of its quads and gets the partner's, role 1 the a-row-1 halves: two
+                        // b-quads per lane without a trip through shared memory (16 shuffles instead of
+                        // 8 stores, a barrier and 8 loads).
+                        const bool r1 = (threadIdx.x & 16u) != 0;
+                        auto xch = [&](double2& keep_or_send0, double2& keep_or_send1) {
+                            // role 0 sends element [2] / [3] and keeps [0] / [1]; role 1 the other way round
+                            double2 snd = r1 ? keep_or_send0 : keep_or_send1;
+                            snd.x = __shfl_xor_sync(0xffffffffu, snd.x, 16);
+                            snd.y = __shfl_xor_sync(0xffffffffu, snd.y, 16);
+                            if (r1)
+                                keep_or_send0 = snd;
+                            else
+                                keep_or_send1 = snd;
+                        };
+                        xch(va[0], va[2]);
+                        xch(vb[0], vb[2]);
+                        xch(va[1], va[3]);
+                        xch(vb[1], vb[3]);
+                        double2 wa[4] = {va[0], vb[0], va[2], vb[2]}, wb[4] = {va[1], vb[1], va[3], vb[3]};
+                        const uint32_t p2 = pre->end[ps], e2 = pre->end[ps + 1];
+                        for (uint32_t pp = p2; pp < e2; ++pp)
+                            prog_quad2(cf.pkind[pp], cf.s + 16 * pp, wa, wb);
+                        const uint32_t sb2 = 1u << cf.pbit[p2], qa = pre->base[ps + 1] & 0xffffu, qb = pre->base[ps + 1] >> 16;
+                        const uint32_t q1 = sb2, q2 = sb2 * M, q3 = q2 + sb2;
+                        sb[qa] = wa[0];
+                        sb[qa + q1] = wa[1];
+                        sb[qa + q2] = wa[2];
+                        sb[qa + q3] = wa[3];
+                        sb[qb] = wb[0];
+                        sb[qb + q1] = wb[1];
+                        sb[qb + q2] = wb[2];
+                        sb[qb + q3] = wb[3];
+                        p = e2;
+                        if (p < cf.nsteps)
+                            asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NC) : "memory");  // consumer warps only
+                        continue;
+                    }
                     sb[ba] = va[0];
                     sb[ba + o1] = va[1];
                     sb[ba + o2] = va[2];
@@ -978,6 +1022,7 @@ __device__ __forceinline__ void pipe_compute(const Geo& G, const Tabs& T, const 
                     if (p < cf.nsteps)
                         asm volatile("bar.sync %0, %1;" ::"r"(barid), "n"(NC) : "memory");  // consumer warps only
                 }
+            }
             return;
         }
         for (uint32_t p = 0; p < cf.nsteps;) {
@@ -1178,6 +1223,7 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
     // ---- consumer warps: transform each staged item in place
     ProgPre pre;
     pre.ok = false;
+    pre.pairm = 0;
     if constexpr (MODE == M_PROG) {
         const uint32_t lq = G.logM - 1, tid = threadIdx.x;
         uint32_t p = 0;
@@ -1212,6 +1258,48 @@ __global__ void __launch_bounds__(NTHR_PIPE, 1) pipe_kernel(const Geo G, const C
             }
         }
         pre.ok = p >= cf.nsteps && !(G.dbg & 2048u);  // bit 11: the one-quad loop
+        // Pairs of passes (0, 1), (2, 3) on skewed whole 32 x 32 tiles, two quads per thread (bit 15: off).
+        // Block bits <- thread bits 0-3, 5-8 (bit 4 is the role): the free column bits below 3 first, then
+        // tile bits (tiles lie 1 / 2 bank groups apart), so a quarter-warp's 8 lanes spread over the bank
+        // groups as far as the pair allows; then the other column bits, the row bits, the other tile bits.
+        pre.pairm = 0;
+        if (pre.ok && G.logM == 5 && (G.TS & 7u) == 1u && (G.U << (2 * lq)) == 2 * NCONS && !(G.dbg & 32768u)) {
+            for (int ps = 0; ps + 1 < ProgPre::MAXP; ps += 2) {
+                if (!pre.end[ps + 1])
+                    break;
+                const uint32_t a = cf.pbit[pre.end[ps] - 1], b = cf.pbit[pre.end[ps + 1] - 1];
+                if (a == b)
+                    break;
+                uint32_t fb[3], k = 0;
+                for (uint32_t q = 0; q < 5; ++q)
+                    if (q != a && q != b)
+                        fb[k++] = q;
+                const uint32_t tb = (tid & 15u) | ((tid >> 5) << 4), role = (tid >> 4) & 1u;
+                uint32_t x0 = 0, y0 = 0, u = 0, i = 0, usedc = 0, usedu = 0;
+                for (uint32_t j = 0; j < 3; ++j)
+                    if (fb[j] < 3) {
+                        y0 |= ((tb >> i++) & 1u) << fb[j];
+                        usedc |= 1u << j;
+                    }
+                for (uint32_t ub = 0; ub < 2 && i < 3; ++ub) {
+                    u |= ((tb >> i++) & 1u) << ub;
+                    usedu |= 1u << ub;
+                }
+                for (uint32_t j = 0; j < 3; ++j)
+                    if (!((usedc >> j) & 1u))
+                        y0 |= ((tb >> i++) & 1u) << fb[j];
+                for (uint32_t j = 0; j < 3; ++j)
+                    x0 |= ((tb >> i++) & 1u) << fb[j];
+                for (uint32_t ub = 0; ub < 2; ++ub)
+                    if (!((usedu >> ub) & 1u))
+                        u |= ((tb >> i++) & 1u) << ub;
+                const uint32_t B = u * G.A * G.TS + x0 * G.M + y0, sa = 1u << a, sb2 = 1u << b;
+                const uint32_t ba = B + role * sb2 * G.M, qa = B + role * sa * G.M;
+                pre.base[ps] = ba | ((ba + sb2) << 16);
+                pre.base[ps + 1] = qa | ((qa + sa) << 16);
+                pre.pairm |= 1u << ps;
+            }
+        }
     }
     for (uint64_t i = 0; i < nlocal; ++i) {
         const uint32_t s = (uint32_t)(i % S);
