@@ -707,9 +707,9 @@ __device__ __forceinline__ void grid_prog_step(const Geo& G, const Tabs& T, cons
 // computed once per kernel (gather_ws_kernel), per item only the adjoint flags are looked up.  Both
 // quads are loaded before either chain runs (the compiler cannot hoist shared loads over shared
 // stores itself), and the adjoint flag rides in bit 31 of each address.
-template <int NS>
-__device__ __forceinline__ void grid_prog_step2(const Geo& G, const Coef<NS>& cf, uint32_t p, uint32_t p1, uint64_t am,
-                                                double2* sb, uint32_t t0ab, uint32_t ad, uint32_t dlt) {
+template <int NS, bool PLAIN>
+__device__ __forceinline__ void grid_prog_step2_(const Geo& G, const Coef<NS>& cf, uint32_t p, uint32_t p1, uint64_t am,
+                                                 double2* sb, uint32_t t0ab, uint32_t ad, uint32_t dlt) {
     // t0ab: the (0, 0) logical tile of this thread's two quads for this pass (bits 0-7, 8-15);
     // ad: direct in-box offset of its position, dlt: transposed minus direct offset
     const uint32_t g = G.g, sh = 2 * G.logS0, l = cf.pbit[p];  // box slots per tile << 6 == S0^2
@@ -718,14 +718,21 @@ __device__ __forceinline__ void grid_prog_step2(const Geo& G, const Coef<NS>& cf
 #pragma unroll
     for (uint32_t h = 0; h < 2; ++h) {
         const uint32_t t0 = (t0ab >> (8 * h)) & 0xffu;
-        const uint64_t amt = am >> t0;  // the quad's adjoint flags at bit offsets 0, o1, o2, o3 (<= 36)
         const uint32_t base = (t0 << sh) + ad;
-        const uint32_t f0 = (uint32_t)amt & 1u, f1 = (uint32_t)(amt >> o1) & 1u, f2 = (uint32_t)(amt >> o2) & 1u,
-                       f3 = (uint32_t)(amt >> o3) & 1u;
-        a[4 * h + 0] = (base + f0 * dlt) | (f0 << 31);
-        a[4 * h + 1] = (base + (o1 << sh) + f1 * dlt) | (f1 << 31);
-        a[4 * h + 2] = (base + (o2 << sh) + f2 * dlt) | (f2 << 31);
-        a[4 * h + 3] = (base + (o3 << sh) + f3 * dlt) | (f3 << 31);
+        if constexpr (PLAIN) {  // every tile of the unit in stored orientation: no transposed offsets, no flips
+            a[4 * h + 0] = base;
+            a[4 * h + 1] = base + (o1 << sh);
+            a[4 * h + 2] = base + (o2 << sh);
+            a[4 * h + 3] = base + (o3 << sh);
+        } else {
+            const uint64_t amt = am >> t0;  // the quad's adjoint flags at bit offsets 0, o1, o2, o3 (<= 36)
+            const uint32_t f0 = (uint32_t)amt & 1u, f1 = (uint32_t)(amt >> o1) & 1u, f2 = (uint32_t)(amt >> o2) & 1u,
+                           f3 = (uint32_t)(amt >> o3) & 1u;
+            a[4 * h + 0] = (base + f0 * dlt) | (f0 << 31);
+            a[4 * h + 1] = (base + (o1 << sh) + f1 * dlt) | (f1 << 31);
+            a[4 * h + 2] = (base + (o2 << sh) + f2 * dlt) | (f2 << 31);
+            a[4 * h + 3] = (base + (o3 << sh) + f3 * dlt) | (f3 << 31);
+        }
     }
     double2 va[4], vb[4];
 #pragma unroll
@@ -733,20 +740,119 @@ __device__ __forceinline__ void grid_prog_step2(const Geo& G, const Coef<NS>& cf
         va[c] = sb[a[c] & 0x7fffffffu];
         vb[c] = sb[a[4 + c] & 0x7fffffffu];
     }
+    if constexpr (!PLAIN) {
 #pragma unroll
-    for (uint32_t c = 0; c < 4; ++c) {
-        va[c].y = flip_sign(va[c].y, a[c] & 0x80000000u);
-        vb[c].y = flip_sign(vb[c].y, a[4 + c] & 0x80000000u);
+        for (uint32_t c = 0; c < 4; ++c) {
+            va[c].y = flip_sign(va[c].y, a[c] & 0x80000000u);
+            vb[c].y = flip_sign(vb[c].y, a[4 + c] & 0x80000000u);
+        }
     }
     for (uint32_t pp = p; pp < p1; ++pp)
         prog_quad2(cf.pkind[pp], cf.s + 16 * pp, va, vb);
 #pragma unroll
     for (uint32_t c = 0; c < 4; ++c) {
-        va[c].y = flip_sign(va[c].y, a[c] & 0x80000000u);
-        vb[c].y = flip_sign(vb[c].y, a[4 + c] & 0x80000000u);
+        if constexpr (!PLAIN) {
+            va[c].y = flip_sign(va[c].y, a[c] & 0x80000000u);
+            vb[c].y = flip_sign(vb[c].y, a[4 + c] & 0x80000000u);
+        }
         sb[a[c] & 0x7fffffffu] = va[c];
         sb[a[4 + c] & 0x7fffffffu] = vb[c];
     }
+}
+template <int NS>
+__device__ __forceinline__ void grid_prog_step2(const Geo& G, const Coef<NS>& cf, uint32_t p, uint32_t p1, uint64_t am,
+                                                double2* sb, uint32_t t0ab, uint32_t ad, uint32_t dlt) {
+    if (am == 0)  // off-diagonal units away from the diagonal: every logical tile is a stored tile
+        grid_prog_step2_<NS, true>(G, cf, p, p1, am, sb, t0ab, ad, dlt);
+    else
+        grid_prog_step2_<NS, false>(G, cf, p, p1, am, sb, t0ab, ad, dlt);
+}
+
+// Two passes of a grid program in one shared-memory round trip (as pipe_compute's paired in-tile
+// passes): lanes l and l ^ 16 hold, at one staged position, the four quads of the first qubit (local
+// index la) that make up one 4 x 4 block of logical tiles over the qubits (la, lb) -- this lane the
+// two with tile-row bit lb = its role.  After the first chains role 0 keeps the halves with row bit
+// la = 0 and gets the partner's, role 1 those with row bit la = 1: two quads of the second qubit per
+// lane.  tA / tB: the (0, 0) tiles of the lane's two quads in the first / second pass.
+template <int NS, bool PLAIN>
+__device__ __forceinline__ void grid_prog_pair2_(const Geo& G, const Coef<NS>& cf, uint32_t p, uint32_t p1, uint32_t p2,
+                                                 uint64_t am, double2* sb, uint32_t tA, uint32_t tB, uint32_t ad,
+                                                 uint32_t dlt, bool r1) {
+    const uint32_t g = G.g, sh = 2 * G.logS0;
+    auto addrs = [&](uint32_t t0ab, uint32_t l, uint32_t (&a)[8]) {
+        const uint32_t o1 = 1u << l, o2 = o1 << g, o3 = o1 + o2;
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+            const uint32_t t0 = (t0ab >> (8 * h)) & 0xffu;
+            const uint32_t base = (t0 << sh) + ad;
+            if constexpr (PLAIN) {  // every tile of the unit in stored orientation: no transposed offsets, no flips
+                a[4 * h + 0] = base;
+                a[4 * h + 1] = base + (o1 << sh);
+                a[4 * h + 2] = base + (o2 << sh);
+                a[4 * h + 3] = base + (o3 << sh);
+            } else {
+                const uint64_t amt = am >> t0;
+                const uint32_t f0 = (uint32_t)amt & 1u, f1 = (uint32_t)(amt >> o1) & 1u, f2 = (uint32_t)(amt >> o2) & 1u,
+                               f3 = (uint32_t)(amt >> o3) & 1u;
+                a[4 * h + 0] = (base + f0 * dlt) | (f0 << 31);
+                a[4 * h + 1] = (base + (o1 << sh) + f1 * dlt) | (f1 << 31);
+                a[4 * h + 2] = (base + (o2 << sh) + f2 * dlt) | (f2 << 31);
+                a[4 * h + 3] = (base + (o3 << sh) + f3 * dlt) | (f3 << 31);
+            }
+        }
+    };
+    uint32_t a[8];
+    addrs(tA, cf.pbit[p], a);
+    double2 va[4], vb[4];
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) {
+        va[c] = sb[a[c] & 0x7fffffffu];
+        vb[c] = sb[a[4 + c] & 0x7fffffffu];
+    }
+    if constexpr (!PLAIN) {
+#pragma unroll
+        for (uint32_t c = 0; c < 4; ++c) {
+            va[c].y = flip_sign(va[c].y, a[c] & 0x80000000u);
+            vb[c].y = flip_sign(vb[c].y, a[4 + c] & 0x80000000u);
+        }
+    }
+    for (uint32_t pp = p; pp < p1; ++pp)
+        prog_quad2(cf.pkind[pp], cf.s + 16 * pp, va, vb);
+    auto xch = [&](double2& e0, double2& e2) {  // role 0 sends e2 and keeps e0, role 1 the other way round
+        double2 snd = r1 ? e0 : e2;
+        snd.x = __shfl_xor_sync(0xffffffffu, snd.x, 16);
+        snd.y = __shfl_xor_sync(0xffffffffu, snd.y, 16);
+        if (r1)
+            e0 = snd;
+        else
+            e2 = snd;
+    };
+    xch(va[0], va[2]);
+    xch(vb[0], vb[2]);
+    xch(va[1], va[3]);
+    xch(vb[1], vb[3]);
+    double2 wa[4] = {va[0], vb[0], va[2], vb[2]}, wb[4] = {va[1], vb[1], va[3], vb[3]};
+    for (uint32_t pp = p1; pp < p2; ++pp)
+        prog_quad2(cf.pkind[pp], cf.s + 16 * pp, wa, wb);
+    addrs(tB, cf.pbit[p1], a);
+#pragma unroll
+    for (uint32_t c = 0; c < 4; ++c) {
+        if constexpr (!PLAIN) {
+            wa[c].y = flip_sign(wa[c].y, a[c] & 0x80000000u);
+            wb[c].y = flip_sign(wb[c].y, a[4 + c] & 0x80000000u);
+        }
+        sb[a[c] & 0x7fffffffu] = wa[c];
+        sb[a[4 + c] & 0x7fffffffu] = wb[c];
+    }
+}
+template <int NS>
+__device__ __forceinline__ void grid_prog_pair2(const Geo& G, const Coef<NS>& cf, uint32_t p, uint32_t p1, uint32_t p2,
+                                                uint64_t am, double2* sb, uint32_t tA, uint32_t tB, uint32_t ad,
+                                                uint32_t dlt, bool r1) {
+    if (am == 0)  // off-diagonal units away from the diagonal: every logical tile is a stored tile
+        grid_prog_pair2_<NS, true>(G, cf, p, p1, p2, am, sb, tA, tB, ad, dlt, r1);
+    else
+        grid_prog_pair2_<NS, false>(G, cf, p, p1, p2, am, sb, tA, tB, ad, dlt, r1);
 }
 
 // BULK (G.bulk): sub-block rows are contiguous runs of S0 >= 16 elements; every tile is staged in its
@@ -874,11 +980,20 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
         }
         // grid programs on TMA boxes: this thread's position and its in-box offsets (direct / transposed;
         // the swizzle term (x ^ y) & 7 is symmetric), fixed for the whole kernel (grid_prog_step2)
-        uint32_t pg_ad = 0, pg_dlt = 0, pg_t[3] = {0, 0, 0}, pg_end[3] = {0, 0, 0};
-        bool pg_two = false;
+        uint32_t pg_ad = 0, pg_dlt = 0, pg_t[3] = {0, 0, 0}, pg_end[3] = {0, 0, 0}, pg_tA = 0, pg_tB = 0, pg_half = 0;
+        bool pg_two = false, pg_pair = false;
         if constexpr (MODE == M_PROG && TMAB) {
-            const uint32_t nbx = G.S0 >> 3, lp = 2 * G.logS0, pos = tid & ((1u << lp) - 1), pi = pos >> G.logS0,
-                           pj = pos & (G.S0 - 1);
+            // Paired passes (grid_prog_pair2; bit 15: off): lane bits 0-3 and the low warp bits give the
+            // position, lane bit 4 the role, the other warp bits the 4 x 4 tile block (3 grid qubits: 4 per
+            // position); the same bits select the two quads of an unpaired pass.
+            const uint32_t nbx = G.S0 >> 3, lp = 2 * G.logS0;
+            pg_pair = !(G.dbg & 32768u) && (lp == 6 || lp == 8) && NCW == 512;
+            const uint32_t wlo = (tid >> 5) & ((1u << (lp - 4)) - 1);
+            const uint32_t pos = pg_pair ? (tid & 15u) | (wlo << 4) : tid & ((1u << lp) - 1);
+            const uint32_t role = (tid >> 4) & 1u, beta = (tid >> 5) >> (lp - 4);
+            const uint32_t tq0 = pg_pair ? (beta << 1) | role : tid >> lp;
+            pg_half = (pos >> (lp - 1)) & 1u;
+            const uint32_t pi = pos >> G.logS0, pj = pos & (G.S0 - 1);
             const uint32_t sw = (pi ^ pj) & 7u;
             pg_ad = (((pi >> 3) * nbx + (pj >> 3)) << 6) + (pi & 7u) * 8u + sw;
             pg_dlt = (((pj >> 3) * nbx + (pi >> 3)) << 6) + (pj & 7u) * 8u + sw - pg_ad;
@@ -895,7 +1010,7 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                     uint32_t t0ab = 0;
 #pragma unroll
                     for (uint32_t h = 0; h < 2; ++h) {
-                        const uint32_t tq = (tid >> lp) + h * (NCW >> lp);
+                        const uint32_t tq = tq0 + h * (NCW >> lp);
                         const uint32_t rr = tq >> (G.g - 1), cc = tq & hm;
                         const uint32_t R0 = ((rr & ~lo) << 1) | (rr & lo), C0 = ((cc & ~lo) << 1) | (cc & lo);
                         t0ab |= ((R0 << G.g) | C0) << (8 * h);
@@ -906,6 +1021,19 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                 }
             // bit 11: the one-quad loop
             pg_two = p >= cf.nsteps && ((1u << (2 * G.g - 2)) << lp) == 2 * NCW && !(G.dbg & 2048u);
+            pg_pair = pg_pair && pg_two && pg_end[1] && (G.g == 2 || G.g == 3);
+            if (pg_pair) {
+                const uint32_t la = cf.pbit[0], lb = cf.pbit[pg_end[0]], g = G.g;
+                uint32_t R0 = 0, C0 = 0;
+                if (g == 3) {  // the block: the row / column bit of the third qubit
+                    const uint32_t f = 3u - la - lb;
+                    R0 = (beta >> 1) << f;
+                    C0 = (beta & 1u) << f;
+                }
+                const uint32_t a0 = ((R0 | (role << lb)) << g) | C0, b0 = ((R0 | (role << la)) << g) | C0;
+                pg_tA = a0 | ((a0 + (1u << lb)) << 8);
+                pg_tB = b0 | ((b0 + (1u << la)) << 8);
+            }
         }
         for (uint64_t i = 0; i < nlocal; ++i) {
             const uint32_t s = (uint32_t)(i % S);
@@ -932,8 +1060,18 @@ __global__ void __launch_bounds__((MODE == M_SF2 || MODE == M_SF3 || NARROW) ? 5
                     // phase over the other's FP64 chains; after the last pass the stage's `done`
                     // mbarrier is the only synchronisation.  Bit 13: one barrier over all transform
                     // warps after every pass.
-                    const uint32_t half = (tid >> (2 * G.logS0 - 1)) & 1u;
+                    const uint32_t half = pg_half;
                     uint32_t p = 0;
+                    if (pg_pair) {
+                        grid_prog_pair2<NS>(G, cf, 0, pg_end[0], pg_end[1], am[i % TSL][0], sb, pg_tA, pg_tB, pg_ad, pg_dlt,
+                                            (tid & 16u) != 0);
+                        p = pg_end[1];
+                        if (p < cf.nsteps) {
+                            asm volatile("bar.sync %0, %1;" ::"r"(5 + half), "n"(NCW / 2) : "memory");
+                            grid_prog_step2<NS>(G, cf, p, pg_end[2], am[i % TSL][0], sb, pg_t[2], pg_ad, pg_dlt);
+                            p = pg_end[2];
+                        }
+                    }
 #pragma unroll
                     for (int ps = 0; ps < 3; ++ps) {
                         if (p < cf.nsteps) {
