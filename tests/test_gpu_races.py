@@ -15,6 +15,9 @@ and pass oracle parity:
 * HS_DEBUG_GRID=1 / 3 / 37 / 296 -- the persistent kernels run with that many CTAs: every item is
   processed by a different CTA, in a different per-CTA order, so cross-CTA write overlaps (two
   units writing one tile) or order dependences change the digest.
+* HS_DEBUG_FLAGS bits 13 / 14 / 15 -- the schedule variants of the fused passes (one barrier over all
+  transform warps, CX layers without sibling tile groups, program passes without the shuffle
+  pairing): the same arithmetic per element in another schedule, so the same digest.
 """
 import os
 import subprocess
@@ -31,6 +34,10 @@ SETTINGS = [
     {"HS_DEBUG_GRID": "3"},
     {"HS_DEBUG_FLAGS": "1024", "HS_DEBUG_GRID": "37"},
     {"HS_DEBUG_GRID": "296"},
+    # schedule variants of the fused passes (the same arithmetic per element, so the same bits):
+    # unpaired program passes, one barrier over all transform warps, CX layers without sibling groups
+    {"HS_DEBUG_FLAGS": str(32768 + 8192 + 16384)},
+    {"HS_DEBUG_FLAGS": str(32768 + 1024), "HS_DEBUG_GRID": "3"},
 ]
 
 
