@@ -52,6 +52,41 @@ def test_fused_equals_sequential(name, n, m):
     assert np.max(np.abs(got - want)) <= 1e-12 * fro, (name, plan.launches)
 
 
+@pytest.mark.parametrize("n,seed", [(10, 1), (11, 2), (12, 3)])
+def test_fused_random_qubit_subsets(n, seed):
+    """Runs of single-qubit operations on random qubit subsets, in random order: programs on 1-5
+    in-tile qubits (every pair the shuffle-paired passes can meet, e.g. (1, 4), (0, 3)), grid programs
+    on 2 and 3 grid qubits that are not neighbours, every step kind (transfer matrix, Hadamard,
+    diagonal, real pair, real pair with complex diagonal, butterfly), against one-op-at-a-time."""
+    from paper_2604_15765_b200 import fusion
+    from paper_2604_15765_b200 import harness as HS
+    from paper_2604_15765_b200 import hermsim as H
+    m = 5
+    rng = np.random.default_rng(500 + seed)
+    makers = [lambda: H.depolarising(float(rng.uniform(0.01, 0.2))), lambda: H.amplitude_damping(float(rng.uniform(0.01, 0.3))),
+              lambda: H.native_gate("rz", float(rng.uniform(-3, 3))), lambda: H.native_gate("h"),
+              lambda: H.native_gate("s"), lambda: H.make_generic("haar1", HS.haar(1, int(rng.integers(1 << 20))))]
+    psi = HS.rank_psi(n, 13, 4)
+    a, b = H.TiledHermitian(n, m), H.TiledHermitian(n, m)
+    opts = H.ApplyOptions(count_subcases=False)
+    for rep in range(8):
+        a.fill_mixture(psi)
+        b.fill_mixture(psi)
+        qs = [int(q) for q in rng.choice(n, size=int(rng.integers(2, n + 1)), replace=False)]
+        ops = []
+        for _ in range(int(rng.integers(1, 4))):  # up to three operations per qubit, interleaved over the qubits
+            for q in rng.permutation(qs):
+                ops.append((makers[int(rng.integers(len(makers)))](), [int(q)]))
+        for spec, tg in ops:
+            H.apply(a, spec, tg, opts)
+        plan = fusion.apply_sequence(b, ops)
+        want, got = a.download(), b.download()
+        fro = H.frobenius(a)
+        assert np.max(np.abs(got - want)) <= 1e-12 * fro, (n, rep, sorted(qs), plan.launches)
+    a.free()
+    b.free()
+
+
 def test_fused_against_reference(oracle):
     """The fused C2 pass against the compiled reference applying the same 2n operations."""
     from paper_2604_15765_b200 import fusion
