@@ -1018,7 +1018,10 @@ const bool g_kraus2_direct = [] {
 // NaN after its write-back has left the stage and before the next load is issued, so a transform
 // that reads a stage before its load landed, or a write-back that reads after the refill started,
 // puts NaN into the result (the race / synchronisation check that replaces compute-sanitizer, which
-// this pool does not run: tests/test_gpu_races.py).
+// this pool does not run: tests/test_gpu_races.py).  Schedule variants for A/B runs, same results bit
+// for bit: bit 11 one quad per thread in program passes, bit 12 unskewed program tiles, bit 13 one
+// barrier over all transform warps after every grid-program pass, bit 14 CX layers without sibling
+// tile groups, bit 15 program passes without the shuffle pairing.
 uint32_t debug_flags() {
     static const uint32_t v = [] {
         const char* e = getenv("HS_DEBUG_FLAGS");
